@@ -1,0 +1,146 @@
+/*
+ * splat_b200.h -- C ABI of the B200-native Splat-LOAM hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  All device pointers are
+ * CUDA device memory owned by the caller unless stated otherwise; every call
+ * is stream-ordered on the given cudaStream_t (passed as void*) and never
+ * aborts: it returns an ss_status code which the Python host layer maps onto
+ * the reference's exception classes (splatscan/errors.py:8-25).
+ *
+ * Reference interfaces each entry point replaces (paths relative to the
+ * reference tree, pkg/src/splatscan/):
+ *   ss_render_forward        rasterizer.py:455-499  rasterize_forward
+ *   ss_records_*             rasterizer.py:136-148  BlendRecords
+ *   ss_render_backward       rasterizer.py:534-701  rasterize_backward
+ *                            (+ splats.py:133-163 tangent_raw_gradients and the
+ *                             raw-space chain rule of mapping.py:479-494 when
+ *                             raw_space = 1)
+ *   ss_mapping_loss          mapping.py:128-196     range/normal/opacity losses
+ *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
+ *                            the H/b accumulation of registration.py:470-477)
+ *   ss_photo_objective       registration.py:379-384 _objective on a trial pose
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (host layer maps them to splatscan.errors) ---------- */
+typedef enum {
+  SS_OK = 0,
+  SS_ERR_INVALID_ARGUMENT = 1, /* GeometryError: bad sizes / camera / config   */
+  SS_ERR_STALE_RECORDS = 2,    /* GeometryError: records do not match model    */
+  SS_ERR_UNSUPPORTED = 3,      /* GeometryError: e.g. tile_size not 8 or 16    */
+  SS_ERR_CUDA = 4,             /* RuntimeError: CUDA launch / allocation error */
+  SS_ERR_CAPACITY = 5,         /* internal: pair capacity exceeded, retry      */
+  SS_ERR_DEGENERATE = 6        /* GeometryError: zero / parallel raw tangents  */
+} ss_status;
+
+/* SphericalCamera (geometry.py:68-115) */
+typedef struct {
+  int32_t width, height;
+  double az_min, az_max, el_min, el_max;
+} ss_camera;
+
+/* RasterConfig (rasterizer.py:69-78) */
+typedef struct {
+  int32_t tile_size;  /* 8 (reference default) or 16 */
+  int32_t chunk_size; /* accepted for API parity; output-neutral */
+  double alpha_cutoff, alpha_clamp, min_transmittance, denom_eps, cutoff_sigma, bbox_pad_px;
+} ss_raster_cfg;
+
+/* SplatModel raw storage (splats.py:166-212), float32 device arrays */
+typedef struct {
+  int32_t n;
+  const float* centers;       /* n x 3 */
+  const float* raw_t_alpha;   /* n x 3 */
+  const float* raw_t_beta;    /* n x 3 */
+  const float* log_scales;    /* n x 2 */
+  const float* logit_opacity; /* n     */
+} ss_splats;
+
+/* Opaque records of one forward render (tile lists, per-pixel blend state).
+ * Owns its device buffers (stream-ordered allocations). */
+typedef struct ss_records ss_records;
+
+ss_records* ss_records_create(void);
+void ss_records_destroy(ss_records* rec, void* stream);
+
+/* Forward render.  pose_Rt = row-major R (9) then t (3), sensor-in-world
+ * (se3.py:3-7).  Outputs (device, float32): range H*W, normal H*W*3,
+ * opacity H*W.  Fills `rec` for ss_render_backward.  One host
+ * synchronisation happens when the pair capacity must grow. */
+int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_splats* splats,
+                      const ss_raster_cfg* cfg, float* out_range, float* out_normal,
+                      float* out_opacity, ss_records* rec, void* stream);
+
+/* Number of (tile, splat) pairs and tiles of a finished forward. */
+int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y);
+/* Copy tile_ptr (tiles+1) and pair_splats (n_pairs) into caller device
+ * buffers as int64, matching BlendRecords (rasterizer.py:145-146). */
+int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_splats, void* stream);
+
+/* Work counts of a finished forward for the roofline: evaluations E =
+ * sum over tiles of pixels x list length, contributions U = (pixel, splat)
+ * pairs with nonzero blend weight.  Synchronises the stream. */
+int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contributions, void* stream);
+
+/* Optional CUDA-event timing of every kernel stage launched with `rec`
+ * (0 preprocess, 1 scan, 2 scatter, 3 sort, 4 sort_long, 5 forward,
+ * 6 backward, 7 finalize).  ss_records_stage_times waits for the events,
+ * returns summed milliseconds and launch counts per stage and resets. */
+int ss_records_profile(ss_records* rec, int enable);
+int ss_records_stage_times(ss_records* rec, double* ms, int32_t* launches, int32_t n_stages);
+
+/* Backward.  dD: H*W, dN: H*W*3, dO: H*W float32 pixel gradients
+ * (PixelGradients, rasterizer.py:90-96).
+ * raw_space = 0: grads = n x 15 plain-space SplatGradients
+ *   [d_centers 3 | d_t_alpha 3 | d_t_beta 3 | d_normal 3 | d_scales 2 | d_opacity 1]
+ * raw_space = 1: grads = n x 12 raw-parameter gradients
+ *   [centers 3 | raw_t_alpha 3 | raw_t_beta 3 | log_scales 2 | logit_opacity 1]
+ *   d_scales_extra (n x 2, may be NULL) adds the scale-loss gradient first
+ *   (mapping.py:492). */
+int ss_render_backward(const ss_records* rec, const ss_splats* splats, const float* dD,
+                       const float* dN, const float* dO, const float* d_scales_extra,
+                       float* grads, int raw_space, void* stream);
+
+/* Mapping loss of one keyframe (mapping.py:128-196) on device images.
+ * kf_range/kf_valid: target range image; kf_normal/kf_nvalid: target normals.
+ * Writes pixel gradients dD, dN, dO and accumulates the four loss parts
+ * [range, opacity, normal, unused] into parts4 (float64, device, zeroed by
+ * the caller). */
+int ss_mapping_loss(int32_t width, int32_t height, const float* range, const float* normal,
+                    const float* opacity, const float* kf_range, const uint8_t* kf_valid,
+                    const float* kf_normal, const uint8_t* kf_nvalid, double w_opacity,
+                    double w_normal, double range_floor, float* dD, float* dN, float* dO,
+                    double* parts4, void* stream);
+
+/* ---- photometric registration (registration.py:277-384) -------------- */
+typedef struct {
+  double huber_photo, trim_factor, spread_gate;
+} ss_reg_cfg;
+
+/* One linearisation: residuals of anchors X_w (M x 3, float32) against the
+ * scan range image at pose T (row-major R then t), trimmed at
+ * max(trim_factor*median|r|, trim_floor), Huber-weighted and reduced into
+ * out[0:21] = upper-triangular sum J^T W J (row-major 6x6 upper),
+ * out[21:27] = J^T W r, out[27] = Huber objective, out[28] = m (kept count),
+ * out[29] = sum r^2.  Sums are unnormalised float64 (caller scales by 1/m).
+ * `workspace` must hold at least ss_photo_workspace_bytes(M) bytes. */
+size_t ss_photo_workspace_bytes(int32_t M);
+int ss_photo_system(const float* X_w, int32_t M, const float* scan_range,
+                    const uint8_t* scan_valid, const ss_camera* cam, const double* T_Rt,
+                    double trim_floor, const ss_reg_cfg* cfg, double* out30, void* workspace,
+                    void* stream);
+
+const char* ss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,527 @@
+// K3 forward blend, K4 backward, and the per-splat gradient finalize.
+//
+// Reference behaviour (pkg/src/splatscan/):
+//   rasterizer.py:363-399   ray/splat intersection and cutoffs
+//   rasterizer.py:402-452   transmittance and front-to-back blend
+//   rasterizer.py:534-701   analytic backward, world-frame mapping
+//   splats.py:133-163       Gram-Schmidt backward; mapping.py:479-494 raw chain
+//
+// Formulation.  The reference intersects the pixel's two origin planes
+// (h_x, h_y) with the splat.  With A = Bb x Bc, Bv = Bc x Ba, C = Ba x Bb the
+// same intersection is, by the Binet-Cauchy identity (h_x x h_y = -v),
+//     sa = (v.A)/(v.C),  sb = (v.Bv)/(v.C),  range = |nu| = det/(v.C),
+// det = Bc.C, den = -(v.C).  The cutoff alpha >= 1/255 is the quadratic cone
+// q(v) = (v.A)^2 + (v.Bv)^2 - K (v.C)^2 <= 0 with K = 2 ln(255 o).  To avoid
+// cancellation of v.A (|A| ~ s |Bc|) in float32, every product with A and Bv
+// is taken relative to the tile's centre ray v_t: v.A = c0 + d.A with
+// c0 = (v_t - u_c).A formed from the float64 difference of unit vectors.
+//
+// Work decomposition: one warp per 8x8 tile (two pixels per lane), each warp
+// stages its tile list through shared memory 32 entries at a time.  The
+// forward records, per pixel, the final transmittance, the last contributing
+// list position and a bitmask of contributing entries; the backward walks the
+// list back to front (suffix sums accumulate, no total-minus-prefix
+// cancellation) visiting only entries some pixel of the tile contributed to,
+// and reduces each splat's 14 accumulators across the warp through shared
+// memory before one vector of float atomics.
+#include "common.cuh"
+
+namespace ss {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kStride = 36;  // 32-bit words per staged entry: 16 floats + 5 double2 (144 B)
+
+struct BlendParams {
+  CamK cam;
+  float alpha_cutoff, alpha_clamp, min_T, denom_eps;
+};
+
+template <int TS>
+struct TileShape {
+  static constexpr int PPL = TS * TS / 32;  // pixels per lane
+};
+
+struct PixelGeo {
+  double v[3];   // unit sample ray (float64)
+  float d[3];    // v_p - v_t (float32 of a float64 difference)
+  float pp[6];   // d.x^2, d.y^2, d.z^2, 2dxdy, 2dxdz, 2dydz
+  int row, col;
+  bool inside;   // inside the image
+  bool ray_ok;   // reference ray_ok (rasterizer.py:167-168)
+};
+
+template <int TS>
+__device__ __forceinline__ void tile_center(const CamK& k, int tr, int tc, double vt[3]) {
+  int r0 = tr * TS, c0 = tc * TS;
+  int rh = min(TS, k.H - r0), cw = min(TS, k.W - c0);
+  ray_at(k, (double)c0 + 0.5 * (cw - 1) + k.off_u, (double)r0 + 0.5 * (rh - 1) + k.off_v, vt);
+}
+
+template <int TS>
+__device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, const double vt[3], PixelGeo& g) {
+  g.row = tr * TS + p / TS;
+  g.col = tc * TS + p % TS;
+  g.inside = g.row < k.H && g.col < k.W;
+  ray_at(k, (double)g.col + k.off_u, (double)g.row + k.off_v, g.v);
+  g.ray_ok = g.inside && sqrt(g.v[1] * g.v[1] + g.v[0] * g.v[0]) > 1e-9;
+  for (int c = 0; c < 3; ++c) g.d[c] = (float)(g.v[c] - vt[c]);
+  g.pp[0] = g.d[0] * g.d[0];
+  g.pp[1] = g.d[1] * g.d[1];
+  g.pp[2] = g.d[2] * g.d[2];
+  g.pp[3] = 2.f * g.d[0] * g.d[1];
+  g.pp[4] = 2.f * g.d[0] * g.d[2];
+  g.pp[5] = 2.f * g.d[1] * g.d[2];
+}
+
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+__device__ __forceinline__ double dot3d(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+// Stage one list entry (lane-parallel, float64 setup relative to the tile ray v_t):
+//   cheap cone test  q(v_t + d) = q0 + g.d + d^T Q d  (float32 coefficients, q0
+//   lowered by a rounding bound so the test never rejects a hit), and the
+//   float64 A, Bv, C for the exact intersection of candidate pixels.
+__device__ __forceinline__ void stage_entry(float* dst, int sid, const SplatRec* __restrict__ rec,
+                                            const SplatRec64* __restrict__ rec64, const double vt[3], float dmax) {
+  const float4 p0 = __ldg(&rec[sid].r0);
+  const float4 p1 = __ldg(&rec[sid].r1);
+  double B[10];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    double2 x = __ldg(&rec64[sid].v[q]);
+    B[2 * q] = x.x;
+    B[2 * q + 1] = x.y;
+  }
+  const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
+  double A[3], Bv[3], C[3];
+  cross3(Bb, Bc, A);
+  cross3(Bc, Ba, Bv);
+  cross3(Ba, Bb, C);
+  const double det = dot3d(Bc, C);
+  const double K = (double)p0.y;
+  const double c0 = dot3d(vt, A), c1 = dot3d(vt, Bv), w2t = dot3d(vt, C);
+  const double q0 = c0 * c0 + c1 * c1 - K * w2t * w2t;
+  double g[3], Q[6];
+  for (int c = 0; c < 3; ++c) g[c] = 2.0 * (c0 * A[c] + c1 * Bv[c] - K * w2t * C[c]);
+  Q[0] = A[0] * A[0] + Bv[0] * Bv[0] - K * C[0] * C[0];
+  Q[1] = A[1] * A[1] + Bv[1] * Bv[1] - K * C[1] * C[1];
+  Q[2] = A[2] * A[2] + Bv[2] * Bv[2] - K * C[2] * C[2];
+  Q[3] = A[0] * A[1] + Bv[0] * Bv[1] - K * C[0] * C[1];
+  Q[4] = A[0] * A[2] + Bv[0] * Bv[2] - K * C[0] * C[2];
+  Q[5] = A[1] * A[2] + Bv[1] * Bv[2] - K * C[1] * C[2];
+  // magnitude of every term the float32 evaluation sums (bounds its rounding)
+  const double dm = dmax;
+  double E = fabs(q0) + (fabs(g[0]) + fabs(g[1]) + fabs(g[2])) * dm +
+             (fabs(Q[0]) + fabs(Q[1]) + fabs(Q[2]) + 2.0 * (fabs(Q[3]) + fabs(Q[4]) + fabs(Q[5]))) * dm * dm;
+  E += (c0 * c0 + c1 * c1 + fabs(K) * w2t * w2t);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  d4[0] = make_float4((float)(q0 - 1e-5 * E), (float)g[0], (float)g[1], (float)g[2]);
+  d4[1] = make_float4((float)Q[0], (float)Q[1], (float)Q[2], (float)Q[3]);
+  d4[2] = make_float4((float)Q[4], (float)Q[5], p0.x, (float)det);
+  d4[3] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
+  double2* d2 = reinterpret_cast<double2*>(dst + 16);
+  d2[0] = make_double2(A[0], A[1]);
+  d2[1] = make_double2(A[2], Bv[0]);
+  d2[2] = make_double2(Bv[1], Bv[2]);
+  d2[3] = make_double2(C[0], C[1]);
+  d2[4] = make_double2(C[2], 0.0);
+}
+
+struct Entry {
+  double A[3], Bv[3], C[3];
+  float o, det, n[3];
+  int sid;
+};
+
+__device__ __forceinline__ void load_entry(const float* e, Entry& x) {
+  const float4* e4 = reinterpret_cast<const float4*>(e);
+  const float4 f2 = e4[2], f3 = e4[3];
+  x.o = f2.z;
+  x.det = f2.w;
+  x.n[0] = f3.x;
+  x.n[1] = f3.y;
+  x.n[2] = f3.z;
+  x.sid = __float_as_int(f3.w);
+  const double2* d2 = reinterpret_cast<const double2*>(e + 16);
+  const double2 a = d2[0], b = d2[1], c = d2[2], d = d2[3], f = d2[4];
+  x.A[0] = a.x; x.A[1] = a.y; x.A[2] = b.x;
+  x.Bv[0] = b.y; x.Bv[1] = c.x; x.Bv[2] = c.y;
+  x.C[0] = d.x; x.C[1] = d.y; x.C[2] = f.x;
+}
+
+struct Hit {
+  float sa, sb, lam, r, G, alpha;
+  bool use, clamped;
+};
+
+// Exact per-pixel intersection + cutoffs (rasterizer.py:369-388): the three
+// dot products in float64 (grazing splats amplify direction error by
+// 1/|v.n|), everything after them in float32.
+__device__ __forceinline__ void intersect(const Entry& x, const double v[3], bool ray_ok, const BlendParams& bp, Hit& h) {
+  const float w0 = (float)dot3d(v, x.A);
+  const float w1 = (float)dot3d(v, x.Bv);
+  const float w2 = (float)dot3d(v, x.C);
+  bool ok = ray_ok && fabsf(w2) >= bp.denom_eps;
+  const float r = __fdividef(1.f, w2);
+  h.r = r;
+  h.sa = w0 * r;
+  h.sb = w1 * r;
+  h.lam = x.det * r;
+  ok = ok && h.lam > 0.f;  // nu . v > 0
+  const float s2 = h.sa * h.sa + h.sb * h.sb;
+  h.G = __expf(-0.5f * s2);
+  const float araw = x.o * h.G;
+  h.clamped = araw > bp.alpha_clamp;
+  const float a = fminf(araw, bp.alpha_clamp);
+  h.use = ok && a >= bp.alpha_cutoff;
+  h.alpha = a;
+}
+
+template <int TS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_forward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
+              const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
+              float* __restrict__ out_D, float* __restrict__ out_N, float* __restrict__ out_O,
+              float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask) {
+  constexpr int PPL = TileShape<TS>::PPL;
+  __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kWarpsPerBlock + warp;
+  if (t >= ntiles) return;
+  const CamK& k = bp.cam;
+  const int tr = t / k.tx, tc = t % k.tx;
+  double vt[3];
+  tile_center<TS>(k, tr, tc, vt);
+  PixelGeo px[PPL];
+  float T[PPL], D[PPL], O[PPL], N[PPL][3];
+  int last[PPL];
+  bool live[PPL];
+  float dmax = 0.f;
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    pixel_geo<TS>(k, tr, tc, lane + 32 * j, vt, px[j]);
+    T[j] = 1.f; D[j] = 0.f; O[j] = 0.f; N[j][0] = N[j][1] = N[j][2] = 0.f;
+    last[j] = 0;
+    live[j] = px[j].ray_ok;
+    if (px[j].ray_ok) dmax = fmaxf(dmax, fmaxf(fabsf(px[j].d[0]), fmaxf(fabsf(px[j].d[1]), fabsf(px[j].d[2]))));
+  }
+  for (int off = 16; off > 0; off >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+  const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+  const int cbase = chunk_ptr[t];
+  float* st = stage[warp];
+  for (int base = 0, chunk = 0; base < L; base += 32, ++chunk) {
+    bool any_live = false;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) any_live |= live[j];
+    if (!__any_sync(0xffffffffu, any_live)) break;
+    if (base + lane < L) stage_entry(st + lane * kStride, pairs[lo + base + lane], rec, rec64, vt, dmax);
+    __syncwarp();
+    const int cnt = min(32, L - base);
+    unsigned word[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) word[j] = 0u;
+    for (int i = 0; i < cnt; ++i) {
+      const float* e = st + i * kStride;
+      const float4 f0 = *reinterpret_cast<const float4*>(e);
+      const float4 f1 = *reinterpret_cast<const float4*>(e + 4);
+      const float4 f2 = *reinterpret_cast<const float4*>(e + 8);
+      bool cand[PPL];
+      bool anyc = false;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        const float* d = px[j].d;
+        const float* pp = px[j].pp;
+        float q = f0.x + f0.y * d[0] + f0.z * d[1] + f0.w * d[2] + f1.x * pp[0] + f1.y * pp[1] + f1.z * pp[2] +
+                  f1.w * pp[3] + f2.x * pp[4] + f2.y * pp[5];
+        cand[j] = live[j] && q <= 0.f;
+        anyc |= cand[j];
+      }
+      if (!anyc) continue;
+      Entry x;
+      load_entry(e, x);
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        if (!cand[j]) continue;
+        Hit h;
+        intersect(x, px[j].v, px[j].ray_ok, bp, h);
+        if (!h.use) continue;
+        float w = h.alpha * T[j];
+        D[j] += w * h.lam;
+        O[j] += w;
+        N[j][0] += w * x.n[0];
+        N[j][1] += w * x.n[1];
+        N[j][2] += w * x.n[2];
+        T[j] *= (1.f - h.alpha);
+        word[j] |= 1u << i;
+        last[j] = base + i + 1;
+        if (T[j] < bp.min_T) live[j] = false;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    if (!px[j].inside) continue;
+    size_t p = (size_t)px[j].row * k.W + px[j].col;
+    out_D[p] = D[j];
+    out_O[p] = O[j];
+    out_N[3 * p] = N[j][0];
+    out_N[3 * p + 1] = N[j][1];
+    out_N[3 * p + 2] = N[j][2];
+    out_T[p] = T[j];
+    out_last[p] = last[j];
+  }
+}
+
+constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
+constexpr int kRedStride = 15;
+
+template <int TS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_backward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
+               const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
+               const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
+               const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
+               float* __restrict__ acc) {
+  constexpr int PPL = TileShape<TS>::PPL;
+  __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
+  __shared__ float red[kWarpsPerBlock][32 * kRedStride];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kWarpsPerBlock + warp;
+  if (t >= ntiles) return;
+  const CamK& k = bp.cam;
+  const int tr = t / k.tx, tc = t % k.tx;
+  double vt[3];
+  tile_center<TS>(k, tr, tc, vt);
+  PixelGeo px[PPL];
+  float T[PPL], Sd[PPL], So[PPL], Sn[PPL][3], gD[PPL], gO[PPL], gN[PPL][3];
+  int last[PPL];
+  int maxlast = 0;
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    pixel_geo<TS>(k, tr, tc, lane + 32 * j, vt, px[j]);
+    last[j] = 0;
+    T[j] = 1.f;
+    gD[j] = gO[j] = gN[j][0] = gN[j][1] = gN[j][2] = 0.f;
+    if (px[j].inside) {
+      size_t p = (size_t)px[j].row * k.W + px[j].col;
+      last[j] = in_last[p];
+      T[j] = in_T[p];
+      gD[j] = gD_img[p];
+      gO[j] = gO_img[p];
+      gN[j][0] = gN_img[3 * p];
+      gN[j][1] = gN_img[3 * p + 1];
+      gN[j][2] = gN_img[3 * p + 2];
+    }
+    Sd[j] = So[j] = Sn[j][0] = Sn[j][1] = Sn[j][2] = 0.f;
+    maxlast = max(maxlast, last[j]);
+  }
+  maxlast = __reduce_max_sync(0xffffffffu, maxlast);
+  if (maxlast == 0) return;
+  const int lo = tile_ptr[t];
+  const int cbase = chunk_ptr[t];
+  float* st = stage[warp];
+  float* rw = red[warp];
+  for (int chunk = (maxlast - 1) >> 5; chunk >= 0; --chunk) {
+    const int base = chunk * 32;
+    unsigned word[PPL];
+    unsigned mine = 0u;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) {
+      word[j] = base < last[j] ? bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] : 0u;
+      mine |= word[j];
+    }
+    unsigned any = __reduce_or_sync(0xffffffffu, mine);
+    if (!any) continue;
+    if ((any >> lane) & 1u) stage_entry(st + lane * kStride, pairs[lo + base + lane], rec, rec64, vt, 0.f);
+    __syncwarp();
+    while (any) {
+      const int i = 31 - __clz(any);
+      any &= ~(1u << i);
+      Entry x;
+      load_entry(st + i * kStride, x);
+      float a[14];
+#pragma unroll
+      for (int q = 0; q < 14; ++q) a[q] = 0.f;
+      bool act = false;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        if (!((word[j] >> i) & 1u)) continue;
+        act = true;
+        Hit h;
+        intersect(x, px[j].v, px[j].ray_ok, bp, h);
+        const float om = 1.f - h.alpha;
+        const float iom = __fdividef(1.f, om);
+        const float Tb = T[j] * iom;
+        float dal = gD[j] * (h.lam * Tb - Sd[j] * iom) + gO[j] * (Tb - So[j] * iom);
+        dal += gN[j][0] * (x.n[0] * Tb - Sn[j][0] * iom) + gN[j][1] * (x.n[1] * Tb - Sn[j][1] * iom) +
+               gN[j][2] * (x.n[2] * Tb - Sn[j][2] * iom);
+        const float w = h.alpha * Tb;
+        const float gl = gD[j] * w;
+        float gsa = 0.f, gsb = 0.f, go = 0.f;
+        if (!h.clamped) {
+          gsa = -dal * h.alpha * h.sa;
+          gsb = -dal * h.alpha * h.sb;
+          go = dal * h.G;
+        }
+        const float gw0 = gsa * h.r, gw1 = gsb * h.r;
+        const float gw2 = -(gsa * h.sa + gsb * h.sb + gl * h.lam) * h.r;
+        const float v0 = (float)px[j].v[0], v1 = (float)px[j].v[1], v2 = (float)px[j].v[2];
+        a[0] += gw0 * v0; a[1] += gw0 * v1; a[2] += gw0 * v2;
+        a[3] += gw1 * v0; a[4] += gw1 * v1; a[5] += gw1 * v2;
+        a[6] += gw2 * v0; a[7] += gw2 * v1; a[8] += gw2 * v2;
+        a[9] += gl * h.r;
+        a[10] += w * gN[j][0]; a[11] += w * gN[j][1]; a[12] += w * gN[j][2];
+        a[13] += go;
+        Sd[j] += w * h.lam;
+        So[j] += w;
+        Sn[j][0] += w * x.n[0];
+        Sn[j][1] += w * x.n[1];
+        Sn[j][2] += w * x.n[2];
+        T[j] = Tb;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, act);
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < 14; ++q) rw[lane * kRedStride + q] = a[q];
+      }
+      __syncwarp();
+      if (lane < 14) {
+        float s = 0.f;
+        unsigned mm = m;
+        while (mm) {
+          const int l = __ffs(mm) - 1;
+          mm &= mm - 1;
+          s += rw[l * kRedStride + lane];
+        }
+        atomicAdd(&acc[(size_t)x.sid * kAcc + lane], s);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Camera-frame accumulators -> plain-space (15) or raw-space (12) gradients
+// (rasterizer.py:686-700, splats.py:133-163, mapping.py:479-494).
+__global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc, const float* __restrict__ d_scales_extra,
+                           float* __restrict__ out, int raw_space) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sp.n) return;
+  double a[3], b[3];
+  for (int c = 0; c < 3; ++c) {
+    a[c] = sp.raw_ta[3 * i + c];
+    b[c] = sp.raw_tb[3 * i + c];
+  }
+  double na = sqrt(dot3d(a, a));
+  double u[3] = {a[0] / na, a[1] / na, a[2] / na};
+  double ub = dot3d(u, b);
+  double w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
+  double nw = sqrt(dot3d(w, w));
+  double v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
+  double s0 = exp((double)sp.log_scales[2 * i]), s1 = exp((double)sp.log_scales[2 * i + 1]);
+  double m[3] = {(double)sp.centers[3 * i] - pose.t[0], (double)sp.centers[3 * i + 1] - pose.t[1],
+                 (double)sp.centers[3 * i + 2] - pose.t[2]};
+  const double* R = pose.R;
+  double Bc[3], tac[3], tbc[3], Ba[3], Bb[3];
+  for (int c = 0; c < 3; ++c) {
+    Bc[c] = m[0] * R[c] + m[1] * R[3 + c] + m[2] * R[6 + c];
+    tac[c] = u[0] * R[c] + u[1] * R[3 + c] + u[2] * R[6 + c];
+    tbc[c] = v[0] * R[c] + v[1] * R[3 + c] + v[2] * R[6 + c];
+    Ba[c] = s0 * tac[c];
+    Bb[c] = s1 * tbc[c];
+  }
+  double A[3], Bv[3], C[3];
+  cross3(Bb, Bc, A);
+  cross3(Bc, Ba, Bv);
+  cross3(Ba, Bb, C);
+  const float* g = acc + (size_t)i * kAcc;
+  double V0[3] = {g[0], g[1], g[2]}, V1[3] = {g[3], g[4], g[5]}, V2[3] = {g[6], g[7], g[8]};
+  double Gd = g[9];
+  double Nc[3] = {g[10], g[11], g[12]};
+  double Oc = g[13];
+  double t1[3], t2[3], gBa[3], gBb[3], gBc[3];
+  cross3(V1, Bc, t1);
+  cross3(Bb, V2, t2);
+  for (int c = 0; c < 3; ++c) gBa[c] = t1[c] + t2[c] + Gd * A[c];
+  cross3(Bc, V0, t1);
+  cross3(V2, Ba, t2);
+  for (int c = 0; c < 3; ++c) gBb[c] = t1[c] + t2[c] + Gd * Bv[c];
+  cross3(V0, Bb, t1);
+  cross3(Ba, V1, t2);
+  for (int c = 0; c < 3; ++c) gBc[c] = t1[c] + t2[c] + Gd * C[c];
+  // camera frame -> world frame: x @ R.T
+  double dmu[3], dta[3], dtb[3], dn[3];
+  for (int c = 0; c < 3; ++c) {
+    dmu[c] = gBc[0] * R[3 * c] + gBc[1] * R[3 * c + 1] + gBc[2] * R[3 * c + 2];
+    dta[c] = s0 * (gBa[0] * R[3 * c] + gBa[1] * R[3 * c + 1] + gBa[2] * R[3 * c + 2]);
+    dtb[c] = s1 * (gBb[0] * R[3 * c] + gBb[1] * R[3 * c + 1] + gBb[2] * R[3 * c + 2]);
+    dn[c] = Nc[0] * R[3 * c] + Nc[1] * R[3 * c + 1] + Nc[2] * R[3 * c + 2];
+  }
+  double ds0 = dot3d(gBa, tac), ds1 = dot3d(gBb, tbc);
+  if (!raw_space) {
+    float* o = out + (size_t)i * 15;
+    for (int c = 0; c < 3; ++c) {
+      o[c] = (float)dmu[c];
+      o[3 + c] = (float)dta[c];
+      o[6 + c] = (float)dtb[c];
+      o[9 + c] = (float)dn[c];
+    }
+    o[12] = (float)ds0;
+    o[13] = (float)ds1;
+    o[14] = (float)Oc;
+    return;
+  }
+  // Gram-Schmidt backward (splats.py:154-163)
+  double gu[3], gv[3], cv[3], cn[3];
+  cross3(v, dn, cv);
+  cross3(dn, u, cn);
+  for (int c = 0; c < 3; ++c) {
+    gu[c] = dta[c] + cv[c];
+    gv[c] = dtb[c] + cn[c];
+  }
+  double vg = dot3d(v, gv);
+  double q[3] = {(gv[0] - vg * v[0]) / nw, (gv[1] - vg * v[1]) / nw, (gv[2] - vg * v[2]) / nw};
+  double qu = dot3d(q, u);
+  double inner[3], gb[3];
+  for (int c = 0; c < 3; ++c) {
+    gb[c] = q[c] - qu * u[c];
+    inner[c] = gu[c] - ub * q[c] - qu * b[c];
+  }
+  double ui = dot3d(u, inner);
+  float* o = out + (size_t)i * 12;
+  for (int c = 0; c < 3; ++c) {
+    o[c] = (float)dmu[c];
+    o[3 + c] = (float)((inner[c] - ui * u[c]) / na);
+    o[6 + c] = (float)gb[c];
+  }
+  double e0 = d_scales_extra ? (double)d_scales_extra[2 * i] : 0.0;
+  double e1 = d_scales_extra ? (double)d_scales_extra[2 * i + 1] : 0.0;
+  o[9] = (float)((ds0 + e0) * s0);
+  o[10] = (float)((ds1 + e1) * s1);
+  double x = (double)sp.logit_opacity[i], op;
+  if (x >= 0) {
+    op = 1.0 / (1.0 + exp(-x));
+  } else {
+    double e = exp(x);
+    op = e / (1.0 + e);
+  }
+  o[11] = (float)(Oc * op * (1.0 - op));
+}
+
+template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
+                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*);
+template __global__ void k_forward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
+                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*);
+template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
+                                       const SplatRec64*, const float*, const int*, const unsigned*, const float*,
+                                       const float*, const float*, float*);
+template __global__ void k_backward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
+                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
+                                        const float*, const float*, float*);
+
+}  // namespace ss

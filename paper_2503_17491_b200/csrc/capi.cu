@@ -1,0 +1,412 @@
+// C ABI of the B200 hot path (declared in include/splat_b200.h).
+// Unity build: the kernel sources are included here so the library is one
+// translation unit without relocatable device code.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "binning.cu"
+#include "blend.cu"
+#include "loss.cu"
+#include "registration.cu"
+
+using namespace ss;
+
+namespace {
+
+// numpy-style float modulo on the host (np.mod semantics)
+double host_py_mod(double a, double b) {
+  double m = std::fmod(a, b);
+  if (m != 0.0 && ((b < 0.0) != (m < 0.0))) m += b;
+  return m;
+}
+
+// Camera constants with the reference's operation order
+// (geometry.py:95-109, 160-174; rasterizer.py:252-276).
+int make_camk(const ss_camera* c, int T, double pad_px, CamK& k) {
+  if (!c || c->width < 2 || c->height < 2) return SS_ERR_INVALID_ARGUMENT;
+  if (!(c->az_max > c->az_min && c->el_max > c->el_min)) return SS_ERR_INVALID_ARGUMENT;
+  if (T != 8 && T != 16) return SS_ERR_UNSUPPORTED;
+  double fov_h = c->az_max - c->az_min, fov_v = c->el_max - c->el_min;
+  k.W = c->width;
+  k.H = c->height;
+  k.T = T;
+  k.tx = (c->width + T - 1) / T;
+  k.ty = (c->height + T - 1) / T;
+  k.fx = (double)(-(c->width - 1)) / fov_h;
+  k.fy = (double)(-(c->height - 1)) / fov_v;
+  k.cx = 0.5 * c->width * (1.0 + (c->az_max + c->az_min) / fov_h);
+  k.cy = 0.5 * c->height * (1.0 + (c->el_max + c->el_min) / fov_v);
+  volatile double fu = k.fx * c->az_max;
+  volatile double fv = k.fy * c->el_max;
+  double first_u = fu + k.cx, first_v = fv + k.cy;
+  k.off_u = host_py_mod(first_u + 0.5, 1.0) - 0.5;
+  k.off_v = host_py_mod(first_v + 0.5, 1.0) - 0.5;
+  k.pad_az = pad_px * (1.0 / std::fabs(k.fx));
+  k.pad_el = pad_px * (1.0 / std::fabs(k.fy));
+  return SS_OK;
+}
+
+template <typename T>
+int grow(T*& ptr, size_t& cap, size_t need, cudaStream_t s) {
+  if (need <= cap && ptr) return SS_OK;
+  if (ptr) cudaFreeAsync(ptr, s);
+  ptr = nullptr;
+  size_t c = need + need / 4 + 64;
+  if (cudaMallocAsync((void**)&ptr, c * sizeof(T), s) != cudaSuccess) {
+    cap = 0;
+    return SS_ERR_CUDA;
+  }
+  cap = c;
+  return SS_OK;
+}
+
+SplatsK to_k(const ss_splats* s) {
+  SplatsK k;
+  k.n = s->n;
+  k.centers = s->centers;
+  k.raw_ta = s->raw_t_alpha;
+  k.raw_tb = s->raw_t_beta;
+  k.log_scales = s->log_scales;
+  k.logit_opacity = s->logit_opacity;
+  return k;
+}
+
+}  // namespace
+
+struct ss_records {
+  CamK cam{};
+  PoseK pose{};
+  BlendParams bp{};
+  int n = 0, ntiles = 0, valid = 0;
+  long long n_pairs = 0, n_chunks = 0;
+  SplatRec* rec = nullptr;
+  size_t cap_rec = 0;
+  SplatRec64* rec64 = nullptr;
+  size_t cap_rec64 = 0;
+  unsigned long long* key = nullptr;
+  size_t cap_key = 0;
+  int4* rect = nullptr;
+  size_t cap_rect = 0;
+  int* tiles = nullptr;  // tile_count | tile_ptr | chunk_ptr | cursor | long_list
+  size_t cap_tiles = 0;
+  int* misc = nullptr;  // status, n_long
+  size_t cap_misc = 0;
+  long long* totals = nullptr;
+  size_t cap_totals = 0;
+  int* pairs = nullptr;
+  size_t cap_pairs = 0;
+  int* tmp = nullptr;
+  size_t cap_tmp = 0;
+  unsigned* bitmask = nullptr;
+  size_t cap_bitmask = 0;
+  float* Tf = nullptr;
+  size_t cap_Tf = 0;
+  int* last = nullptr;
+  size_t cap_last = 0;
+  float* acc = nullptr;
+  size_t cap_acc = 0;
+  long long* h_totals = nullptr;  // pinned: totals[2], status
+  // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+// Stage markers around each kernel when profiling is enabled.
+struct StageTimer {
+  ss_records* r;
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  StageTimer(ss_records* r_, int st, cudaStream_t s_) : r(r_), stage(st), s(s_) {
+    if (r->profiling) {
+      a = r->take_event();
+      b = r->take_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~StageTimer() {
+    if (r->profiling) {
+      cudaEventRecord(b, s);
+      r->ev_used.push_back({stage, {a, b}});
+    }
+  }
+};
+enum { ST_PREPROCESS, ST_SCAN, ST_SCATTER, ST_SORT, ST_SORT_LONG, ST_FORWARD, ST_BACKWARD, ST_FINALIZE, ST_COUNT };
+
+__global__ void k_count_contrib(long long nwords, const unsigned* __restrict__ bm, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x)
+    c += __popc(bm[i]);
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+}  // namespace
+
+extern "C" {
+
+const char* ss_version(void) { return "paper_2503_17491_b200 0.1 (sm_100a)"; }
+
+ss_records* ss_records_create(void) {
+  ss_records* r = new (std::nothrow) ss_records();
+  if (!r) return nullptr;
+  if (cudaMallocHost((void**)&r->h_totals, 4 * sizeof(long long)) != cudaSuccess) {
+    delete r;
+    return nullptr;
+  }
+  return r;
+}
+
+void ss_records_destroy(ss_records* r, void* stream) {
+  if (!r) return;
+  cudaStream_t s = (cudaStream_t)stream;
+  void* bufs[] = {r->rec, r->rec64, r->key, r->rect, r->tiles, r->misc, r->totals, r->pairs,
+                  r->tmp, r->bitmask, r->Tf, r->last, r->acc};
+  cudaStreamSynchronize(s);
+  for (auto& u : r->ev_used) {
+    cudaEventDestroy(u.second.first);
+    cudaEventDestroy(u.second.second);
+  }
+  for (auto e : r->ev_pool) cudaEventDestroy(e);
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, s);
+  if (r->h_totals) {
+    cudaStreamSynchronize(s);
+    cudaFreeHost(r->h_totals);
+  }
+  delete r;
+}
+
+int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_splats* splats, const ss_raster_cfg* cfg,
+                      float* out_range, float* out_normal, float* out_opacity, ss_records* rec, void* stream) {
+  if (!cam || !pose_Rt || !splats || !cfg || !rec || !out_range || !out_normal || !out_opacity)
+    return SS_ERR_INVALID_ARGUMENT;
+  if (splats->n < 0) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  CamK k;
+  int st = make_camk(cam, cfg->tile_size, cfg->bbox_pad_px, k);
+  if (st) return st;
+  rec->valid = 0;
+  rec->cam = k;
+  for (int q = 0; q < 9; ++q) rec->pose.R[q] = pose_Rt[q];
+  for (int q = 0; q < 3; ++q) rec->pose.t[q] = pose_Rt[9 + q];
+  rec->bp.cam = k;
+  rec->bp.alpha_cutoff = (float)cfg->alpha_cutoff;
+  rec->bp.alpha_clamp = (float)cfg->alpha_clamp;
+  rec->bp.min_T = (float)cfg->min_transmittance;
+  rec->bp.denom_eps = (float)cfg->denom_eps;
+  RasterK rk{cfg->alpha_cutoff, cfg->alpha_clamp, cfg->min_transmittance, cfg->denom_eps, cfg->cutoff_sigma};
+  const int n = splats->n;
+  const int ntiles = k.tx * k.ty;
+  const size_t P = (size_t)k.W * k.H;
+  rec->n = n;
+  rec->ntiles = ntiles;
+  if (grow(rec->rec, rec->cap_rec, (size_t)n + 1, s) || grow(rec->rec64, rec->cap_rec64, (size_t)n + 1, s) ||
+      grow(rec->key, rec->cap_key, (size_t)n + 1, s) || grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) ||
+      grow(rec->tiles, rec->cap_tiles, (size_t)5 * (ntiles + 1), s) || grow(rec->misc, rec->cap_misc, 4, s) ||
+      grow(rec->totals, rec->cap_totals, 2, s) || grow(rec->Tf, rec->cap_Tf, P, s) ||
+      grow(rec->last, rec->cap_last, P, s))
+    return SS_ERR_CUDA;
+  int* tile_count = rec->tiles;
+  int* tile_ptr = rec->tiles + (ntiles + 1);
+  int* chunk_ptr = rec->tiles + 2 * (ntiles + 1);
+  int* cursor = rec->tiles + 3 * (ntiles + 1);
+  int* long_list = rec->tiles + 4 * (ntiles + 1);
+  int* status = rec->misc;
+  int* n_long = rec->misc + 1;
+  SS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(int) * ntiles, s));
+  SS_CUDA_TRY(cudaMemsetAsync(rec->misc, 0, sizeof(int) * 4, s));
+  PoseK pk = rec->pose;
+  SplatsK sk = to_k(splats);
+  if (n > 0) {
+    StageTimer tm(rec, ST_PREPROCESS, s);
+    k_preprocess<<<(n + 255) / 256, 256, 0, s>>>(sk, pk, k, rk, rec->rec, rec->rec64, rec->key, rec->rect, tile_count,
+                                                  status);
+    SS_CUDA_TRY(cudaGetLastError());
+  }
+  {
+    StageTimer tm(rec, ST_SCAN, s);
+    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, cursor, rec->totals);
+  }
+  SS_CUDA_TRY(cudaGetLastError());
+  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals, rec->totals, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals + 2, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  int dev_status = *(int*)(rec->h_totals + 2);
+  if (dev_status) return dev_status;
+  rec->n_pairs = rec->h_totals[0];
+  rec->n_chunks = rec->h_totals[1];
+  if (rec->n_pairs > 0x7fffffffLL) return SS_ERR_CAPACITY;
+  const int TT = k.T * k.T;
+  if (grow(rec->pairs, rec->cap_pairs, (size_t)rec->n_pairs + 1, s) ||
+      grow(rec->tmp, rec->cap_tmp, (size_t)rec->n_pairs + 1, s) ||
+      grow(rec->bitmask, rec->cap_bitmask, (size_t)rec->n_chunks * TT + 1, s))
+    return SS_ERR_CUDA;
+  if (n > 0 && rec->n_pairs > 0) {
+    {
+      StageTimer tm(rec, ST_SCATTER, s);
+      k_scatter_pairs<<<(n + 255) / 256, 256, 0, s>>>(n, k.tx, rec->rect, cursor, rec->pairs);
+    }
+    {
+      StageTimer tm(rec, ST_SORT, s);
+      k_sort_tiles<<<ntiles, 256, 0, s>>>(tile_ptr, rec->pairs, rec->key, long_list, n_long);
+    }
+    {
+      StageTimer tm(rec, ST_SORT_LONG, s);
+      k_sort_long<<<32, 512, 0, s>>>(tile_ptr, rec->pairs, rec->tmp, rec->key, long_list, n_long);
+    }
+    SS_CUDA_TRY(cudaGetLastError());
+  }
+  const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  StageTimer tmf(rec, ST_FORWARD, s);
+  if (k.T == 8)
+    k_forward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                        rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+                                                        rec->last, rec->bitmask);
+  else
+    k_forward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                         rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+                                                         rec->last, rec->bitmask);
+  SS_CUDA_TRY(cudaGetLastError());
+  rec->valid = 1;
+  return SS_OK;
+}
+
+int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y) {
+  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  if (n_pairs) *n_pairs = rec->n_pairs;
+  if (tiles_x) *tiles_x = rec->cam.tx;
+  if (tiles_y) *tiles_y = rec->cam.ty;
+  return SS_OK;
+}
+
+int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_splats, void* stream) {
+  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  cudaStream_t s = (cudaStream_t)stream;
+  int nt = rec->ntiles + 1;
+  if (tile_ptr) k_widen_i32<<<(nt + 255) / 256, 256, 0, s>>>(nt, rec->tiles + (rec->ntiles + 1), (long long*)tile_ptr);
+  if (pair_splats && rec->n_pairs > 0)
+    k_widen_i32<<<(int)((rec->n_pairs + 255) / 256), 256, 0, s>>>((int)rec->n_pairs, rec->pairs,
+                                                                   (long long*)pair_splats);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const float* dD, const float* dN,
+                       const float* dO, const float* d_scales_extra, float* grads, int raw_space, void* stream) {
+  ss_records* rec = const_cast<ss_records*>(rec_c);
+  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  if (!splats || splats->n != rec->n) return SS_ERR_STALE_RECORDS;
+  if (!dD || !dN || !dO || !grads) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = rec->n;
+  if (n == 0) return SS_OK;
+  if (grow(rec->acc, rec->cap_acc, (size_t)n * kAcc, s)) return SS_ERR_CUDA;
+  SS_CUDA_TRY(cudaMemsetAsync(rec->acc, 0, sizeof(float) * (size_t)n * kAcc, s));
+  const int ntiles = rec->ntiles;
+  const int* tile_ptr = rec->tiles + (ntiles + 1);
+  const int* chunk_ptr = rec->tiles + 2 * (ntiles + 1);
+  if (rec->n_pairs > 0) {
+    const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    StageTimer tm(rec, ST_BACKWARD, s);
+    if (rec->cam.T == 8)
+      k_backward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                           rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
+                                                           rec->acc);
+    else
+      k_backward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
+                                                            rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
+                                                            dN, dO, rec->acc);
+    SS_CUDA_TRY(cudaGetLastError());
+  }
+  {
+    StageTimer tm(rec, ST_FINALIZE, s);
+    k_finalize<<<(n + 255) / 256, 256, 0, s>>>(to_k(splats), rec->pose, rec->acc, d_scales_extra, grads, raw_space);
+  }
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_records_profile(ss_records* rec, int enable) {
+  if (!rec) return SS_ERR_INVALID_ARGUMENT;
+  rec->profiling = enable != 0;
+  return SS_OK;
+}
+
+int ss_records_stage_times(ss_records* rec, double* ms, int32_t* launches, int32_t n_stages) {
+  if (!rec || !ms || n_stages < ST_COUNT) return SS_ERR_INVALID_ARGUMENT;
+  for (int q = 0; q < n_stages; ++q) {
+    ms[q] = 0.0;
+    if (launches) launches[q] = 0;
+  }
+  for (auto& u : rec->ev_used) {
+    cudaEventSynchronize(u.second.second);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, u.second.first, u.second.second);
+    ms[u.first] += t;
+    if (launches) launches[u.first] += 1;
+    rec->ev_pool.push_back(u.second.first);
+    rec->ev_pool.push_back(u.second.second);
+  }
+  rec->ev_used.clear();
+  return SS_OK;
+}
+
+int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contributions, void* stream) {
+  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  cudaStream_t s = (cudaStream_t)stream;
+  // E = sum over tiles of (pixels in the tile) x (list length), U = popcount of the contribution masks
+  std::vector<int> tp(rec->ntiles + 1);
+  SS_CUDA_TRY(cudaMemcpyAsync(tp.data(), rec->tiles + (rec->ntiles + 1), sizeof(int) * (rec->ntiles + 1),
+                              cudaMemcpyDeviceToHost, s));
+  unsigned long long* d_u = nullptr;
+  SS_CUDA_TRY(cudaMallocAsync((void**)&d_u, sizeof(unsigned long long), s));
+  SS_CUDA_TRY(cudaMemsetAsync(d_u, 0, sizeof(unsigned long long), s));
+  long long nwords = rec->n_chunks * (long long)rec->cam.T * rec->cam.T;
+  if (nwords > 0) k_count_contrib<<<148 * 4, 256, 0, s>>>(nwords, rec->bitmask, d_u);
+  unsigned long long hu = 0;
+  SS_CUDA_TRY(cudaMemcpyAsync(&hu, d_u, sizeof(hu), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaFreeAsync(d_u, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  long long E = 0;
+  const CamK& k = rec->cam;
+  for (int t = 0; t < rec->ntiles; ++t) {
+    int tr = t / k.tx, tc = t % k.tx;
+    long long ph = std::min(k.T, k.H - tr * k.T), pw = std::min(k.T, k.W - tc * k.T);
+    E += ph * pw * (long long)(tp[t + 1] - tp[t]);
+  }
+  if (evaluations) *evaluations = E;
+  if (contributions) *contributions = (int64_t)hu;
+  return SS_OK;
+}
+
+int ss_mapping_loss(int32_t width, int32_t height, const float* range, const float* normal, const float* opacity,
+                    const float* kf_range, const uint8_t* kf_valid, const float* kf_normal, const uint8_t* kf_nvalid,
+                    double w_opacity, double w_normal, double range_floor, float* dD, float* dN, float* dO,
+                    double* parts4, void* stream) {
+  if (width <= 0 || height <= 0) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int P = width * height;
+  int blocks = (P + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_mapping_loss<<<blocks, 256, 0, s>>>(P, range, normal, opacity, kf_range, kf_valid, kf_normal, kf_nvalid,
+                                        w_opacity, w_normal, range_floor, dD, dN, dO, parts4);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+}  // extern "C"

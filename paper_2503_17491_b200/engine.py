@@ -1,0 +1,162 @@
+"""Device engine: torch-owned device memory + the C-ABI kernels.
+
+PyTorch provides device memory and the current CUDA stream (plumbing only);
+all hot-path arithmetic runs in the sm_100a kernels of libsplatb200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SsCamera, SsRasterCfg, SsSplats, check, lib
+
+CUTOFF_SIGMA = float(np.sqrt(2.0 * np.log(255.0)))  # rasterizer.py:66
+
+PARAM_NAMES = ("centers", "raw_t_alpha", "raw_t_beta", "log_scales", "logit_opacity")
+PARAM_WIDTH = {"centers": 3, "raw_t_alpha": 3, "raw_t_beta": 3, "log_scales": 2, "logit_opacity": 1}
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_17491_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ss_camera(cam) -> SsCamera:
+    return SsCamera(int(cam.width), int(cam.height), float(cam.az_min), float(cam.az_max), float(cam.el_min),
+                    float(cam.el_max))
+
+
+def ss_cfg(cfg) -> SsRasterCfg:
+    return SsRasterCfg(int(cfg.tile_size), int(getattr(cfg, "chunk_size", 256)), float(cfg.alpha_cutoff),
+                       float(cfg.alpha_clamp), float(cfg.min_transmittance), float(cfg.denom_eps),
+                       float(cfg.cutoff_sigma), float(cfg.bbox_pad_px))
+
+
+def ss_splats(t: dict) -> SsSplats:
+    n = int(t["centers"].shape[0])
+    for k in PARAM_NAMES:
+        x = t[k]
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.shape[0] != n:
+            raise ValueError(f"{k}: expected contiguous float32 CUDA tensor with {n} rows")
+    return SsSplats(n, *(t[k].data_ptr() for k in PARAM_NAMES))
+
+
+def splats_to_device(model, device=None) -> dict:
+    """float32 device copies of a SplatModel's raw parameters (reference or ours)."""
+    device = device or require_cuda()
+    out = {}
+    for k in PARAM_NAMES:
+        a = np.ascontiguousarray(np.asarray(getattr(model, k), dtype=np.float32)).reshape(len(model), PARAM_WIDTH[k])
+        if k == "logit_opacity":
+            a = a.reshape(-1)
+        out[k] = torch.from_numpy(a).to(device, non_blocking=False)
+    return out
+
+
+class Records:
+    """Owner of one ss_records handle (tile lists + per-pixel blend state)."""
+
+    _pool: list = []
+
+    def __init__(self):
+        ptr = lib().ss_records_create()
+        if not ptr:
+            raise RuntimeError("ss_records_create failed")
+        self.ptr = ctypes.c_void_p(ptr)
+
+    @classmethod
+    def acquire(cls) -> "Records":
+        return cls._pool.pop() if cls._pool else cls()
+
+    def release(self) -> None:
+        Records._pool.append(self)
+
+    def counts(self):
+        n = ctypes.c_int64(0)
+        tx = ctypes.c_int32(0)
+        ty = ctypes.c_int32(0)
+        check(lib().ss_records_counts(self.ptr, ctypes.byref(n), ctypes.byref(tx), ctypes.byref(ty)), "records")
+        return int(n.value), int(tx.value), int(ty.value)
+
+    def export(self):
+        """(tile_ptr int64, pair_splats int64) as device tensors (BlendRecords layout)."""
+        n, tx, ty = self.counts()
+        dev = require_cuda()
+        tp = torch.empty(tx * ty + 1, dtype=torch.int64, device=dev)
+        ps = torch.empty(n, dtype=torch.int64, device=dev)
+        check(lib().ss_records_export(self.ptr, ctypes.c_void_p(tp.data_ptr()),
+                                      ctypes.c_void_p(ps.data_ptr() if n else 0), ctypes.c_void_p(stream_ptr())),
+              "records export")
+        return tp, ps
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            if _lib._lib is not None and self.ptr:
+                _lib._lib.ss_records_destroy(self.ptr, ctypes.c_void_p(stream_ptr()))
+        except Exception:
+            pass
+
+
+def forward(cam, pose_rt: np.ndarray, splats: dict, cfg, records: Records):
+    """Render; returns (range [H,W], normal [H,W,3], opacity [H,W]) float32 device tensors."""
+    dev = require_cuda()
+    H, W = int(cam.height), int(cam.width)
+    D = torch.empty((H, W), dtype=torch.float32, device=dev)
+    N = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    O = torch.empty((H, W), dtype=torch.float32, device=dev)
+    c = ss_camera(cam)
+    sp = ss_splats(splats)
+    k = ss_cfg(cfg)
+    prt = np.ascontiguousarray(pose_rt, dtype=np.float64)
+    st = lib().ss_render_forward(ctypes.byref(c), prt.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sp),
+                                 ctypes.byref(k), ctypes.c_void_p(D.data_ptr()), ctypes.c_void_p(N.data_ptr()),
+                                 ctypes.c_void_p(O.data_ptr()), records.ptr, ctypes.c_void_p(stream_ptr()))
+    check(st, "rasterize_forward")
+    return D, N, O
+
+
+def backward(records: Records, splats: dict, dD, dN, dO, raw_space: bool, d_scales_extra=None):
+    """Splat gradients: (n, 15) plain-space or (n, 12) raw-space float32 device tensor."""
+    dev = require_cuda()
+    n = int(splats["centers"].shape[0])
+    out = torch.empty((n, 12 if raw_space else 15), dtype=torch.float32, device=dev)
+    dD = dD.contiguous().float()
+    dN = dN.contiguous().float()
+    dO = dO.contiguous().float()
+    ex = 0
+    if d_scales_extra is not None:
+        d_scales_extra = d_scales_extra.contiguous().float()
+        ex = d_scales_extra.data_ptr()
+    sp = ss_splats(splats)
+    st = lib().ss_render_backward(records.ptr, ctypes.byref(sp), ctypes.c_void_p(dD.data_ptr()),
+                                  ctypes.c_void_p(dN.data_ptr()), ctypes.c_void_p(dO.data_ptr()), ctypes.c_void_p(ex),
+                                  ctypes.c_void_p(out.data_ptr()), int(bool(raw_space)),
+                                  ctypes.c_void_p(stream_ptr()))
+    check(st, "rasterize_backward")
+    return out
+
+
+def mapping_loss(D, N, O, kf_range, kf_valid, kf_normal, kf_nvalid, w_opacity=0.05, w_normal=0.1,
+                 range_floor=1.0):
+    """Fused loss (mapping.py:128-163 terms): returns (dD, dN, dO, parts[3] float64 device)."""
+    H, W = D.shape
+    dD = torch.empty_like(D)
+    dN = torch.empty_like(N)
+    dO = torch.empty_like(O)
+    parts = torch.zeros(4, dtype=torch.float64, device=D.device)
+    st = lib().ss_mapping_loss(W, H, D.data_ptr(), N.data_ptr(), O.data_ptr(), kf_range.data_ptr(),
+                               kf_valid.data_ptr(), kf_normal.data_ptr(), kf_nvalid.data_ptr(), float(w_opacity),
+                               float(w_normal), float(range_floor), dD.data_ptr(), dN.data_ptr(), dO.data_ptr(),
+                               parts.data_ptr(), stream_ptr())
+    check(st, "mapping_loss")
+    return dD, dN, dO, parts

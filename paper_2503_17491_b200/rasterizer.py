@@ -1,0 +1,200 @@
+"""Drop-in replacement of the reference rasterizer API (pkg/src/splatscan/rasterizer.py).
+
+Same names, argument meaning and error behaviour as the reference:
+  RasterConfig        rasterizer.py:69-78
+  RenderOutput        rasterizer.py:81-87   (host float64 images, like the reference)
+  PixelGradients      rasterizer.py:90-96
+  SplatGradients      rasterizer.py:99-124
+  BlendRecords        rasterizer.py:136-148 (tile_ptr / pair_splats materialise lazily)
+  rasterize_forward   rasterizer.py:455-499
+  rasterize_backward  rasterizer.py:534-701 (GeometryError on stale records, zeros when empty)
+
+All arithmetic runs in the sm_100a kernels (engine.py -> libsplatb200.so).
+Device tensors of every result stay attached (``.device``) so GPU callers
+never pay the host copies.
+"""
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine
+from .errors import GeometryError
+from .geometry import pose_rt
+
+__all__ = ["RasterConfig", "RenderOutput", "PixelGradients", "SplatGradients", "BlendRecords",
+           "rasterize_forward", "rasterize_backward"]
+
+
+@dataclass(frozen=True)
+class RasterConfig:
+    tile_size: int = 8
+    chunk_size: int = 256
+    alpha_cutoff: float = 1.0 / 255.0
+    alpha_clamp: float = 0.99
+    min_transmittance: float = 1e-4
+    denom_eps: float = 1e-12
+    cutoff_sigma: float = engine.CUTOFF_SIGMA
+    bbox_pad_px: float = 0.5
+
+
+class _Lazy:
+    """Host view of a device tensor, copied on first access."""
+
+    def __init__(self, t: torch.Tensor, dtype=np.float64):
+        self.t = t
+        self.dtype = dtype
+        self._host = None
+
+    def host(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self.t.detach().cpu().numpy().astype(self.dtype)
+        return self._host
+
+
+class RenderOutput:
+    """Blended range, camera-frame normal and opacity images (rasterizer.py:81-87)."""
+
+    def __init__(self, range=None, normal=None, opacity=None, device: dict | None = None):
+        self._dev = device or {}
+        self._host = {"range": range, "normal": normal, "opacity": opacity}
+
+    def _get(self, k):
+        if self._host[k] is None:
+            self._host[k] = self._dev[k].detach().cpu().numpy().astype(np.float64)
+        return self._host[k]
+
+    range = property(lambda self: self._get("range"), lambda self, v: self._host.__setitem__("range", v))
+    normal = property(lambda self: self._get("normal"), lambda self, v: self._host.__setitem__("normal", v))
+    opacity = property(lambda self: self._get("opacity"), lambda self, v: self._host.__setitem__("opacity", v))
+
+    @property
+    def device(self) -> dict:
+        return self._dev
+
+
+@dataclass
+class PixelGradients:
+    d_range: np.ndarray
+    d_normal: np.ndarray
+    d_opacity: np.ndarray
+
+
+@dataclass
+class SplatGradients:
+    d_centers: np.ndarray
+    d_t_alpha: np.ndarray
+    d_t_beta: np.ndarray
+    d_normal: np.ndarray
+    d_scales: np.ndarray
+    d_opacity: np.ndarray
+
+    @classmethod
+    def zeros(cls, n: int) -> "SplatGradients":
+        return cls(np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 2)),
+                   np.zeros(n))
+
+    @classmethod
+    def from_packed(cls, g: np.ndarray) -> "SplatGradients":
+        g = np.asarray(g, dtype=np.float64)
+        return cls(g[:, 0:3].copy(), g[:, 3:6].copy(), g[:, 6:9].copy(), g[:, 9:12].copy(), g[:, 12:14].copy(),
+                   g[:, 14].copy())
+
+
+class BlendRecords:
+    """Binning and identity snapshot for replaying a render (rasterizer.py:136-148)."""
+
+    def __init__(self, cam, pose, config, n_splats, model_version, tiles_x, tiles_y, handle=None,
+                 tile_ptr=None, pair_splats=None):
+        self.cam = cam
+        self.pose = pose
+        self.config = config
+        self.n_splats = n_splats
+        self.model_version = model_version
+        self.tiles_x = tiles_x
+        self.tiles_y = tiles_y
+        self._handle = handle
+        self._tile_ptr = tile_ptr
+        self._pair_splats = pair_splats
+
+    def _export(self):
+        if self._tile_ptr is None:
+            tp, ps = self._handle.export()
+            self._tile_ptr = tp.cpu().numpy()
+            self._pair_splats = ps.cpu().numpy()
+
+    @property
+    def tile_ptr(self) -> np.ndarray:
+        self._export()
+        return self._tile_ptr
+
+    @property
+    def pair_splats(self) -> np.ndarray:
+        self._export()
+        return self._pair_splats
+
+
+# float32 device copies of models, keyed by object identity and version
+_dev_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _device_params(model) -> dict:
+    key = (int(getattr(model, "version", 0)), len(model))
+    try:
+        hit = _dev_cache.get(model)
+    except TypeError:
+        hit = None
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    t = engine.splats_to_device(model)
+    try:
+        _dev_cache[model] = (key, t)
+    except TypeError:
+        pass
+    return t
+
+
+def rasterize_forward(cam, pose, model, cfg: RasterConfig | None = None):
+    """Render ``model`` from ``pose`` onto ``cam`` (rasterizer.py:455-499)."""
+    cfg = cfg or RasterConfig()
+    H, W = cam.height, cam.width
+    T = cfg.tile_size
+    tx, ty = (W + T - 1) // T, (H + T - 1) // T
+    pose_c = pose.copy()
+    if len(model) == 0:
+        rec = BlendRecords(cam, pose_c, cfg, 0, model.version, tx, ty,
+                           tile_ptr=np.zeros(tx * ty + 1, dtype=np.int64), pair_splats=np.zeros(0, dtype=np.int64))
+        return RenderOutput(np.zeros((H, W)), np.zeros((H, W, 3)), np.zeros((H, W))), rec
+    params = _device_params(model)
+    handle = engine.Records()
+    D, N, O = engine.forward(cam, pose_rt(pose), params, cfg, handle)
+    out = RenderOutput(device={"range": D, "normal": N, "opacity": O})
+    rec = BlendRecords(cam, pose_c, cfg, len(model), model.version, tx, ty, handle=handle)
+    rec._params = params
+    return out, rec
+
+
+def _dev(x, like_shape):
+    if isinstance(x, torch.Tensor):
+        return x.to(engine.require_cuda(), torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)).reshape(like_shape)).to(
+        engine.require_cuda())
+
+
+def rasterize_backward(model, records: BlendRecords, render: RenderOutput, pixel_grads: PixelGradients):
+    """Gradients of a pixel-space loss w.r.t. plain splat parameters (rasterizer.py:534-701)."""
+    if records.n_splats != len(model) or records.model_version != model.version:
+        raise GeometryError("blend records are stale for this model")
+    n = len(model)
+    if n == 0 or records._handle is None:
+        return SplatGradients.zeros(n)
+    H, W = records.cam.height, records.cam.width
+    params = getattr(records, "_params", None) or _device_params(model)
+    g = engine.backward(records._handle, params, _dev(pixel_grads.d_range, (H, W)),
+                        _dev(pixel_grads.d_normal, (H, W, 3)), _dev(pixel_grads.d_opacity, (H, W)), raw_space=False)
+    out = SplatGradients.from_packed(g.cpu().numpy())
+    out.device = g
+    return out

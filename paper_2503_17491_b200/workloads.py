@@ -1,0 +1,165 @@
+"""Seeded synthetic workloads (BASELINE.json configs 0-4).
+
+The paper's datasets are not available; these generators stand in for them
+with the shapes, sizes and value distributions BASELINE.json names.  Inputs
+are drawn in numpy with ``default_rng(seed)`` and rounded to float32; the CPU
+oracle receives the same float32 values promoted to float64.
+
+Pinned choices (BASELINE leaves them open; recorded in DESIGN.md):
+  * "uniform in a spherical shell" = uniform RADIUS in [2, 50] m.
+  * rotations: unit quaternion q ~ N(0, I4) normalised, (w, x, y, z); the raw
+    tangents stored are the first two columns of R(q).
+  * scene: ground z = -1.7 m (60 m half extent); four walls at x, y = +-30 m,
+    z in [-1.7, 6.3]; 20 boxes, centre xy ~ U(-25, 25), half sizes ~ U(0.5, 2.5),
+    resting on the ground; all drawn with default_rng(0).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .geometry import SE3Pose, SphericalCamera, so3_exp
+
+
+def synth_camera(width: int, height: int, el_deg: float = 22.5) -> SphericalCamera:
+    """Camera on the raycast_scan grid: az in [-pi, pi - 2pi/W] (synth.py:277-281)."""
+    return SphericalCamera(width, height, -np.pi, np.pi - 2.0 * np.pi / width, -np.deg2rad(el_deg),
+                           np.deg2rad(el_deg))
+
+
+def quat_tangents(q: np.ndarray):
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    ta = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)], axis=1)
+    tb = np.stack([2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)], axis=1)
+    return ta, tb
+
+
+def random_splats(n: int, seed: int, rmin: float = 2.0, rmax: float = 50.0, zclip=(-2.0, 6.0),
+                  mean_log_scale: float = float(np.log(0.05)), sigma_log_scale: float = 0.5,
+                  draw: str = "uniform-radius") -> dict:
+    """Config 0/1 splats in the fixed draw order of SURVEY 8(d); float32 arrays."""
+    rng = np.random.default_rng(seed)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    if draw == "uniform-radius":
+        r = rng.uniform(rmin, rmax, n)
+    else:
+        r = np.cbrt(rng.uniform(rmin ** 3, rmax ** 3, n))
+    c = d * r[:, None]
+    c[:, 2] = np.clip(c[:, 2], *zclip)
+    ls = rng.normal(mean_log_scale, sigma_log_scale, (n, 2))
+    ta, tb = quat_tangents(rng.normal(size=(n, 4)))
+    lo = rng.normal(0.0, 1.0, n)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    return {"centers": f(c), "raw_t_alpha": f(ta), "raw_t_beta": f(tb), "log_scales": f(ls), "logit_opacity": f(lo)}
+
+
+# --- procedural scene and ray casting -------------------------------------------------
+
+
+class Scene:
+    """Axis-aligned rectangles and boxes (ground, four walls, boxes)."""
+
+    def __init__(self, seed: int = 0, n_boxes: int = 20):
+        rng = np.random.default_rng(seed)
+        # rectangles: (axis of the normal, offset, centre of the other two coords, half extents)
+        self.rects = [(2, -1.7, (0.0, 0.0), (60.0, 60.0))]
+        for ax, off in ((0, 30.0), (0, -30.0), (1, 30.0), (1, -30.0)):
+            # in-plane coords: the other horizontal axis (half 30) and z (centre 2.3, half 4)
+            self.rects.append((ax, off, (0.0, 2.3), (30.0, 4.0)))
+        xy = rng.uniform(-25.0, 25.0, (n_boxes, 2))
+        half = rng.uniform(0.5, 2.5, (n_boxes, 3))
+        self.box_lo = np.concatenate([xy - half[:, :2], (-1.7) * np.ones((n_boxes, 1))], axis=1)
+        self.box_hi = np.concatenate([xy + half[:, :2], (-1.7 + 2 * half[:, 2:3])], axis=1)
+
+    def raycast(self, origin: np.ndarray, dirs: np.ndarray):
+        """Nearest hit distance (inf if none) and world normal per ray."""
+        o = np.asarray(origin, dtype=float).reshape(1, 3)
+        d = np.asarray(dirs, dtype=float).reshape(-1, 3)
+        n = d.shape[0]
+        best = np.full(n, np.inf)
+        nrm = np.zeros((n, 3))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            for ax, off, cen, half in self.rects:
+                others = [a for a in range(3) if a != ax]
+                t = (off - o[0, ax]) / d[:, ax]
+                hit = o[0, None, :] + t[:, None] * d
+                ok = (t > 1e-9) & (np.abs(hit[:, others[0]] - cen[0]) <= half[0]) & \
+                     (np.abs(hit[:, others[1]] - cen[1]) <= half[1])
+                closer = ok & (t < best)
+                best = np.where(closer, t, best)
+                nn = np.zeros(3)
+                nn[ax] = 1.0
+                nrm[closer] = nn
+            inv = 1.0 / d
+            for lo, hi in zip(self.box_lo, self.box_hi):
+                t1 = (lo[None, :] - o) * inv
+                t2 = (hi[None, :] - o) * inv
+                tmin = np.minimum(t1, t2)
+                tmax = np.maximum(t1, t2)
+                tn = np.max(tmin, axis=1)
+                tf = np.min(tmax, axis=1)
+                ok = (tn <= tf) & (tf > 1e-9)
+                t = np.where(tn > 1e-9, tn, tf)
+                closer = ok & (t < best)
+                ax = np.argmax(tmin, axis=1)
+                best = np.where(closer, t, best)
+                nn = np.zeros((n, 3))
+                nn[np.arange(n), ax] = 1.0
+                nrm[closer] = nn[closer]
+        return best, nrm
+
+
+def target_images(scene: Scene, cam: SphericalCamera, pose: SE3Pose | None = None, max_range: float = 100.0):
+    """Ray-cast range image of ``scene`` on ``cam``'s sample rays plus smoothed-range normals.
+
+    Normals follow make_keyframe (mapping.py:110-113): 3x3 median of the valid
+    ranges (seam wrap), central differences with four valid neighbours,
+    oriented toward the sensor (geometry.py:271-338)."""
+    from scipy import ndimage
+
+    pose = pose or SE3Pose.identity()
+    H, W = cam.height, cam.width
+    dirs = cam.pixel_directions.reshape(-1, 3)
+    t, _ = scene.raycast(pose.translation, dirs @ pose.rotation.T)
+    valid = np.isfinite(t) & (t <= max_range)
+    rng = np.where(valid, t, 0.0).reshape(H, W)
+    valid = valid.reshape(H, W)
+    filled = np.pad(np.where(valid, rng, np.inf), ((0, 0), (1, 1)), mode="wrap")
+    sm = ndimage.median_filter(filled, size=3, mode="nearest")[:, 1:-1]
+    sm = np.where(valid & np.isfinite(sm), sm, rng)
+    pts = sm[..., None] * cam.pixel_directions
+    wrap = cam.full_circle
+    left, right = np.roll(pts, 1, axis=1), np.roll(pts, -1, axis=1)
+    lv, rv = np.roll(valid, 1, axis=1), np.roll(valid, -1, axis=1)
+    if not wrap:
+        lv[:, 0] = False
+        rv[:, -1] = False
+    up = np.zeros_like(pts); up[1:] = pts[:-1]
+    dn = np.zeros_like(pts); dn[:-1] = pts[1:]
+    uv = np.zeros_like(valid); uv[1:] = valid[:-1]
+    dv = np.zeros_like(valid); dv[:-1] = valid[1:]
+    ok = valid & lv & rv & uv & dv
+    nrm = np.cross(right - left, dn - up)
+    nn = np.linalg.norm(nrm, axis=-1)
+    ok &= nn > 1e-12
+    nrm = nrm / np.maximum(nn, 1e-12)[..., None]
+    flip = np.sum(nrm * cam.pixel_directions, axis=-1) > 0
+    nrm[flip] = -nrm[flip]
+    nrm[~ok] = 0.0
+    return {"range": rng.astype(np.float32), "valid": valid, "normal": nrm.astype(np.float32), "nvalid": ok}
+
+
+def config(index: int) -> dict:
+    """Camera, splats and loss target of BASELINE.json configs 0 and 1."""
+    if index == 0:
+        cam, n, seed = synth_camera(1024, 64), 50_000, 0
+    elif index == 1:
+        cam, n, seed = synth_camera(2048, 128), 500_000, 1
+    else:
+        raise ValueError("configs 0 and 1 are single renders; see bench.py for 2-4")
+    return {"camera": cam, "splats": random_splats(n, seed), "pose": SE3Pose.identity(), "seed": seed}
+
+
+def random_pose(rng, rot_deg: float, trans: float) -> SE3Pose:
+    return SE3Pose(so3_exp(np.deg2rad(rot_deg) * rng.normal(size=3)), rng.normal(size=3) * trans)

@@ -1,0 +1,131 @@
+"""Generate golden vectors from the LIVE reference (run in the build container).
+
+The reference package `splatscan` is importable here from
+/root/reference/pkg/src; it does not exist on the GPU box, so its outputs are
+frozen into small .npz fixtures committed next to this script.  The fixtures
+pin the CPU oracle (oracle/) and, through it, the CUDA path.
+
+Cases (inputs are float32-rounded values promoted to float64, exactly what the
+GPU path consumes):
+  full      64x16 full-circle camera of pkg/tests/conftest.py:15-17, 300 splats
+            on a 2-8 m shell with 25% forced behind the sensor, random pose
+  synth     128x32 synth-grid camera (synth.py:277-281), config-0-style draw of
+            2000 splats, identity pose, extra splats on the seam
+  partial   96x24 partial field of view, 400 splats, random pose
+  tile16    the `full` inputs rendered with tile_size=16
+Each case stores the reference's tile lists, images, plain-space gradients for
+seeded pixel gradients, and raw-space gradients (mapping.py:479-494).
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from splatscan.geometry import SphericalCamera  # noqa: E402
+from splatscan.rasterizer import (PixelGradients, RasterConfig, rasterize_backward,  # noqa: E402
+                                  rasterize_forward, reference_rasterize)
+from splatscan.se3 import SE3Pose, so3_exp  # noqa: E402
+from splatscan.splats import SplatModel, tangent_raw_gradients  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def quat_frames(q):
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    ta = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)], axis=1)
+    tb = np.stack([2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)], axis=1)
+    return ta, tb
+
+
+def shell_model(rng, n, rmin, rmax, behind=0.0, zclip=None, mean_log_s=np.log(0.05), sig=0.5):
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    if behind > 0:
+        k = int(n * behind)
+        d[:k, 0] = -np.abs(d[:k, 0])
+    c = d * rng.uniform(rmin, rmax, n)[:, None]
+    if zclip is not None:
+        c[:, 2] = np.clip(c[:, 2], *zclip)
+    ls = rng.normal(mean_log_s, sig, (n, 2))
+    ta, tb = quat_frames(rng.normal(size=(n, 4)))
+    lo = rng.normal(0.0, 1.0, n)
+    return dict(centers=c, raw_t_alpha=ta, raw_t_beta=tb, log_scales=ls, logit_opacity=lo)
+
+
+def to_model(p):
+    p = {k: f32(v) for k, v in p.items()}
+    m = SplatModel(p["centers"], p["raw_t_alpha"], p["raw_t_beta"], p["log_scales"], p["logit_opacity"])
+    return m, p
+
+
+def random_pose(rng, rot_deg=20.0, trans=0.5):
+    R = so3_exp(np.deg2rad(rot_deg) * rng.normal(size=3) / np.sqrt(3))
+    return SE3Pose(R, rng.normal(size=3) * trans)
+
+
+def make_case(name, cam, model, params, pose, cfg, rng):
+    render, rec = rasterize_forward(cam, pose, model, cfg)
+    H, W = cam.height, cam.width
+    gD = rng.choice([-1.0, 1.0], size=(H, W)) * (render.opacity > 0)
+    gN = 0.1 * rng.normal(size=(H, W, 3))
+    gO = 0.05 * rng.normal(size=(H, W))
+    g = rasterize_backward(model, rec, render, PixelGradients(gD, gN, gO))
+    plain = np.concatenate([g.d_centers, g.d_t_alpha, g.d_t_beta, g.d_normal, g.d_scales,
+                            g.d_opacity[:, None]], axis=1)
+    ga, gb = tangent_raw_gradients(model.raw_t_alpha, model.raw_t_beta, g.d_t_alpha, g.d_t_beta, g.d_normal)
+    s = model.scales
+    o = model.opacities
+    raw = np.concatenate([g.d_centers, ga, gb, g.d_scales * s, (g.d_opacity * o * (1 - o))[:, None]], axis=1)
+    brute = reference_rasterize(cam, pose, model, cfg) if W * H <= 4096 else None
+    bz = np.zeros(0)
+    np.savez_compressed(
+        os.path.join(OUT, f"golden_{name}.npz"),
+        cam=np.array([cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max]),
+        tile_size=cfg.tile_size, R=pose.rotation, t=pose.translation,
+        fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy, grid_offset=cam.grid_offset,
+        dirs=cam.pixel_directions if W * H <= 2048 else np.zeros(0),
+        **{f"p_{k}": v for k, v in params.items()},
+        tile_ptr=rec.tile_ptr, pair_splats=rec.pair_splats, tiles_x=rec.tiles_x, tiles_y=rec.tiles_y,
+        range=render.range, normal=render.normal, opacity=render.opacity,
+        brute_range=brute.range if brute else bz, brute_normal=brute.normal if brute else bz,
+        brute_opacity=brute.opacity if brute else bz,
+        gD=gD, gN=gN, gO=gO, plain=plain, raw=raw,
+    )
+    print(name, "pairs", rec.pair_splats.shape[0], "covered px", int((render.opacity > 0).sum()))
+
+
+def main():
+    rng = np.random.default_rng(20251019)
+    # full-circle conftest camera, behind-sensor splats, random pose
+    cam = SphericalCamera(64, 16, -np.pi, np.pi, -np.deg2rad(20.0), np.deg2rad(15.0))
+    p = shell_model(rng, 300, 2.0, 8.0, behind=0.25, mean_log_s=np.log(0.15), sig=0.4)
+    m, p = to_model(p)
+    pose = random_pose(rng)
+    make_case("full", cam, m, p, pose, RasterConfig(), rng)
+    make_case("tile16", cam, m, p, pose, RasterConfig(tile_size=16), rng)
+    # synth-grid camera, config-0 style draw, seam splats
+    W, H = 128, 32
+    cam = SphericalCamera(W, H, -np.pi, np.pi - 2 * np.pi / W, -np.deg2rad(22.5), np.deg2rad(22.5))
+    p = shell_model(rng, 2000, 2.0, 50.0, zclip=(-2.0, 6.0), mean_log_s=np.log(0.3))
+    k = 60  # centres straddling the azimuth seam
+    az = np.pi + rng.normal(0, 0.02, k)
+    r = rng.uniform(3, 20, k)
+    p["centers"][:k] = np.stack([r * np.cos(az), r * np.sin(az), rng.uniform(-1, 2, k)], axis=1)
+    m, p = to_model(p)
+    make_case("synth", cam, m, p, SE3Pose.identity(), RasterConfig(), rng)
+    # partial field of view
+    cam = SphericalCamera(96, 24, -1.0, 0.7, -0.35, 0.25)
+    p = shell_model(rng, 400, 2.0, 12.0, mean_log_s=np.log(0.2), sig=0.4)
+    p["centers"][:, 0] = np.abs(p["centers"][:, 0])
+    m, p = to_model(p)
+    make_case("partial", cam, m, p, random_pose(rng, 5.0, 0.2), RasterConfig(), rng)
+
+
+if __name__ == "__main__":
+    main()
