@@ -1,0 +1,319 @@
+"""Benchmark: fwd+bwd spherical 2DGS renders/s at 128x2048 with 500k splats (BASELINE config 1).
+
+One step = one forward render + fused mapping loss (range L1 + 0.1 normal,
+mapping.py:128-151) + backward to the raw splat parameters, on the B200
+kernels of libsplatb200.so.  Inputs are the seeded synthetic config-1 splats
+(SURVEY 8(d)); with N GPUs each rank optimises its own independent map
+(config 4a, weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+``--impl reference`` times the CPU oracle port of the reference's algorithm
+(oracle/, float64, all host threads) on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd spherical 2DGS renders/s (128×2048, 500k G, fp32)"
+UNIT = "renders/s"
+WORKLOAD = "config1: forward + mapping loss + backward to raw params, 128x2048 spherical camera, 500k splats, seed 1"
+STAGES = ["preprocess", "scan", "scatter", "sort", "sort_long", "forward", "backward", "finalize"]
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def loss_grads_host(D, N, tgt):
+    M = tgt["valid"]
+    w = 1.0 / np.maximum(tgt["range"].astype(np.float64), 1.0)
+    gD = np.where(M, w * np.sign(D - tgt["range"]), 0.0)
+    gN = np.where((M & tgt["nvalid"])[..., None], -0.1 * tgt["normal"].astype(np.float64), 0.0)
+    return gD, gN, np.zeros_like(gD)
+
+
+def oracle_render_step(cam, params, tgt):
+    """One fwd+loss+bwd render with the float64 CPU oracle (the reference's algorithm)."""
+    from oracle import oracle as O
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    R, t = np.eye(3), np.zeros(3)
+    arr = O.splat_arrays(params, R, t)
+    tp, ps, _, _ = O.bin_splats(ct, arr)
+    D, N, Op, _ = O.forward_lists(ct, arr, tp, ps)
+    gD, gN, gO = loss_grads_host(D, N, tgt)
+    pl = O.backward_lists(ct, arr, R, tp, ps, D, N, Op, gD, gN, gO, max_threads=64)
+    return O.raw_gradients(params, pl)
+
+
+def cpu_info():
+    from oracle import oracle as O
+    return O.num_threads()
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.marks = [None, None]
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self, i):
+        self.marks[i] = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        t0, t1 = self.marks
+        inside = [s for ts, s in self.samples if t0 is not None and t0 <= ts <= t1]
+        window = "timed"
+        if not inside:  # timed region shorter than the sampling period: nearest samples
+            inside = [s for ts, s in sorted(self.samples, key=lambda x: abs(x[0] - (t0 or 0)))[:3]]
+            window = "nearest"
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for s in inside:
+            f = [x.strip() for x in s.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle port on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2503_17491_b200 import workloads as W
+    c = W.config(1)
+    cam, params = c["camera"], c["splats"]
+    tgt = W.target_images(W.Scene(0), cam)
+    cores = cpu_info()
+    for _ in range(max(args.warmup_ref, 0)):
+        oracle_render_step(cam, params, tgt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_render_step(cam, params, tgt)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup_ref, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
+            "config": {"workload": WORKLOAD, "renders_per_step": 1},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": "full config-1 fwd+loss+bwd render per step, C float64 oracle (oracle/)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, ws, rank, local):
+    import torch
+
+    from paper_2503_17491_b200 import _lib, engine
+    from paper_2503_17491_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+    c = W.config(1)
+    cam = c["camera"]
+    # weak scaling: rank r optimises its own independent map (seed 1 + r)
+    params_np = W.random_splats(500_000, 1 + rank)
+    tgt = W.target_images(W.Scene(0), cam)
+    splats = {k: torch.from_numpy(v).to(dev) for k, v in params_np.items()}
+    kf_range = torch.from_numpy(tgt["range"]).to(dev)
+    kf_valid = torch.from_numpy(tgt["valid"].astype(np.uint8)).to(dev)
+    kf_normal = torch.from_numpy(tgt["normal"]).to(dev)
+    kf_nvalid = torch.from_numpy(tgt["nvalid"].astype(np.uint8)).to(dev)
+    from paper_2503_17491_b200.rasterizer import RasterConfig
+    cfg = RasterConfig()
+    pose12 = np.concatenate([np.eye(3).reshape(9), np.zeros(3)])
+    rec = engine.Records()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step(sp):
+        D, N, O = engine.forward(cam, pose12, sp, cfg, rec)
+        dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf_range, kf_valid, kf_normal, kf_nvalid, w_opacity=0.0,
+                                                w_normal=0.1)
+        g = engine.backward(rec, sp, dD, dN, dO, raw_space=True)
+        return g, parts
+
+    for _ in range(max(args.warmup, 3)):
+        step(splats)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.1)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    L.ss_records_profile(rec.ptr, 1)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.mark(0)
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        starts[i].record()
+        step(splats)
+        ends[i].record()
+    torch.cuda.synchronize()
+    sampler.mark(1)
+    L.ss_records_profile(rec.ptr, 0)
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    stage_ms = (ctypes.c_double * 8)()
+    stage_n = (ctypes.c_int32 * 8)()
+    L.ss_records_stage_times(rec.ptr, stage_ms, stage_n, 8)
+    clocks = sampler.stop()
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * 1000.0 / ms_step
+
+    # work counts (reference algorithm's units) for the roofline
+    E = ctypes.c_int64(0)
+    U = ctypes.c_int64(0)
+    engine.forward(cam, pose12, splats, cfg, rec)
+    L.ss_records_work(rec.ptr, ctypes.byref(E), ctypes.byref(U), ctypes.c_void_p(engine.stream_ptr()))
+    n_pairs, _, _ = rec.counts()
+    E, U, N = E.value, U.value, 500_000
+    peak = ctypes.c_double(0.0)
+    L.ss_fp32_peak_tflops(ctypes.byref(peak), ctypes.c_void_p(engine.stream_ptr()))
+    stage = {STAGES[i]: (stage_ms[i] / max(stage_n[i], 1)) for i in range(8)}
+    flops = {"forward": 46 * E + 34 * U, "backward": 46 * E + 170 * U}
+    top = max(("forward", "backward"), key=lambda k: stage[k])
+    achieved = flops[top] / (stage[top] * 1e-3) / 1e12
+    step_flops = 92 * E + 204 * U + 300 * N
+    roofline = {"bound": "fp32", "kernel": f"k_{top}<8>", "achieved": achieved, "peak": peak.value,
+                "unit": "TFLOP/s", "frac": achieved / peak.value,
+                "peak_source": "FFMA probe measured live (ss_fp32_peak_tflops); MEASURED_PEAKS.json has no FP32 figure",
+                "algorithmic_flops_per_launch": flops[top], "traffic": None,
+                "units": {"E_pair_evaluations": E, "U_contributions": U, "TP_tile_pairs": n_pairs, "N_splats": N},
+                "step_fraction": stage[top] / ms_step,
+                "step_achieved_tflops": step_flops / (ms_step * 1e-3) / 1e12}
+
+    # e2e: pinned host parameters -> device, step, gradients + loss back to the host
+    host = {k: torch.from_numpy(v).pin_memory() for k, v in params_np.items()}
+    dev_in = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+    g_host = torch.empty((500_000, 12), dtype=torch.float32).pin_memory()
+    loss_host = torch.empty(4, dtype=torch.float64).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = g_host.numel() * 4 + 4 * 8
+
+    def e2e_step():
+        for k in host:
+            dev_in[k].copy_(host[k], non_blocking=True)
+        g, parts = step(dev_in)
+        g_host.copy_(g, non_blocking=True)
+        loss_host.copy_(parts, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": ws * args.steps * 1000.0 / ems, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        t0 = time.perf_counter()
+        oracle_render_step(cam, params_np, tgt)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cpu_info(), "kind": "port",
+               "sample": "1 full config-1 fwd+loss+bwd render, C float64 oracle (oracle/), all host threads"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d)); independent map per rank",
+                "config": {"workload": WORKLOAD, "renders_per_step": ws, "camera": "128x2048",
+                           "splats_per_rank": 500_000, "parallelism": f"independent maps x{ws}",
+                           "l2": "flushed between timed steps (256 MiB write outside the events)"},
+                "clocks": clocks, "gpu_launches": int(sum(stage_n)) + args.steps, "stage_ms": stage,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_b200(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

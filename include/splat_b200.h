@@ -138,6 +138,10 @@ int ss_photo_system(const float* X_w, int32_t M, const float* scan_range,
                     double trim_floor, const ss_reg_cfg* cfg, double* out30, void* workspace,
                     void* stream);
 
+/* Measured FP32 FMA throughput of the current device (TFLOP/s), the roofline
+ * denominator of the FP32-bound blend kernels.  Synchronises the stream. */
+int ss_fp32_peak_tflops(double* tflops, void* stream);
+
 const char* ss_version(void);
 
 #ifdef __cplusplus

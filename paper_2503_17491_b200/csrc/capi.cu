@@ -74,6 +74,21 @@ SplatsK to_k(const ss_splats* s) {
   return k;
 }
 
+// FP32 FMA throughput probe (roofline denominator; MEASURED_PEAKS.json has no FP32 figure).
+__global__ void k_ffma_probe(float* out, int iters, float a, float b) {
+  float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+        x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.f) out[0] = s;
+}
+
 }  // namespace
 
 struct ss_records {
@@ -338,6 +353,35 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
     k_finalize<<<(n + 255) / 256, 256, 0, s>>>(to_k(splats), rec->pose, rec->acc, d_scales_extra, grads, raw_space);
   }
   SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_fp32_peak_tflops(double* tflops, void* stream) {
+  if (!tflops) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  SS_CUDA_TRY(cudaGetDevice(&dev));
+  SS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float* out = nullptr;
+  SS_CUDA_TRY(cudaMallocAsync((void**)&out, sizeof(float), s));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256, iters = 2048;
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, s);
+    k_ffma_probe<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 1e-4f);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(out, s);
+  *tflops = 2.0 * 8 * 16 * (double)iters * blocks * threads / (best * 1e-3) / 1e12;
   return SS_OK;
 }
 
