@@ -73,11 +73,19 @@ void ss_records_destroy(ss_records* rec, void* stream);
 
 /* Forward render.  pose_Rt = row-major R (9) then t (3), sensor-in-world
  * (se3.py:3-7).  Outputs (device, float32): range H*W, normal H*W*3,
- * opacity H*W.  Fills `rec` for ss_render_backward.  One host
- * synchronisation happens when the pair capacity must grow. */
+ * opacity H*W.  Fills `rec` for ss_render_backward.  Fully stream-ordered
+ * (no host synchronisation, CUDA-graph capturable): the (tile, splat) pair
+ * buffers are sized speculatively, so completion must be confirmed with
+ * ss_records_check before host use of the results. */
 int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_splats* splats,
                       const ss_raster_cfg* cfg, float* out_range, float* out_normal,
                       float* out_opacity, ss_records* rec, void* stream);
+
+/* Confirm a forward: wait = 1 blocks until it finished; wait = 0 polls.
+ * Returns SS_ERR_CAPACITY when the speculative pair capacity was exceeded
+ * (outputs invalid; the next ss_render_forward on `rec` allocates enough,
+ * so re-run), or the device-side status (e.g. SS_ERR_DEGENERATE). */
+int ss_records_check(ss_records* rec, int wait);
 
 /* Number of (tile, splat) pairs and tiles of a finished forward. */
 int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y);
@@ -91,7 +99,7 @@ int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_sp
 int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contributions, void* stream);
 
 /* Optional CUDA-event timing of every kernel stage launched with `rec`
- * (0 preprocess, 1 scan, 2 scatter, 3 sort, 4 sort_long, 5 forward,
+ * (0 preprocess, 1 emit, 2 bucket, 3 tile_sort, 4 unused, 5 forward,
  * 6 backward, 7 finalize).  ss_records_stage_times waits for the events,
  * returns summed milliseconds and launch counts per stage and resets. */
 int ss_records_profile(ss_records* rec, int enable);

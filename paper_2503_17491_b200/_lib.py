@@ -79,6 +79,8 @@ def lib() -> ctypes.CDLL:
     L.ss_render_backward.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, ctypes.c_int, vp]
     L.ss_fp32_peak_tflops.argtypes = [ctypes.POINTER(d), vp]
     L.ss_fp32_peak_tflops.restype = ctypes.c_int
+    L.ss_records_check.argtypes = [vp, ctypes.c_int]
+    L.ss_records_check.restype = ctypes.c_int
     L.ss_records_work.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
     L.ss_records_profile.argtypes = [vp, ctypes.c_int]
     L.ss_records_stage_times.argtypes = [vp, ctypes.POINTER(d), ctypes.POINTER(i32), i32]
@@ -95,7 +97,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_forward", "ss_records_counts",
-            "ss_records_export", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
+            "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system"]
 

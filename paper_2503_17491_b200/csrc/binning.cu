@@ -6,80 +6,109 @@
 //   rasterizer.py:244-306          cone-bound tile incidence (float64, bit-exact)
 //   rasterizer.py:318-339          per-tile lists ordered by (tile, f64 range, index)
 //
-// Design: the incidence predicate is evaluated exactly as the reference does
-// (float64, no contraction) but only on the tiles near the splat's cone
-// instead of the dense N x tiles matrix.  Lists are bucketed per tile with
-// atomics and each tile's bucket is then sorted in shared memory by the
-// 96-bit key (float64 range bits, splat index); tiles longer than the shared
-// memory capacity fall back to a global-memory merge sort.
+// Design.  The incidence predicate is evaluated exactly as the reference
+// does (float64, no contraction) on the tiles near the splat's cone only.
+// Pipeline (no cross-block dependency chains, no global atomics, no host
+// synchronisation):
+//   1. preprocess: records, tile rectangle, pair count, per-block count sums;
+//   2. scan of the block sums; emit every (tile, splat) pair at its offset;
+//   3. counting sort of the pairs by tile from per-block shared-memory
+//      histograms (order inside a tile is irrelevant, see 4);
+//   4. per tile, a shared-memory LSD radix sort by a 16-bit monotone key
+//      (float64 range -> float32 rounded down -> relative to the tile's
+//      minimum), then runs of equal keys are put in exact (float64 range,
+//      splat index) order.  Lists longer than the shared-memory capacity
+//      take a global merge-sort fallback with the exact comparator.
+// Pair buffers are sized speculatively; an overflow flag is checked by the
+// host after the fact (ss_records_check).
 #include "common.cuh"
 
 namespace ss {
 
 struct Incidence {
   double azc, elc, omega, dgam;
-  bool alive;
 };
 
-__device__ __forceinline__ bool col_hit(const CamK& k, const Incidence& g, int c) {
-  double cc, hw;
-  tile_col_interval(k, c, cc, hw);
-  double d = x_sub(g.azc, cc);
-  d = fabs(x_sub(py_mod(x_add(d, SS_PI), 2.0 * SS_PI), SS_PI));
-  return d <= x_add(x_add(g.dgam, hw), k.pad_az);
-}
-__device__ __forceinline__ bool row_hit(const CamK& k, const Incidence& g, int r) {
-  double rc, hw;
-  tile_row_interval(k, r, rc, hw);
-  double d = fabs(x_sub(g.elc, rc));
-  return d <= x_add(x_add(g.omega, hw), k.pad_el);
+// np.mod(x, 2*pi) for x = d + pi with d a difference of two angles in
+// [-pi, pi]: fmod is exact, so the subtraction below is bit-identical.
+__device__ __forceinline__ double mod_2pi(double x) {
+  const double tp = 2.0 * SS_PI;
+  if (x >= 0.0 && x < tp) return x;
+  if (x >= tp && x < 2.0 * tp) return x_sub(x, tp);
+  return py_mod(x, tp);
 }
 
-// x @ R for a row vector x (numpy matmul of an (N,3) array with R).
+__device__ __forceinline__ bool col_hit(const CamK& k, const double2* __restrict__ colt, const Incidence& g, int c) {
+  const double2 ch = colt[c];
+  double d = x_sub(g.azc, ch.x);
+  d = fabs(x_sub(mod_2pi(x_add(d, SS_PI)), SS_PI));
+  return d <= x_add(x_add(g.dgam, ch.y), k.pad_az);
+}
+__device__ __forceinline__ bool row_hit(const CamK& k, const double2* __restrict__ rowt, const Incidence& g, int r) {
+  const double2 rh = rowt[r];
+  const double d = fabs(x_sub(g.elc, rh.x));
+  return d <= x_add(x_add(g.omega, rh.y), k.pad_el);
+}
+
+// Per-tile-column and -row angular intervals (rasterizer.py:278-294).
+__global__ void k_tile_intervals(CamK k, double2* __restrict__ colt, double2* __restrict__ rowt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double c, h;
+  if (i < k.tx) {
+    tile_col_interval(k, i, c, h);
+    colt[i] = make_double2(c, h);
+  } else if (i < k.tx + k.ty) {
+    tile_row_interval(k, i - k.tx, c, h);
+    rowt[i - k.tx] = make_double2(c, h);
+  }
+}
+
+// x @ R for a row vector x (numpy matmul of an (N,3) array with R uses FMA, OpenBLAS dgemm).
 __device__ __forceinline__ double rowmat(const double x[3], const double* R, int c) {
   return fma(x[2], R[6 + c], fma(x[1], R[3 + c], x_mul(x[0], R[c])));
 }
 
-__global__ void k_preprocess(SplatsK sp, PoseK pose, CamK cam, RasterK rk, SplatRec* __restrict__ rec,
-                             SplatRec64* __restrict__ rec64, unsigned long long* __restrict__ key,
-                             int4* __restrict__ rect, int* __restrict__ tile_count, int* __restrict__ status) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= sp.n) return;
-  int4 empty = make_int4(0, -1, 0, 0);
+__device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK cam, RasterK rk, const double2* __restrict__ colt,
+                                   const double2* __restrict__ rowt, SplatRec* __restrict__ rec,
+                                   SplatRec64* __restrict__ rec64, unsigned long long* __restrict__ key64,
+                                   uint32_t* __restrict__ key32, int4* __restrict__ rect, int* __restrict__ status,
+                                   int i) {
+  const int4 empty = make_int4(0, -1, 0, 0);
+  key32[i] = 0xffffffffu;
+  rect[i] = empty;
   // --- Gram-Schmidt (splats.py:112-130), float64
   double a[3], b[3];
   for (int c = 0; c < 3; ++c) {
     a[c] = (double)sp.raw_ta[3 * i + c];
     b[c] = (double)sp.raw_tb[3 * i + c];
   }
-  double na = sqrt(x_add(x_add(x_mul(a[0], a[0]), x_mul(a[1], a[1])), x_mul(a[2], a[2])));
+  const double na = sqrt(x_add(x_add(x_mul(a[0], a[0]), x_mul(a[1], a[1])), x_mul(a[2], a[2])));
   if (na < 1e-12) {
     atomicExch(status, (int)SS_ERR_DEGENERATE);
-    rect[i] = empty;
-    return;
+    return 0u;
   }
-  double u[3] = {a[0] / na, a[1] / na, a[2] / na};
-  double ub = u[0] * b[0] + u[1] * b[1] + u[2] * b[2];
-  double w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
-  double nw = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  const double u[3] = {a[0] / na, a[1] / na, a[2] / na};
+  const double ub = u[0] * b[0] + u[1] * b[1] + u[2] * b[2];
+  const double w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
+  const double nw = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
   if (nw < 1e-12) {
     atomicExch(status, (int)SS_ERR_DEGENERATE);
-    rect[i] = empty;
-    return;
+    return 0u;
   }
-  double v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
-  double nn[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
-  double s0 = exp((double)sp.log_scales[2 * i]), s1 = exp((double)sp.log_scales[2 * i + 1]);
-  double x = (double)sp.logit_opacity[i], o;
+  const double v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
+  const double nn[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+  const double s0 = exp((double)sp.log_scales[2 * i]), s1 = exp((double)sp.log_scales[2 * i + 1]);
+  const double x = (double)sp.logit_opacity[i];
+  double o;
   if (x >= 0) {
     o = 1.0 / (1.0 + exp(-x));
   } else {
-    double e = exp(x);
+    const double e = exp(x);
     o = e / (1.0 + e);
   }
   // --- camera-frame arrays (rasterizer.py:223-241)
-  double m[3] = {x_sub((double)sp.centers[3 * i], pose.t[0]), x_sub((double)sp.centers[3 * i + 1], pose.t[1]),
-                 x_sub((double)sp.centers[3 * i + 2], pose.t[2])};
+  const double m[3] = {x_sub((double)sp.centers[3 * i], pose.t[0]), x_sub((double)sp.centers[3 * i + 1], pose.t[1]),
+                       x_sub((double)sp.centers[3 * i + 2], pose.t[2])};
   double Bc[3], Ba[3], Bb[3], nc[3];
   for (int c = 0; c < 3; ++c) {
     Bc[c] = rowmat(m, pose.R, c);
@@ -87,11 +116,11 @@ __global__ void k_preprocess(SplatsK sp, PoseK pose, CamK cam, RasterK rk, Splat
     Bb[c] = s1 * rowmat(v, pose.R, c);
     nc[c] = rowmat(nn, pose.R, c);
   }
-  double range = sqrt(x_add(x_add(x_mul(Bc[0], Bc[0]), x_mul(Bc[1], Bc[1])), x_mul(Bc[2], Bc[2])));
+  const double range = sqrt(x_add(x_add(x_mul(Bc[0], Bc[0]), x_mul(Bc[1], Bc[1])), x_mul(Bc[2], Bc[2])));
 
   // --- render records for the blend kernels
-  double kq = o / rk.alpha_cutoff;
-  float Kp = kq > 1.0 ? (float)(2.0 * log(kq) * (1.0 + 1e-4) + 1e-4) : -1.0f;
+  const double kq = o / rk.alpha_cutoff;
+  const float Kp = kq > 1.0 ? (float)(2.0 * log(kq) * (1.0 + 1e-4) + 1e-4) : -1.0f;
   SplatRec r;
   r.r0 = make_float4((float)o, Kp, (float)nc[0], (float)nc[1]);
   r.r1 = make_float4((float)nc[2], 0.f, 0.f, 0.f);
@@ -103,115 +132,225 @@ __global__ void k_preprocess(SplatsK sp, PoseK pose, CamK cam, RasterK rk, Splat
   r64.v[3] = make_double2(Bc[0], Bc[1]);
   r64.v[4] = make_double2(Bc[2], range);
   rec64[i] = r64;
-  key[i] = (unsigned long long)__double_as_longlong(range);
+  key64[i] = (unsigned long long)__double_as_longlong(range);
 
   // --- cone-bound incidence (rasterizer.py:256-305), float64 without contraction
   Incidence g;
-  double reach = x_mul(rk.cutoff_sigma, fmax(s0, s1));
-  bool near_ = range <= x_add(reach, 1e-12);
+  const double reach = x_mul(rk.cutoff_sigma, fmax(s0, s1));
+  const bool near_ = range <= x_add(reach, 1e-12);
   double so = x_div(reach, fmax(range, 1e-12));
   so = fmin(fmax(so, 0.0), 1.0);
   double omega = asin(so);
   g.azc = atan2(Bc[1], Bc[0]);
   g.elc = atan2(Bc[2], hypot(Bc[0], Bc[1]));
-  bool pole = x_add(fabs(g.elc), omega) >= (SS_PI / 2 - 1e-9);
-  double ce = fmax(cos(g.elc), 1e-12);
-  double q = fmin(fmax(x_div(so, ce), 0.0), 1.0);
+  const bool pole = x_add(fabs(g.elc), omega) >= (SS_PI / 2 - 1e-9);
+  const double ce = fmax(cos(g.elc), 1e-12);
+  const double q = fmin(fmax(x_div(so, ce), 0.0), 1.0);
   double dgam = asin(q);
   if (near_ || pole) dgam = SS_PI;
   if (near_) omega = SS_PI;
   g.omega = omega;
   g.dgam = dgam;
-  g.alive = range > 1e-9;
-  if (!g.alive) {
-    rect[i] = empty;
-    return;
-  }
+  if (!(range > 1e-9)) return 0u;  // not alive (rasterizer.py:303-305)
   int r_lo = -1, r_hi = -2;
   for (int rr = 0; rr < cam.ty; ++rr) {
-    if (row_hit(cam, g, rr)) {
+    if (row_hit(cam, rowt, g, rr)) {
       if (r_lo < 0) r_lo = rr;
       r_hi = rr;
     }
   }
-  if (r_lo < 0) {
-    rect[i] = empty;
-    return;
-  }
-  int tx = cam.tx;
-  int c_start = 0, ncols = 0;
-  int h = -1;
+  if (r_lo < 0) return 0u;
+  const int tx = cam.tx;
+  int c_start = 0, ncols = 0, h = -1;
   if (dgam < 0.5 * SS_PI) {
-    double uu = cam.fx * g.azc + cam.cx - cam.off_u;
-    int c0 = (int)floor(uu / cam.T);
+    const double uu = cam.fx * g.azc + cam.cx - cam.off_u;
+    const int c0 = (int)floor(uu / cam.T);
     for (int dc = 0; dc < 3 && h < 0; ++dc) {
       int c = c0 + (dc == 0 ? 0 : (dc == 1 ? -1 : 1));
       c = ((c % tx) + tx) % tx;
-      if (col_hit(cam, g, c)) h = c;
+      if (col_hit(cam, colt, g, c)) h = c;
     }
   }
   if (h >= 0) {
+    // the hit set is one circular run around h (interval overlap on a circle)
     int lo = h, cnt = 1;
     while (cnt < tx) {
-      int c = (lo - 1 + tx) % tx;
-      if (!col_hit(cam, g, c)) break;
+      const int c = (lo - 1 + tx) % tx;
+      if (!col_hit(cam, colt, g, c)) break;
       lo = c;
       ++cnt;
     }
     int hi = h;
     while (cnt < tx) {
-      int c = (hi + 1) % tx;
-      if (!col_hit(cam, g, c)) break;
+      const int c = (hi + 1) % tx;
+      if (!col_hit(cam, colt, g, c)) break;
       hi = c;
       ++cnt;
     }
     c_start = lo;
     ncols = cnt;
   } else {
-    // wide cone or centre column missed (partial-FoV cameras): scan all
-    // columns; the hit set is one circular run.
+    // wide cone or centre column missed (partial field of view): scan all columns
     int first_miss = -1, nhit = 0;
     for (int c = 0; c < tx; ++c) {
-      bool hc = col_hit(cam, g, c);
+      const bool hc = col_hit(cam, colt, g, c);
       nhit += hc;
       if (!hc && first_miss < 0) first_miss = c;
     }
     if (nhit == tx) {
-      c_start = 0;
       ncols = tx;
     } else if (nhit > 0) {
       int c = first_miss;
-      while (!col_hit(cam, g, c)) c = (c + 1) % tx;
+      while (!col_hit(cam, colt, g, c)) c = (c + 1) % tx;
       c_start = c;
       ncols = nhit;
     }
   }
-  if (ncols == 0) {
-    rect[i] = empty;
+  if (ncols == 0) return 0u;
+  rect[i] = make_int4(r_lo, r_hi, c_start, ncols);
+  key32[i] = __float_as_uint(__double2float_rd(range));  // monotone in the float64 range
+  return (uint32_t)((r_hi - r_lo + 1) * ncols);
+}
+
+
+__global__ void __launch_bounds__(256)
+    k_preprocess(SplatsK sp, PoseK pose, CamK cam, RasterK rk, const double2* __restrict__ colt,
+                 const double2* __restrict__ rowt, SplatRec* __restrict__ rec, SplatRec64* __restrict__ rec64,
+                 unsigned long long* __restrict__ key64, uint32_t* __restrict__ key32, int4* __restrict__ rect,
+                 uint32_t* __restrict__ block_sum, int* __restrict__ status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t cnt = 0;
+  if (i < sp.n) cnt = preprocess_one(sp, pose, cam, rk, colt, rowt, rec, rec64, key64, key32, rect, status, i);
+  // block sum of pair counts (for the emission scan)
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  __shared__ uint32_t ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+    block_sum[blockIdx.x] = s;
+  }
+}
+
+
+// Exclusive scan of the per-block pair counts (one block); totals[0] = pairs.
+__global__ void k_scan_blocks(int nb, uint32_t* __restrict__ block_sum, long long* __restrict__ totals) {
+  __shared__ unsigned long long part[1024];
+  const int tid = threadIdx.x;
+  const int per = (nb + 1023) / 1024;
+  const int b = tid * per, e = min(b + per, nb);
+  unsigned long long s = 0;
+  for (int q = b; q < e; ++q) s += block_sum[q];
+  part[tid] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const unsigned long long x = tid >= off ? part[tid - off] : 0ull;
+    __syncthreads();
+    part[tid] += x;
+    __syncthreads();
+  }
+  unsigned long long run = part[tid] - s;
+  for (int q = b; q < e; ++q) {
+    const uint32_t c = block_sum[q];
+    block_sum[q] = (uint32_t)run;
+    run += c;
+  }
+  if (tid == 1023) totals[0] = (long long)part[1023];
+}
+
+// Emit the pairs of every splat at its offset (index order).  Overflow of
+// the speculative capacity sets a flag.
+__global__ void __launch_bounds__(256)
+    k_emit(int n, const int4* __restrict__ rect, const uint32_t* __restrict__ block_off, int tx, long long cap,
+           uint32_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_splat, int* __restrict__ overflow) {
+  __shared__ uint32_t ws[8];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4 r = make_int4(0, -1, 0, 0);
+  if (i < n) r = rect[i];
+  const uint32_t cnt = (r.y >= r.x) ? (uint32_t)((r.y - r.x + 1) * r.w) : 0u;
+  uint32_t inc = cnt;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  uint32_t wex = 0;
+  for (int w = 0; w < warp; ++w) wex += ws[w];
+  if (cnt == 0) return;
+  const long long off = (long long)block_off[blockIdx.x] + wex + (inc - cnt);
+  if (off + cnt > cap) {
+    atomicExch(overflow, 1);
     return;
   }
-  rect[i] = make_int4(r_lo, r_hi, c_start, ncols);
-  for (int rr = r_lo; rr <= r_hi; ++rr) {
-    int base = rr * tx;
-    for (int j = 0; j < ncols; ++j) {
-      int c = c_start + j;
+  long long q = off;
+  for (int rr = r.x; rr <= r.y; ++rr) {
+    const int base = rr * tx;
+    for (int j = 0; j < r.w; ++j) {
+      int c = r.z + j;
       if (c >= tx) c -= tx;
-      atomicAdd(&tile_count[base + c], 1);
+      pair_tile[q] = (uint32_t)(base + c);
+      pair_splat[q] = (uint32_t)i;
+      ++q;
     }
   }
 }
 
-// Exclusive scans of per-tile pair counts and 32-entry chunk counts; one block.
+// Counting sort of the pairs by tile without global atomics:
+//   k_tile_hist_blocks  per block of kPairChunk pairs, a shared-memory tile
+//                       histogram written as row b of a blocks x tiles matrix;
+//   k_tile_prefix       per tile, exclusive prefix over blocks + tile totals;
+//   k_scan_tiles        tile_ptr and chunk_ptr (32-entry chunks);
+//   k_tile_scatter      each block re-reads its pairs and places them with
+//                       shared-memory cursors (order inside a tile is
+//                       irrelevant: k_tile_sort establishes it).
+constexpr int kPairChunk = 16384;
+constexpr int kMaxTiles = 16384;  // shared-memory histogram capacity
+
+__global__ void __launch_bounds__(1024)
+    k_tile_hist_blocks(const uint32_t* __restrict__ pair_tile, const long long* __restrict__ totals, long long cap,
+                       int ntiles, uint32_t* __restrict__ mat, const int* __restrict__ overflow) {
+  extern __shared__ uint32_t h[];
+  const long long n = min(totals[0], cap);
+  const long long b0 = (long long)blockIdx.x * kPairChunk;
+  if (b0 >= n && blockIdx.x > 0) return;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  if (!*overflow) {
+    const long long e = min(b0 + kPairChunk, n);
+    for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[pair_tile[i]], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) mat[(size_t)blockIdx.x * ntiles + t] = h[t];
+}
+
+__global__ void k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
+                              uint32_t* __restrict__ mat, int* __restrict__ tile_count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const long long n = min(totals[0], cap);
+  const int nb = (int)max(1LL, (n + kPairChunk - 1) / kPairChunk);
+  uint32_t s = 0;
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t c = mat[(size_t)b * ntiles + t];
+    mat[(size_t)b * ntiles + t] = s;
+    s += c;
+  }
+  tile_count[t] = (int)s;
+}
+
 __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int* __restrict__ tile_ptr,
-                             int* __restrict__ chunk_ptr, int* __restrict__ cursor, long long* __restrict__ totals) {
+                             int* __restrict__ chunk_ptr, long long* __restrict__ totals) {
   __shared__ long long s_p[1024];
   __shared__ long long s_c[1024];
-  int tid = threadIdx.x, nt = blockDim.x;
-  int per = (ntiles + nt - 1) / nt;
-  int b = tid * per, e = min(b + per, ntiles);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (ntiles + nt - 1) / nt;
+  const int b = tid * per, e = min(b + per, ntiles);
   long long sp = 0, sc = 0;
   for (int t = b; t < e; ++t) {
-    int c = tile_count[t];
+    const int c = tile_count[t];
     sp += c;
     sc += (c + 31) >> 5;
   }
@@ -219,8 +358,8 @@ __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int
   s_c[tid] = sc;
   __syncthreads();
   for (int off = 1; off < nt; off <<= 1) {
-    long long vp = tid >= off ? s_p[tid - off] : 0;
-    long long vc = tid >= off ? s_c[tid - off] : 0;
+    const long long vp = tid >= off ? s_p[tid - off] : 0;
+    const long long vc = tid >= off ? s_c[tid - off] : 0;
     __syncthreads();
     s_p[tid] += vp;
     s_c[tid] += vc;
@@ -228,9 +367,8 @@ __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int
   }
   long long rp = s_p[tid] - sp, rc = s_c[tid] - sc;
   for (int t = b; t < e; ++t) {
-    int c = tile_count[t];
+    const int c = tile_count[t];
     tile_ptr[t] = (int)rp;
-    cursor[t] = (int)rp;
     chunk_ptr[t] = (int)rc;
     rp += c;
     rc += (c + 31) >> 5;
@@ -238,86 +376,200 @@ __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int
   if (tid == nt - 1) {
     tile_ptr[ntiles] = (int)s_p[nt - 1];
     chunk_ptr[ntiles] = (int)s_c[nt - 1];
-    totals[0] = s_p[nt - 1];
     totals[1] = s_c[nt - 1];
   }
 }
 
-__global__ void k_scatter_pairs(int n, int tx, const int4* __restrict__ rect, int* __restrict__ cursor,
-                                int* __restrict__ pairs) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int4 r = rect[i];
-  for (int rr = r.x; rr <= r.y; ++rr) {
-    int base = rr * tx;
-    for (int j = 0; j < r.w; ++j) {
-      int c = r.z + j;
-      if (c >= tx) c -= tx;
-      int pos = atomicAdd(&cursor[base + c], 1);
-      pairs[pos] = i;
-    }
+__global__ void __launch_bounds__(1024)
+    k_tile_scatter(const uint32_t* __restrict__ pair_tile, const uint32_t* __restrict__ pair_splat,
+                   const long long* __restrict__ totals, long long cap, int ntiles, const uint32_t* __restrict__ mat,
+                   const int* __restrict__ tile_ptr, uint32_t* __restrict__ bucketed, const int* __restrict__ overflow) {
+  extern __shared__ uint32_t cur[];
+  if (*overflow) return;
+  const long long n = min(totals[0], cap);
+  const long long b0 = (long long)blockIdx.x * kPairChunk;
+  if (b0 >= n) return;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) cur[t] = (uint32_t)tile_ptr[t] + mat[(size_t)blockIdx.x * ntiles + t];
+  __syncthreads();
+  const long long e = min(b0 + kPairChunk, n);
+  for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) {
+    const uint32_t pos = atomicAdd(&cur[pair_tile[i]], 1u);
+    bucketed[pos] = pair_splat[i];
   }
 }
 
-constexpr int kSortMax = 2048;
-
-__device__ __forceinline__ bool key_less(unsigned long long ka, int va, unsigned long long kb, int vb) {
+__device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t va, unsigned long long kb, uint32_t vb) {
   return ka < kb || (ka == kb && va < vb);
 }
 
-// Per-tile bitonic sort by (float64 range bits, splat index) in shared memory.
-__global__ void __launch_bounds__(256) k_sort_tiles(const int* __restrict__ tile_ptr, int* __restrict__ pairs,
-                                                    const unsigned long long* __restrict__ key,
-                                                    int* __restrict__ long_list, int* __restrict__ n_long) {
-  __shared__ unsigned long long sk[kSortMax];
-  __shared__ int sv[kSortMax];
-  int t = blockIdx.x;
-  int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile
+constexpr int kTileSortIPL = kTileSortMax / 256;  // items per lane per warp segment
+constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> fallback
+
+// Per-tile ordering in shared memory.  The 32-bit key (float64 range rounded
+// down to float32) is reduced to 16 bits relative to the tile's smallest key
+// (monotone), sorted by two 8-bit LSD passes with warp multisplit ranking,
+// and runs of equal 16-bit keys are then put in exact (float64 range, splat
+// index) order by insertion sort.  One block (8 warps) per tile.
+__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
+                                                   const uint32_t* __restrict__ key32,
+                                                   const unsigned long long* __restrict__ key64,
+                                                   int* __restrict__ long_list, int* __restrict__ n_long,
+                                                   const int* __restrict__ overflow) {
+  __shared__ uint16_t sk[2][kTileSortMax];
+  __shared__ uint32_t sv[2][kTileSortMax];
+  __shared__ uint16_t wcnt[8][256];
+  __shared__ uint32_t dtot[256];
+  __shared__ uint32_t red_min[8], red_max[8];
+  __shared__ int s_bad;
+  if (*overflow) return;
+  const int t = blockIdx.x;
+  const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
   if (L <= 1) return;
-  if (L > kSortMax) {
+  if (L > kTileSortMax) {
     if (threadIdx.x == 0) long_list[atomicAdd(n_long, 1)] = t;
     return;
   }
-  int n = 1;
-  while (n < L) n <<= 1;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  uint32_t kk[kTileSortIPL];
+#pragma unroll
+  for (int j = 0; j < kTileSortIPL; ++j) {
+    const int i = tid + 256 * j;
+    kk[j] = 0;
     if (i < L) {
-      int v = pairs[lo + i];
-      sv[i] = v;
-      sk[i] = key[v];
-    } else {
-      sv[i] = 0x7fffffff;
-      sk[i] = ~0ull;
+      const uint32_t v = pairs[lo + i];
+      kk[j] = key32[v];
+      sv[0][i] = v;
+      kmin = min(kmin, kk[j]);
+      kmax = max(kmax, kk[j]);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+  }
+  if (lane == 0) {
+    red_min[warp] = kmin;
+    red_max[warp] = kmax;
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int w = 0; w < 8; ++w) {
+    kmin = min(kmin, red_min[w]);
+    kmax = max(kmax, red_max[w]);
+  }
+  const uint32_t span = kmax - kmin;
+  const int shift = span >= 65536u ? (32 - __clz(span)) - 16 : 0;
+#pragma unroll
+  for (int j = 0; j < kTileSortIPL; ++j) {
+    const int i = tid + 256 * j;
+    if (i < L) sk[0][i] = (uint16_t)((kk[j] - kmin) >> shift);
+  }
+  __syncthreads();
+  const int seg = ((L + 255) / 256) * 32;  // warp w owns [w*seg, (w+1)*seg), lane-striped
+  const uint32_t lt = lanemask_lt();
+  const uint32_t sspan = span >> shift;
+  int cur = 0;
+  for (int p = 0; p < 2; ++p) {
+    const int sh = 8 * p;
+    if (p == 1 && sspan < 256u) break;  // high digit constant
+    for (int i = tid; i < 8 * 256; i += 256) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    uint16_t lr[kTileSortIPL];
+    int dg[kTileSortIPL];
+#pragma unroll
+    for (int j = 0; j < kTileSortIPL; ++j) {
+      const int idx = warp * seg + j * 32 + lane;
+      const bool ok = (j * 32 < seg) && idx < L;
+      dg[j] = ok ? (int)((sk[cur][idx] >> sh) & 0xffu) : 256;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg[j]);
+      const int leader = 31 - __clz(peers);
+      uint16_t before = 0;
+      if (dg[j] < 256) before = wcnt[warp][dg[j]];
+      __syncwarp();
+      if (lane == leader && dg[j] < 256) wcnt[warp][dg[j]] = (uint16_t)(before + __popc(peers));
+      __syncwarp();
+      lr[j] = (uint16_t)(before + __popc(peers & lt));
+    }
+    __syncthreads();
+    {
+      uint32_t s = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t c = wcnt[w][tid];
+        wcnt[w][tid] = (uint16_t)s;
+        s += c;
+      }
+      uint32_t inc = s;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      if (lane == 31) dtot[warp] = inc;
+      __syncthreads();
+      uint32_t wex = 0;
+      for (int w = 0; w < warp; ++w) wex += dtot[w];
+      __syncthreads();
+      dtot[tid] = wex + inc - s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTileSortIPL; ++j) {
+      if (dg[j] < 256) {
+        const int idx = warp * seg + j * 32 + lane;
+        const uint32_t pos = dtot[dg[j]] + wcnt[warp][dg[j]] + lr[j];
+        sk[cur ^ 1][pos] = sk[cur][idx];
+        sv[cur ^ 1][pos] = sv[cur][idx];
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  // exact (float64, index) order inside runs of equal sort keys
+  for (int i = tid; i < L; i += 256) {
+    const uint16_t k = sk[cur][i];
+    if (i > 0 && sk[cur][i - 1] == k) continue;
+    if (i + 1 >= L || sk[cur][i + 1] != k) continue;
+    int j = i + 1;
+    while (j < L && sk[cur][j] == k) ++j;
+    if (j - i > kMaxTieRun) {
+      s_bad = 1;
+      continue;
+    }
+    for (int x = i + 1; x < j; ++x) {
+      const uint32_t v = sv[cur][x];
+      const unsigned long long kv = key64[v];
+      int y = x - 1;
+      while (y >= i) {
+        const uint32_t w = sv[cur][y];
+        if (key_less(key64[w], w, kv, v)) break;
+        sv[cur][y + 1] = w;
+        --y;
+      }
+      sv[cur][y + 1] = v;
     }
   }
   __syncthreads();
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
-        int a = 2 * j * (i / j) + (i % j);
-        int b = a + j;
-        bool up = (a & k) == 0;
-        unsigned long long ka = sk[a], kb = sk[b];
-        int va = sv[a], vb = sv[b];
-        bool gt = key_less(kb, vb, ka, va);
-        if (gt == up) {
-          sk[a] = kb;
-          sk[b] = ka;
-          sv[a] = vb;
-          sv[b] = va;
-        }
-      }
-      __syncthreads();
-    }
+  if (s_bad) {  // long run of near-equal ranges: exact merge sort instead
+    if (tid == 0) long_list[atomicAdd(n_long, 1)] = t;
+    return;
   }
-  for (int i = threadIdx.x; i < L; i += blockDim.x) pairs[lo + i] = sv[i];
+  for (int i = tid; i < L; i += 256) pairs[lo + i] = sv[cur][i];
 }
 
-__device__ int count_less(const int* run, int len, const unsigned long long* key, unsigned long long k, int v) {
+__device__ int count_less(const uint32_t* run, int len, const unsigned long long* key, unsigned long long k,
+                          uint32_t v) {
   int lo = 0, hi = len;
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    int w = run[mid];
+    const int mid = (lo + hi) >> 1;
+    const uint32_t w = run[mid];
     if (key_less(key[w], w, k, v))
       lo = mid + 1;
     else
@@ -326,23 +578,23 @@ __device__ int count_less(const int* run, int len, const unsigned long long* key
   return lo;
 }
 
-// Fallback for lists longer than kSortMax: bottom-up merge sort in global
-// memory, one block per long tile (rare: a few very large or near splats).
-__global__ void k_sort_long(const int* __restrict__ tile_ptr, int* __restrict__ pairs, int* __restrict__ tmp,
+// Fallback for lists longer than kTileSortMax: bottom-up merge sort in global
+// memory by the exact (float64 range, index) key, one block per long tile.
+__global__ void k_sort_long(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs, uint32_t* __restrict__ tmp,
                             const unsigned long long* __restrict__ key, const int* __restrict__ long_list,
                             const int* __restrict__ n_long) {
-  int nl = *n_long;
-  for (int idx = blockIdx.x; idx < nl; idx += gridDim.x) {
-    int t = long_list[idx];
-    int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
-    int* src = pairs + lo;
-    int* dst = tmp + lo;
+  const int nl = *n_long;
+  for (int r = blockIdx.x; r < nl; r += gridDim.x) {
+    const int t = long_list[r];
+    const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+    uint32_t* src = pairs + lo;
+    uint32_t* dst = tmp + lo;
     for (int w = 1; w < L; w <<= 1) {
       for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        int start = (i / (2 * w)) * (2 * w);
-        int mid = min(start + w, L), end = min(start + 2 * w, L);
-        int v = src[i];
-        unsigned long long k = key[v];
+        const int start = (i / (2 * w)) * (2 * w);
+        const int mid = min(start + w, L), end = min(start + 2 * w, L);
+        const uint32_t v = src[i];
+        const unsigned long long k = key[v];
         int pos;
         if (i < mid)
           pos = (i - start) + count_less(src + mid, end - mid, key, k, v);
@@ -351,19 +603,18 @@ __global__ void k_sort_long(const int* __restrict__ tile_ptr, int* __restrict__ 
         dst[start + pos] = v;
       }
       __syncthreads();
-      int* s = src;
+      uint32_t* s = src;
       src = dst;
       dst = s;
     }
-    if (src != pairs + lo) {
+    if (src != pairs + lo)
       for (int i = threadIdx.x; i < L; i += blockDim.x) pairs[lo + i] = src[i];
-    }
     __syncthreads();
   }
 }
 
 __global__ void k_widen_i32(int n, const int* __restrict__ in, long long* __restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[i];
 }
 

@@ -185,8 +185,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_forward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
               const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
               float* __restrict__ out_D, float* __restrict__ out_N, float* __restrict__ out_O,
-              float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask) {
+              float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask,
+              const int* __restrict__ overflow) {
   constexpr int PPL = TileShape<TS>::PPL;
+  if (*overflow) return;  // pair capacity exceeded: the host re-runs the render
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * kWarpsPerBlock + warp;
@@ -287,8 +289,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
                const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
                const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
-               float* __restrict__ acc) {
+               float* __restrict__ acc, const int* __restrict__ overflow) {
   constexpr int PPL = TileShape<TS>::PPL;
+  if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   __shared__ float red[kWarpsPerBlock][32 * kRedStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -514,14 +517,14 @@ __global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc
 }
 
 template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*);
+                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*);
 template __global__ void k_forward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*);
+                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*);
 template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                       const float*, const float*, float*);
+                                       const float*, const float*, float*, const int*);
 template __global__ void k_backward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                         const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                        const float*, const float*, float*);
+                                        const float*, const float*, float*, const int*);
 
 }  // namespace ss

@@ -95,35 +95,54 @@ struct ss_records {
   CamK cam{};
   PoseK pose{};
   BlendParams bp{};
-  int n = 0, ntiles = 0, valid = 0;
+  int n = 0, ntiles = 0, valid = 0, pending = 0;
+  uint32_t epoch = 0;
   long long n_pairs = 0, n_chunks = 0;
+  long long cap_pairs = 0;  // speculative pair capacity of the current forward
+  long long want_pairs = 0; // capacity requested for the next forward
+  // per splat
   SplatRec* rec = nullptr;
   size_t cap_rec = 0;
   SplatRec64* rec64 = nullptr;
   size_t cap_rec64 = 0;
-  unsigned long long* key = nullptr;
-  size_t cap_key = 0;
+  unsigned long long* key64 = nullptr;
+  size_t cap_key64 = 0;
+  uint32_t* key32 = nullptr;
+  size_t cap_key32 = 0;
   int4* rect = nullptr;
   size_t cap_rect = 0;
-  int* tiles = nullptr;  // tile_count | tile_ptr | chunk_ptr | cursor | long_list
+  uint32_t* bsum = nullptr;  // per preprocess block pair counts -> offsets
+  size_t cap_bsum = 0;
+  uint32_t* mat = nullptr;  // pair blocks x tiles histogram -> offsets
+  size_t cap_mat = 0;
+  // per camera / tile
+  double2* tint = nullptr;  // tx column + ty row intervals
+  size_t cap_tint = 0;
+  int* tiles = nullptr;  // tile_ptr | chunk_ptr | tile_count | cursor | long_list
   size_t cap_tiles = 0;
-  int* misc = nullptr;  // status, n_long
+  // pairs: emitted (tile, splat) and the bucketed per-tile lists
+  uint32_t* ptile = nullptr;
+  size_t cap_ptile = 0;
+  uint32_t* psplat = nullptr;
+  size_t cap_psplat = 0;
+  uint32_t* pbucket = nullptr;
+  size_t cap_pbucket = 0;
+  int* pairs = nullptr;  // == pbucket: final per-tile lists
+  unsigned* bitmask = nullptr;
+  size_t cap_bitmask = 0;
+  int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long
   size_t cap_misc = 0;
   long long* totals = nullptr;
   size_t cap_totals = 0;
-  int* pairs = nullptr;
-  size_t cap_pairs = 0;
-  int* tmp = nullptr;
-  size_t cap_tmp = 0;
-  unsigned* bitmask = nullptr;
-  size_t cap_bitmask = 0;
+  // per pixel
   float* Tf = nullptr;
   size_t cap_Tf = 0;
   int* last = nullptr;
   size_t cap_last = 0;
   float* acc = nullptr;
   size_t cap_acc = 0;
-  long long* h_totals = nullptr;  // pinned: totals[2], status
+  long long* h_totals = nullptr;  // pinned: totals[2], status, overflow
+  cudaEvent_t done = nullptr;
   // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -161,7 +180,7 @@ struct StageTimer {
     }
   }
 };
-enum { ST_PREPROCESS, ST_SCAN, ST_SCATTER, ST_SORT, ST_SORT_LONG, ST_FORWARD, ST_BACKWARD, ST_FINALIZE, ST_COUNT };
+enum { ST_PREPROCESS, ST_EMIT, ST_BUCKET, ST_TILE_SORT, ST_UNUSED, ST_FORWARD, ST_BACKWARD, ST_FINALIZE, ST_COUNT };
 
 __global__ void k_count_contrib(long long nwords, const unsigned* __restrict__ bm, unsigned long long* out) {
   unsigned long long c = 0;
@@ -170,11 +189,20 @@ __global__ void k_count_contrib(long long nwords, const unsigned* __restrict__ b
   for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
   if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
 }
+
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  const int bytes = (int)(sizeof(uint32_t) * kMaxTiles);
+  cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = true;
+}
 }  // namespace
 
 extern "C" {
 
-const char* ss_version(void) { return "paper_2503_17491_b200 0.1 (sm_100a)"; }
+const char* ss_version(void) { return "paper_2503_17491_b200 0.2 (sm_100a)"; }
 
 ss_records* ss_records_create(void) {
   ss_records* r = new (std::nothrow) ss_records();
@@ -183,29 +211,31 @@ ss_records* ss_records_create(void) {
     delete r;
     return nullptr;
   }
+  cudaEventCreateWithFlags(&r->done, cudaEventDisableTiming);
   return r;
 }
 
 void ss_records_destroy(ss_records* r, void* stream) {
   if (!r) return;
   cudaStream_t s = (cudaStream_t)stream;
-  void* bufs[] = {r->rec, r->rec64, r->key, r->rect, r->tiles, r->misc, r->totals, r->pairs,
-                  r->tmp, r->bitmask, r->Tf, r->last, r->acc};
+  void* bufs[] = {r->rec,    r->rec64,   r->key64, r->key32,  r->rect, r->bsum, r->mat, r->tint,
+                  r->tiles,  r->ptile,   r->psplat, r->pbucket, r->bitmask, r->misc, r->totals,
+                  r->Tf,     r->last,    r->acc};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, s);
   cudaStreamSynchronize(s);
   for (auto& u : r->ev_used) {
     cudaEventDestroy(u.second.first);
     cudaEventDestroy(u.second.second);
   }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
-  for (void* b : bufs)
-    if (b) cudaFreeAsync(b, s);
-  if (r->h_totals) {
-    cudaStreamSynchronize(s);
-    cudaFreeHost(r->h_totals);
-  }
+  if (r->done) cudaEventDestroy(r->done);
+  if (r->h_totals) cudaFreeHost(r->h_totals);
   delete r;
 }
 
+// Enqueue a complete forward render; no host synchronisation.  The caller
+// checks capacity with ss_records_check (and re-runs on SS_ERR_CAPACITY).
 int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_splats* splats, const ss_raster_cfg* cfg,
                       float* out_range, float* out_normal, float* out_opacity, ss_records* rec, void* stream) {
   if (!cam || !pose_Rt || !splats || !cfg || !rec || !out_range || !out_normal || !out_opacity)
@@ -216,6 +246,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int st = make_camk(cam, cfg->tile_size, cfg->bbox_pad_px, k);
   if (st) return st;
   rec->valid = 0;
+  rec->pending = 1;
   rec->cam = k;
   for (int q = 0; q < 9; ++q) rec->pose.R[q] = pose_Rt[q];
   for (int q = 0; q < 3; ++q) rec->pose.t[q] = pose_Rt[9 + q];
@@ -228,80 +259,120 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   const int n = splats->n;
   const int ntiles = k.tx * k.ty;
   const size_t P = (size_t)k.W * k.H;
+  const int TT = k.T * k.T;
   rec->n = n;
   rec->ntiles = ntiles;
+  long long cap = std::max<long long>(rec->want_pairs, std::max<long long>(8LL * n, 65536));
+  if (cap > 0x7fff0000LL) cap = 0x7fff0000LL;
+  rec->cap_pairs = cap;
+  const int nb = (n + 255) / 256;
+  if (ntiles > kMaxTiles) return SS_ERR_UNSUPPORTED;
+  const int pblocks = (int)((cap + kPairChunk - 1) / kPairChunk);
   if (grow(rec->rec, rec->cap_rec, (size_t)n + 1, s) || grow(rec->rec64, rec->cap_rec64, (size_t)n + 1, s) ||
-      grow(rec->key, rec->cap_key, (size_t)n + 1, s) || grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) ||
-      grow(rec->tiles, rec->cap_tiles, (size_t)5 * (ntiles + 1), s) || grow(rec->misc, rec->cap_misc, 4, s) ||
-      grow(rec->totals, rec->cap_totals, 2, s) || grow(rec->Tf, rec->cap_Tf, P, s) ||
-      grow(rec->last, rec->cap_last, P, s))
+      grow(rec->key64, rec->cap_key64, (size_t)n + 1, s) || grow(rec->key32, rec->cap_key32, (size_t)n + 1, s) ||
+      grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) || grow(rec->bsum, rec->cap_bsum, (size_t)nb + 1, s) ||
+      grow(rec->mat, rec->cap_mat, (size_t)pblocks * ntiles, s) ||
+      grow(rec->tint, rec->cap_tint, (size_t)(k.tx + k.ty), s) ||
+      grow(rec->tiles, rec->cap_tiles, (size_t)5 * (ntiles + 1), s) ||
+      grow(rec->ptile, rec->cap_ptile, (size_t)cap, s) || grow(rec->psplat, rec->cap_psplat, (size_t)cap, s) ||
+      grow(rec->pbucket, rec->cap_pbucket, (size_t)cap, s) ||
+      grow(rec->bitmask, rec->cap_bitmask, ((size_t)cap / 32 + ntiles + 1) * TT, s) ||
+      grow(rec->misc, rec->cap_misc, 16, s) || grow(rec->totals, rec->cap_totals, 2, s) ||
+      grow(rec->Tf, rec->cap_Tf, P, s) || grow(rec->last, rec->cap_last, P, s))
     return SS_ERR_CUDA;
-  int* tile_count = rec->tiles;
-  int* tile_ptr = rec->tiles + (ntiles + 1);
-  int* chunk_ptr = rec->tiles + 2 * (ntiles + 1);
-  int* cursor = rec->tiles + 3 * (ntiles + 1);
+  int* tile_ptr = rec->tiles;
+  int* chunk_ptr = rec->tiles + (ntiles + 1);
+  int* tile_count = rec->tiles + 2 * (ntiles + 1);
   int* long_list = rec->tiles + 4 * (ntiles + 1);
   int* status = rec->misc;
-  int* n_long = rec->misc + 1;
+  int* overflow = rec->misc + 1;
+  int* n_long = rec->misc + 2;
+  double2* colt = rec->tint;
+  double2* rowt = rec->tint + k.tx;
+  SS_CUDA_TRY(cudaMemsetAsync(rec->misc, 0, sizeof(int) * 16, s));
+  SS_CUDA_TRY(cudaMemsetAsync(rec->totals, 0, sizeof(long long) * 2, s));
   SS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(int) * ntiles, s));
-  SS_CUDA_TRY(cudaMemsetAsync(rec->misc, 0, sizeof(int) * 4, s));
   PoseK pk = rec->pose;
   SplatsK sk = to_k(splats);
-  if (n > 0) {
+  {
     StageTimer tm(rec, ST_PREPROCESS, s);
-    k_preprocess<<<(n + 255) / 256, 256, 0, s>>>(sk, pk, k, rk, rec->rec, rec->rec64, rec->key, rec->rect, tile_count,
-                                                  status);
-    SS_CUDA_TRY(cudaGetLastError());
+    k_tile_intervals<<<(k.tx + k.ty + 127) / 128, 128, 0, s>>>(k, colt, rowt);
+    if (n > 0)
+      k_preprocess<<<nb, 256, 0, s>>>(sk, pk, k, rk, colt, rowt, rec->rec, rec->rec64, rec->key64, rec->key32,
+                                      rec->rect, rec->bsum, status);
+  }
+  if (n > 0) {
+    StageTimer tm(rec, ST_EMIT, s);
+    k_scan_blocks<<<1, 1024, 0, s>>>(nb, rec->bsum, rec->totals);
+    k_emit<<<nb, 256, 0, s>>>(n, rec->rect, rec->bsum, k.tx, cap, rec->ptile, rec->psplat, overflow);
   }
   {
-    StageTimer tm(rec, ST_SCAN, s);
-    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, cursor, rec->totals);
+    StageTimer tm(rec, ST_BUCKET, s);
+    const size_t hsm = sizeof(uint32_t) * ntiles;
+    set_smem_attrs();
+    k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow);
+    k_tile_prefix<<<(ntiles + 255) / 256, 256, 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count);
+    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals);
+    k_tile_scatter<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
+                                              rec->pbucket, overflow);
+  }
+  {
+    StageTimer tm(rec, ST_TILE_SORT, s);
+    k_tile_sort<<<ntiles, 256, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
+    k_sort_long<<<16, 512, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key64, long_list, n_long);
+  }
+  rec->pairs = (int*)rec->pbucket;
+  const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  {
+    StageTimer tmf(rec, ST_FORWARD, s);
+    if (k.T == 8)
+      k_forward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                          rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+                                                          rec->last, rec->bitmask, overflow);
+    else
+      k_forward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+                                                           rec->last, rec->bitmask, overflow);
   }
   SS_CUDA_TRY(cudaGetLastError());
   SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals, rec->totals, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals + 2, status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SS_CUDA_TRY(cudaStreamSynchronize(s));
-  int dev_status = *(int*)(rec->h_totals + 2);
-  if (dev_status) return dev_status;
+  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals + 2, rec->misc, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaEventRecord(rec->done, s));
+  return SS_OK;
+}
+
+// Completes a forward: waits (wait=1) or polls (wait=0, SS_ERR_CAPACITY
+// never raised before completion) for its counters.  Returns SS_ERR_CAPACITY
+// when the speculative pair capacity was too small (the next forward on
+// these records will allocate enough; re-run it), or the device status.
+int ss_records_check(ss_records* rec, int wait) {
+  if (!rec) return SS_ERR_INVALID_ARGUMENT;
+  if (!rec->pending) return rec->valid ? SS_OK : SS_ERR_STALE_RECORDS;
+  if (wait) {
+    SS_CUDA_TRY(cudaEventSynchronize(rec->done));
+  } else if (cudaEventQuery(rec->done) != cudaSuccess) {
+    return SS_OK;
+  }
+  rec->pending = 0;
+  const int dev_status = ((int*)(rec->h_totals + 2))[0];
+  const int overflow = ((int*)(rec->h_totals + 2))[1];
   rec->n_pairs = rec->h_totals[0];
   rec->n_chunks = rec->h_totals[1];
-  if (rec->n_pairs > 0x7fffffffLL) return SS_ERR_CAPACITY;
-  const int TT = k.T * k.T;
-  if (grow(rec->pairs, rec->cap_pairs, (size_t)rec->n_pairs + 1, s) ||
-      grow(rec->tmp, rec->cap_tmp, (size_t)rec->n_pairs + 1, s) ||
-      grow(rec->bitmask, rec->cap_bitmask, (size_t)rec->n_chunks * TT + 1, s))
-    return SS_ERR_CUDA;
-  if (n > 0 && rec->n_pairs > 0) {
-    {
-      StageTimer tm(rec, ST_SCATTER, s);
-      k_scatter_pairs<<<(n + 255) / 256, 256, 0, s>>>(n, k.tx, rec->rect, cursor, rec->pairs);
-    }
-    {
-      StageTimer tm(rec, ST_SORT, s);
-      k_sort_tiles<<<ntiles, 256, 0, s>>>(tile_ptr, rec->pairs, rec->key, long_list, n_long);
-    }
-    {
-      StageTimer tm(rec, ST_SORT_LONG, s);
-      k_sort_long<<<32, 512, 0, s>>>(tile_ptr, rec->pairs, rec->tmp, rec->key, long_list, n_long);
-    }
-    SS_CUDA_TRY(cudaGetLastError());
+  if (dev_status) return dev_status;
+  if (overflow || rec->n_pairs > rec->cap_pairs) {
+    rec->want_pairs = rec->n_pairs + rec->n_pairs / 4 + 1024;
+    return SS_ERR_CAPACITY;
   }
-  const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  StageTimer tmf(rec, ST_FORWARD, s);
-  if (k.T == 8)
-    k_forward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
-                                                        rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                        rec->last, rec->bitmask);
-  else
-    k_forward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
-                                                         rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                         rec->last, rec->bitmask);
-  SS_CUDA_TRY(cudaGetLastError());
+  rec->want_pairs = std::max(rec->want_pairs, rec->n_pairs + rec->n_pairs / 8);
   rec->valid = 1;
   return SS_OK;
 }
 
 int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y) {
+  if (rec && rec->pending) {
+    int cs = ss_records_check(const_cast<ss_records*>(rec), 1);
+    if (cs) return cs;
+  }
   if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
   if (n_pairs) *n_pairs = rec->n_pairs;
   if (tiles_x) *tiles_x = rec->cam.tx;
@@ -310,10 +381,14 @@ int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x,
 }
 
 int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_splats, void* stream) {
+  if (rec && rec->pending) {
+    int cs = ss_records_check(const_cast<ss_records*>(rec), 1);
+    if (cs) return cs;
+  }
   if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
   cudaStream_t s = (cudaStream_t)stream;
   int nt = rec->ntiles + 1;
-  if (tile_ptr) k_widen_i32<<<(nt + 255) / 256, 256, 0, s>>>(nt, rec->tiles + (rec->ntiles + 1), (long long*)tile_ptr);
+  if (tile_ptr) k_widen_i32<<<(nt + 255) / 256, 256, 0, s>>>(nt, rec->tiles, (long long*)tile_ptr);
   if (pair_splats && rec->n_pairs > 0)
     k_widen_i32<<<(int)((rec->n_pairs + 255) / 256), 256, 0, s>>>((int)rec->n_pairs, rec->pairs,
                                                                    (long long*)pair_splats);
@@ -324,7 +399,12 @@ int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_sp
 int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const float* dD, const float* dN,
                        const float* dO, const float* d_scales_extra, float* grads, int raw_space, void* stream) {
   ss_records* rec = const_cast<ss_records*>(rec_c);
-  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  if (!rec) return SS_ERR_STALE_RECORDS;
+  if (rec->pending) {
+    int cs = ss_records_check(rec, 0);  // stream order covers a forward still in flight
+    if (cs) return cs;
+  }
+  if (!rec->pending && !rec->valid) return SS_ERR_STALE_RECORDS;
   if (!splats || splats->n != rec->n) return SS_ERR_STALE_RECORDS;
   if (!dD || !dN || !dO || !grads) return SS_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -333,19 +413,19 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   if (grow(rec->acc, rec->cap_acc, (size_t)n * kAcc, s)) return SS_ERR_CUDA;
   SS_CUDA_TRY(cudaMemsetAsync(rec->acc, 0, sizeof(float) * (size_t)n * kAcc, s));
   const int ntiles = rec->ntiles;
-  const int* tile_ptr = rec->tiles + (ntiles + 1);
-  const int* chunk_ptr = rec->tiles + 2 * (ntiles + 1);
-  if (rec->n_pairs > 0) {
+  const int* tile_ptr = rec->tiles;
+  const int* chunk_ptr = rec->tiles + (ntiles + 1);
+  {
     const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
     StageTimer tm(rec, ST_BACKWARD, s);
     if (rec->cam.T == 8)
       k_backward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                           rec->acc);
+                                                           rec->acc, rec->misc + 1);
     else
       k_backward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-                                                            dN, dO, rec->acc);
+                                                            dN, dO, rec->acc, rec->misc + 1);
     SS_CUDA_TRY(cudaGetLastError());
   }
   {
@@ -411,11 +491,15 @@ int ss_records_stage_times(ss_records* rec, double* ms, int32_t* launches, int32
 }
 
 int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contributions, void* stream) {
+  if (rec && rec->pending) {
+    int cs = ss_records_check(const_cast<ss_records*>(rec), 1);
+    if (cs) return cs;
+  }
   if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
   cudaStream_t s = (cudaStream_t)stream;
   // E = sum over tiles of (pixels in the tile) x (list length), U = popcount of the contribution masks
   std::vector<int> tp(rec->ntiles + 1);
-  SS_CUDA_TRY(cudaMemcpyAsync(tp.data(), rec->tiles + (rec->ntiles + 1), sizeof(int) * (rec->ntiles + 1),
+  SS_CUDA_TRY(cudaMemcpyAsync(tp.data(), rec->tiles, sizeof(int) * (rec->ntiles + 1),
                               cudaMemcpyDeviceToHost, s));
   unsigned long long* d_u = nullptr;
   SS_CUDA_TRY(cudaMallocAsync((void**)&d_u, sizeof(unsigned long long), s));
@@ -445,8 +529,8 @@ int ss_mapping_loss(int32_t width, int32_t height, const float* range, const flo
   if (width <= 0 || height <= 0) return SS_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   int P = width * height;
-  int blocks = (P + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  int blocks = (P + 1023) / 1024;
+  if (blocks > 148 * 2) blocks = 148 * 2;
   k_mapping_loss<<<blocks, 256, 0, s>>>(P, range, normal, opacity, kf_range, kf_valid, kf_normal, kf_nvalid,
                                         w_opacity, w_normal, range_floor, dD, dN, dO, parts4);
   SS_CUDA_TRY(cudaGetLastError());

@@ -21,10 +21,12 @@ __global__ void k_mapping_loss(int P, const float* __restrict__ D, const float* 
       double diff = (double)D[p] - kr;
       ld += w * fabs(diff);
       gd = (float)(diff > 0 ? w : (diff < 0 ? -w : 0.0));
-      double o = O[p];
-      double cl = fmax(o, 1e-6);
-      lo += -log(cl);
-      if (o > 1e-6) go = (float)(w_opacity * (-1.0 / cl));
+      if (w_opacity != 0.0) {
+        double o = O[p];
+        double cl = fmax(o, 1e-6);
+        lo += -log(cl);
+        if (o > 1e-6) go = (float)(w_opacity * (-1.0 / cl));
+      }
       if (kf_nvalid[p]) {
         double n0 = kf_normal[3 * p], n1 = kf_normal[3 * p + 1], n2 = kf_normal[3 * p + 2];
         ln += 1.0 - ((double)N[3 * p] * n0 + (double)N[3 * p + 1] * n1 + (double)N[3 * p + 2] * n2);
@@ -44,10 +46,18 @@ __global__ void k_mapping_loss(int P, const float* __restrict__ D, const float* 
     lo += __shfl_xor_sync(0xffffffffu, lo, off);
     ln += __shfl_xor_sync(0xffffffffu, ln, off);
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&parts[0], ld);
-    atomicAdd(&parts[1], lo);
-    atomicAdd(&parts[2], ln);
+  __shared__ double red[3][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = ld;
+    red[1][warp] = lo;
+    red[2][warp] = ln;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[threadIdx.x][w];
+    atomicAdd(&parts[threadIdx.x], s);
   }
 }
 

@@ -81,6 +81,10 @@ class Records:
     def release(self) -> None:
         Records._pool.append(self)
 
+    def check(self, wait: bool = True) -> int:
+        """Status of the last forward (SS_ERR_CAPACITY means: re-run it)."""
+        return int(lib().ss_records_check(self.ptr, int(bool(wait))))
+
     def counts(self):
         n = ctypes.c_int64(0)
         tx = ctypes.c_int32(0)
@@ -107,21 +111,37 @@ class Records:
             pass
 
 
-def forward(cam, pose_rt: np.ndarray, splats: dict, cfg, records: Records):
-    """Render; returns (range [H,W], normal [H,W,3], opacity [H,W]) float32 device tensors."""
+def forward(cam, pose_rt: np.ndarray, splats: dict, cfg, records: Records, sync: bool = True, out=None):
+    """Render; returns (range [H,W], normal [H,W,3], opacity [H,W]) float32 device tensors.
+
+    The C-ABI forward is fully stream-ordered with a speculative pair
+    capacity.  With ``sync`` (default) the call waits for completion and
+    transparently re-runs when the capacity was too small; with
+    ``sync=False`` the caller must call ``records.check()`` before trusting
+    the outputs (bench / CUDA-graph loops)."""
     dev = require_cuda()
     H, W = int(cam.height), int(cam.width)
-    D = torch.empty((H, W), dtype=torch.float32, device=dev)
-    N = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
-    O = torch.empty((H, W), dtype=torch.float32, device=dev)
+    if out is None:
+        D = torch.empty((H, W), dtype=torch.float32, device=dev)
+        N = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+        O = torch.empty((H, W), dtype=torch.float32, device=dev)
+    else:
+        D, N, O = out
     c = ss_camera(cam)
     sp = ss_splats(splats)
     k = ss_cfg(cfg)
     prt = np.ascontiguousarray(pose_rt, dtype=np.float64)
-    st = lib().ss_render_forward(ctypes.byref(c), prt.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sp),
-                                 ctypes.byref(k), ctypes.c_void_p(D.data_ptr()), ctypes.c_void_p(N.data_ptr()),
-                                 ctypes.c_void_p(O.data_ptr()), records.ptr, ctypes.c_void_p(stream_ptr()))
-    check(st, "rasterize_forward")
+    for _attempt in range(4):
+        st = lib().ss_render_forward(ctypes.byref(c), prt.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sp),
+                                     ctypes.byref(k), ctypes.c_void_p(D.data_ptr()), ctypes.c_void_p(N.data_ptr()),
+                                     ctypes.c_void_p(O.data_ptr()), records.ptr, ctypes.c_void_p(stream_ptr()))
+        check(st, "rasterize_forward")
+        if not sync:
+            break
+        st = records.check(wait=True)
+        if st != _lib.SS_ERR_CAPACITY:
+            check(st, "rasterize_forward")
+            break
     return D, N, O
 
 

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+rc=$?
+tail -5 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py ${@} > gpurun_out/bench.log 2>&1
+tail -3 gpurun_out/bench.log
+exit $rc
