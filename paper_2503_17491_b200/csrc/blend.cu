@@ -130,6 +130,66 @@ __device__ __forceinline__ void stage_entry(float* dst, int sid, const SplatRec*
   d2[4] = make_double2(C[2], 0.0);
 }
 
+// Backward staging: only what the exact intersection and the gradient need.
+__device__ __forceinline__ void stage_entry_bwd(float* dst, int sid, const SplatRec* __restrict__ rec,
+                                                const SplatRec64* __restrict__ rec64) {
+  const float4 p0 = __ldg(&rec[sid].r0);
+  const float4 p1 = __ldg(&rec[sid].r1);
+  double B[10];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    double2 x = __ldg(&rec64[sid].v[q]);
+    B[2 * q] = x.x;
+    B[2 * q + 1] = x.y;
+  }
+  const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
+  double A[3], Bv[3], C[3];
+  cross3(Bb, Bc, A);
+  cross3(Bc, Ba, Bv);
+  cross3(Ba, Bb, C);
+  const double det = dot3d(Bc, C);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  d4[2] = make_float4(0.f, 0.f, p0.x, (float)det);
+  d4[3] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
+  double2* d2 = reinterpret_cast<double2*>(dst + 16);
+  d2[0] = make_double2(A[0], A[1]);
+  d2[1] = make_double2(A[2], Bv[0]);
+  d2[2] = make_double2(Bv[1], Bv[2]);
+  d2[3] = make_double2(C[0], C[1]);
+  d2[4] = make_double2(C[2], 0.0);
+}
+
+// Butterfly reduce-scatter of 16 per-lane values across the warp: afterwards
+// lane l holds the warp sum of value index ((l >> 1) & 15) (lanes l, l^1 agree).
+__device__ __forceinline__ float warp_reduce_scatter16(float (&a)[16], int lane) {
+  const bool hi4 = lane & 16, hi3 = lane & 8, hi2 = lane & 4, hi1 = lane & 2;
+  float b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = hi4 ? a[i] : a[8 + i];
+    const float keep = hi4 ? a[8 + i] : a[i];
+    b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = hi3 ? b[i] : b[4 + i];
+    const float keep = hi3 ? b[4 + i] : b[i];
+    c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float d[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = hi2 ? c[i] : c[2 + i];
+    const float keep = hi2 ? c[2 + i] : c[i];
+    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const float send = hi1 ? d[0] : d[1];
+  const float keep = hi1 ? d[1] : d[0];
+  float e = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  return e + __shfl_xor_sync(0xffffffffu, e, 1);
+}
+
 struct Entry {
   double A[3], Bv[3], C[3];
   float o, det, n[3];
@@ -284,7 +344,7 @@ constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
 constexpr int kRedStride = 15;
 
 template <int TS>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? 5 : 1)
     k_backward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
                const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
                const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
@@ -293,7 +353,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
-  __shared__ float red[kWarpsPerBlock][32 * kRedStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * kWarpsPerBlock + warp;
   if (t >= ntiles) return;
@@ -329,7 +388,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int lo = tile_ptr[t];
   const int cbase = chunk_ptr[t];
   float* st = stage[warp];
-  float* rw = red[warp];
   for (int chunk = (maxlast - 1) >> 5; chunk >= 0; --chunk) {
     const int base = chunk * 32;
     unsigned word[PPL];
@@ -341,16 +399,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     unsigned any = __reduce_or_sync(0xffffffffu, mine);
     if (!any) continue;
-    if ((any >> lane) & 1u) stage_entry(st + lane * kStride, pairs[lo + base + lane], rec, rec64, vt, 0.f);
+    if ((any >> lane) & 1u) stage_entry_bwd(st + lane * kStride, pairs[lo + base + lane], rec, rec64);
     __syncwarp();
     while (any) {
       const int i = 31 - __clz(any);
       any &= ~(1u << i);
       Entry x;
       load_entry(st + i * kStride, x);
-      float a[14];
+      float a[16];
 #pragma unroll
-      for (int q = 0; q < 14; ++q) a[q] = 0.f;
+      for (int q = 0; q < 16; ++q) a[q] = 0.f;
       bool act = false;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
@@ -388,24 +446,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         Sn[j][2] += w * x.n[2];
         T[j] = Tb;
       }
-      const unsigned m = __ballot_sync(0xffffffffu, act);
-      if (act) {
-#pragma unroll
-        for (int q = 0; q < 14; ++q) rw[lane * kRedStride + q] = a[q];
-      }
-      __syncwarp();
-      if (lane < 14) {
-        float s = 0.f;
-        unsigned mm = m;
-        while (mm) {
-          const int l = __ffs(mm) - 1;
-          mm &= mm - 1;
-          s += rw[l * kRedStride + lane];
-        }
-        atomicAdd(&acc[(size_t)x.sid * kAcc + lane], s);
-      }
-      __syncwarp();
+      (void)act;
+      const float tot = warp_reduce_scatter16(a, lane);
+      const int vi = (lane >> 1) & 15;
+      if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
     }
+    __syncwarp();
   }
 }
 
