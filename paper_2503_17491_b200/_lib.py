@@ -10,7 +10,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplatb200.so")
+LIB_PATH = os.environ.get("SPLAT_B200_LIB", os.path.join(_HERE, "libsplatb200.so"))  # env: A/B builds
 CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 

@@ -613,6 +613,42 @@ __global__ void k_sort_long(const int* __restrict__ tile_ptr, uint32_t* __restri
   }
 }
 
+// Tile processing order for the blend kernels: longest lists first (the
+// kernels fetch tiles dynamically, so this is longest-processing-time-first
+// scheduling).  Counting sort on min(L, 4095) / 4, one block.
+__global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_ptr,
+                                                     int* __restrict__ order, int* __restrict__ counters) {
+  __shared__ int hist[1024];
+  const int tid = threadIdx.x;
+  hist[tid] = 0;
+  if (tid < 4) counters[tid] = 0;
+  __syncthreads();
+  for (int t = tid; t < ntiles; t += 1024) {
+    const int L = tile_ptr[t + 1] - tile_ptr[t];
+    atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1);
+  }
+  __syncthreads();
+  // exclusive scan of hist (bucket 0 = longest)
+  const int v = hist[tid];
+  int inc = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, off);
+    if ((tid & 31) >= off) inc += y;
+  }
+  __shared__ int wsum[32];
+  if ((tid & 31) == 31) wsum[tid >> 5] = inc;
+  __syncthreads();
+  int wex = 0;
+  for (int w = 0; w < (tid >> 5); ++w) wex += wsum[w];
+  __syncthreads();
+  hist[tid] = wex + inc - v;
+  __syncthreads();
+  for (int t = tid; t < ntiles; t += 1024) {
+    const int L = tile_ptr[t + 1] - tile_ptr[t];
+    order[atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1)] = t;
+  }
+}
+
 __global__ void k_widen_i32(int n, const int* __restrict__ in, long long* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[i];

@@ -29,6 +29,12 @@
 namespace ss {
 
 constexpr int kWarpsPerBlock = 4;
+#ifndef SS_FWD_MINB
+#define SS_FWD_MINB 5
+#endif
+#ifndef SS_BWD_MINB
+#define SS_BWD_MINB 5
+#endif
 constexpr int kStride = 36;  // 32-bit words per staged entry: 16 floats + 5 double2 (144 B)
 
 struct BlendParams {
@@ -241,19 +247,24 @@ __device__ __forceinline__ void intersect(const Entry& x, const double v[3], boo
 }
 
 template <int TS>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1)
     k_forward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
               const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
               float* __restrict__ out_D, float* __restrict__ out_N, float* __restrict__ out_O,
               float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask,
-              const int* __restrict__ overflow) {
+              const int* __restrict__ overflow, const int* __restrict__ order, int* __restrict__ counter) {
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;  // pair capacity exceeded: the host re-runs the render
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kWarpsPerBlock + warp;
-  if (t >= ntiles) return;
   const CamK& k = bp.cam;
+  // persistent warps: fetch tiles longest-first until none are left
+  while (true) {
+  int ti = 0;
+  if (lane == 0) ti = atomicAdd(counter, 1);
+  ti = __shfl_sync(0xffffffffu, ti, 0);
+  if (ti >= ntiles) return;
+  const int t = order[ti];
   const int tr = t / k.tx, tc = t % k.tx;
   double vt[3];
   tile_center<TS>(k, tr, tc, vt);
@@ -285,41 +296,73 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     unsigned word[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) word[j] = 0u;
-    for (int i = 0; i < cnt; ++i) {
-      const float* e = st + i * kStride;
-      const float4 f0 = *reinterpret_cast<const float4*>(e);
-      const float4 f1 = *reinterpret_cast<const float4*>(e + 4);
-      const float4 f2 = *reinterpret_cast<const float4*>(e + 8);
-      bool cand[PPL];
-      bool anyc = false;
+    // two entries per iteration: four independent cone-test chains in flight
+    for (int i = 0; i < cnt; i += 2) {
+      const bool has2 = i + 1 < cnt;
+      const float* e0 = st + i * kStride;
+      const float* e1 = st + (has2 ? i + 1 : i) * kStride;
+      const float4 a0 = *reinterpret_cast<const float4*>(e0);
+      const float4 a1 = *reinterpret_cast<const float4*>(e0 + 4);
+      const float4 a2 = *reinterpret_cast<const float4*>(e0 + 8);
+      const float4 b0 = *reinterpret_cast<const float4*>(e1);
+      const float4 b1 = *reinterpret_cast<const float4*>(e1 + 4);
+      const float4 b2 = *reinterpret_cast<const float4*>(e1 + 8);
+      bool ca[PPL], cb[PPL];
+      bool anya = false, anyb = false;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         const float* d = px[j].d;
         const float* pp = px[j].pp;
-        float q = f0.x + f0.y * d[0] + f0.z * d[1] + f0.w * d[2] + f1.x * pp[0] + f1.y * pp[1] + f1.z * pp[2] +
-                  f1.w * pp[3] + f2.x * pp[4] + f2.y * pp[5];
-        cand[j] = live[j] && q <= 0.f;
-        anyc |= cand[j];
+        const float qa = (a0.x + a0.y * d[0] + a0.z * d[1] + a0.w * d[2]) +
+                         (a1.x * pp[0] + a1.y * pp[1] + a1.z * pp[2] + a1.w * pp[3] + a2.x * pp[4] + a2.y * pp[5]);
+        const float qb = (b0.x + b0.y * d[0] + b0.z * d[1] + b0.w * d[2]) +
+                         (b1.x * pp[0] + b1.y * pp[1] + b1.z * pp[2] + b1.w * pp[3] + b2.x * pp[4] + b2.y * pp[5]);
+        ca[j] = live[j] && qa <= 0.f;
+        cb[j] = has2 && qb <= 0.f;
+        anya |= ca[j];
+        anyb |= cb[j];
       }
-      if (!anyc) continue;
-      Entry x;
-      load_entry(e, x);
+      if (anya) {
+        Entry x;
+        load_entry(e0, x);
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) {
-        if (!cand[j]) continue;
-        Hit h;
-        intersect(x, px[j].v, px[j].ray_ok, bp, h);
-        if (!h.use) continue;
-        float w = h.alpha * T[j];
-        D[j] += w * h.lam;
-        O[j] += w;
-        N[j][0] += w * x.n[0];
-        N[j][1] += w * x.n[1];
-        N[j][2] += w * x.n[2];
-        T[j] *= (1.f - h.alpha);
-        word[j] |= 1u << i;
-        last[j] = base + i + 1;
-        if (T[j] < bp.min_T) live[j] = false;
+        for (int j = 0; j < PPL; ++j) {
+          if (!ca[j]) continue;
+          Hit h;
+          intersect(x, px[j].v, px[j].ray_ok, bp, h);
+          if (!h.use) continue;
+          const float w = h.alpha * T[j];
+          D[j] += w * h.lam;
+          O[j] += w;
+          N[j][0] += w * x.n[0];
+          N[j][1] += w * x.n[1];
+          N[j][2] += w * x.n[2];
+          T[j] *= (1.f - h.alpha);
+          word[j] |= 1u << i;
+          last[j] = base + i + 1;
+          if (T[j] < bp.min_T) live[j] = false;
+        }
+      }
+      if (anyb) {
+        Entry x;
+        load_entry(e1, x);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          if (!(cb[j] && live[j])) continue;  // the pixel may have saturated at entry i
+          Hit h;
+          intersect(x, px[j].v, px[j].ray_ok, bp, h);
+          if (!h.use) continue;
+          const float w = h.alpha * T[j];
+          D[j] += w * h.lam;
+          O[j] += w;
+          N[j][0] += w * x.n[0];
+          N[j][1] += w * x.n[1];
+          N[j][2] += w * x.n[2];
+          T[j] *= (1.f - h.alpha);
+          word[j] |= 1u << (i + 1);
+          last[j] = base + i + 2;
+          if (T[j] < bp.min_T) live[j] = false;
+        }
       }
     }
 #pragma unroll
@@ -338,25 +381,31 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     out_T[p] = T[j];
     out_last[p] = last[j];
   }
+  }
 }
 
 constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
 constexpr int kRedStride = 15;
 
 template <int TS>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? 5 : 1)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
     k_backward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
                const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
                const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
                const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
-               float* __restrict__ acc, const int* __restrict__ overflow) {
+               float* __restrict__ acc, const int* __restrict__ overflow, const int* __restrict__ order,
+               int* __restrict__ counter) {
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kWarpsPerBlock + warp;
-  if (t >= ntiles) return;
   const CamK& k = bp.cam;
+  while (true) {
+  int ti = 0;
+  if (lane == 0) ti = atomicAdd(counter, 1);
+  ti = __shfl_sync(0xffffffffu, ti, 0);
+  if (ti >= ntiles) return;
+  const int t = order[ti];
   const int tr = t / k.tx, tc = t % k.tx;
   double vt[3];
   tile_center<TS>(k, tr, tc, vt);
@@ -384,7 +433,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? 5 : 1)
     maxlast = max(maxlast, last[j]);
   }
   maxlast = __reduce_max_sync(0xffffffffu, maxlast);
-  if (maxlast == 0) return;
+  if (maxlast == 0) continue;
   const int lo = tile_ptr[t];
   const int cbase = chunk_ptr[t];
   float* st = stage[warp];
@@ -452,6 +501,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? 5 : 1)
       if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
     }
     __syncwarp();
+  }
   }
 }
 
@@ -563,14 +613,14 @@ __global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc
 }
 
 template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*);
+                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*, const int*, int*);
 template __global__ void k_forward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*);
+                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*, const int*, int*);
 template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                       const float*, const float*, float*, const int*);
+                                       const float*, const float*, float*, const int*, const int*, int*);
 template __global__ void k_backward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                         const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                        const float*, const float*, float*, const int*);
+                                        const float*, const float*, float*, const int*, const int*, int*);
 
 }  // namespace ss

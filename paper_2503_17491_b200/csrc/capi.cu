@@ -63,6 +63,17 @@ int grow(T*& ptr, size_t& cap, size_t need, cudaStream_t s) {
   return SS_OK;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 SplatsK to_k(const ss_splats* s) {
   SplatsK k;
   k.n = s->n;
@@ -273,7 +284,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) || grow(rec->bsum, rec->cap_bsum, (size_t)nb + 1, s) ||
       grow(rec->mat, rec->cap_mat, (size_t)pblocks * ntiles, s) ||
       grow(rec->tint, rec->cap_tint, (size_t)(k.tx + k.ty), s) ||
-      grow(rec->tiles, rec->cap_tiles, (size_t)5 * (ntiles + 1), s) ||
+      grow(rec->tiles, rec->cap_tiles, (size_t)6 * (ntiles + 1), s) ||
       grow(rec->ptile, rec->cap_ptile, (size_t)cap, s) || grow(rec->psplat, rec->cap_psplat, (size_t)cap, s) ||
       grow(rec->pbucket, rec->cap_pbucket, (size_t)cap, s) ||
       grow(rec->bitmask, rec->cap_bitmask, ((size_t)cap / 32 + ntiles + 1) * TT, s) ||
@@ -284,6 +295,8 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* chunk_ptr = rec->tiles + (ntiles + 1);
   int* tile_count = rec->tiles + 2 * (ntiles + 1);
   int* long_list = rec->tiles + 4 * (ntiles + 1);
+  int* order = rec->tiles + 5 * (ntiles + 1);
+  int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -320,19 +333,20 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     StageTimer tm(rec, ST_TILE_SORT, s);
     k_tile_sort<<<ntiles, 256, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
     k_sort_long<<<16, 512, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key64, long_list, n_long);
+    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order, counters);
   }
   rec->pairs = (int*)rec->pbucket;
-  const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
   {
     StageTimer tmf(rec, ST_FORWARD, s);
     if (k.T == 8)
       k_forward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                          rec->last, rec->bitmask, overflow);
+                                                          rec->last, rec->bitmask, overflow, order, counters);
     else
       k_forward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                           rec->last, rec->bitmask, overflow);
+                                                           rec->last, rec->bitmask, overflow, order, counters);
   }
   SS_CUDA_TRY(cudaGetLastError());
   SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals, rec->totals, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
@@ -416,16 +430,18 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   const int* tile_ptr = rec->tiles;
   const int* chunk_ptr = rec->tiles + (ntiles + 1);
   {
-    const int blocks = (ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
+    int* order = rec->tiles + 5 * (ntiles + 1);
+    int* counters = rec->misc + 4;
     StageTimer tm(rec, ST_BACKWARD, s);
     if (rec->cam.T == 8)
       k_backward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                           rec->acc, rec->misc + 1);
+                                                           rec->acc, rec->misc + 1, order, counters + 1);
     else
       k_backward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-                                                            dN, dO, rec->acc, rec->misc + 1);
+                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1);
     SS_CUDA_TRY(cudaGetLastError());
   }
   {

@@ -6,12 +6,20 @@ from collections import Counter
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+pick = sys.argv[3] if len(sys.argv) > 3 else None
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(txt.splitlines()))
 hdr = None
 ins = []
+take = pick is None
 for r in rows:
+    if r and r[0] == "Kernel Name":
+        take = pick is None or pick in r[1]
+        hdr = None
+        continue
+    if not take:
+        continue
     if r and r[0] == "Address":
         hdr = r
         continue
