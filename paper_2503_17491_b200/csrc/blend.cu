@@ -10,20 +10,30 @@
 // (h_x, h_y) with the splat.  With A = Bb x Bc, Bv = Bc x Ba, C = Ba x Bb the
 // same intersection is, by the Binet-Cauchy identity (h_x x h_y = -v),
 //     sa = (v.A)/(v.C),  sb = (v.Bv)/(v.C),  range = |nu| = det/(v.C),
-// det = Bc.C, den = -(v.C).  The cutoff alpha >= 1/255 is the quadratic cone
-// q(v) = (v.A)^2 + (v.Bv)^2 - K (v.C)^2 <= 0 with K = 2 ln(255 o).  To avoid
-// cancellation of v.A (|A| ~ s |Bc|) in float32, every product with A and Bv
-// is taken relative to the tile's centre ray v_t: v.A = c0 + d.A with
-// c0 = (v_t - u_c).A formed from the float64 difference of unit vectors.
+// det = Bc.C, den = -(v.C).  alpha >= 1/255 is the quadratic cone
+// q(v) = (v.A)^2 + (v.Bv)^2 - K (v.C)^2 <= 0 with K = 2 ln(255 o).
 //
-// Work decomposition: one warp per 8x8 tile (two pixels per lane), each warp
-// stages its tile list through shared memory 32 entries at a time.  The
-// forward records, per pixel, the final transmittance, the last contributing
-// list position and a bitmask of contributing entries; the backward walks the
-// list back to front (suffix sums accumulate, no total-minus-prefix
-// cancellation) visiting only entries some pixel of the tile contributed to,
-// and reduces each splat's 14 accumulators across the warp through shared
-// memory before one vector of float atomics.
+// Every tile gets an orthonormal frame (t = centre ray, e1 = azimuth, e2 =
+// elevation direction) and every pixel ray is v = w t + x e1 + y e2 (exact,
+// float64).  Per (tile, splat) pair the warp stages, in float64, the nine dot
+// products of (t, e1, e2) with (A, Bv, C); then
+//   * the cone test of a pixel is six float32 FMAs,
+//       q = w^2 q_tt + 2wx q_t1 + 2wy q_t2 + x^2 q_11 + 2xy q_12 + y^2 q_22,
+//     with q_tt lowered by a bound on the float32 rounding so the test never
+//     rejects a hit;
+//   * the exact intersection of a candidate pixel is three float64 3-term
+//     dot products (grazing splats amplify direction error by 1/|v.n|), the
+//     rest of the pair math is float32.
+//
+// Work decomposition: one warp per 8x8 tile (two pixels per lane), warps are
+// persistent and take tiles longest list first.  Each warp stages its tile
+// list through shared memory 32 entries at a time.  The forward records, per
+// pixel, the final transmittance, the last contributing list position and a
+// bitmask of contributing entries; the backward walks the list back to front
+// (suffix sums accumulate: no total-minus-prefix cancellation) visiting only
+// entries some pixel of the tile contributed to, and reduces each splat's 14
+// accumulators across the warp with a butterfly reduce-scatter before one
+// warp-wide float atomic.
 #include "common.cuh"
 
 namespace ss {
@@ -33,9 +43,11 @@ constexpr int kWarpsPerBlock = 4;
 #define SS_FWD_MINB 5
 #endif
 #ifndef SS_BWD_MINB
-#define SS_BWD_MINB 5
+#define SS_BWD_MINB 4
 #endif
-constexpr int kStride = 36;  // 32-bit words per staged entry: 16 floats + 5 double2 (144 B)
+// 32-bit words per staged entry: 12 floats (+4 spare) and 5 double2 (144 B).
+// The 144-byte stride keeps the staging lanes' 16-byte stores conflict-free.
+constexpr int kStride = 36;
 
 struct BlendParams {
   CamK cam;
@@ -47,104 +59,74 @@ struct TileShape {
   static constexpr int PPL = TS * TS / 32;  // pixels per lane
 };
 
-struct PixelGeo {
-  double v[3];   // unit sample ray (float64)
-  float d[3];    // v_p - v_t (float32 of a float64 difference)
-  float pp[6];   // d.x^2, d.y^2, d.z^2, 2dxdy, 2dxdz, 2dydz
-  int row, col;
-  bool inside;   // inside the image
-  bool ray_ok;   // reference ray_ok (rasterizer.py:167-168)
+// Orthonormal tile frame: centre ray t, azimuth direction e1, elevation direction e2.
+struct TileFrame {
+  double t[3], e1[3], e2[3];
 };
 
-template <int TS>
-__device__ __forceinline__ void tile_center(const CamK& k, int tr, int tc, double vt[3]) {
-  int r0 = tr * TS, c0 = tc * TS;
-  int rh = min(TS, k.H - r0), cw = min(TS, k.W - c0);
-  ray_at(k, (double)c0 + 0.5 * (cw - 1) + k.off_u, (double)r0 + 0.5 * (rh - 1) + k.off_v, vt);
-}
+struct Pix {
+  double w, x, y;  // v = w t + x e1 + y e2 (float64)
+  float p[6];      // w^2, 2wx, 2wy, x^2, 2xy, y^2
+  float vf[3];     // v, float32
+  int row, col;
+  bool inside;     // inside the image
+  bool ray_ok;     // reference ray_ok (rasterizer.py:167-168)
+};
 
-template <int TS>
-__device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, const double vt[3], PixelGeo& g) {
-  g.row = tr * TS + p / TS;
-  g.col = tc * TS + p % TS;
-  g.inside = g.row < k.H && g.col < k.W;
-  ray_at(k, (double)g.col + k.off_u, (double)g.row + k.off_v, g.v);
-  g.ray_ok = g.inside && sqrt(g.v[1] * g.v[1] + g.v[0] * g.v[0]) > 1e-9;
-  for (int c = 0; c < 3; ++c) g.d[c] = (float)(g.v[c] - vt[c]);
-  g.pp[0] = g.d[0] * g.d[0];
-  g.pp[1] = g.d[1] * g.d[1];
-  g.pp[2] = g.d[2] * g.d[2];
-  g.pp[3] = 2.f * g.d[0] * g.d[1];
-  g.pp[4] = 2.f * g.d[0] * g.d[2];
-  g.pp[5] = 2.f * g.d[1] * g.d[2];
-}
-
+__device__ __forceinline__ double dot3d(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 __device__ __forceinline__ void cross3(const double* a, const double* b, double* o) {
   o[0] = a[1] * b[2] - a[2] * b[1];
   o[1] = a[2] * b[0] - a[0] * b[2];
   o[2] = a[0] * b[1] - a[1] * b[0];
 }
-__device__ __forceinline__ double dot3d(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 
-// Stage one list entry (lane-parallel, float64 setup relative to the tile ray v_t):
-//   cheap cone test  q(v_t + d) = q0 + g.d + d^T Q d  (float32 coefficients, q0
-//   lowered by a rounding bound so the test never rejects a hit), and the
-//   float64 A, Bv, C for the exact intersection of candidate pixels.
-__device__ __forceinline__ void stage_entry(float* dst, int sid, const SplatRec* __restrict__ rec,
-                                            const SplatRec64* __restrict__ rec64, const double vt[3], float dmax) {
-  const float4 p0 = __ldg(&rec[sid].r0);
-  const float4 p1 = __ldg(&rec[sid].r1);
-  double B[10];
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    double2 x = __ldg(&rec64[sid].v[q]);
-    B[2 * q] = x.x;
-    B[2 * q + 1] = x.y;
-  }
-  const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
-  double A[3], Bv[3], C[3];
-  cross3(Bb, Bc, A);
-  cross3(Bc, Ba, Bv);
-  cross3(Ba, Bb, C);
-  const double det = dot3d(Bc, C);
-  const double K = (double)p0.y;
-  const double c0 = dot3d(vt, A), c1 = dot3d(vt, Bv), w2t = dot3d(vt, C);
-  const double q0 = c0 * c0 + c1 * c1 - K * w2t * w2t;
-  double g[3], Q[6];
-  for (int c = 0; c < 3; ++c) g[c] = 2.0 * (c0 * A[c] + c1 * Bv[c] - K * w2t * C[c]);
-  Q[0] = A[0] * A[0] + Bv[0] * Bv[0] - K * C[0] * C[0];
-  Q[1] = A[1] * A[1] + Bv[1] * Bv[1] - K * C[1] * C[1];
-  Q[2] = A[2] * A[2] + Bv[2] * Bv[2] - K * C[2] * C[2];
-  Q[3] = A[0] * A[1] + Bv[0] * Bv[1] - K * C[0] * C[1];
-  Q[4] = A[0] * A[2] + Bv[0] * Bv[2] - K * C[0] * C[2];
-  Q[5] = A[1] * A[2] + Bv[1] * Bv[2] - K * C[1] * C[2];
-  // magnitude of every term the float32 evaluation sums (bounds its rounding)
-  const double dm = dmax;
-  double E = fabs(q0) + (fabs(g[0]) + fabs(g[1]) + fabs(g[2])) * dm +
-             (fabs(Q[0]) + fabs(Q[1]) + fabs(Q[2]) + 2.0 * (fabs(Q[3]) + fabs(Q[4]) + fabs(Q[5]))) * dm * dm;
-  E += (c0 * c0 + c1 * c1 + fabs(K) * w2t * w2t);
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  d4[0] = make_float4((float)(q0 - 1e-5 * E), (float)g[0], (float)g[1], (float)g[2]);
-  d4[1] = make_float4((float)Q[0], (float)Q[1], (float)Q[2], (float)Q[3]);
-  d4[2] = make_float4((float)Q[4], (float)Q[5], p0.x, (float)det);
-  d4[3] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
-  double2* d2 = reinterpret_cast<double2*>(dst + 16);
-  d2[0] = make_double2(A[0], A[1]);
-  d2[1] = make_double2(A[2], Bv[0]);
-  d2[2] = make_double2(Bv[1], Bv[2]);
-  d2[3] = make_double2(C[0], C[1]);
-  d2[4] = make_double2(C[2], 0.0);
+template <int TS>
+__device__ __forceinline__ void tile_frame(const CamK& k, int tr, int tc, TileFrame& f) {
+  const int r0 = tr * TS, c0 = tc * TS;
+  const int rh = min(TS, k.H - r0), cw = min(TS, k.W - c0);
+  const double az = ((double)c0 + 0.5 * (cw - 1) + k.off_u - k.cx) / k.fx;
+  const double el = ((double)r0 + 0.5 * (rh - 1) + k.off_v - k.cy) / k.fy;
+  double sa, ca, se, ce;
+  sincos(az, &sa, &ca);
+  sincos(el, &se, &ce);
+  f.t[0] = ce * ca; f.t[1] = ce * sa; f.t[2] = se;
+  f.e1[0] = -sa; f.e1[1] = ca; f.e1[2] = 0.0;
+  f.e2[0] = -se * ca; f.e2[1] = -se * sa; f.e2[2] = ce;
 }
 
-// Backward staging: only what the exact intersection and the gradient need.
-__device__ __forceinline__ void stage_entry_bwd(float* dst, int sid, const SplatRec* __restrict__ rec,
-                                                const SplatRec64* __restrict__ rec64) {
+template <int TS>
+__device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, const TileFrame& f, Pix& g) {
+  g.row = tr * TS + p / TS;
+  g.col = tc * TS + p % TS;
+  g.inside = g.row < k.H && g.col < k.W;
+  double v[3];
+  ray_at(k, (double)g.col + k.off_u, (double)g.row + k.off_v, v);
+  g.ray_ok = g.inside && sqrt(v[1] * v[1] + v[0] * v[0]) > 1e-9;
+  g.w = dot3d(v, f.t);
+  g.x = dot3d(v, f.e1);
+  g.y = dot3d(v, f.e2);
+  g.p[0] = (float)(g.w * g.w);
+  g.p[1] = (float)(2.0 * g.w * g.x);
+  g.p[2] = (float)(2.0 * g.w * g.y);
+  g.p[3] = (float)(g.x * g.x);
+  g.p[4] = (float)(2.0 * g.x * g.y);
+  g.p[5] = (float)(g.y * g.y);
+  for (int c = 0; c < 3; ++c) g.vf[c] = (float)v[c];
+}
+
+// Stage one list entry (lane-parallel, float64): the nine frame dot products
+// and, for the forward, the cone-test coefficients.  xm, ym bound |x|, |y|
+// over the tile's pixels.
+template <bool kCone>
+__device__ __forceinline__ void stage_entry(float* dst, int sid, const SplatRec* __restrict__ rec,
+                                            const SplatRec64* __restrict__ rec64, const TileFrame& f, float xm,
+                                            float ym) {
   const float4 p0 = __ldg(&rec[sid].r0);
   const float4 p1 = __ldg(&rec[sid].r1);
   double B[10];
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
-    double2 x = __ldg(&rec64[sid].v[q]);
+    const double2 x = __ldg(&rec64[sid].v[q]);
     B[2 * q] = x.x;
     B[2 * q + 1] = x.y;
   }
@@ -154,15 +136,83 @@ __device__ __forceinline__ void stage_entry_bwd(float* dst, int sid, const Splat
   cross3(Bc, Ba, Bv);
   cross3(Ba, Bb, C);
   const double det = dot3d(Bc, C);
+  const double kt[3] = {dot3d(f.t, A), dot3d(f.t, Bv), dot3d(f.t, C)};
+  const double k1[3] = {dot3d(f.e1, A), dot3d(f.e1, Bv), dot3d(f.e1, C)};
+  const double k2[3] = {dot3d(f.e2, A), dot3d(f.e2, Bv), dot3d(f.e2, C)};
   float4* d4 = reinterpret_cast<float4*>(dst);
-  d4[2] = make_float4(0.f, 0.f, p0.x, (float)det);
-  d4[3] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
+  if (kCone) {
+    const double K = (double)p0.y;
+    const double qtt = kt[0] * kt[0] + kt[1] * kt[1] - K * kt[2] * kt[2];
+    const double qt1 = kt[0] * k1[0] + kt[1] * k1[1] - K * kt[2] * k1[2];
+    const double qt2 = kt[0] * k2[0] + kt[1] * k2[1] - K * kt[2] * k2[2];
+    const double q11 = k1[0] * k1[0] + k1[1] * k1[1] - K * k1[2] * k1[2];
+    const double q12 = k1[0] * k2[0] + k1[1] * k2[1] - K * k1[2] * k2[2];
+    const double q22 = k2[0] * k2[0] + k2[1] * k2[1] - K * k2[2] * k2[2];
+    // magnitude of every term the float32 evaluation sums (bounds its rounding)
+    const double X = xm, Y = ym;
+    const double E = fabs(qtt) + 2.0 * X * fabs(qt1) + 2.0 * Y * fabs(qt2) + X * X * fabs(q11) +
+                     2.0 * X * Y * fabs(q12) + Y * Y * fabs(q22) +
+                     (kt[0] * kt[0] + kt[1] * kt[1] + fabs(K) * kt[2] * kt[2]);
+    d4[0] = make_float4((float)(qtt - 1e-5 * E), (float)qt1, (float)qt2, (float)q11);
+    d4[1] = make_float4((float)q12, (float)q22, p0.x, (float)det);
+  } else {
+    d4[1] = make_float4(0.f, 0.f, p0.x, (float)det);
+  }
+  d4[2] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
   double2* d2 = reinterpret_cast<double2*>(dst + 16);
-  d2[0] = make_double2(A[0], A[1]);
-  d2[1] = make_double2(A[2], Bv[0]);
-  d2[2] = make_double2(Bv[1], Bv[2]);
-  d2[3] = make_double2(C[0], C[1]);
-  d2[4] = make_double2(C[2], 0.0);
+  d2[0] = make_double2(kt[0], kt[1]);
+  d2[1] = make_double2(kt[2], k1[0]);
+  d2[2] = make_double2(k1[1], k1[2]);
+  d2[3] = make_double2(k2[0], k2[1]);
+  d2[4] = make_double2(k2[2], 0.0);
+}
+
+struct Entry {
+  double kt[3], k1[3], k2[3];
+  float o, det, n[3];
+  int sid;
+};
+
+__device__ __forceinline__ void load_entry(const float* e, Entry& x) {
+  const float4* e4 = reinterpret_cast<const float4*>(e);
+  const float4 f1 = e4[1], f2 = e4[2];
+  x.o = f1.z;
+  x.det = f1.w;
+  x.n[0] = f2.x;
+  x.n[1] = f2.y;
+  x.n[2] = f2.z;
+  x.sid = __float_as_int(f2.w);
+  const double2* d2 = reinterpret_cast<const double2*>(e + 16);
+  const double2 a = d2[0], b = d2[1], c = d2[2], d = d2[3], g = d2[4];
+  x.kt[0] = a.x; x.kt[1] = a.y; x.kt[2] = b.x;
+  x.k1[0] = b.y; x.k1[1] = c.x; x.k1[2] = c.y;
+  x.k2[0] = d.x; x.k2[1] = d.y; x.k2[2] = g.x;
+}
+
+struct Hit {
+  float sa, sb, lam, r, G, alpha;
+  bool use, clamped;
+};
+
+// Exact per-pixel intersection + cutoffs (rasterizer.py:369-388).
+__device__ __forceinline__ void intersect(const Entry& x, const Pix& p, const BlendParams& bp, Hit& h) {
+  const float w0 = (float)(p.w * x.kt[0] + p.x * x.k1[0] + p.y * x.k2[0]);
+  const float w1 = (float)(p.w * x.kt[1] + p.x * x.k1[1] + p.y * x.k2[1]);
+  const float w2 = (float)(p.w * x.kt[2] + p.x * x.k1[2] + p.y * x.k2[2]);
+  bool ok = p.ray_ok && fabsf(w2) >= bp.denom_eps;
+  const float r = __fdividef(1.f, w2);
+  h.r = r;
+  h.sa = w0 * r;
+  h.sb = w1 * r;
+  h.lam = x.det * r;
+  ok = ok && h.lam > 0.f;  // nu . v > 0
+  const float s2 = h.sa * h.sa + h.sb * h.sb;
+  h.G = __expf(-0.5f * s2);
+  const float araw = x.o * h.G;
+  h.clamped = araw > bp.alpha_clamp;
+  const float a = fminf(araw, bp.alpha_clamp);
+  h.use = ok && a >= bp.alpha_cutoff;
+  h.alpha = a;
 }
 
 // Butterfly reduce-scatter of 16 per-lane values across the warp: afterwards
@@ -192,58 +242,16 @@ __device__ __forceinline__ float warp_reduce_scatter16(float (&a)[16], int lane)
   }
   const float send = hi1 ? d[0] : d[1];
   const float keep = hi1 ? d[1] : d[0];
-  float e = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  const float e = keep + __shfl_xor_sync(0xffffffffu, send, 2);
   return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
-struct Entry {
-  double A[3], Bv[3], C[3];
-  float o, det, n[3];
-  int sid;
-};
-
-__device__ __forceinline__ void load_entry(const float* e, Entry& x) {
-  const float4* e4 = reinterpret_cast<const float4*>(e);
-  const float4 f2 = e4[2], f3 = e4[3];
-  x.o = f2.z;
-  x.det = f2.w;
-  x.n[0] = f3.x;
-  x.n[1] = f3.y;
-  x.n[2] = f3.z;
-  x.sid = __float_as_int(f3.w);
-  const double2* d2 = reinterpret_cast<const double2*>(e + 16);
-  const double2 a = d2[0], b = d2[1], c = d2[2], d = d2[3], f = d2[4];
-  x.A[0] = a.x; x.A[1] = a.y; x.A[2] = b.x;
-  x.Bv[0] = b.y; x.Bv[1] = c.x; x.Bv[2] = c.y;
-  x.C[0] = d.x; x.C[1] = d.y; x.C[2] = f.x;
-}
-
-struct Hit {
-  float sa, sb, lam, r, G, alpha;
-  bool use, clamped;
-};
-
-// Exact per-pixel intersection + cutoffs (rasterizer.py:369-388): the three
-// dot products in float64 (grazing splats amplify direction error by
-// 1/|v.n|), everything after them in float32.
-__device__ __forceinline__ void intersect(const Entry& x, const double v[3], bool ray_ok, const BlendParams& bp, Hit& h) {
-  const float w0 = (float)dot3d(v, x.A);
-  const float w1 = (float)dot3d(v, x.Bv);
-  const float w2 = (float)dot3d(v, x.C);
-  bool ok = ray_ok && fabsf(w2) >= bp.denom_eps;
-  const float r = __fdividef(1.f, w2);
-  h.r = r;
-  h.sa = w0 * r;
-  h.sb = w1 * r;
-  h.lam = x.det * r;
-  ok = ok && h.lam > 0.f;  // nu . v > 0
-  const float s2 = h.sa * h.sa + h.sb * h.sb;
-  h.G = __expf(-0.5f * s2);
-  const float araw = x.o * h.G;
-  h.clamped = araw > bp.alpha_clamp;
-  const float a = fminf(araw, bp.alpha_clamp);
-  h.use = ok && a >= bp.alpha_cutoff;
-  h.alpha = a;
+// Warp-uniform tile ticket (persistent warps, longest lists first).
+__device__ __forceinline__ int next_tile(int* counter, const int* order, int ntiles, int lane) {
+  int ti = 0;
+  if (lane == 0) ti = atomicAdd(counter, 1);
+  ti = __shfl_sync(0xffffffffu, ti, 0);
+  return ti < ntiles ? order[ti] : -1;
 }
 
 template <int TS>
@@ -258,78 +266,67 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
-  // persistent warps: fetch tiles longest-first until none are left
-  while (true) {
-  int ti = 0;
-  if (lane == 0) ti = atomicAdd(counter, 1);
-  ti = __shfl_sync(0xffffffffu, ti, 0);
-  if (ti >= ntiles) return;
-  const int t = order[ti];
-  const int tr = t / k.tx, tc = t % k.tx;
-  double vt[3];
-  tile_center<TS>(k, tr, tc, vt);
-  PixelGeo px[PPL];
-  float T[PPL], D[PPL], O[PPL], N[PPL][3];
-  int last[PPL];
-  bool live[PPL];
-  float dmax = 0.f;
-#pragma unroll
-  for (int j = 0; j < PPL; ++j) {
-    pixel_geo<TS>(k, tr, tc, lane + 32 * j, vt, px[j]);
-    T[j] = 1.f; D[j] = 0.f; O[j] = 0.f; N[j][0] = N[j][1] = N[j][2] = 0.f;
-    last[j] = 0;
-    live[j] = px[j].ray_ok;
-    if (px[j].ray_ok) dmax = fmaxf(dmax, fmaxf(fabsf(px[j].d[0]), fmaxf(fabsf(px[j].d[1]), fabsf(px[j].d[2]))));
-  }
-  for (int off = 16; off > 0; off >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
-  const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
-  const int cbase = chunk_ptr[t];
   float* st = stage[warp];
-  for (int base = 0, chunk = 0; base < L; base += 32, ++chunk) {
-    bool any_live = false;
+  for (int t = next_tile(counter, order, ntiles, lane); t >= 0; t = next_tile(counter, order, ntiles, lane)) {
+    const int tr = t / k.tx, tc = t % k.tx;
+    TileFrame f;
+    tile_frame<TS>(k, tr, tc, f);
+    Pix px[PPL];
+    float T[PPL], D[PPL], O[PPL], N[PPL][3];
+    int last[PPL];
+    bool live[PPL];
+    float xm = 0.f, ym = 0.f;
 #pragma unroll
-    for (int j = 0; j < PPL; ++j) any_live |= live[j];
-    if (!__any_sync(0xffffffffu, any_live)) break;
-    if (base + lane < L) stage_entry(st + lane * kStride, pairs[lo + base + lane], rec, rec64, vt, dmax);
-    __syncwarp();
-    const int cnt = min(32, L - base);
-    unsigned word[PPL];
-#pragma unroll
-    for (int j = 0; j < PPL; ++j) word[j] = 0u;
-    // two entries per iteration: four independent cone-test chains in flight
-    for (int i = 0; i < cnt; i += 2) {
-      const bool has2 = i + 1 < cnt;
-      const float* e0 = st + i * kStride;
-      const float* e1 = st + (has2 ? i + 1 : i) * kStride;
-      const float4 a0 = *reinterpret_cast<const float4*>(e0);
-      const float4 a1 = *reinterpret_cast<const float4*>(e0 + 4);
-      const float4 a2 = *reinterpret_cast<const float4*>(e0 + 8);
-      const float4 b0 = *reinterpret_cast<const float4*>(e1);
-      const float4 b1 = *reinterpret_cast<const float4*>(e1 + 4);
-      const float4 b2 = *reinterpret_cast<const float4*>(e1 + 8);
-      bool ca[PPL], cb[PPL];
-      bool anya = false, anyb = false;
-#pragma unroll
-      for (int j = 0; j < PPL; ++j) {
-        const float* d = px[j].d;
-        const float* pp = px[j].pp;
-        const float qa = (a0.x + a0.y * d[0] + a0.z * d[1] + a0.w * d[2]) +
-                         (a1.x * pp[0] + a1.y * pp[1] + a1.z * pp[2] + a1.w * pp[3] + a2.x * pp[4] + a2.y * pp[5]);
-        const float qb = (b0.x + b0.y * d[0] + b0.z * d[1] + b0.w * d[2]) +
-                         (b1.x * pp[0] + b1.y * pp[1] + b1.z * pp[2] + b1.w * pp[3] + b2.x * pp[4] + b2.y * pp[5]);
-        ca[j] = live[j] && qa <= 0.f;
-        cb[j] = has2 && qb <= 0.f;
-        anya |= ca[j];
-        anyb |= cb[j];
+    for (int j = 0; j < PPL; ++j) {
+      pixel_geo<TS>(k, tr, tc, lane + 32 * j, f, px[j]);
+      T[j] = 1.f; D[j] = 0.f; O[j] = 0.f; N[j][0] = N[j][1] = N[j][2] = 0.f;
+      last[j] = 0;
+      live[j] = px[j].ray_ok;
+      if (px[j].ray_ok) {
+        xm = fmaxf(xm, fabsf((float)px[j].x));
+        ym = fmaxf(ym, fabsf((float)px[j].y));
       }
-      if (anya) {
-        Entry x;
-        load_entry(e0, x);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, off));
+      ym = fmaxf(ym, __shfl_xor_sync(0xffffffffu, ym, off));
+    }
+    xm *= 1.0001f;
+    ym *= 1.0001f;
+    const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+    const int cbase = chunk_ptr[t];
+    for (int base = 0, chunk = 0; base < L; base += 32, ++chunk) {
+      bool any_live = false;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) any_live |= live[j];
+      if (!__any_sync(0xffffffffu, any_live)) break;
+      if (base + lane < L) stage_entry<true>(st + lane * kStride, pairs[lo + base + lane], rec, rec64, f, xm, ym);
+      __syncwarp();
+      const int cnt = min(32, L - base);
+      unsigned word[PPL];
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) word[j] = 0u;
+      for (int i = 0; i < cnt; ++i) {
+        const float* e = st + i * kStride;
+        const float4 c0 = *reinterpret_cast<const float4*>(e);
+        const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
+        bool cand[PPL];
+        bool anyc = false;
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
-          if (!ca[j]) continue;
+          const float* p = px[j].p;
+          const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
+          cand[j] = live[j] && q <= 0.f;
+          anyc |= cand[j];
+        }
+        if (!anyc) continue;
+        Entry x;
+        load_entry(e, x);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          if (!cand[j]) continue;
           Hit h;
-          intersect(x, px[j].v, px[j].ray_ok, bp, h);
+          intersect(x, px[j], bp, h);
           if (!h.use) continue;
           const float w = h.alpha * T[j];
           D[j] += w * h.lam;
@@ -343,49 +340,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
           if (T[j] < bp.min_T) live[j] = false;
         }
       }
-      if (anyb) {
-        Entry x;
-        load_entry(e1, x);
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-          if (!(cb[j] && live[j])) continue;  // the pixel may have saturated at entry i
-          Hit h;
-          intersect(x, px[j].v, px[j].ray_ok, bp, h);
-          if (!h.use) continue;
-          const float w = h.alpha * T[j];
-          D[j] += w * h.lam;
-          O[j] += w;
-          N[j][0] += w * x.n[0];
-          N[j][1] += w * x.n[1];
-          N[j][2] += w * x.n[2];
-          T[j] *= (1.f - h.alpha);
-          word[j] |= 1u << (i + 1);
-          last[j] = base + i + 2;
-          if (T[j] < bp.min_T) live[j] = false;
-        }
-      }
+      for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
+      __syncwarp();
     }
 #pragma unroll
-    for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
-    __syncwarp();
-  }
-#pragma unroll
-  for (int j = 0; j < PPL; ++j) {
-    if (!px[j].inside) continue;
-    size_t p = (size_t)px[j].row * k.W + px[j].col;
-    out_D[p] = D[j];
-    out_O[p] = O[j];
-    out_N[3 * p] = N[j][0];
-    out_N[3 * p + 1] = N[j][1];
-    out_N[3 * p + 2] = N[j][2];
-    out_T[p] = T[j];
-    out_last[p] = last[j];
-  }
+    for (int j = 0; j < PPL; ++j) {
+      if (!px[j].inside) continue;
+      const size_t p = (size_t)px[j].row * k.W + px[j].col;
+      out_D[p] = D[j];
+      out_O[p] = O[j];
+      out_N[3 * p] = N[j][0];
+      out_N[3 * p + 1] = N[j][1];
+      out_N[3 * p + 2] = N[j][2];
+      out_T[p] = T[j];
+      out_last[p] = last[j];
+    }
   }
 }
 
 constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
-constexpr int kRedStride = 15;
 
 template <int TS>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
@@ -400,108 +374,100 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
-  while (true) {
-  int ti = 0;
-  if (lane == 0) ti = atomicAdd(counter, 1);
-  ti = __shfl_sync(0xffffffffu, ti, 0);
-  if (ti >= ntiles) return;
-  const int t = order[ti];
-  const int tr = t / k.tx, tc = t % k.tx;
-  double vt[3];
-  tile_center<TS>(k, tr, tc, vt);
-  PixelGeo px[PPL];
-  float T[PPL], Sd[PPL], So[PPL], Sn[PPL][3], gD[PPL], gO[PPL], gN[PPL][3];
-  int last[PPL];
-  int maxlast = 0;
-#pragma unroll
-  for (int j = 0; j < PPL; ++j) {
-    pixel_geo<TS>(k, tr, tc, lane + 32 * j, vt, px[j]);
-    last[j] = 0;
-    T[j] = 1.f;
-    gD[j] = gO[j] = gN[j][0] = gN[j][1] = gN[j][2] = 0.f;
-    if (px[j].inside) {
-      size_t p = (size_t)px[j].row * k.W + px[j].col;
-      last[j] = in_last[p];
-      T[j] = in_T[p];
-      gD[j] = gD_img[p];
-      gO[j] = gO_img[p];
-      gN[j][0] = gN_img[3 * p];
-      gN[j][1] = gN_img[3 * p + 1];
-      gN[j][2] = gN_img[3 * p + 2];
-    }
-    Sd[j] = So[j] = Sn[j][0] = Sn[j][1] = Sn[j][2] = 0.f;
-    maxlast = max(maxlast, last[j]);
-  }
-  maxlast = __reduce_max_sync(0xffffffffu, maxlast);
-  if (maxlast == 0) continue;
-  const int lo = tile_ptr[t];
-  const int cbase = chunk_ptr[t];
   float* st = stage[warp];
-  for (int chunk = (maxlast - 1) >> 5; chunk >= 0; --chunk) {
-    const int base = chunk * 32;
-    unsigned word[PPL];
-    unsigned mine = 0u;
+  for (int t = next_tile(counter, order, ntiles, lane); t >= 0; t = next_tile(counter, order, ntiles, lane)) {
+    const int tr = t / k.tx, tc = t % k.tx;
+    TileFrame f;
+    tile_frame<TS>(k, tr, tc, f);
+    Pix px[PPL];
+    float T[PPL], Sd[PPL], So[PPL], Sn[PPL][3], gD[PPL], gO[PPL], gN[PPL][3];
+    int last[PPL];
+    int maxlast = 0;
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
-      word[j] = base < last[j] ? bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] : 0u;
-      mine |= word[j];
+      pixel_geo<TS>(k, tr, tc, lane + 32 * j, f, px[j]);
+      last[j] = 0;
+      T[j] = 1.f;
+      gD[j] = gO[j] = gN[j][0] = gN[j][1] = gN[j][2] = 0.f;
+      if (px[j].inside) {
+        const size_t p = (size_t)px[j].row * k.W + px[j].col;
+        last[j] = in_last[p];
+        T[j] = in_T[p];
+        gD[j] = gD_img[p];
+        gO[j] = gO_img[p];
+        gN[j][0] = gN_img[3 * p];
+        gN[j][1] = gN_img[3 * p + 1];
+        gN[j][2] = gN_img[3 * p + 2];
+      }
+      Sd[j] = So[j] = Sn[j][0] = Sn[j][1] = Sn[j][2] = 0.f;
+      maxlast = max(maxlast, last[j]);
     }
-    unsigned any = __reduce_or_sync(0xffffffffu, mine);
-    if (!any) continue;
-    if ((any >> lane) & 1u) stage_entry_bwd(st + lane * kStride, pairs[lo + base + lane], rec, rec64);
-    __syncwarp();
-    while (any) {
-      const int i = 31 - __clz(any);
-      any &= ~(1u << i);
-      Entry x;
-      load_entry(st + i * kStride, x);
-      float a[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) a[q] = 0.f;
-      bool act = false;
+    maxlast = __reduce_max_sync(0xffffffffu, maxlast);
+    if (maxlast == 0) continue;
+    const int lo = tile_ptr[t];
+    const int cbase = chunk_ptr[t];
+    for (int chunk = (maxlast - 1) >> 5; chunk >= 0; --chunk) {
+      const int base = chunk * 32;
+      unsigned word[PPL];
+      unsigned mine = 0u;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
-        if (!((word[j] >> i) & 1u)) continue;
-        act = true;
-        Hit h;
-        intersect(x, px[j].v, px[j].ray_ok, bp, h);
-        const float om = 1.f - h.alpha;
-        const float iom = __fdividef(1.f, om);
-        const float Tb = T[j] * iom;
-        float dal = gD[j] * (h.lam * Tb - Sd[j] * iom) + gO[j] * (Tb - So[j] * iom);
-        dal += gN[j][0] * (x.n[0] * Tb - Sn[j][0] * iom) + gN[j][1] * (x.n[1] * Tb - Sn[j][1] * iom) +
-               gN[j][2] * (x.n[2] * Tb - Sn[j][2] * iom);
-        const float w = h.alpha * Tb;
-        const float gl = gD[j] * w;
-        float gsa = 0.f, gsb = 0.f, go = 0.f;
-        if (!h.clamped) {
-          gsa = -dal * h.alpha * h.sa;
-          gsb = -dal * h.alpha * h.sb;
-          go = dal * h.G;
-        }
-        const float gw0 = gsa * h.r, gw1 = gsb * h.r;
-        const float gw2 = -(gsa * h.sa + gsb * h.sb + gl * h.lam) * h.r;
-        const float v0 = (float)px[j].v[0], v1 = (float)px[j].v[1], v2 = (float)px[j].v[2];
-        a[0] += gw0 * v0; a[1] += gw0 * v1; a[2] += gw0 * v2;
-        a[3] += gw1 * v0; a[4] += gw1 * v1; a[5] += gw1 * v2;
-        a[6] += gw2 * v0; a[7] += gw2 * v1; a[8] += gw2 * v2;
-        a[9] += gl * h.r;
-        a[10] += w * gN[j][0]; a[11] += w * gN[j][1]; a[12] += w * gN[j][2];
-        a[13] += go;
-        Sd[j] += w * h.lam;
-        So[j] += w;
-        Sn[j][0] += w * x.n[0];
-        Sn[j][1] += w * x.n[1];
-        Sn[j][2] += w * x.n[2];
-        T[j] = Tb;
+        word[j] = base < last[j] ? bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] : 0u;
+        mine |= word[j];
       }
-      (void)act;
-      const float tot = warp_reduce_scatter16(a, lane);
-      const int vi = (lane >> 1) & 15;
-      if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
+      unsigned any = __reduce_or_sync(0xffffffffu, mine);
+      if (!any) continue;
+      if ((any >> lane) & 1u) stage_entry<false>(st + lane * kStride, pairs[lo + base + lane], rec, rec64, f, 0.f, 0.f);
+      __syncwarp();
+      while (any) {
+        const int i = 31 - __clz(any);
+        any &= ~(1u << i);
+        Entry x;
+        load_entry(st + i * kStride, x);
+        float a[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = 0.f;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          if (!((word[j] >> i) & 1u)) continue;
+          Hit h;
+          intersect(x, px[j], bp, h);
+          const float om = 1.f - h.alpha;
+          const float iom = __fdividef(1.f, om);
+          const float Tb = T[j] * iom;
+          float dal = gD[j] * (h.lam * Tb - Sd[j] * iom) + gO[j] * (Tb - So[j] * iom);
+          dal += gN[j][0] * (x.n[0] * Tb - Sn[j][0] * iom) + gN[j][1] * (x.n[1] * Tb - Sn[j][1] * iom) +
+                 gN[j][2] * (x.n[2] * Tb - Sn[j][2] * iom);
+          const float w = h.alpha * Tb;
+          const float gl = gD[j] * w;
+          float gsa = 0.f, gsb = 0.f, go = 0.f;
+          if (!h.clamped) {
+            gsa = -dal * h.alpha * h.sa;
+            gsb = -dal * h.alpha * h.sb;
+            go = dal * h.G;
+          }
+          const float gw0 = gsa * h.r, gw1 = gsb * h.r;
+          const float gw2 = -(gsa * h.sa + gsb * h.sb + gl * h.lam) * h.r;
+          const float v0 = px[j].vf[0], v1 = px[j].vf[1], v2 = px[j].vf[2];
+          a[0] += gw0 * v0; a[1] += gw0 * v1; a[2] += gw0 * v2;
+          a[3] += gw1 * v0; a[4] += gw1 * v1; a[5] += gw1 * v2;
+          a[6] += gw2 * v0; a[7] += gw2 * v1; a[8] += gw2 * v2;
+          a[9] += gl * h.r;
+          a[10] += w * gN[j][0]; a[11] += w * gN[j][1]; a[12] += w * gN[j][2];
+          a[13] += go;
+          Sd[j] += w * h.lam;
+          So[j] += w;
+          Sn[j][0] += w * x.n[0];
+          Sn[j][1] += w * x.n[1];
+          Sn[j][2] += w * x.n[2];
+          T[j] = Tb;
+        }
+        const float tot = warp_reduce_scatter16(a, lane);
+        const int vi = (lane >> 1) & 15;
+        if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
+      }
+      __syncwarp();
     }
-    __syncwarp();
-  }
   }
 }
 
@@ -612,10 +578,13 @@ __global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc
   o[11] = (float)(Oc * op * (1.0 - op));
 }
 
+
 template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*, const int*, int*);
+                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*,
+                                      const int*, int*);
 template __global__ void k_forward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*, const int*, int*);
+                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*,
+                                       const int*, int*);
 template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
                                        const float*, const float*, float*, const int*, const int*, int*);
