@@ -259,8 +259,10 @@ __global__ void k_scan_blocks(int nb, uint32_t* __restrict__ block_sum, long lon
   if (tid == 1023) totals[0] = (long long)part[1023];
 }
 
-// Emit the pairs of every splat at its offset (index order).  Overflow of
-// the speculative capacity sets a flag.
+// Emit the pairs of every splat at its offset (index order).  Each warp
+// writes the pairs of its 32 splats cooperatively (coalesced), decoding
+// (splat, tile) from the warp's inclusive count prefix.  Overflow of the
+// speculative capacity sets a flag.
 __global__ void __launch_bounds__(256)
     k_emit(int n, const int4* __restrict__ rect, const uint32_t* __restrict__ block_off, int tx, long long cap,
            uint32_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_splat, int* __restrict__ overflow) {
@@ -279,21 +281,30 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   uint32_t wex = 0;
   for (int w = 0; w < warp; ++w) wex += ws[w];
-  if (cnt == 0) return;
-  const long long off = (long long)block_off[blockIdx.x] + wex + (inc - cnt);
-  if (off + cnt > cap) {
-    atomicExch(overflow, 1);
+  const uint32_t wtot = __shfl_sync(0xffffffffu, inc, 31);
+  const long long off = (long long)block_off[blockIdx.x] + wex;
+  if (off + wtot > cap) {
+    if (lane == 0 && wtot) atomicExch(overflow, 1);
     return;
   }
-  long long q = off;
-  for (int rr = r.x; rr <= r.y; ++rr) {
-    const int base = rr * tx;
-    for (int j = 0; j < r.w; ++j) {
-      int c = r.z + j;
+  // pair q of this warp belongs to the lane whose inclusive prefix first exceeds q
+  for (uint32_t q0 = 0; q0 < wtot; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    int owner = 0;
+    for (int b = 16; b > 0; b >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, inc, owner + b - 1);
+      if (v <= q) owner += b;
+    }
+    const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, owner);
+    const int4 ro = make_int4(__shfl_sync(0xffffffffu, r.x, owner), 0, __shfl_sync(0xffffffffu, r.z, owner),
+                              __shfl_sync(0xffffffffu, r.w, owner));
+    if (q < wtot) {
+      const uint32_t k = q - ex;
+      const int rr = ro.x + (int)(k / (uint32_t)ro.w);
+      int c = ro.z + (int)(k % (uint32_t)ro.w);
       if (c >= tx) c -= tx;
-      pair_tile[q] = (uint32_t)(base + c);
-      pair_splat[q] = (uint32_t)i;
-      ++q;
+      pair_tile[off + q] = (uint32_t)(rr * tx + c);
+      pair_splat[off + q] = (uint32_t)(blockIdx.x * blockDim.x + warp * 32 + owner);
     }
   }
 }
@@ -326,19 +337,40 @@ __global__ void __launch_bounds__(1024)
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) mat[(size_t)blockIdx.x * ntiles + t] = h[t];
 }
 
-__global__ void k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
-                              uint32_t* __restrict__ mat, int* __restrict__ tile_count) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
+// Per tile, exclusive prefix of the block histograms over the pair blocks
+// (in place) and the tile totals.  Block = 32 tiles x 32 block-segments.
+__global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
+                                                      uint32_t* __restrict__ mat, int* __restrict__ tile_count) {
+  __shared__ uint32_t part[32][33];
+  const int tx = threadIdx.x, seg = threadIdx.y;
+  const int t = blockIdx.x * 32 + tx;
   const long long n = min(totals[0], cap);
   const int nb = (int)max(1LL, (n + kPairChunk - 1) / kPairChunk);
+  const int per = (nb + 31) / 32;
+  const int b0 = min(seg * per, nb), b1 = min(b0 + per, nb);
   uint32_t s = 0;
-  for (int b = 0; b < nb; ++b) {
-    const uint32_t c = mat[(size_t)b * ntiles + t];
-    mat[(size_t)b * ntiles + t] = s;
-    s += c;
+  if (t < ntiles)
+    for (int b = b0; b < b1; ++b) s += mat[(size_t)b * ntiles + t];
+  part[seg][tx] = s;
+  __syncthreads();
+  if (seg == 0) {
+    uint32_t run = 0;
+    for (int g = 0; g < 32; ++g) {
+      const uint32_t c = part[g][tx];
+      part[g][tx] = run;
+      run += c;
+    }
+    if (t < ntiles) tile_count[t] = (int)run;
   }
-  tile_count[t] = (int)s;
+  __syncthreads();
+  if (t < ntiles) {
+    uint32_t run = part[seg][tx];
+    for (int b = b0; b < b1; ++b) {
+      const uint32_t c = mat[(size_t)b * ntiles + t];
+      mat[(size_t)b * ntiles + t] = run;
+      run += c;
+    }
+  }
 }
 
 __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int* __restrict__ tile_ptr,

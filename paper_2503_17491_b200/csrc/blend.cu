@@ -473,43 +473,39 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
 
 // Camera-frame accumulators -> plain-space (15) or raw-space (12) gradients
 // (rasterizer.py:686-700, splats.py:133-163, mapping.py:479-494).
-__global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc, const float* __restrict__ d_scales_extra,
-                           float* __restrict__ out, int raw_space) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+// The cross products with the camera-frame splat vectors (|Bc| ~ tens of
+// metres against nearly parallel accumulated rays) are float64 from the
+// forward's records; the rest of the chain is float32.
+__global__ void __launch_bounds__(256) k_finalize(SplatsK sp, PoseK pose, const SplatRec64* __restrict__ rec64,
+                                                  const float* __restrict__ acc,
+                                                  const float* __restrict__ d_scales_extra, float* __restrict__ out,
+                                                  int raw_space) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sp.n) return;
-  double a[3], b[3];
-  for (int c = 0; c < 3; ++c) {
-    a[c] = sp.raw_ta[3 * i + c];
-    b[c] = sp.raw_tb[3 * i + c];
+  double B[10];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const double2 x = __ldg(&rec64[i].v[q]);
+    B[2 * q] = x.x;
+    B[2 * q + 1] = x.y;
   }
-  double na = sqrt(dot3d(a, a));
-  double u[3] = {a[0] / na, a[1] / na, a[2] / na};
-  double ub = dot3d(u, b);
-  double w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
-  double nw = sqrt(dot3d(w, w));
-  double v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
-  double s0 = exp((double)sp.log_scales[2 * i]), s1 = exp((double)sp.log_scales[2 * i + 1]);
-  double m[3] = {(double)sp.centers[3 * i] - pose.t[0], (double)sp.centers[3 * i + 1] - pose.t[1],
-                 (double)sp.centers[3 * i + 2] - pose.t[2]};
-  const double* R = pose.R;
-  double Bc[3], tac[3], tbc[3], Ba[3], Bb[3];
-  for (int c = 0; c < 3; ++c) {
-    Bc[c] = m[0] * R[c] + m[1] * R[3 + c] + m[2] * R[6 + c];
-    tac[c] = u[0] * R[c] + u[1] * R[3 + c] + u[2] * R[6 + c];
-    tbc[c] = v[0] * R[c] + v[1] * R[3 + c] + v[2] * R[6 + c];
-    Ba[c] = s0 * tac[c];
-    Bb[c] = s1 * tbc[c];
+  const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
+  const float4* g4 = reinterpret_cast<const float4*>(acc + (size_t)i * kAcc);
+  const float4 ga = g4[0], gb = g4[1], gc = g4[2], gd = g4[3];
+  const double V0[3] = {ga.x, ga.y, ga.z}, V1[3] = {ga.w, gb.x, gb.y}, V2[3] = {gb.z, gb.w, gc.x};
+  const double Gd = gc.y;
+  const float Nc[3] = {gc.z, gc.w, gd.x};
+  const float Oc = gd.y;
+  if (Gd == 0.0 && V0[0] == 0.0 && V0[1] == 0.0 && V0[2] == 0.0 && V1[0] == 0.0 && V1[1] == 0.0 && V1[2] == 0.0 &&
+      V2[0] == 0.0 && V2[1] == 0.0 && V2[2] == 0.0 && Nc[0] == 0.f && Nc[1] == 0.f && Nc[2] == 0.f && Oc == 0.f) {
+    float* o = out + (size_t)i * (raw_space ? 12 : 15);
+    for (int q = 0; q < (raw_space ? 12 : 15); ++q) o[q] = 0.f;  // splat touched no pixel
+    return;
   }
-  double A[3], Bv[3], C[3];
+  double A[3], Bv[3], C[3], t1[3], t2[3], gBa[3], gBb[3], gBc[3];
   cross3(Bb, Bc, A);
   cross3(Bc, Ba, Bv);
   cross3(Ba, Bb, C);
-  const float* g = acc + (size_t)i * kAcc;
-  double V0[3] = {g[0], g[1], g[2]}, V1[3] = {g[3], g[4], g[5]}, V2[3] = {g[6], g[7], g[8]};
-  double Gd = g[9];
-  double Nc[3] = {g[10], g[11], g[12]};
-  double Oc = g[13];
-  double t1[3], t2[3], gBa[3], gBb[3], gBc[3];
   cross3(V1, Bc, t1);
   cross3(Bb, V2, t2);
   for (int c = 0; c < 3; ++c) gBa[c] = t1[c] + t2[c] + Gd * A[c];
@@ -519,65 +515,67 @@ __global__ void k_finalize(SplatsK sp, PoseK pose, const float* __restrict__ acc
   cross3(V0, Bb, t1);
   cross3(Ba, V1, t2);
   for (int c = 0; c < 3; ++c) gBc[c] = t1[c] + t2[c] + Gd * C[c];
-  // camera frame -> world frame: x @ R.T
-  double dmu[3], dta[3], dtb[3], dn[3];
-  for (int c = 0; c < 3; ++c) {
-    dmu[c] = gBc[0] * R[3 * c] + gBc[1] * R[3 * c + 1] + gBc[2] * R[3 * c + 2];
-    dta[c] = s0 * (gBa[0] * R[3 * c] + gBa[1] * R[3 * c + 1] + gBa[2] * R[3 * c + 2]);
-    dtb[c] = s1 * (gBb[0] * R[3 * c] + gBb[1] * R[3 * c + 1] + gBb[2] * R[3 * c + 2]);
-    dn[c] = Nc[0] * R[3 * c] + Nc[1] * R[3 * c + 1] + Nc[2] * R[3 * c + 2];
+  const float s0 = __expf(sp.log_scales[2 * i]), s1 = __expf(sp.log_scales[2 * i + 1]);
+  // d_scales: dBa/ds_a = ta_c = Ba / s_a (rasterizer.py:693-699)
+  const float ds0 = (float)(dot3d(gBa, Ba) / (double)s0), ds1 = (float)(dot3d(gBb, Bb) / (double)s1);
+  const double* R = pose.R;
+  float dmu[3], dta[3], dtb[3], dn[3];
+  for (int c = 0; c < 3; ++c) {  // camera frame -> world frame: x @ R.T
+    dmu[c] = (float)(gBc[0] * R[3 * c] + gBc[1] * R[3 * c + 1] + gBc[2] * R[3 * c + 2]);
+    dta[c] = s0 * (float)(gBa[0] * R[3 * c] + gBa[1] * R[3 * c + 1] + gBa[2] * R[3 * c + 2]);
+    dtb[c] = s1 * (float)(gBb[0] * R[3 * c] + gBb[1] * R[3 * c + 1] + gBb[2] * R[3 * c + 2]);
+    dn[c] = (float)(Nc[0] * R[3 * c] + Nc[1] * R[3 * c + 1] + Nc[2] * R[3 * c + 2]);
   }
-  double ds0 = dot3d(gBa, tac), ds1 = dot3d(gBb, tbc);
   if (!raw_space) {
     float* o = out + (size_t)i * 15;
     for (int c = 0; c < 3; ++c) {
-      o[c] = (float)dmu[c];
-      o[3 + c] = (float)dta[c];
-      o[6 + c] = (float)dtb[c];
-      o[9 + c] = (float)dn[c];
+      o[c] = dmu[c];
+      o[3 + c] = dta[c];
+      o[6 + c] = dtb[c];
+      o[9 + c] = dn[c];
     }
-    o[12] = (float)ds0;
-    o[13] = (float)ds1;
-    o[14] = (float)Oc;
+    o[12] = ds0;
+    o[13] = ds1;
+    o[14] = Oc;
     return;
   }
-  // Gram-Schmidt backward (splats.py:154-163)
-  double gu[3], gv[3], cv[3], cn[3];
-  cross3(v, dn, cv);
-  cross3(dn, u, cn);
+  // Gram-Schmidt backward (splats.py:154-163), float32
+  const float a[3] = {sp.raw_ta[3 * i], sp.raw_ta[3 * i + 1], sp.raw_ta[3 * i + 2]};
+  const float b[3] = {sp.raw_tb[3 * i], sp.raw_tb[3 * i + 1], sp.raw_tb[3 * i + 2]};
+  const float na = sqrtf(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+  const float u[3] = {a[0] / na, a[1] / na, a[2] / na};
+  const float ub = u[0] * b[0] + u[1] * b[1] + u[2] * b[2];
+  const float w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
+  const float nw = sqrtf(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  const float v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
+  const float gu[3] = {dta[0] + (v[1] * dn[2] - v[2] * dn[1]), dta[1] + (v[2] * dn[0] - v[0] * dn[2]),
+                       dta[2] + (v[0] * dn[1] - v[1] * dn[0])};
+  const float gv[3] = {dtb[0] + (dn[1] * u[2] - dn[2] * u[1]), dtb[1] + (dn[2] * u[0] - dn[0] * u[2]),
+                       dtb[2] + (dn[0] * u[1] - dn[1] * u[0])};
+  const float vg = v[0] * gv[0] + v[1] * gv[1] + v[2] * gv[2];
+  const float q[3] = {(gv[0] - vg * v[0]) / nw, (gv[1] - vg * v[1]) / nw, (gv[2] - vg * v[2]) / nw};
+  const float qu = q[0] * u[0] + q[1] * u[1] + q[2] * u[2];
+  float inner[3], gb_[3];
   for (int c = 0; c < 3; ++c) {
-    gu[c] = dta[c] + cv[c];
-    gv[c] = dtb[c] + cn[c];
-  }
-  double vg = dot3d(v, gv);
-  double q[3] = {(gv[0] - vg * v[0]) / nw, (gv[1] - vg * v[1]) / nw, (gv[2] - vg * v[2]) / nw};
-  double qu = dot3d(q, u);
-  double inner[3], gb[3];
-  for (int c = 0; c < 3; ++c) {
-    gb[c] = q[c] - qu * u[c];
+    gb_[c] = q[c] - qu * u[c];
     inner[c] = gu[c] - ub * q[c] - qu * b[c];
   }
-  double ui = dot3d(u, inner);
+  const float ui = u[0] * inner[0] + u[1] * inner[1] + u[2] * inner[2];
   float* o = out + (size_t)i * 12;
   for (int c = 0; c < 3; ++c) {
-    o[c] = (float)dmu[c];
-    o[3 + c] = (float)((inner[c] - ui * u[c]) / na);
-    o[6 + c] = (float)gb[c];
+    o[c] = dmu[c];
+    o[3 + c] = (inner[c] - ui * u[c]) / na;
+    o[6 + c] = gb_[c];
   }
-  double e0 = d_scales_extra ? (double)d_scales_extra[2 * i] : 0.0;
-  double e1 = d_scales_extra ? (double)d_scales_extra[2 * i + 1] : 0.0;
-  o[9] = (float)((ds0 + e0) * s0);
-  o[10] = (float)((ds1 + e1) * s1);
-  double x = (double)sp.logit_opacity[i], op;
-  if (x >= 0) {
-    op = 1.0 / (1.0 + exp(-x));
-  } else {
-    double e = exp(x);
-    op = e / (1.0 + e);
-  }
-  o[11] = (float)(Oc * op * (1.0 - op));
+  const float e0 = d_scales_extra ? d_scales_extra[2 * i] : 0.f;
+  const float e1 = d_scales_extra ? d_scales_extra[2 * i + 1] : 0.f;
+  o[9] = (ds0 + e0) * s0;
+  o[10] = (ds1 + e1) * s1;
+  const float xo = sp.logit_opacity[i];
+  const float ex = __expf(-fabsf(xo));
+  const float op = xo >= 0.f ? 1.f / (1.f + ex) : ex / (1.f + ex);
+  o[11] = Oc * op * (1.f - op);
 }
-
 
 template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*,

@@ -324,7 +324,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     const size_t hsm = sizeof(uint32_t) * ntiles;
     set_smem_attrs();
     k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow);
-    k_tile_prefix<<<(ntiles + 255) / 256, 256, 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count);
+    k_tile_prefix<<<(ntiles + 31) / 32, dim3(32, 32), 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count);
     k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals);
     k_tile_scatter<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
                                               rec->pbucket, overflow);
@@ -446,7 +446,8 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   }
   {
     StageTimer tm(rec, ST_FINALIZE, s);
-    k_finalize<<<(n + 255) / 256, 256, 0, s>>>(to_k(splats), rec->pose, rec->acc, d_scales_extra, grads, raw_space);
+    k_finalize<<<(n + 255) / 256, 256, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc, d_scales_extra, grads,
+                                                raw_space);
   }
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
