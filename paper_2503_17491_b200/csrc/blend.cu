@@ -34,6 +34,8 @@
 // entries some pixel of the tile contributed to, and reduces each splat's 14
 // accumulators across the warp with a butterfly reduce-scatter before one
 // warp-wide float atomic.
+#include <cuda_pipeline.h>
+
 #include "common.cuh"
 
 namespace ss {
@@ -117,16 +119,30 @@ __device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, 
 // Stage one list entry (lane-parallel, float64): the nine frame dot products
 // and, for the forward, the cone-test coefficients.  xm, ym bound |x|, |y|
 // over the tile's pixels.
+// Raw per-entry record copy (7 x 16 B) brought into shared memory with
+// cp.async one chunk ahead of its use.
+struct RawEntry {
+  float4 r0, r1;
+  double2 v[5];
+};
+
+__device__ __forceinline__ void prefetch_entry(RawEntry* dst, int sid, const SplatRec* __restrict__ rec,
+                                               const SplatRec64* __restrict__ rec64) {
+  __pipeline_memcpy_async(&dst->r0, &rec[sid].r0, 16);
+  __pipeline_memcpy_async(&dst->r1, &rec[sid].r1, 16);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) __pipeline_memcpy_async(&dst->v[q], &rec64[sid].v[q], 16);
+}
+
 template <bool kCone>
-__device__ __forceinline__ void stage_entry(float* dst, int sid, const SplatRec* __restrict__ rec,
-                                            const SplatRec64* __restrict__ rec64, const TileFrame& f, float xm,
+__device__ __forceinline__ void stage_entry(float* dst, int sid, const RawEntry& raw, const TileFrame& f, float xm,
                                             float ym) {
-  const float4 p0 = __ldg(&rec[sid].r0);
-  const float4 p1 = __ldg(&rec[sid].r1);
+  const float4 p0 = raw.r0;
+  const float4 p1 = raw.r1;
   double B[10];
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
-    const double2 x = __ldg(&rec64[sid].v[q]);
+    const double2 x = raw.v[q];
     B[2 * q] = x.x;
     B[2 * q + 1] = x.y;
   }
@@ -264,6 +280,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;  // pair capacity exceeded: the host re-runs the render
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
+  __shared__ __align__(16) RawEntry raw_all[kWarpsPerBlock][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
   float* st = stage[warp];
@@ -295,13 +312,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
     ym *= 1.0001f;
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     const int cbase = chunk_ptr[t];
+    // records of chunk c+1 are copied (cp.async) while chunk c is processed
+    int sid_cur = lane < L ? pairs[lo + lane] : -1;
+    if (sid_cur >= 0) prefetch_entry(&raw_all[warp][0][lane], sid_cur, rec, rec64);
+    __pipeline_commit();
+    int sid_next = 32 + lane < L ? pairs[lo + 32 + lane] : -1;
     for (int base = 0, chunk = 0; base < L; base += 32, ++chunk) {
       bool any_live = false;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) any_live |= live[j];
       if (!__any_sync(0xffffffffu, any_live)) break;
-      if (base + lane < L) stage_entry<true>(st + lane * kStride, pairs[lo + base + lane], rec, rec64, f, xm, ym);
+      if (sid_next >= 0) prefetch_entry(&raw_all[warp][(chunk + 1) & 1][lane], sid_next, rec, rec64);
+      __pipeline_commit();
+      const int sid_after = base + 64 + lane < L ? pairs[lo + base + 64 + lane] : -1;
+      __pipeline_wait_prior(1);  // this lane's copy for chunk c has landed
+      if (sid_cur >= 0) stage_entry<true>(st + lane * kStride, sid_cur, raw_all[warp][chunk & 1][lane], f, xm, ym);
       __syncwarp();
+      sid_cur = sid_next;
+      sid_next = sid_after;
       const int cnt = min(32, L - base);
       unsigned word[PPL];
 #pragma unroll
@@ -344,6 +372,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
       __syncwarp();
     }
+    __pipeline_wait_prior(0);
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
       if (!px[j].inside) continue;
@@ -417,7 +447,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       }
       unsigned any = __reduce_or_sync(0xffffffffu, mine);
       if (!any) continue;
-      if ((any >> lane) & 1u) stage_entry<false>(st + lane * kStride, pairs[lo + base + lane], rec, rec64, f, 0.f, 0.f);
+      if ((any >> lane) & 1u) {
+        const int sid = pairs[lo + base + lane];
+        RawEntry re;
+        re.r0 = __ldg(&rec[sid].r0);
+        re.r1 = __ldg(&rec[sid].r1);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) re.v[q] = __ldg(&rec64[sid].v[q]);
+        stage_entry<false>(st + lane * kStride, sid, re, f, 0.f, 0.f);
+      }
       __syncwarp();
       while (any) {
         const int i = 31 - __clz(any);
