@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
+  __shared__ __align__(16) RawEntry raw_all[kWarpsPerBlock][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
   float* st = stage[warp];
@@ -436,27 +437,50 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     if (maxlast == 0) continue;
     const int lo = tile_ptr[t];
     const int cbase = chunk_ptr[t];
-    for (int chunk = (maxlast - 1) >> 5; chunk >= 0; --chunk) {
+    // Software pipeline over chunks (back to front): the contribution words
+    // and splat ids of chunk c-2 are loaded and the active records of chunk
+    // c-1 are copied (cp.async) while chunk c is processed.
+    auto load_words = [&](int c, unsigned (&wd)[PPL], int& sid) {
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) wd[j] = c >= 0 ? bitmask[(size_t)(cbase + c) * (TS * TS) + lane + 32 * j] : 0u;
+      sid = (c >= 0 && c * 32 + lane < tile_ptr[t + 1] - lo) ? pairs[lo + c * 32 + lane] : -1;
+    };
+    auto or_words = [&](const unsigned (&wd)[PPL]) {
+      unsigned m = 0u;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) m |= wd[j];
+      return __reduce_or_sync(0xffffffffu, m);
+    };
+    const int top = (maxlast - 1) >> 5;
+    unsigned wcur[PPL], wnext[PPL], wnn[PPL];
+    int scur, snext, snn;
+    load_words(top, wcur, scur);
+    unsigned any_cur = or_words(wcur);
+    if (((any_cur >> lane) & 1u) && scur >= 0) prefetch_entry(&raw_all[warp][top & 1][lane], scur, rec, rec64);
+    __pipeline_commit();
+    load_words(top - 1, wnext, snext);
+    for (int chunk = top; chunk >= 0; --chunk) {
       const int base = chunk * 32;
+      const unsigned any_next = or_words(wnext);
+      if (((any_next >> lane) & 1u) && snext >= 0)
+        prefetch_entry(&raw_all[warp][(chunk - 1) & 1][lane], snext, rec, rec64);
+      __pipeline_commit();
+      load_words(chunk - 2, wnn, snn);
       unsigned word[PPL];
-      unsigned mine = 0u;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) word[j] = base < last[j] ? wcur[j] : 0u;
+      unsigned any = any_cur;
+      __pipeline_wait_prior(1);  // this lane's copy for `chunk` has landed
+      if ((any >> lane) & 1u) stage_entry<false>(st + lane * kStride, scur, raw_all[warp][chunk & 1][lane], f, 0.f, 0.f);
+      __syncwarp();
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
-        word[j] = base < last[j] ? bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] : 0u;
-        mine |= word[j];
+        wcur[j] = wnext[j];
+        wnext[j] = wnn[j];
       }
-      unsigned any = __reduce_or_sync(0xffffffffu, mine);
-      if (!any) continue;
-      if ((any >> lane) & 1u) {
-        const int sid = pairs[lo + base + lane];
-        RawEntry re;
-        re.r0 = __ldg(&rec[sid].r0);
-        re.r1 = __ldg(&rec[sid].r1);
-#pragma unroll
-        for (int q = 0; q < 5; ++q) re.v[q] = __ldg(&rec64[sid].v[q]);
-        stage_entry<false>(st + lane * kStride, sid, re, f, 0.f, 0.f);
-      }
-      __syncwarp();
+      any_cur = any_next;
+      scur = snext;
+      snext = snn;
       while (any) {
         const int i = 31 - __clz(any);
         any &= ~(1u << i);
@@ -506,6 +530,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       }
       __syncwarp();
     }
+    __pipeline_wait_prior(0);
+    __syncwarp();
   }
 }
 
