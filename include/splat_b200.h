@@ -16,9 +16,11 @@
  *                             raw-space chain rule of mapping.py:479-494 when
  *                             raw_space = 1)
  *   ss_mapping_loss          mapping.py:128-196     range/normal/opacity losses
+ *   ss_reg_anchors           registration.py:190-213 sample_model (+ :430 thinning)
+ *   ss_range_image           geometry.py:252-268     build_range_image
  *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
- *                            the H/b accumulation of registration.py:470-477)
- *   ss_photo_objective       registration.py:379-384 _objective on a trial pose
+ *                            the H/b accumulation of registration.py:470-477,
+ *                            objective of registration.py:379-384)
  */
 #ifndef SPLAT_B200_H
 #define SPLAT_B200_H
@@ -128,23 +130,40 @@ int ss_mapping_loss(int32_t width, int32_t height, const float* range, const flo
                     double w_normal, double range_floor, float* dD, float* dN, float* dO,
                     double* parts4, void* stream);
 
-/* ---- photometric registration (registration.py:277-384) -------------- */
+/* ---- photometric registration (registration.py:170-384) -------------- */
 typedef struct {
   double huber_photo, trim_factor, spread_gate;
 } ss_reg_cfg;
 
-/* One linearisation: residuals of anchors X_w (M x 3, float32) against the
- * scan range image at pose T (row-major R then t), trimmed at
- * max(trim_factor*median|r|, trim_floor), Huber-weighted and reduced into
- * out[0:21] = upper-triangular sum J^T W J (row-major 6x6 upper),
- * out[21:27] = J^T W r, out[27] = Huber objective, out[28] = m (kept count),
- * out[29] = sum r^2.  Sums are unnormalised float64 (caller scales by 1/m).
- * `workspace` must hold at least ss_photo_workspace_bytes(M) bytes. */
+/* Anchors of sample_model (registration.py:190-213, 430): from a render of
+ * the model at pose_Rt on geo_cam (range D, opacity O, float32 device),
+ * pixels with O > vis_opacity and D > 0, minus range jumps > spread_gate,
+ * back-projected at depth D/O and mapped to the world; every `thin`-th kept
+ * pixel (row-major) becomes an anchor.  X_out: cap x 3 float64 (device).
+ * counts_out (host): [kept pixels, anchors].  Synchronises the stream.
+ * workspace: ss_anchor_workspace_bytes(width, height) bytes of device memory. */
+size_t ss_anchor_workspace_bytes(int32_t width, int32_t height);
+int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, const double* pose_Rt,
+                   double vis_opacity, double spread_gate, int32_t thin, double* X_out, int32_t cap,
+                   int32_t* counts_out, void* workspace, void* stream);
+
+/* build_range_image (geometry.py:252-268): sensor-frame points (n x 3
+ * float64, device) -> nearest range per pixel (float64 H*W) and valid mask. */
+int ss_range_image(const ss_camera* cam, const double* pts, int32_t n, double* range_out, uint8_t* valid_out,
+                   void* stream);
+
+/* One evaluation of _photo_system (registration.py:316-362) with Huber
+ * weights: residuals of anchors X_w (M x 3 float64) against the scan range
+ * image at pose T (row-major R then t), trimmed at
+ * max(trim_factor * median|r|, trim_floor), reduced into out30 (host):
+ *   [0:21] sum w J^T J (upper triangle, row-major), [21:27] sum w J^T r,
+ *   [27] sum Huber(r), [28] kept count m, [29] sum r^2   (unnormalised).
+ * objective_only = 1 skips the Jacobian (trial poses of the LM loop).
+ * workspace: ss_photo_workspace_bytes(M) bytes.  Synchronises the stream. */
 size_t ss_photo_workspace_bytes(int32_t M);
-int ss_photo_system(const float* X_w, int32_t M, const float* scan_range,
-                    const uint8_t* scan_valid, const ss_camera* cam, const double* T_Rt,
-                    double trim_floor, const ss_reg_cfg* cfg, double* out30, void* workspace,
-                    void* stream);
+int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
+                    const ss_camera* cam, const double* T_Rt, double trim_floor, const ss_reg_cfg* cfg,
+                    int32_t objective_only, double* out30, void* workspace, void* stream);
 
 /* Measured FP32 FMA throughput of the current device (TFLOP/s), the roofline
  * denominator of the FP32-bound blend kernels.  Synchronises the stream. */

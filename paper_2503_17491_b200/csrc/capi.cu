@@ -539,6 +539,117 @@ int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contri
   return SS_OK;
 }
 
+// ---- photometric registration ------------------------------------------------
+namespace {
+int make_regcam(const ss_camera* c, RegCam& r) {
+  CamK k;
+  const int st = make_camk(c, 8, 0.5, k);
+  if (st) return st;
+  r.W = k.W;
+  r.H = k.H;
+  r.fx = k.fx;
+  r.fy = k.fy;
+  r.cx = k.cx;
+  r.cy = k.cy;
+  r.off_u = k.off_u;
+  r.off_v = k.off_v;
+  return SS_OK;
+}
+bool full_circle(const ss_camera* c) {  // geometry.py:117-121
+  const double fov = c->az_max - c->az_min;
+  const double pitch = fov / (c->width - 1);
+  return fov + pitch >= 2.0 * SS_PI - 0.5 * pitch;
+}
+}  // namespace
+
+size_t ss_anchor_workspace_bytes(int32_t width, int32_t height) {
+  const size_t P = (size_t)width * height;
+  return P * 10 + ((P + 255) / 256 + 1) * 4 + 64;
+}
+
+int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, const double* pose_Rt,
+                   double vis_opacity, double spread_gate, int32_t thin, double* X_out, int32_t cap,
+                   int32_t* counts_out, void* workspace, void* stream) {
+  if (!geo_cam || !D || !O || !pose_Rt || !X_out || !counts_out || !workspace || thin < 1)
+    return SS_ERR_INVALID_ARGUMENT;
+  RegCam rc;
+  int st = make_regcam(geo_cam, rc);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int P = rc.W * rc.H;
+  const int nb = (P + 255) / 256;
+  unsigned char* w = (unsigned char*)workspace;
+  double* depth = (double*)w;
+  uint8_t* m = (uint8_t*)(w + (size_t)P * 8);
+  uint8_t* keep = m + P;
+  uint32_t* bsum = (uint32_t*)(((uintptr_t)(keep + P) + 15) & ~(uintptr_t)15);
+  int* counts = (int*)(bsum + nb + 1);
+  PoseK pk;
+  for (int q = 0; q < 9; ++q) pk.R[q] = pose_Rt[q];
+  for (int q = 0; q < 3; ++q) pk.t[q] = pose_Rt[9 + q];
+  k_anchor_depth<<<nb, 256, 0, s>>>(P, D, O, vis_opacity, depth, m);
+  k_anchor_keep<<<nb, 256, 0, s>>>(rc.W, rc.H, full_circle(geo_cam) ? 1 : 0, spread_gate, depth, m, keep, bsum);
+  k_excl_scan_small<<<1, 1024, 0, s>>>(nb, bsum);
+  k_anchor_emit<<<nb, 256, 0, s>>>(rc.W, rc.H, rc, pk, thin, depth, keep, bsum, X_out, cap, counts);
+  SS_CUDA_TRY(cudaGetLastError());
+  SS_CUDA_TRY(cudaMemcpyAsync(counts_out, counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  return SS_OK;
+}
+
+int ss_range_image(const ss_camera* cam, const double* pts, int32_t n, double* range_out, uint8_t* valid_out,
+                   void* stream) {
+  if (!cam || (!pts && n > 0) || !range_out || !valid_out || n < 0) return SS_ERR_INVALID_ARGUMENT;
+  RegCam rc;
+  int st = make_regcam(cam, rc);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int P = rc.W * rc.H;
+  unsigned long long* img = (unsigned long long*)range_out;
+  // +inf bit pattern in every pixel, then scatter-min of the point ranges
+  const double inf = __builtin_inf();
+  unsigned long long infbits;
+  std::memcpy(&infbits, &inf, sizeof(infbits));
+  SS_CUDA_TRY(cudaMemsetAsync(img, 0, sizeof(double) * P, s));
+  k_fill_u64<<<(P + 255) / 256, 256, 0, s>>>(P, img, infbits);
+  if (n > 0) k_range_scatter<<<(n + 255) / 256, 256, 0, s>>>(pts, n, rc, img);
+  k_range_finish<<<(P + 255) / 256, 256, 0, s>>>(P, img, valid_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+size_t ss_photo_workspace_bytes(int32_t M) { return (size_t)(M > 0 ? M : 1) * (sizeof(PhotoTmp) + 8) + 512; }
+
+int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
+                    const ss_camera* cam, const double* T_Rt, double trim_floor, const ss_reg_cfg* cfg,
+                    int32_t objective_only, double* out30, void* workspace, void* stream) {
+  if (!X_w || M <= 0 || !scan_range || !scan_valid || !cam || !T_Rt || !cfg || !out30 || !workspace)
+    return SS_ERR_INVALID_ARGUMENT;
+  RegCam rc;
+  int st = make_regcam(cam, rc);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* w = (unsigned char*)workspace;
+  PhotoTmp* tmp = (PhotoTmp*)w;
+  unsigned long long* bits = (unsigned long long*)(w + (size_t)M * sizeof(PhotoTmp));
+  double* dev_out = (double*)(w + (size_t)M * (sizeof(PhotoTmp) + 8));
+  double* median = dev_out + 30;
+  int* n_ok = (int*)(median + 1);
+  PoseK pk;
+  for (int q = 0; q < 9; ++q) pk.R[q] = T_Rt[q];
+  for (int q = 0; q < 3; ++q) pk.t[q] = T_Rt[9 + q];
+  SS_CUDA_TRY(cudaMemsetAsync(dev_out, 0, sizeof(double) * 32 + 16, s));
+  const int nb = (M + 255) / 256;
+  k_photo_resid<<<nb, 256, 0, s>>>(X_w, M, pk, rc, scan_range, scan_valid, cfg->spread_gate, tmp, bits, n_ok);
+  k_photo_median<<<1, 1024, 0, s>>>(bits, M, n_ok, median);
+  k_photo_accum<<<nb, 256, 0, s>>>(M, rc, tmp, bits, median, cfg->trim_factor, trim_floor, cfg->huber_photo,
+                                    objective_only, dev_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  SS_CUDA_TRY(cudaMemcpyAsync(out30, dev_out, sizeof(double) * 30, cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  return SS_OK;
+}
+
 int ss_mapping_loss(int32_t width, int32_t height, const float* range, const float* normal, const float* opacity,
                     const float* kf_range, const uint8_t* kf_valid, const float* kf_normal, const uint8_t* kf_nvalid,
                     double w_opacity, double w_normal, double range_floor, float* dD, float* dN, float* dO,

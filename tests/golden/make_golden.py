@@ -127,5 +127,65 @@ def main():
     make_case("partial", cam, m, p, random_pose(rng, 5.0, 0.2), RasterConfig(), rng)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def make_registration_case():
+    """Photometric registration on a small room scene (registration.py:387-524)."""
+    from splatscan import registration as REG
+    from splatscan.registration import RegistrationConfig, register
+    from splatscan.synth import ScanSpec, raycast_scan, room_with_boxes
+
+    rng = np.random.default_rng(7)
+    scene = room_with_boxes(n_boxes=4, seed=0)
+    spec = ScanSpec(width=256, height=32)
+    truth = SE3Pose(so3_exp(np.deg2rad([0.0, 0.0, 10.0])), np.array([0.3, -0.2, 0.1]))
+    sc = raycast_scan(scene, truth, spec)
+    scan_pts = f32(sc.cloud)
+    # splats on the visible surfaces (pkg/tests/conftest.py:38-51), float32-rounded
+    pts, normals = scene.visible_surface_points(9000, np.zeros((1, 3)), rng)
+    idx = rng.choice(pts.shape[0], min(3000, pts.shape[0]), replace=False)
+    pts, normals = pts[idx], normals[idx]
+    ref = np.where(np.abs(normals[:, 2:3]) < 0.9, [[0.0, 0.0, 1.0]], [[1.0, 0.0, 0.0]])
+    ta = np.cross(normals, ref)
+    ta /= np.linalg.norm(ta, axis=1, keepdims=True)
+    tb = np.cross(normals, ta)
+    p = dict(centers=pts, raw_t_alpha=ta, raw_t_beta=tb, log_scales=np.full((len(pts), 2), np.log(0.12)),
+             logit_opacity=np.full(len(pts), np.log(0.95 / 0.05)))
+    model, p = to_model(p)
+    initial = truth.compose(SE3Pose(so3_exp(np.deg2rad([1.0, -1.5, 2.0])), np.array([0.12, -0.08, 0.05])))
+    cfg = RegistrationConfig(mode="photometric", max_iters=15)
+    cam = sc.camera
+    # one linearisation at a pose off the anchor grid (at `initial` itself the
+    # anchors re-project exactly onto scan grid lines, where floor() is decided
+    # by the last ulp of numpy's own atan2)
+    T0 = initial.retract(np.array([2e-3, -1e-3, 1e-3, 1e-3, 2e-3, -1e-3]))
+    geo_cam = SphericalCamera(cam.width * 2, cam.height * 2, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    model_pts, _, _ = REG.sample_model(model, geo_cam, initial, cfg)
+    X_w = model_pts[::4]
+    scan_img = REG.build_range_image(cam, scan_pts)
+    sysr = REG._photo_system(X_w, scan_img, cam, T0, cfg, max(cfg.trim_floor_photo, 0.5))
+    r, J = sysr
+    w = REG._huber_weights(r, cfg.huber_photo)
+    H0 = (J.T * w) @ J
+    b0 = J.T @ (w * r)
+    res = register(model, scan_pts, cam, initial, cfg)
+    np.savez_compressed(
+        os.path.join(OUT, "golden_register.npz"),
+        cam=np.array([cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max]),
+        **{f"p_{k}": np.asarray(v, np.float32) for k, v in p.items()},
+        scan=np.asarray(scan_pts, np.float32), initial_R=initial.rotation, initial_t=initial.translation,
+        T0_R=T0.rotation, T0_t=T0.translation,
+        truth_R=truth.rotation, truth_t=truth.translation, n_model_pts=model_pts.shape[0], X_w=X_w,
+        scan_range=scan_img.range, scan_valid=scan_img.valid, H0=H0, b0=b0, m0=r.shape[0],
+        huber0=REG._huber_value(r, cfg.huber_photo), sum_r2_0=float(r @ r),
+        final_R=res.pose.rotation, final_t=res.pose.translation, iterations=res.iterations,
+        converged=res.converged, photo_rms=res.photo_rms, n_photo=res.n_photo,
+    )
+    err_t = np.linalg.norm(res.pose.translation - truth.translation)
+    print("register: anchors", X_w.shape[0], "m0", r.shape[0], "iters", res.iterations, "err_t", err_t)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "register":
+    make_registration_case()
