@@ -238,10 +238,15 @@ def run_b200(args, ws, rank, local):
     top = max(("forward", "backward"), key=lambda k: stage[k])
     achieved = flops[top] / (stage[top] * 1e-3) / 1e12
     step_flops = 92 * E + 204 * U + 300 * N
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"k_{top}<8>")
     roofline = {"bound": "fp32", "kernel": f"k_{top}<8>", "achieved": achieved, "peak": peak.value,
                 "unit": "TFLOP/s", "frac": achieved / peak.value,
                 "peak_source": "FFMA probe measured live (ss_fp32_peak_tflops); MEASURED_PEAKS.json has no FP32 figure",
-                "algorithmic_flops_per_launch": flops[top], "traffic": None,
+                "algorithmic_flops_per_launch": flops[top],
+                "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write, profiles/r01_traffic.json)",
                 "units": {"E_pair_evaluations": E, "U_contributions": U, "TP_tile_pairs": n_pairs, "N_splats": N},
                 "step_fraction": stage[top] / ms_step,
                 "step_achieved_tflops": step_flops / (ms_step * 1e-3) / 1e12}
