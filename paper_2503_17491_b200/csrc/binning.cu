@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
   for (int j = 0; j < kTileSortIPL; ++j) {
     const int i = tid + 256 * j;
     kk[j] = 0;
+    if (256 * j >= L) break;
     if (i < L) {
       const uint32_t v = pairs[lo + i];
       kk[j] = key32[v];
@@ -502,6 +503,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
 #pragma unroll
   for (int j = 0; j < kTileSortIPL; ++j) {
     const int i = tid + 256 * j;
+    if (256 * j >= L) break;
     if (i < L) sk[0][i] = (uint16_t)((kk[j] - kmin) >> shift);
   }
   __syncthreads();
@@ -518,8 +520,10 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
     int dg[kTileSortIPL];
 #pragma unroll
     for (int j = 0; j < kTileSortIPL; ++j) {
+      dg[j] = 256;
+      if (j * 32 >= seg) break;  // warp-uniform
       const int idx = warp * seg + j * 32 + lane;
-      const bool ok = (j * 32 < seg) && idx < L;
+      const bool ok = idx < L;
       dg[j] = ok ? (int)((sk[cur][idx] >> sh) & 0xffu) : 256;
       const uint32_t peers = __match_any_sync(0xffffffffu, dg[j]);
       const int leader = 31 - __clz(peers);
@@ -554,6 +558,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kTileSortIPL; ++j) {
+      if (j * 32 >= seg) break;
       if (dg[j] < 256) {
         const int idx = warp * seg + j * 32 + lane;
         const uint32_t pos = dtot[dg[j]] + wcnt[warp][dg[j]] + lr[j];
