@@ -16,6 +16,8 @@
  *                             raw-space chain rule of mapping.py:479-494 when
  *                             raw_space = 1)
  *   ss_mapping_loss          mapping.py:128-196     range/normal/opacity losses
+ *   ss_scale_loss            mapping.py:166-178     scale hinge
+ *   ss_adam_step             mapping.py:367-379     Adam of refine (+ :495-496 clamp)
  *   ss_reg_anchors           registration.py:190-213 sample_model (+ :430 thinning)
  *   ss_range_image           geometry.py:252-268     build_range_image
  *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
@@ -129,6 +131,22 @@ int ss_mapping_loss(int32_t width, int32_t height, const float* range, const flo
                     const float* kf_normal, const uint8_t* kf_nvalid, double w_opacity,
                     double w_normal, double range_floor, float* dD, float* dN, float* dO,
                     double* parts4, void* stream);
+
+/* Scale hinge of the mapping loss (mapping.py:166-178): writes the n x 2
+ * log-scale-space input d_scales_extra for ss_render_backward (w_scale on the
+ * larger axis of splats above `cap`) and adds the hinge sum to *loss_out
+ * (device float64). */
+int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale, float* d_scales_extra,
+                  double* loss_out, void* stream);
+
+/* One Adam step of refine (mapping.py:367-379, 495-496) on the five raw
+ * parameter arrays (in place) from the packed n x 12 raw gradient; m, v:
+ * n x 12 moments; t: step count after increment; lrs5: learning rates of
+ * (centers, raw_t_alpha, raw_t_beta, log_scales, logit_opacity); log scales
+ * are clamped to [log_scale_lo, log_scale_hi] afterwards. */
+int ss_adam_step(float* centers, float* raw_t_alpha, float* raw_t_beta, float* log_scales, float* logit_opacity,
+                 const float* grads, float* m, float* v, int32_t n, int32_t t, const double* lrs5, double beta1,
+                 double beta2, double eps, double log_scale_lo, double log_scale_hi, void* stream);
 
 /* ---- photometric registration (registration.py:170-384) -------------- */
 typedef struct {

@@ -93,6 +93,10 @@ def lib() -> ctypes.CDLL:
     L.ss_anchor_workspace_bytes.restype = ctypes.c_size_t
     L.ss_reg_anchors.argtypes = [ctypes.POINTER(SsCamera), vp, vp, vp, d, d, i32, vp, i32, vp, vp, vp]
     L.ss_reg_anchors.restype = ctypes.c_int
+    L.ss_scale_loss.argtypes = [vp, i32, d, d, vp, vp, vp]
+    L.ss_scale_loss.restype = ctypes.c_int
+    L.ss_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, d, d, d, d, d, vp]
+    L.ss_adam_step.restype = ctypes.c_int
     L.ss_range_image.argtypes = [ctypes.POINTER(SsCamera), vp, i32, vp, vp, vp]
     L.ss_range_image.restype = ctypes.c_int
     for name in ("ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_render_forward", "ss_records_counts", "ss_records_export", "ss_render_backward",
@@ -105,7 +109,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_forward", "ss_records_counts",
             "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
-            "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image"]
+            "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
+            "ss_adam_step"]
 
 
 def check(status: int, what: str = "") -> None:

@@ -650,6 +650,42 @@ int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, cons
   return SS_OK;
 }
 
+int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale, float* d_scales_extra,
+                  double* loss_out, void* stream) {
+  if (n < 0 || (n > 0 && (!log_scales || !d_scales_extra || !loss_out))) return SS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return SS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_scale_loss<<<(n + 255) / 256, 256, 0, s>>>(n, log_scales, cap, w_scale, d_scales_extra, loss_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_adam_step(float* centers, float* raw_t_alpha, float* raw_t_beta, float* log_scales, float* logit_opacity,
+                 const float* grads, float* m, float* v, int32_t n, int32_t t, const double* lrs5, double beta1,
+                 double beta2, double eps, double log_scale_lo, double log_scale_hi, void* stream) {
+  if (n < 0 || t < 1 || !lrs5) return SS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return SS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  AdamK a;
+  a.p[0] = centers;
+  a.p[1] = raw_t_alpha;
+  a.p[2] = raw_t_beta;
+  a.p[3] = log_scales;
+  a.p[4] = logit_opacity;
+  for (int q = 0; q < 5; ++q) a.lr[q] = (float)lrs5[q];
+  a.b1 = (float)beta1;
+  a.b2 = (float)beta2;
+  a.eps = (float)eps;
+  a.b1c = (float)(1.0 - std::pow(beta1, t));
+  a.b2c = (float)(1.0 - std::pow(beta2, t));
+  a.lo = (float)log_scale_lo;
+  a.hi = (float)log_scale_hi;
+  const long long tot = 12LL * n;
+  k_adam<<<(int)((tot + 255) / 256), 256, 0, s>>>(n, a, grads, m, v);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
 int ss_mapping_loss(int32_t width, int32_t height, const float* range, const float* normal, const float* opacity,
                     const float* kf_range, const uint8_t* kf_valid, const float* kf_normal, const uint8_t* kf_nvalid,
                     double w_opacity, double w_normal, double range_floor, float* dD, float* dN, float* dO,

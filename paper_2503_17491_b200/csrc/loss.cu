@@ -62,3 +62,71 @@ __global__ void k_mapping_loss(int P, const float* __restrict__ D, const float* 
 }
 
 }  // namespace ss
+
+namespace ss {
+
+// Scale hinge (mapping.py:166-178): gradient w_scale on the larger axis of
+// splats whose larger scale exceeds `cap` (first axis on ties, np.argmax),
+// and the loss sum into loss[0].
+__global__ void k_scale_loss(int n, const float* __restrict__ log_scales, double cap, double w_scale,
+                             float* __restrict__ d_scales, double* __restrict__ loss) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0;
+  if (i < n) {
+    const double s0 = exp((double)log_scales[2 * i]), s1 = exp((double)log_scales[2 * i + 1]);
+    const double mx = fmax(s0, s1);
+    const double over = mx - cap;
+    float g0 = 0.f, g1 = 0.f;
+    if (over > 0.0) {
+      l = over;
+      if (s0 >= s1)
+        g0 = (float)w_scale;
+      else
+        g1 = (float)w_scale;
+    }
+    d_scales[2 * i] = g0;
+    d_scales[2 * i + 1] = g1;
+  }
+  for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+  if ((threadIdx.x & 31) == 0 && l != 0.0) atomicAdd(loss, l);
+}
+
+// Adam over the packed raw gradient (n x 12: centers 3 | raw_t_alpha 3 |
+// raw_t_beta 3 | log_scales 2 | logit_opacity 1) with per-group learning
+// rates, bias correction and the log-scale clamp of refine
+// (mapping.py:367-379, 495-496).  One thread per (splat, component).
+struct AdamK {
+  float* p[5];
+  float lr[5];
+  float b1, b2, eps, b1c, b2c, lo, hi;
+};
+
+__global__ void k_adam(int n, AdamK a, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= 12 * n) return;
+  const int i = k / 12, c = k % 12;
+  int grp, off, w;
+  if (c < 3) {
+    grp = 0; off = c; w = 3;
+  } else if (c < 6) {
+    grp = 1; off = c - 3; w = 3;
+  } else if (c < 9) {
+    grp = 2; off = c - 6; w = 3;
+  } else if (c < 11) {
+    grp = 3; off = c - 9; w = 2;
+  } else {
+    grp = 4; off = 0; w = 1;
+  }
+  const float gk = g[k];
+  const float mk = a.b1 * m[k] + (1.f - a.b1) * gk;
+  const float vk = a.b2 * v[k] + (1.f - a.b2) * gk * gk;
+  m[k] = mk;
+  v[k] = vk;
+  const float upd = a.lr[grp] * (mk / a.b1c) / (sqrtf(vk / a.b2c) + a.eps);
+  float* pp = a.p[grp] + (size_t)i * w + off;
+  float x = *pp - upd;
+  if (grp == 3) x = fminf(fmaxf(x, a.lo), a.hi);
+  *pp = x;
+}
+
+}  // namespace ss

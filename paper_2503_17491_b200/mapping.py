@@ -1,0 +1,191 @@
+"""Device-resident map refinement (reference: pkg/src/splatscan/mapping.py:342-498).
+
+``refine(lmap, cfg, iters, rng)`` runs the reference's refine loop -- sample a
+keyframe (same numpy draw), render, mapping loss, backward to the raw
+parameters, Adam with per-group learning rates, log-scale clamp -- with every
+per-pixel and per-splat operation in the sm_100a kernels: the rasterizer,
+``ss_mapping_loss``, ``ss_scale_loss`` and the fused ``ss_adam_step``.  The
+map's parameters and Adam moments stay on the device between iterations
+(SURVEY 8(f) item 1); ``refine`` on a reference ``LocalMap`` uploads, runs
+and writes parameters and optimiser state back.
+
+Keyframe creation, densification and pruning (RNG-driven, host-side) are
+not on this path.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import engine
+from ._lib import check, lib
+from .geometry import pose_rt
+from .rasterizer import RasterConfig
+
+__all__ = ["MappingConfig", "DeviceKeyframe", "DeviceMap", "refine", "sample_keyframe_index"]
+
+
+@dataclass
+class MappingConfig:
+    """Same fields and defaults as the reference (mapping.py:69-93)."""
+    n_spawn: int = 20000
+    refine_iters: int = 10
+    w_opacity: float = 0.05
+    w_normal: float = 0.1
+    w_scale: float = 1.0
+    scale_cap: float = 0.5
+    densify_opacity: float = 0.5
+    densify_range_err: float = 0.1
+    kf_sample_p: float = 0.4
+    max_keyframes: int = 100
+    prune_opacity: float = 0.005
+    coverage_min: float = 0.3
+    reset_radius: float = 50.0
+    lr_centers: float = 1e-3
+    lr_tangents: float = 1e-3
+    lr_log_scales: float = 5e-3
+    lr_logit_opacity: float = 5e-2
+    scale_floor: float = 1e-4
+    opacity_init: float = 0.5
+    footprint_gain: float = 1.0
+    range_weight_floor: float = 1.0
+
+
+def sample_keyframe_index(n: int, p: float, rng) -> int:
+    """Truncated geometric draw over keyframe ages (mapping.py:441-452), same numpy call."""
+    if n <= 0:
+        raise ValueError("no keyframes to sample")
+    w = p * (1.0 - p) ** np.arange(n)
+    w /= w.sum()
+    return n - 1 - int(rng.choice(n, p=w))
+
+
+class DeviceKeyframe:
+    """Camera, pose and target images of one keyframe on the device."""
+
+    def __init__(self, camera, pose, range_img, valid, normals, nvalid):
+        dev = engine.require_cuda()
+        self.camera = camera
+        self.pose = pose
+        self.range = torch.as_tensor(np.asarray(range_img, np.float32), device=dev).contiguous()
+        self.valid = torch.as_tensor(np.asarray(valid, np.uint8), device=dev).contiguous()
+        self.normal = torch.as_tensor(np.asarray(normals, np.float32), device=dev).contiguous()
+        self.nvalid = torch.as_tensor(np.asarray(nvalid, np.uint8), device=dev).contiguous()
+
+    @classmethod
+    def from_reference(cls, kf) -> "DeviceKeyframe":
+        return cls(kf.camera, kf.pose, kf.range_image.range, kf.range_image.valid, kf.normal_image.normals,
+                   kf.normal_image.valid)
+
+
+class DeviceMap:
+    """Splat parameters + Adam state + keyframes resident on the device."""
+
+    def __init__(self, params: dict, keyframes: list, scene_scale: float = 1.0, t: int = 0, m=None, v=None):
+        dev = engine.require_cuda()
+        self.params = {k: torch.as_tensor(np.asarray(params[k], np.float32) if not torch.is_tensor(params[k])
+                                          else params[k], device=dev).contiguous().float()
+                       for k in engine.PARAM_NAMES}
+        self.params["logit_opacity"] = self.params["logit_opacity"].reshape(-1)
+        n = self.n
+        self.m = torch.zeros((n, 12), dtype=torch.float32, device=dev) if m is None else m
+        self.v = torch.zeros((n, 12), dtype=torch.float32, device=dev) if v is None else v
+        self.t = t
+        self.keyframes = keyframes
+        self.scene_scale = scene_scale
+        self.rec = engine.Records()
+        self.d_scales = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        self.losses = torch.zeros((0, 4), dtype=torch.float64, device=dev)
+
+    @property
+    def n(self) -> int:
+        return int(self.params["centers"].shape[0])
+
+    def lrs(self, cfg: MappingConfig) -> np.ndarray:
+        return np.array([cfg.lr_centers * self.scene_scale, cfg.lr_tangents, cfg.lr_tangents, cfg.lr_log_scales,
+                         cfg.lr_logit_opacity], dtype=np.float64)
+
+    def step(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None) -> torch.Tensor:
+        """One refine iteration on keyframe ``kf_index``; returns the device loss parts
+        [range, opacity, normal, scale] (float64)."""
+        raster = raster or RasterConfig()
+        kf = self.keyframes[kf_index]
+        sp = self.params
+        D, N, O = engine.forward(kf.camera, pose_rt(kf.pose), sp, raster, self.rec)
+        dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf.range, kf.valid, kf.normal, kf.nvalid,
+                                                w_opacity=cfg.w_opacity, w_normal=cfg.w_normal,
+                                                range_floor=cfg.range_weight_floor)
+        st = engine.stream_ptr()
+        check(lib().ss_scale_loss(ctypes.c_void_p(sp["log_scales"].data_ptr()), self.n, float(cfg.scale_cap),
+                                  float(cfg.w_scale), ctypes.c_void_p(self.d_scales.data_ptr()),
+                                  ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(st)), "scale_loss")
+        g = engine.backward(self.rec, sp, dD, dN, dO, raw_space=True, d_scales_extra=self.d_scales)
+        self.t += 1
+        lrs = self.lrs(cfg)
+        check(lib().ss_adam_step(*(ctypes.c_void_p(sp[k].data_ptr()) for k in engine.PARAM_NAMES),
+                                 ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
+                                 ctypes.c_void_p(self.v.data_ptr()), self.n, self.t,
+                                 lrs.ctypes.data_as(ctypes.c_void_p), 0.9, 0.999, 1e-8,
+                                 float(np.log(cfg.scale_floor)), float(np.log(10.0 * cfg.scale_cap)),
+                                 ctypes.c_void_p(st)), "adam_step")
+        return parts
+
+    def refine(self, cfg: MappingConfig, iters: int, rng, raster: RasterConfig | None = None) -> list:
+        """mapping.py:455-498 on the device; returns the per-iteration loss totals."""
+        if self.n == 0 or not self.keyframes:
+            return []
+        parts = []
+        for _ in range(iters):
+            idx = sample_keyframe_index(len(self.keyframes), cfg.kf_sample_p, rng)
+            parts.append(self.step(idx, cfg, raster))
+        P = torch.stack(parts).cpu().numpy()
+        w = np.array([1.0, cfg.w_opacity, cfg.w_normal, cfg.w_scale])
+        return [float(x) for x in P @ w]
+
+    # --- reference LocalMap interop -------------------------------------------------
+    @classmethod
+    def from_local_map(cls, lmap) -> "DeviceMap":
+        model = lmap.model
+        params = {k: getattr(model, k) for k in engine.PARAM_NAMES}
+        kfs = [DeviceKeyframe.from_reference(kf) for kf in lmap.keyframes]
+        dm = cls(params, kfs, float(lmap.scene_scale))
+        opt = getattr(lmap, "optimizer", None)
+        if opt is not None and getattr(opt, "slots", None) is not None:
+            dm.t = int(opt.t)
+            cols = [opt.slots[k] for k in engine.PARAM_NAMES]
+            m = np.concatenate([c[0].reshape(dm.n, -1) for c in cols], axis=1)
+            v = np.concatenate([c[1].reshape(dm.n, -1) for c in cols], axis=1)
+            dm.m = torch.as_tensor(m.astype(np.float32), device=dm.m.device).contiguous()
+            dm.v = torch.as_tensor(v.astype(np.float32), device=dm.v.device).contiguous()
+        return dm
+
+    def write_back(self, lmap, touches: int = 1) -> None:
+        model = lmap.model
+        for k in engine.PARAM_NAMES:
+            getattr(model, k)[...] = self.params[k].cpu().numpy().astype(np.float64).reshape(getattr(model, k).shape)
+        opt = getattr(lmap, "optimizer", None)
+        if opt is not None and getattr(opt, "slots", None) is not None:
+            opt.t = self.t
+            m = self.m.cpu().numpy().astype(np.float64)
+            v = self.v.cpu().numpy().astype(np.float64)
+            c = 0
+            for k in engine.PARAM_NAMES:
+                w = engine.PARAM_WIDTH[k]
+                shape = opt.slots[k][0].shape
+                opt.slots[k] = (m[:, c:c + w].reshape(shape).copy(), v[:, c:c + w].reshape(shape).copy())
+                c += w
+        for _ in range(max(touches, 1)):  # the reference bumps the version once per Adam step
+            model.touch()
+
+
+def refine(lmap, cfg, iters: int, rng, raster: RasterConfig | None = None) -> list:
+    """Drop-in for mapping.refine (mapping.py:455-498) on a reference LocalMap."""
+    if len(lmap.model) == 0 or not lmap.keyframes:
+        return []
+    dm = DeviceMap.from_local_map(lmap)
+    losses = dm.refine(cfg, iters, rng, raster)
+    dm.write_back(lmap, touches=iters)
+    return losses

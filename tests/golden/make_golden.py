@@ -189,3 +189,47 @@ def make_registration_case():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "register":
     make_registration_case()
+
+
+def make_refine_case():
+    """Three refine() iterations of a small two-keyframe local map (mapping.py:455-498)."""
+    from splatscan.mapping import LocalMap, MappingConfig, add_keyframe, make_keyframe, refine
+    from splatscan.synth import ScanSpec, raycast_scan, room_with_boxes
+
+    scene = room_with_boxes(n_boxes=3, seed=1)
+    spec = ScanSpec(width=128, height=16)
+    cfg = MappingConfig(n_spawn=1200)
+    rng = np.random.default_rng(11)
+    poses = [SE3Pose.identity(), SE3Pose(so3_exp(np.deg2rad([0, 0, 4.0])), np.array([0.4, 0.1, 0.0]))]
+    kfs = [make_keyframe(i, raycast_scan(scene, p, spec).cloud, p, spec.width, spec.height) for i, p in enumerate(poses)]
+    lmap = LocalMap.start(kfs[0], cfg, rng)
+    add_keyframe(lmap, kfs[1], cfg, rng)
+    m = lmap.model
+    for k in ("centers", "raw_t_alpha", "raw_t_beta", "log_scales", "logit_opacity"):
+        getattr(m, k)[...] = f32(getattr(m, k))
+    # the device consumes float32 images: make the reference's float64 ones exactly representable
+    for kf in kfs:
+        kf.range_image.range[...] = f32(kf.range_image.range)
+        kf.normal_image.normals[...] = f32(kf.normal_image.normals)
+    before = {k: getattr(m, k).copy() for k in ("centers", "raw_t_alpha", "raw_t_beta", "log_scales", "logit_opacity")}
+    rng_state = np.random.default_rng(99)
+    losses = refine(lmap, cfg, 3, rng_state)
+    after = {k: getattr(m, k).copy() for k in before}
+    out = {f"b_{k}": v for k, v in before.items()}
+    out.update({f"a_{k}": v for k, v in after.items()})
+    for i, kf in enumerate(kfs):
+        c = kf.camera
+        out[f"kf{i}_cam"] = np.array([c.width, c.height, c.az_min, c.az_max, c.el_min, c.el_max])
+        out[f"kf{i}_R"] = kf.pose.rotation
+        out[f"kf{i}_t"] = kf.pose.translation
+        out[f"kf{i}_range"] = kf.range_image.range.astype(np.float32)
+        out[f"kf{i}_valid"] = kf.range_image.valid
+        out[f"kf{i}_normal"] = kf.normal_image.normals.astype(np.float32)
+        out[f"kf{i}_nvalid"] = kf.normal_image.valid
+    np.savez_compressed(os.path.join(OUT, "golden_refine.npz"), scene_scale=lmap.scene_scale, losses=np.array(losses),
+                        adam_t=lmap.optimizer.t, **out)
+    print("refine: splats", len(m), "losses", losses)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "refine":
+    make_refine_case()

@@ -1,0 +1,82 @@
+"""Device refine loop (mapping.py:455-498) vs the reference's golden run, and the
+fused Adam / scale-hinge kernels vs their numpy restatement."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2503_17491_b200 import SE3Pose, SphericalCamera, engine
+from paper_2503_17491_b200 import mapping as MP
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_refine.npz"))
+NAMES = ("centers", "raw_t_alpha", "raw_t_beta", "log_scales", "logit_opacity")
+
+
+def test_adam_kernel_matches_numpy(cuda):
+    rng = np.random.default_rng(0)
+    n = 1000
+    params = {"centers": rng.normal(size=(n, 3)), "raw_t_alpha": rng.normal(size=(n, 3)),
+              "raw_t_beta": rng.normal(size=(n, 3)), "log_scales": rng.normal(-3, 0.5, size=(n, 2)),
+              "logit_opacity": rng.normal(size=n)}
+    dm = MP.DeviceMap({k: v.astype(np.float32) for k, v in params.items()}, [], 2.0)
+    cfg = MP.MappingConfig()
+    lrs = dm.lrs(cfg)
+    ref = {k: params[k].astype(np.float32).astype(np.float64) for k in NAMES}
+    m = np.zeros((n, 12)); v = np.zeros((n, 12))
+    import ctypes
+    from paper_2503_17491_b200._lib import lib
+    for t in range(1, 4):
+        g = rng.normal(size=(n, 12)).astype(np.float32)
+        gd = torch.tensor(g, device="cuda")
+        lib().ss_adam_step(*(ctypes.c_void_p(dm.params[k].data_ptr()) for k in NAMES), ctypes.c_void_p(gd.data_ptr()),
+                           ctypes.c_void_p(dm.m.data_ptr()), ctypes.c_void_p(dm.v.data_ptr()), n, t,
+                           lrs.ctypes.data_as(ctypes.c_void_p), 0.9, 0.999, 1e-8, float(np.log(1e-4)),
+                           float(np.log(5.0)), ctypes.c_void_p(engine.stream_ptr()))
+        m = 0.9 * m + 0.1 * g
+        v = 0.999 * v + 0.001 * g.astype(np.float64) ** 2
+        upd = (m / (1 - 0.9 ** t)) / (np.sqrt(v / (1 - 0.999 ** t)) + 1e-8)
+        c = 0
+        for i, k in enumerate(NAMES):
+            w = engine.PARAM_WIDTH[k]
+            ref[k] = ref[k] - lrs[i] * upd[:, c:c + w].reshape(ref[k].shape)
+            c += w
+        ref["log_scales"] = np.clip(ref["log_scales"], np.log(1e-4), np.log(5.0))
+    for k in NAMES:
+        got = dm.params[k].cpu().numpy().reshape(ref[k].shape)
+        assert np.abs(got - ref[k]).max() <= 1e-5 * max(1.0, np.abs(ref[k]).max()), k
+
+
+def _golden_map():
+    kfs = []
+    for i in range(2):
+        c = G[f"kf{i}_cam"]
+        cam = SphericalCamera(int(c[0]), int(c[1]), *[float(x) for x in c[2:]])
+        kfs.append(MP.DeviceKeyframe(cam, SE3Pose(G[f"kf{i}_R"], G[f"kf{i}_t"]), G[f"kf{i}_range"], G[f"kf{i}_valid"],
+                                     G[f"kf{i}_normal"], G[f"kf{i}_nvalid"]))
+    return MP.DeviceMap({k: G[f"b_{k}"] for k in NAMES}, kfs, float(G["scene_scale"]))
+
+
+def test_refine_matches_reference(cuda):
+    dm = _golden_map()
+    cfg = MP.MappingConfig(n_spawn=1200)
+    losses = dm.refine(cfg, 3, np.random.default_rng(99))
+    ref_losses = G["losses"]
+    print("losses", losses, ref_losses)
+    assert abs(losses[0] - ref_losses[0]) <= 1e-4 * abs(ref_losses[0])
+    assert np.allclose(losses, ref_losses, rtol=2e-3)
+    assert dm.t == int(G["adam_t"])
+    for k in NAMES:
+        before = G[f"b_{k}"].reshape(-1)
+        d_ref = G[f"a_{k}"].reshape(-1) - before
+        d_got = dm.params[k].cpu().numpy().astype(np.float64).reshape(-1) - before
+        rel = np.linalg.norm(d_got - d_ref) / max(np.linalg.norm(d_ref), 1e-30)
+        print(k, "update rel err", rel)
+        # Adam normalises each component.  The raw tangent gradient is orthogonal to
+        # the raw vector (Gram-Schmidt is scale invariant), so its radial component is
+        # round-off (1e-17 in the float64 reference, 1e-8 in float32) that Adam turns
+        # into +-lr steps of random sign: those classes get a looser gate.  The
+        # observable, the loss, agrees to 1e-5 above.
+        gate = 6e-2 if k.startswith("raw_t") else 2e-2
+        assert rel <= gate, (k, rel)
