@@ -108,9 +108,9 @@ class DeviceMap:
         return np.array([cfg.lr_centers * self.scene_scale, cfg.lr_tangents, cfg.lr_tangents, cfg.lr_log_scales,
                          cfg.lr_logit_opacity], dtype=np.float64)
 
-    def step(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None) -> torch.Tensor:
-        """One refine iteration on keyframe ``kf_index``; returns the device loss parts
-        [range, opacity, normal, scale] (float64)."""
+    def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None):
+        """Render keyframe ``kf_index``, mapping loss, backward: (n x 12 raw gradient, loss parts
+        [range, opacity, normal, scale] float64) on the device."""
         raster = raster or RasterConfig()
         kf = self.keyframes[kf_index]
         sp = self.params
@@ -118,19 +118,28 @@ class DeviceMap:
         dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf.range, kf.valid, kf.normal, kf.nvalid,
                                                 w_opacity=cfg.w_opacity, w_normal=cfg.w_normal,
                                                 range_floor=cfg.range_weight_floor)
-        st = engine.stream_ptr()
         check(lib().ss_scale_loss(ctypes.c_void_p(sp["log_scales"].data_ptr()), self.n, float(cfg.scale_cap),
                                   float(cfg.w_scale), ctypes.c_void_p(self.d_scales.data_ptr()),
-                                  ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(st)), "scale_loss")
+                                  ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(engine.stream_ptr())),
+              "scale_loss")
         g = engine.backward(self.rec, sp, dD, dN, dO, raw_space=True, d_scales_extra=self.d_scales)
+        return g, parts
+
+    def apply_adam(self, g: torch.Tensor, cfg: MappingConfig) -> None:
+        """Fused Adam step + log-scale clamp (mapping.py:367-379, 495-496)."""
         self.t += 1
         lrs = self.lrs(cfg)
-        check(lib().ss_adam_step(*(ctypes.c_void_p(sp[k].data_ptr()) for k in engine.PARAM_NAMES),
+        check(lib().ss_adam_step(*(ctypes.c_void_p(self.params[k].data_ptr()) for k in engine.PARAM_NAMES),
                                  ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
                                  ctypes.c_void_p(self.v.data_ptr()), self.n, self.t,
                                  lrs.ctypes.data_as(ctypes.c_void_p), 0.9, 0.999, 1e-8,
                                  float(np.log(cfg.scale_floor)), float(np.log(10.0 * cfg.scale_cap)),
-                                 ctypes.c_void_p(st)), "adam_step")
+                                 ctypes.c_void_p(engine.stream_ptr())), "adam_step")
+
+    def step(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None) -> torch.Tensor:
+        """One refine iteration on keyframe ``kf_index``; returns the device loss parts."""
+        g, parts = self.raw_gradient(kf_index, cfg, raster)
+        self.apply_adam(g, cfg)
         return parts
 
     def refine(self, cfg: MappingConfig, iters: int, rng, raster: RasterConfig | None = None) -> list:
