@@ -63,6 +63,20 @@ def splats_to_device(model, device=None) -> dict:
     return out
 
 
+def as_device_params(x) -> dict:
+    """float32 CUDA tensors from a SplatModel, a dict of numpy arrays, or a dict of tensors."""
+    if not isinstance(x, dict):
+        return splats_to_device(x)
+    dev = require_cuda()
+    out = {}
+    for k in PARAM_NAMES:
+        v = x[k]
+        t = v if torch.is_tensor(v) else torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float32)))
+        t = t.to(dev, torch.float32).contiguous()
+        out[k] = t.reshape(-1) if k == "logit_opacity" else t.reshape(-1, PARAM_WIDTH[k])
+    return out
+
+
 class Records:
     """Owner of one ss_records handle (tile lists + per-pixel blend state)."""
 

@@ -90,10 +90,7 @@ def sample_anchors(model_or_params, geo_cam, pose, cfg: RegistrationConfig, rast
 
     Returns (X float64 [n,3] device tensor, number of confident pixels)."""
     raster = raster or RasterConfig()
-    if isinstance(model_or_params, dict):
-        params = model_or_params
-    else:
-        params = engine.splats_to_device(model_or_params)
+    params = engine.as_device_params(model_or_params)
     rec = engine.Records.acquire()
     try:
         D, N, O = engine.forward(geo_cam, pose_rt(pose), params, raster, rec)

@@ -163,3 +163,121 @@ def config(index: int) -> dict:
 
 def random_pose(rng, rot_deg: float, trans: float) -> SE3Pose:
     return SE3Pose(so3_exp(np.deg2rad(rot_deg) * rng.normal(size=3)), rng.normal(size=3) * trans)
+
+
+# --- configs 2 and 3 ----------------------------------------------------------------
+
+def _complete_frames(n: np.ndarray):
+    """Orthonormal tangents with t_alpha x t_beta = n (mapping.py:242-251 construction)."""
+    ref = np.tile([0.0, 0.0, 1.0], (n.shape[0], 1))
+    ref[np.abs(n[:, 2]) > 0.9] = [1.0, 0.0, 0.0]
+    ta = np.cross(n, ref)
+    ta /= np.linalg.norm(ta, axis=1, keepdims=True)
+    return ta, np.cross(n, ta)
+
+
+def keyframe_poses(n: int = 10, seed: int = 0):
+    """Straight 1 m/frame trajectory with yaw noise N(0, 2 deg) (BASELINE config 2)."""
+    rng = np.random.default_rng(seed)
+    return [SE3Pose(so3_exp([0.0, 0.0, np.deg2rad(2.0) * rng.normal()]), np.array([float(i), 0.0, 0.0]))
+            for i in range(n)]
+
+
+def config2_map(n_keyframes: int = 10, per_keyframe: int = 20_000, seed: int = 0, width: int = 1024,
+                height: int = 64):
+    """Local map of BASELINE config 2: keyframes of the procedural scene and surfels
+    back-projected from them (spawn_splats construction, mapping.py:254-303: keyframe
+    normal or facing the sensor, pixel-footprint scales, opacity 0.5), 20k per keyframe."""
+    rng = np.random.default_rng(seed)
+    scene = Scene(0)
+    cam = synth_camera(width, height)
+    kfs, cents, tas, tbs, ls = [], [], [], [], []
+    for pose in keyframe_poses(n_keyframes, seed):
+        tg = target_images(scene, cam, pose)
+        kfs.append((cam, pose, tg))
+        idx = np.flatnonzero(tg["valid"].ravel())
+        idx = rng.choice(idx, size=min(per_keyframe, idx.size), replace=False)
+        rows, cols = np.unravel_index(idx, tg["valid"].shape)
+        d = tg["range"][rows, cols].astype(np.float64)
+        dirs = cam.pixel_directions[rows, cols]
+        pts = d[:, None] * dirs
+        n_s = np.where(tg["nvalid"][rows, cols][:, None], tg["normal"][rows, cols], -dirs)
+        n_s /= np.linalg.norm(n_s, axis=1, keepdims=True)
+        ta, tb = _complete_frames(n_s @ pose.rotation.T)
+        cents.append(pose.apply(pts))
+        tas.append(ta)
+        tbs.append(tb)
+        pa, pe = 1.0 / abs(cam.fx), 1.0 / abs(cam.fy)
+        ls.append(np.log(np.maximum(np.stack([d * pa, d * pe], axis=1), 1e-4)))
+    f = lambda a: np.ascontiguousarray(np.concatenate(a), dtype=np.float32)  # noqa: E731
+    n = sum(c.shape[0] for c in cents)
+    params = {"centers": f(cents), "raw_t_alpha": f(tas), "raw_t_beta": f(tbs), "log_scales": f(ls),
+              "logit_opacity": np.zeros(n, dtype=np.float32)}
+    ranges = np.concatenate([k[2]["range"][k[2]["valid"]] for k in kfs[:1]])
+    return params, kfs, float(np.median(ranges))
+
+
+def surface_samples(scene: Scene, n: int, rng, inside: float = 30.0):
+    """Area-weighted uniform samples on the scene's rectangles (clipped to the walled
+    area |x|, |y| <= inside, the only part a sensor inside can see) and box faces."""
+    faces = []  # (origin, e_u, e_v, half_u, half_v, normal)
+    for ax, off, cen, half in scene.rects:
+        half = (min(half[0], inside), min(half[1], inside))
+        others = [a for a in range(3) if a != ax]
+        o = np.zeros(3); o[ax] = off; o[others[0]] = cen[0]; o[others[1]] = cen[1]
+        eu = np.zeros(3); eu[others[0]] = 1.0
+        ev = np.zeros(3); ev[others[1]] = 1.0
+        nn = np.zeros(3); nn[ax] = 1.0
+        faces.append((o, eu, ev, half[0], half[1], nn))
+    for lo, hi in zip(scene.box_lo, scene.box_hi):
+        c, h = 0.5 * (lo + hi), 0.5 * (hi - lo)
+        for ax in range(3):
+            others = [a for a in range(3) if a != ax]
+            for sgn in (-1.0, 1.0):
+                o = c.copy(); o[ax] += sgn * h[ax]
+                eu = np.zeros(3); eu[others[0]] = 1.0
+                ev = np.zeros(3); ev[others[1]] = 1.0
+                nn = np.zeros(3); nn[ax] = sgn
+                faces.append((o, eu, ev, h[others[0]], h[others[1]], nn))
+    area = np.array([4 * f[3] * f[4] for f in faces])
+    cnt = rng.multinomial(n, area / area.sum())
+    pts, nrm = [], []
+    for f, k in zip(faces, cnt):
+        if k == 0:
+            continue
+        u = rng.uniform(-1, 1, k)[:, None] * f[3]
+        v = rng.uniform(-1, 1, k)[:, None] * f[4]
+        pts.append(f[0] + u * f[1] + v * f[2])
+        nrm.append(np.tile(f[5], (k, 1)))
+    return np.concatenate(pts), np.concatenate(nrm)
+
+
+def config3_problem(n_surfels: int = 300_000, seed: int = 0, width: int = 1024, height: int = 64):
+    """BASELINE config 3: a map of surfels on the visible surfaces of the procedural scene
+    (scale 0.08 m, opacity 0.95; conftest.surface_model construction), a scan ray-cast at
+    the true pose, and an initial pose perturbed by N(0, 0.2 m) / N(0, 2 deg) per axis."""
+    rng = np.random.default_rng(seed)
+    scene = Scene(0)
+    pts, nrm = surface_samples(scene, 3 * n_surfels, rng)
+    seen = np.zeros(pts.shape[0], dtype=bool)
+    for vp in (np.zeros(3), np.array([2.0, 0, 0]), np.array([-2.0, 0, 0])):
+        rest = np.flatnonzero(~seen)
+        vec = pts[rest] - vp
+        dist = np.linalg.norm(vec, axis=1)
+        t, _ = scene.raycast(vp, vec / np.maximum(dist, 1e-9)[:, None])
+        seen[rest[t >= dist - 1e-4]] = True
+    idx = np.flatnonzero(seen)
+    idx = rng.choice(idx, size=min(n_surfels, idx.size), replace=False)
+    pts, nrm = pts[idx], nrm[idx]
+    ta, tb = _complete_frames(nrm)
+    m = pts.shape[0]
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    params = {"centers": f(pts), "raw_t_alpha": f(ta), "raw_t_beta": f(tb),
+              "log_scales": np.full((m, 2), np.log(0.08), np.float32),
+              "logit_opacity": np.full(m, np.log(0.95 / 0.05), np.float32)}
+    truth = SE3Pose.identity()
+    cam = synth_camera(width, height)
+    tg = target_images(scene, cam, truth)
+    scan = (tg["range"][tg["valid"]][:, None].astype(np.float64) * cam.pixel_directions[tg["valid"]])
+    initial = truth.compose(SE3Pose(so3_exp(np.deg2rad(2.0) * rng.normal(size=3)), 0.2 * rng.normal(size=3)))
+    return params, cam, scan, truth, initial
