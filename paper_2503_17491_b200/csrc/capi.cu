@@ -414,10 +414,9 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
                        const float* dO, const float* d_scales_extra, float* grads, int raw_space, void* stream) {
   ss_records* rec = const_cast<ss_records*>(rec_c);
   if (!rec) return SS_ERR_STALE_RECORDS;
-  if (rec->pending) {
-    int cs = ss_records_check(rec, 0);  // stream order covers a forward still in flight
-    if (cs) return cs;
-  }
+  // A forward still in flight (or being captured into a CUDA graph) is fine:
+  // stream order covers it and the kernels skip work if its capacity
+  // overflowed; completed forwards must have been valid.
   if (!rec->pending && !rec->valid) return SS_ERR_STALE_RECORDS;
   if (!splats || splats->n != rec->n) return SS_ERR_STALE_RECORDS;
   if (!dD || !dN || !dO || !grads) return SS_ERR_INVALID_ARGUMENT;
