@@ -331,9 +331,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       sid_cur = sid_next;
       sid_next = sid_after;
       const int cnt = min(32, L - base);
-      unsigned word[PPL];
+      unsigned word[PPL], cw[PPL];
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) word[j] = 0u;
+      for (int j = 0; j < PPL; ++j) word[j] = cw[j] = 0u;
+#ifdef SS_FWD_PERENTRY
       for (int i = 0; i < cnt; ++i) {
         const float* e = st + i * kStride;
         const float4 c0 = *reinterpret_cast<const float4*>(e);
@@ -368,6 +369,48 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
           if (T[j] < bp.min_T) live[j] = false;
         }
       }
+#else
+      // phase A: branch-free cone test of every (pixel, entry) -> candidate bits
+      for (int i = 0; i < cnt; ++i) {
+        const float* e = st + i * kStride;
+        const float4 c0 = *reinterpret_cast<const float4*>(e);
+        const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          const float* p = px[j].p;
+          const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
+          cw[j] |= (q <= 0.f ? 1u : 0u) << i;
+        }
+      }
+      // phase B: every lane walks its own candidates front to back (packed: no
+      // lane idles on another pixel's candidate entry)
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        unsigned m = live[j] ? cw[j] : 0u;
+        while (m) {
+          const int i = __ffs(m) - 1;
+          m &= m - 1;
+          Entry x;
+          load_entry(st + i * kStride, x);
+          Hit h;
+          intersect(x, px[j], bp, h);
+          if (!h.use) continue;
+          const float w = h.alpha * T[j];
+          D[j] += w * h.lam;
+          O[j] += w;
+          N[j][0] += w * x.n[0];
+          N[j][1] += w * x.n[1];
+          N[j][2] += w * x.n[2];
+          T[j] *= (1.f - h.alpha);
+          word[j] |= 1u << i;
+          last[j] = base + i + 1;
+          if (T[j] < bp.min_T) {
+            live[j] = false;
+            m = 0u;
+          }
+        }
+      }
+#endif
 #pragma unroll
       for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
       __syncwarp();
