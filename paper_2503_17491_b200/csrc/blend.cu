@@ -50,6 +50,7 @@ constexpr int kWarpsPerBlock = 4;
 // 32-bit words per staged entry: 12 floats (+4 spare) and 5 double2 (144 B).
 // The 144-byte stride keeps the staging lanes' 16-byte stores conflict-free.
 constexpr int kStride = 36;
+constexpr int kBwdDynSmem = kWarpsPerBlock * 32 * 16 * 4;
 
 struct BlendParams {
   CamK cam;
@@ -262,6 +263,40 @@ __device__ __forceinline__ float warp_reduce_scatter16(float (&a)[16], int lane)
   return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
+// Reduce-scatter of 16 per-lane values through a 32x16 shared-memory
+// transpose (2 KB per warp): lane l stores its row (4 x STS.128, slot
+// swizzled by (l >> 1) & 3 so every quarter-warp store is conflict free),
+// then sums column l & 15 over the 16 rows of its half-warp (rows of the two
+// halves alternate parity, so each LDS is conflict free) and one shuffle
+// adds the other half.  Afterwards lanes l and l + 16 hold the warp sum of
+// value l & 15.  ~40 instructions against ~62 for the shuffle butterfly.
+__device__ __forceinline__ void red_offsets(int lane, int (&o)[8]) {
+  const int h = lane >> 4, c = lane & 15;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int col = 4 * ((c >> 2) ^ x) + (c & 3);
+    o[x] = 256 * h + 16 * h + col;      // even k: row 16h + k + h
+    o[4 + x] = 256 * h - 16 * h + col;  // odd k:  row 16h + k - h
+  }
+}
+
+__device__ __forceinline__ float red_transpose16(const float (&a)[16], float* red, const int (&o)[8], int lane) {
+  float4* row = reinterpret_cast<float4*>(red + lane * 16);
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) row[q ^ sw] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+  __syncwarp();
+  float v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = red[o[(k & 1) * 4 + ((k >> 1) & 3)] + 16 * k];
+  __syncwarp();
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1)
+#pragma unroll
+    for (int k = 0; k < s; ++k) v[k] += v[k + s];
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
 // Warp-uniform tile ticket (persistent warps, longest lists first).
 __device__ __forceinline__ int next_tile(int* counter, const int* order, int ntiles, int lane) {
   int ti = 0;
@@ -446,9 +481,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
   if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   __shared__ __align__(16) RawEntry raw_all[kWarpsPerBlock][2][32];
+  extern __shared__ __align__(16) float4 bwd_dyn_smem[];  // kBwdDynSmem: the reduce-scatter transposes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
   float* st = stage[warp];
+  float* red = reinterpret_cast<float*>(bwd_dyn_smem) + warp * 512;
+  int roff[8];
+  red_offsets(lane, roff);
   for (int t = next_tile(counter, order, ntiles, lane); t >= 0; t = next_tile(counter, order, ntiles, lane)) {
     const int tr = t / k.tx, tc = t % k.tx;
     TileFrame f;
@@ -567,9 +606,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
           Sn[j][2] += w * x.n[2];
           T[j] = Tb;
         }
+#ifdef SS_BWD_BUTTERFLY
         const float tot = warp_reduce_scatter16(a, lane);
         const int vi = (lane >> 1) & 15;
         if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
+#else
+        const float tot = red_transpose16(a, red, roff, lane);
+        if (lane < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + lane], tot);
+#endif
       }
       __syncwarp();
     }

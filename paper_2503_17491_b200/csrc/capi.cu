@@ -207,6 +207,8 @@ void set_smem_attrs() {
   const int bytes = (int)(sizeof(uint32_t) * kMaxTiles);
   cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_backward<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   done = true;
 }
 }  // namespace
@@ -428,17 +430,18 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   const int ntiles = rec->ntiles;
   const int* tile_ptr = rec->tiles;
   const int* chunk_ptr = rec->tiles + (ntiles + 1);
+  set_smem_attrs();
   {
     const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
     int* order = rec->tiles + 5 * (ntiles + 1);
     int* counters = rec->misc + 4;
     StageTimer tm(rec, ST_BACKWARD, s);
     if (rec->cam.T == 8)
-      k_backward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      k_backward<8><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
                                                            rec->acc, rec->misc + 1, order, counters + 1);
     else
-      k_backward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
+      k_backward<16><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
                                                             dN, dO, rec->acc, rec->misc + 1, order, counters + 1);
     SS_CUDA_TRY(cudaGetLastError());
