@@ -206,6 +206,20 @@ __device__ __forceinline__ void load_entry(const float* e, Entry& x) {
   x.k2[0] = d.x; x.k2[1] = d.y; x.k2[2] = g.x;
 }
 
+// Flush-to-zero approximate reciprocal / exp2 (one MUFU each; the IEEE
+// wrappers around MUFU.RCP / MUFU.EX2 cost four extra instructions per call
+// for subnormal operands that never pass the cutoffs).
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct Hit {
   float sa, sb, lam, r, G, alpha;
   bool use, clamped;
@@ -217,14 +231,14 @@ __device__ __forceinline__ void intersect(const Entry& x, const Pix& p, const Bl
   const float w1 = (float)(p.w * x.kt[1] + p.x * x.k1[1] + p.y * x.k2[1]);
   const float w2 = (float)(p.w * x.kt[2] + p.x * x.k1[2] + p.y * x.k2[2]);
   bool ok = p.ray_ok && fabsf(w2) >= bp.denom_eps;
-  const float r = __fdividef(1.f, w2);
+  const float r = rcp_ftz(w2);
   h.r = r;
   h.sa = w0 * r;
   h.sb = w1 * r;
   h.lam = x.det * r;
   ok = ok && h.lam > 0.f;  // nu . v > 0
   const float s2 = h.sa * h.sa + h.sb * h.sb;
-  h.G = __expf(-0.5f * s2);
+  h.G = ex2_ftz(s2 * -0.72134752044448170f);  // exp(-s2 / 2)
   const float araw = x.o * h.G;
   h.clamped = araw > bp.alpha_clamp;
   const float a = fminf(araw, bp.alpha_clamp);
@@ -577,7 +591,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
           Hit h;
           intersect(x, px[j], bp, h);
           const float om = 1.f - h.alpha;
-          const float iom = __fdividef(1.f, om);
+          const float iom = rcp_ftz(om);
           const float Tb = T[j] * iom;
           float dal = gD[j] * (h.lam * Tb - Sd[j] * iom) + gO[j] * (Tb - So[j] * iom);
           dal += gN[j][0] * (x.n[0] * Tb - Sn[j][0] * iom) + gN[j][1] * (x.n[1] * Tb - Sn[j][1] * iom) +
