@@ -31,9 +31,13 @@
 // pixel, the final transmittance, the last contributing list position and a
 // bitmask of contributing entries; the backward walks the list back to front
 // (suffix sums accumulate: no total-minus-prefix cancellation) visiting only
-// entries some pixel of the tile contributed to, and reduces each splat's 14
-// accumulators across the warp with a butterfly reduce-scatter before one
-// warp-wide float atomic.
+// entries some pixel of the tile contributed to.  A splat's 14 accumulators
+// are reduced across the warp through a shared-memory transpose before one
+// warp-wide float atomic, or, when at most kDirectLanes lanes contributed,
+// added by those lanes with float4 vector atomics.  (A packed variant, each
+// lane walking only its own contributions with per-contribution vector
+// atomics, halves the instructions but measured slower: 255 vs 230 us at
+// config 1, bound by 31 M L2 reduction sectors.)
 #include <cuda_pipeline.h>
 
 #include "common.cuh"
@@ -246,37 +250,6 @@ __device__ __forceinline__ void intersect(const Entry& x, const Pix& p, const Bl
   h.alpha = a;
 }
 
-// Butterfly reduce-scatter of 16 per-lane values across the warp: afterwards
-// lane l holds the warp sum of value index ((l >> 1) & 15) (lanes l, l^1 agree).
-__device__ __forceinline__ float warp_reduce_scatter16(float (&a)[16], int lane) {
-  const bool hi4 = lane & 16, hi3 = lane & 8, hi2 = lane & 4, hi1 = lane & 2;
-  float b[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float send = hi4 ? a[i] : a[8 + i];
-    const float keep = hi4 ? a[8 + i] : a[i];
-    b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  float c[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float send = hi3 ? b[i] : b[4 + i];
-    const float keep = hi3 ? b[4 + i] : b[i];
-    c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  float d[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float send = hi2 ? c[i] : c[2 + i];
-    const float keep = hi2 ? c[2 + i] : c[i];
-    d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  const float send = hi1 ? d[0] : d[1];
-  const float keep = hi1 ? d[1] : d[0];
-  const float e = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  return e + __shfl_xor_sync(0xffffffffu, e, 1);
-}
-
 // Reduce-scatter of 16 per-lane values through a 32x16 shared-memory
 // transpose (2 KB per warp): lane l stores its row (4 x STS.128, slot
 // swizzled by (l >> 1) & 3 so every quarter-warp store is conflict free),
@@ -383,42 +356,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       unsigned word[PPL], cw[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) word[j] = cw[j] = 0u;
-#ifdef SS_FWD_PERENTRY
-      for (int i = 0; i < cnt; ++i) {
-        const float* e = st + i * kStride;
-        const float4 c0 = *reinterpret_cast<const float4*>(e);
-        const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
-        bool cand[PPL];
-        bool anyc = false;
-#pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-          const float* p = px[j].p;
-          const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
-          cand[j] = live[j] && q <= 0.f;
-          anyc |= cand[j];
-        }
-        if (!anyc) continue;
-        Entry x;
-        load_entry(e, x);
-#pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-          if (!cand[j]) continue;
-          Hit h;
-          intersect(x, px[j], bp, h);
-          if (!h.use) continue;
-          const float w = h.alpha * T[j];
-          D[j] += w * h.lam;
-          O[j] += w;
-          N[j][0] += w * x.n[0];
-          N[j][1] += w * x.n[1];
-          N[j][2] += w * x.n[2];
-          T[j] *= (1.f - h.alpha);
-          word[j] |= 1u << i;
-          last[j] = base + i + 1;
-          if (T[j] < bp.min_T) live[j] = false;
-        }
-      }
-#else
       // phase A: branch-free cone test of every (pixel, entry) -> candidate bits
       for (int i = 0; i < cnt; ++i) {
         const float* e = st + i * kStride;
@@ -428,9 +365,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
         for (int j = 0; j < PPL; ++j) {
           const float* p = px[j].p;
           const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
-          cw[j] |= (q <= 0.f ? 1u : 0u) << i;
+          // sign bit of q (q < 0 or -0; q = +0 only on the cone's safety margin):
+          // entry i lands at bit cnt-1-i, reversed below
+          cw[j] = (cw[j] << 1) | (__float_as_uint(q) >> 31);
         }
       }
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) cw[j] = __brev(cw[j]) >> (32 - cnt);
       // phase B: every lane walks its own candidates front to back (packed: no
       // lane idles on another pixel's candidate entry)
 #pragma unroll
@@ -459,7 +400,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
           }
         }
       }
-#endif
 #pragma unroll
       for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
       __syncwarp();
@@ -482,6 +422,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 }
 
 constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
+// Entries that at most this many lanes contributed to skip the warp
+// transpose: those lanes add their 14 values with vector atomics (A/B at
+// config 1: 1 -> 252 us, 4 -> 237, 8..16 -> 230, 32 (always) -> 246).
+#ifndef SS_BWD_DIRECT
+#define SS_BWD_DIRECT 12
+#endif
+constexpr int kDirectLanes = SS_BWD_DIRECT;
 
 template <int TS>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
@@ -620,14 +567,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
           Sn[j][2] += w * x.n[2];
           T[j] = Tb;
         }
-#ifdef SS_BWD_BUTTERFLY
-        const float tot = warp_reduce_scatter16(a, lane);
-        const int vi = (lane >> 1) & 15;
-        if (!(lane & 1) && vi < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + vi], tot);
-#else
+        // few contributing lanes: vector atomics straight from those lanes
+        // (no 32-lane transpose for an entry that touched one or two pixels)
+        {
+          unsigned wl = 0u;
+#pragma unroll
+          for (int j = 0; j < PPL; ++j) wl |= word[j];
+          const unsigned lanes = __ballot_sync(0xffffffffu, (wl >> i) & 1u);
+          if (__popc(lanes) <= kDirectLanes) {
+            if ((lanes >> lane) & 1u) {
+              float4* g4 = reinterpret_cast<float4*>(acc + (size_t)x.sid * kAcc);
+              atomicAdd(g4, make_float4(a[0], a[1], a[2], a[3]));
+              atomicAdd(g4 + 1, make_float4(a[4], a[5], a[6], a[7]));
+              atomicAdd(g4 + 2, make_float4(a[8], a[9], a[10], a[11]));
+              atomicAdd(reinterpret_cast<float2*>(g4 + 3), make_float2(a[12], a[13]));
+            }
+            continue;
+          }
+        }
         const float tot = red_transpose16(a, red, roff, lane);
         if (lane < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + lane], tot);
-#endif
       }
       __syncwarp();
     }

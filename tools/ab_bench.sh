@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for f in variants/lib_*.so; do
   n=$(basename $f .so)
-  SPLAT_B200_LIB=$PWD/$f timeout 300 python bench.py --steps ${1:-20} --no-cpu-baseline > gpurun_out/ab_$n.log 2>&1
+  SPLAT_B200_LIB=$PWD/$f timeout 300 python bench.py --steps ${1:-20} --no-cpu-baseline --no-secondary > gpurun_out/ab_$n.log 2>&1
   python - "$n" gpurun_out/ab_$n.log <<'PY'
 import json, sys
 try:
