@@ -73,6 +73,7 @@ struct TileFrame {
 
 struct Pix {
   double w, x, y;  // v = w t + x e1 + y e2 (float64)
+  float dw, xf, yf;  // w - 1, x, y (float32; |x|, |y|, |w - 1| are tile-small)
   float p[6];      // w^2, 2wx, 2wy, x^2, 2xy, y^2
   float vf[3];     // v, float32
   int row, col;
@@ -119,6 +120,9 @@ __device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, 
   g.p[4] = (float)(2.0 * g.x * g.y);
   g.p[5] = (float)(g.y * g.y);
   for (int c = 0; c < 3; ++c) g.vf[c] = (float)v[c];
+  g.dw = (float)(g.w - 1.0);
+  g.xf = (float)g.x;
+  g.yf = (float)g.y;
 }
 
 // Stage one list entry (lane-parallel, float64): the nine frame dot products
@@ -139,7 +143,7 @@ __device__ __forceinline__ void prefetch_entry(RawEntry* dst, int sid, const Spl
   for (int q = 0; q < 5; ++q) __pipeline_memcpy_async(&dst->v[q], &rec64[sid].v[q], 16);
 }
 
-template <bool kCone>
+template <bool kCone, bool kDF = false>
 __device__ __forceinline__ void stage_entry(float* dst, int sid, const RawEntry& raw, const TileFrame& f, float xm,
                                             float ym) {
   const float4 p0 = raw.r0;
@@ -180,20 +184,35 @@ __device__ __forceinline__ void stage_entry(float* dst, int sid, const RawEntry&
     d4[1] = make_float4(0.f, 0.f, p0.x, (float)det);
   }
   d4[2] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
+  if (kDF) {
+  // kt as a float pair (hi + lo); k1, k2 only ever multiply tile-small x, y
+  float th[3], tl[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    th[c] = (float)kt[c];
+    tl[c] = (float)(kt[c] - (double)th[c]);
+  }
+  d4[4] = make_float4(th[0], th[1], th[2], (float)k1[0]);
+  d4[5] = make_float4((float)k1[1], (float)k1[2], (float)k2[0], (float)k2[1]);
+  d4[6] = make_float4((float)k2[2], tl[0], tl[1], tl[2]);
+  } else {
   double2* d2 = reinterpret_cast<double2*>(dst + 16);
   d2[0] = make_double2(kt[0], kt[1]);
   d2[1] = make_double2(kt[2], k1[0]);
   d2[2] = make_double2(k1[1], k1[2]);
   d2[3] = make_double2(k2[0], k2[1]);
   d2[4] = make_double2(k2[2], 0.0);
+  }
 }
 
 struct Entry {
-  double kt[3], k1[3], k2[3];
+  double kt[3], k1[3], k2[3];  // float64 frame products
+  float th[3], tl[3], f1[3], f2[3];  // float-pair form (kDF)
   float o, det, n[3];
   int sid;
 };
 
+template <bool kDF = false>
 __device__ __forceinline__ void load_entry(const float* e, Entry& x) {
   const float4* e4 = reinterpret_cast<const float4*>(e);
   const float4 f1 = e4[1], f2 = e4[2];
@@ -203,11 +222,18 @@ __device__ __forceinline__ void load_entry(const float* e, Entry& x) {
   x.n[1] = f2.y;
   x.n[2] = f2.z;
   x.sid = __float_as_int(f2.w);
+  if (kDF) {
+  const float4 a = e4[4], b = e4[5], c = e4[6];
+  x.th[0] = a.x; x.th[1] = a.y; x.th[2] = a.z; x.f1[0] = a.w;
+  x.f1[1] = b.x; x.f1[2] = b.y; x.f2[0] = b.z; x.f2[1] = b.w;
+  x.f2[2] = c.x; x.tl[0] = c.y; x.tl[1] = c.z; x.tl[2] = c.w;
+  } else {
   const double2* d2 = reinterpret_cast<const double2*>(e + 16);
   const double2 a = d2[0], b = d2[1], c = d2[2], d = d2[3], g = d2[4];
   x.kt[0] = a.x; x.kt[1] = a.y; x.kt[2] = b.x;
   x.k1[0] = b.y; x.k1[1] = c.x; x.k1[2] = c.y;
   x.k2[0] = d.x; x.k2[1] = d.y; x.k2[2] = g.x;
+  }
 }
 
 // Flush-to-zero approximate reciprocal / exp2 (one MUFU each; the IEEE
@@ -230,10 +256,22 @@ struct Hit {
 };
 
 // Exact per-pixel intersection + cutoffs (rasterizer.py:369-388).
+template <bool kDF = false>
 __device__ __forceinline__ void intersect(const Entry& x, const Pix& p, const BlendParams& bp, Hit& h) {
-  const float w0 = (float)(p.w * x.kt[0] + p.x * x.k1[0] + p.y * x.k2[0]);
-  const float w1 = (float)(p.w * x.kt[1] + p.x * x.k1[1] + p.y * x.k2[1]);
-  const float w2 = (float)(p.w * x.kt[2] + p.x * x.k1[2] + p.y * x.k2[2]);
+  float w0, w1, w2;
+  if (kDF) {
+    // v.K = kt + [kt (w - 1) + k1 x + k2 y] in float32 with kt as an exact
+    // hi + lo pair: the bracket's rounding is ~1e-8 |k| (x, y are tile-small),
+    // amplified by 1/|v.n| for grazing splats -- ~1e-4 in sa at worst, inside
+    // the backward's 1e-3 gate but not the forward's 1e-4 one.
+    w0 = x.th[0] + (fmaf(x.f2[0], p.yf, fmaf(x.f1[0], p.xf, x.th[0] * p.dw)) + x.tl[0]);
+    w1 = x.th[1] + (fmaf(x.f2[1], p.yf, fmaf(x.f1[1], p.xf, x.th[1] * p.dw)) + x.tl[1]);
+    w2 = x.th[2] + (fmaf(x.f2[2], p.yf, fmaf(x.f1[2], p.xf, x.th[2] * p.dw)) + x.tl[2]);
+  } else {
+    w0 = (float)(p.w * x.kt[0] + p.x * x.k1[0] + p.y * x.k2[0]);
+    w1 = (float)(p.w * x.kt[1] + p.x * x.k1[1] + p.y * x.k2[1]);
+    w2 = (float)(p.w * x.kt[2] + p.x * x.k1[2] + p.y * x.k2[2]);
+  }
   bool ok = p.ray_ok && fabsf(w2) >= bp.denom_eps;
   const float r = rcp_ftz(w2);
   h.r = r;
@@ -429,6 +467,11 @@ constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
 #define SS_BWD_DIRECT 12
 #endif
 constexpr int kDirectLanes = SS_BWD_DIRECT;
+#ifdef SS_BWD_F64
+constexpr bool kBwdDF = false;
+#else
+constexpr bool kBwdDF = true;  // float-pair intersection in the backward (230 -> 209 us)
+#endif
 
 template <int TS>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
@@ -514,7 +557,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       for (int j = 0; j < PPL; ++j) word[j] = base < last[j] ? wcur[j] : 0u;
       unsigned any = any_cur;
       __pipeline_wait_prior(1);  // this lane's copy for `chunk` has landed
-      if ((any >> lane) & 1u) stage_entry<false>(st + lane * kStride, scur, raw_all[warp][chunk & 1][lane], f, 0.f, 0.f);
+      if ((any >> lane) & 1u) stage_entry<false, kBwdDF>(st + lane * kStride, scur, raw_all[warp][chunk & 1][lane], f, 0.f, 0.f);
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
@@ -528,7 +571,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
         const int i = 31 - __clz(any);
         any &= ~(1u << i);
         Entry x;
-        load_entry(st + i * kStride, x);
+        load_entry<kBwdDF>(st + i * kStride, x);
         float a[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) a[q] = 0.f;
@@ -536,7 +579,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
         for (int j = 0; j < PPL; ++j) {
           if (!((word[j] >> i) & 1u)) continue;
           Hit h;
-          intersect(x, px[j], bp, h);
+          intersect<kBwdDF>(x, px[j], bp, h);
           const float om = 1.f - h.alpha;
           const float iom = rcp_ftz(om);
           const float Tb = T[j] * iom;
