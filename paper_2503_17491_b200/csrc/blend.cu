@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     TileFrame f;
     tile_frame<TS>(k, tr, tc, f);
     Pix px[PPL];
-    float T[PPL], Sd[PPL], So[PPL], Sn[PPL][3], gD[PPL], gO[PPL], gN[PPL][3];
+    float T[PPL], Q[PPL], gD[PPL], gO[PPL], gN[PPL][3];
     int last[PPL];
     int maxlast = 0;
 #pragma unroll
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
         gN[j][1] = gN_img[3 * p + 1];
         gN[j][2] = gN_img[3 * p + 2];
       }
-      Sd[j] = So[j] = Sn[j][0] = Sn[j][1] = Sn[j][2] = 0.f;
+      Q[j] = 0.f;
       maxlast = max(maxlast, last[j]);
     }
     maxlast = __reduce_max_sync(0xffffffffu, maxlast);
@@ -567,25 +567,57 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       any_cur = any_next;
       scur = snext;
       snext = snn;
+      // Walk the chunk's active entries back to front.  Consecutive entries
+      // that few lanes contributed to and whose lane sets are disjoint form
+      // one group: each lane evaluates its own member (every pixel still sees
+      // its contributions back to front) and adds it with vector atomics.
+      // An entry with more lanes is evaluated alone and reduced through the
+      // shared-memory transpose.
+      unsigned wl = 0u;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) wl |= word[j];
+      unsigned lm_next = 0u;  // lane mask of the head entry, if already known
       while (any) {
         const int i = 31 - __clz(any);
+        const unsigned lm = lm_next ? lm_next : __ballot_sync(0xffffffffu, (wl >> i) & 1u);
+        lm_next = 0u;
         any &= ~(1u << i);
+        const bool direct = __popc(lm) <= kDirectLanes;
+        int mi = i;
+        if (direct) {
+          mi = ((lm >> lane) & 1u) ? i : -1;
+#ifndef SS_BWD_NOGROUP
+          unsigned uni = lm;
+          while (any) {
+            const int i2 = 31 - __clz(any);
+            const unsigned l2 = __ballot_sync(0xffffffffu, (wl >> i2) & 1u);
+            if (__popc(l2) > kDirectLanes || (l2 & uni)) {
+              lm_next = l2;
+              break;
+            }
+            uni |= l2;
+            any &= ~(1u << i2);
+            if ((l2 >> lane) & 1u) mi = i2;
+          }
+#endif
+        }
         Entry x;
-        load_entry<kBwdDF>(st + i * kStride, x);
-        float a[16];
+        load_entry<kBwdDF>(st + max(mi, 0) * kStride, x);
+        float a[14];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) a[q] = 0.f;
+        for (int q = 0; q < 14; ++q) a[q] = 0.f;
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
-          if (!((word[j] >> i) & 1u)) continue;
+          if (mi < 0 || !((word[j] >> mi) & 1u)) continue;
           Hit h;
           intersect<kBwdDF>(x, px[j], bp, h);
           const float om = 1.f - h.alpha;
           const float iom = rcp_ftz(om);
           const float Tb = T[j] * iom;
-          float dal = gD[j] * (h.lam * Tb - Sd[j] * iom) + gO[j] * (Tb - So[j] * iom);
-          dal += gN[j][0] * (x.n[0] * Tb - Sn[j][0] * iom) + gN[j][1] * (x.n[1] * Tb - Sn[j][1] * iom) +
-                 gN[j][2] * (x.n[2] * Tb - Sn[j][2] * iom);
+          // dL/dalpha = Tb P - Q / (1 - alpha): P = g.(range, 1, n) of this splat,
+          // Q = g.(suffix sums of w range, w, w n) behind it (rasterizer.py:612-628)
+          const float P = fmaf(gD[j], h.lam, gO[j]) + gN[j][0] * x.n[0] + gN[j][1] * x.n[1] + gN[j][2] * x.n[2];
+          const float dal = Tb * P - iom * Q[j];
           const float w = h.alpha * Tb;
           const float gl = gD[j] * w;
           float gsa = 0.f, gsb = 0.f, go = 0.f;
@@ -603,32 +635,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
           a[9] += gl * h.r;
           a[10] += w * gN[j][0]; a[11] += w * gN[j][1]; a[12] += w * gN[j][2];
           a[13] += go;
-          Sd[j] += w * h.lam;
-          So[j] += w;
-          Sn[j][0] += w * x.n[0];
-          Sn[j][1] += w * x.n[1];
-          Sn[j][2] += w * x.n[2];
+          Q[j] += w * P;
           T[j] = Tb;
         }
-        // few contributing lanes: vector atomics straight from those lanes
-        // (no 32-lane transpose for an entry that touched one or two pixels)
-        {
-          unsigned wl = 0u;
-#pragma unroll
-          for (int j = 0; j < PPL; ++j) wl |= word[j];
-          const unsigned lanes = __ballot_sync(0xffffffffu, (wl >> i) & 1u);
-          if (__popc(lanes) <= kDirectLanes) {
-            if ((lanes >> lane) & 1u) {
-              float4* g4 = reinterpret_cast<float4*>(acc + (size_t)x.sid * kAcc);
-              atomicAdd(g4, make_float4(a[0], a[1], a[2], a[3]));
-              atomicAdd(g4 + 1, make_float4(a[4], a[5], a[6], a[7]));
-              atomicAdd(g4 + 2, make_float4(a[8], a[9], a[10], a[11]));
-              atomicAdd(reinterpret_cast<float2*>(g4 + 3), make_float2(a[12], a[13]));
-            }
-            continue;
+        if (direct) {
+          if (mi >= 0) {
+            float4* g4 = reinterpret_cast<float4*>(acc + (size_t)x.sid * kAcc);
+            atomicAdd(g4, make_float4(a[0], a[1], a[2], a[3]));
+            atomicAdd(g4 + 1, make_float4(a[4], a[5], a[6], a[7]));
+            atomicAdd(g4 + 2, make_float4(a[8], a[9], a[10], a[11]));
+            atomicAdd(reinterpret_cast<float2*>(g4 + 3), make_float2(a[12], a[13]));
           }
+          continue;
         }
-        const float tot = red_transpose16(a, red, roff, lane);
+        float a16[16];
+#pragma unroll
+        for (int q = 0; q < 14; ++q) a16[q] = a[q];
+        a16[14] = a16[15] = 0.f;
+        const float tot = red_transpose16(a16, red, roff, lane);
         if (lane < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + lane], tot);
       }
       __syncwarp();
