@@ -462,9 +462,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
 // Entries that at most this many lanes contributed to skip the warp
 // transpose: those lanes add their 14 values with vector atomics (A/B at
-// config 1: 1 -> 252 us, 4 -> 237, 8..16 -> 230, 32 (always) -> 246).
+// config 1: 1 -> 252 us, 4 -> 237, 8..16 -> 230, 32 (always) -> 246; with
+// grouping: 8 -> 177, 12..20 -> 172, 32 -> 219).
 #ifndef SS_BWD_DIRECT
-#define SS_BWD_DIRECT 12
+#define SS_BWD_DIRECT 16
 #endif
 constexpr int kDirectLanes = SS_BWD_DIRECT;
 #ifdef SS_BWD_F64
@@ -667,32 +668,93 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
 // The cross products with the camera-frame splat vectors (|Bc| ~ tens of
 // metres against nearly parallel accumulated rays) are float64 from the
 // forward's records; the rest of the chain is float32.
-__global__ void __launch_bounds__(256) k_finalize(SplatsK sp, PoseK pose, const SplatRec64* __restrict__ rec64,
-                                                  const float* __restrict__ acc,
-                                                  const float* __restrict__ d_scales_extra, float* __restrict__ out,
-                                                  int raw_space) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= sp.n) return;
+constexpr int kFinBlock = 128;
+
+__global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, const SplatRec64* __restrict__ rec64,
+                                                        const float* __restrict__ acc,
+                                                        const float* __restrict__ d_scales_extra,
+                                                        float* __restrict__ out, int raw_space) {
+  // The block's records and accumulators are staged through shared memory
+  // with coalesced 16-byte loads, its outputs leave the same way.
+  __shared__ double2 s_rec[kFinBlock * 5];
+  __shared__ float4 s_acc[kFinBlock * 4];
+  __shared__ __align__(16) float s_out[kFinBlock * 15];
+  __shared__ __align__(16) float s_ta[kFinBlock * 3];
+  __shared__ __align__(16) float s_tb[kFinBlock * 3];
+  __shared__ __align__(16) float s_ls[kFinBlock * 2];
+  __shared__ __align__(16) float s_ex[kFinBlock * 2];
+  __shared__ __align__(16) float s_lo[kFinBlock];
+  const int base = blockIdx.x * kFinBlock;
+  const int cnt = min(kFinBlock, sp.n - base);
+  const int tid = threadIdx.x;
+  if (cnt == kFinBlock && ((reinterpret_cast<uintptr_t>(sp.raw_ta) | reinterpret_cast<uintptr_t>(sp.raw_tb) |
+                             reinterpret_cast<uintptr_t>(sp.log_scales) | reinterpret_cast<uintptr_t>(sp.logit_opacity) |
+                             reinterpret_cast<uintptr_t>(d_scales_extra)) & 15) == 0) {
+    // full block: every load issued before the first shared store
+    const double2* g = reinterpret_cast<const double2*>(rec64 + base);
+    const float4* a4 = reinterpret_cast<const float4*>(acc + (size_t)base * kAcc);
+    double2 r[5];
+    float4 q4[4], x4[3];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) r[k] = __ldg(g + tid + kFinBlock * k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q4[k] = __ldg(a4 + tid + kFinBlock * k);
+    constexpr int F3 = kFinBlock * 3 / 4, F2 = kFinBlock * 2 / 4, F1 = kFinBlock / 4;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    x4[0] = tid < F3 ? __ldg(reinterpret_cast<const float4*>(sp.raw_ta + 3 * (size_t)base) + tid) : z4;
+    x4[1] = tid < F3 ? __ldg(reinterpret_cast<const float4*>(sp.raw_tb + 3 * (size_t)base) + tid) : z4;
+    x4[2] = tid < F2 ? __ldg(reinterpret_cast<const float4*>(sp.log_scales + 2 * (size_t)base) + tid)
+          : tid < F2 + F1 ? __ldg(reinterpret_cast<const float4*>(sp.logit_opacity + base) + (tid - F2))
+                          : z4;
+    const float4 e4 = (d_scales_extra && tid < F2)
+                          ? __ldg(reinterpret_cast<const float4*>(d_scales_extra + 2 * (size_t)base) + tid)
+                          : z4;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s_rec[tid + kFinBlock * k] = r[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s_acc[tid + kFinBlock * k] = q4[k];
+    if (tid < F3) {
+      reinterpret_cast<float4*>(s_ta)[tid] = x4[0];
+      reinterpret_cast<float4*>(s_tb)[tid] = x4[1];
+    }
+    if (tid < F2) {
+      reinterpret_cast<float4*>(s_ls)[tid] = x4[2];
+      reinterpret_cast<float4*>(s_ex)[tid] = e4;
+    } else if (tid < F2 + F1) {
+      reinterpret_cast<float4*>(s_lo)[tid - F2] = x4[2];
+    }
+  } else {
+    const double2* g = reinterpret_cast<const double2*>(rec64 + base);
+    for (int q = tid; q < cnt * 5; q += kFinBlock) s_rec[q] = __ldg(g + q);
+    const float4* a4 = reinterpret_cast<const float4*>(acc + (size_t)base * kAcc);
+    for (int q = tid; q < cnt * 4; q += kFinBlock) s_acc[q] = __ldg(a4 + q);
+    for (int q = tid; q < cnt * 3; q += kFinBlock) {
+      s_ta[q] = __ldg(sp.raw_ta + 3 * (size_t)base + q);
+      s_tb[q] = __ldg(sp.raw_tb + 3 * (size_t)base + q);
+    }
+    for (int q = tid; q < cnt * 2; q += kFinBlock) {
+      s_ls[q] = __ldg(sp.log_scales + 2 * (size_t)base + q);
+      s_ex[q] = d_scales_extra ? __ldg(d_scales_extra + 2 * (size_t)base + q) : 0.f;
+    }
+    if (tid < cnt) s_lo[tid] = __ldg(sp.logit_opacity + base + tid);
+  }
+  __syncthreads();
+  const int nout = raw_space ? 12 : 15;
+  if (tid < cnt) {
   double B[10];
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
-    const double2 x = __ldg(&rec64[i].v[q]);
+    const double2 x = s_rec[tid * 5 + q];
     B[2 * q] = x.x;
     B[2 * q + 1] = x.y;
   }
   const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
-  const float4* g4 = reinterpret_cast<const float4*>(acc + (size_t)i * kAcc);
-  const float4 ga = g4[0], gb = g4[1], gc = g4[2], gd = g4[3];
+  const float4 ga = s_acc[tid * 4], gb = s_acc[tid * 4 + 1], gc = s_acc[tid * 4 + 2], gd = s_acc[tid * 4 + 3];
   const double V0[3] = {ga.x, ga.y, ga.z}, V1[3] = {ga.w, gb.x, gb.y}, V2[3] = {gb.z, gb.w, gc.x};
   const double Gd = gc.y;
   const float Nc[3] = {gc.z, gc.w, gd.x};
   const float Oc = gd.y;
-  if (Gd == 0.0 && V0[0] == 0.0 && V0[1] == 0.0 && V0[2] == 0.0 && V1[0] == 0.0 && V1[1] == 0.0 && V1[2] == 0.0 &&
-      V2[0] == 0.0 && V2[1] == 0.0 && V2[2] == 0.0 && Nc[0] == 0.f && Nc[1] == 0.f && Nc[2] == 0.f && Oc == 0.f) {
-    float* o = out + (size_t)i * (raw_space ? 12 : 15);
-    for (int q = 0; q < (raw_space ? 12 : 15); ++q) o[q] = 0.f;  // splat touched no pixel
-    return;
-  }
+  float* o = s_out + tid * nout;  // (a splat that touched no pixel gets exact zeros)
   double A[3], Bv[3], C[3], t1[3], t2[3], gBa[3], gBb[3], gBc[3];
   cross3(Bb, Bc, A);
   cross3(Bc, Ba, Bv);
@@ -706,19 +768,26 @@ __global__ void __launch_bounds__(256) k_finalize(SplatsK sp, PoseK pose, const 
   cross3(V0, Bb, t1);
   cross3(Ba, V1, t2);
   for (int c = 0; c < 3; ++c) gBc[c] = t1[c] + t2[c] + Gd * C[c];
-  const float s0 = __expf(sp.log_scales[2 * i]), s1 = __expf(sp.log_scales[2 * i + 1]);
+  const float s0 = __expf(s_ls[2 * tid]), s1 = __expf(s_ls[2 * tid + 1]);
   // d_scales: dBa/ds_a = ta_c = Ba / s_a (rasterizer.py:693-699)
-  const float ds0 = (float)(dot3d(gBa, Ba) / (double)s0), ds1 = (float)(dot3d(gBb, Bb) / (double)s1);
-  const double* R = pose.R;
+  const float ds0 = (float)dot3d(gBa, Ba) * __frcp_rn(s0), ds1 = (float)dot3d(gBb, Bb) * __frcp_rn(s1);
+  // camera frame -> world frame (x @ R.T), float32 after the cancelling float64 products
+  float R[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) R[q] = (float)pose.R[q];
+  const float fa[3] = {(float)gBa[0], (float)gBa[1], (float)gBa[2]};
+  const float fb[3] = {(float)gBb[0], (float)gBb[1], (float)gBb[2]};
+  const float fc[3] = {(float)gBc[0], (float)gBc[1], (float)gBc[2]};
   float dmu[3], dta[3], dtb[3], dn[3];
-  for (int c = 0; c < 3; ++c) {  // camera frame -> world frame: x @ R.T
-    dmu[c] = (float)(gBc[0] * R[3 * c] + gBc[1] * R[3 * c + 1] + gBc[2] * R[3 * c + 2]);
-    dta[c] = s0 * (float)(gBa[0] * R[3 * c] + gBa[1] * R[3 * c + 1] + gBa[2] * R[3 * c + 2]);
-    dtb[c] = s1 * (float)(gBb[0] * R[3 * c] + gBb[1] * R[3 * c + 1] + gBb[2] * R[3 * c + 2]);
-    dn[c] = (float)(Nc[0] * R[3 * c] + Nc[1] * R[3 * c + 1] + Nc[2] * R[3 * c + 2]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dmu[c] = fc[0] * R[3 * c] + fc[1] * R[3 * c + 1] + fc[2] * R[3 * c + 2];
+    dta[c] = s0 * (fa[0] * R[3 * c] + fa[1] * R[3 * c + 1] + fa[2] * R[3 * c + 2]);
+    dtb[c] = s1 * (fb[0] * R[3 * c] + fb[1] * R[3 * c + 1] + fb[2] * R[3 * c + 2]);
+    dn[c] = Nc[0] * R[3 * c] + Nc[1] * R[3 * c + 1] + Nc[2] * R[3 * c + 2];
   }
   if (!raw_space) {
-    float* o = out + (size_t)i * 15;
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
       o[c] = dmu[c];
       o[3 + c] = dta[c];
@@ -728,44 +797,52 @@ __global__ void __launch_bounds__(256) k_finalize(SplatsK sp, PoseK pose, const 
     o[12] = ds0;
     o[13] = ds1;
     o[14] = Oc;
-    return;
+  } else {
+    // Gram-Schmidt backward (splats.py:154-163), float32
+    const float a[3] = {s_ta[3 * tid], s_ta[3 * tid + 1], s_ta[3 * tid + 2]};
+    const float b[3] = {s_tb[3 * tid], s_tb[3 * tid + 1], s_tb[3 * tid + 2]};
+    const float ina = rsqrtf(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const float u[3] = {a[0] * ina, a[1] * ina, a[2] * ina};
+    const float ub = u[0] * b[0] + u[1] * b[1] + u[2] * b[2];
+    const float w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
+    const float inw = rsqrtf(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    const float v[3] = {w[0] * inw, w[1] * inw, w[2] * inw};
+    const float gu[3] = {dta[0] + (v[1] * dn[2] - v[2] * dn[1]), dta[1] + (v[2] * dn[0] - v[0] * dn[2]),
+                         dta[2] + (v[0] * dn[1] - v[1] * dn[0])};
+    const float gv[3] = {dtb[0] + (dn[1] * u[2] - dn[2] * u[1]), dtb[1] + (dn[2] * u[0] - dn[0] * u[2]),
+                         dtb[2] + (dn[0] * u[1] - dn[1] * u[0])};
+    const float vg = v[0] * gv[0] + v[1] * gv[1] + v[2] * gv[2];
+    const float q[3] = {(gv[0] - vg * v[0]) * inw, (gv[1] - vg * v[1]) * inw, (gv[2] - vg * v[2]) * inw};
+    const float qu = q[0] * u[0] + q[1] * u[1] + q[2] * u[2];
+    float inner[3], gb_[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      gb_[c] = q[c] - qu * u[c];
+      inner[c] = gu[c] - ub * q[c] - qu * b[c];
+    }
+    const float ui = u[0] * inner[0] + u[1] * inner[1] + u[2] * inner[2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      o[c] = dmu[c];
+      o[3 + c] = (inner[c] - ui * u[c]) * ina;
+      o[6 + c] = gb_[c];
+    }
+    o[9] = (ds0 + s_ex[2 * tid]) * s0;
+    o[10] = (ds1 + s_ex[2 * tid + 1]) * s1;
+    const float xo = s_lo[tid];
+    const float ex = __expf(-fabsf(xo));
+    const float op = (xo >= 0.f ? 1.f : ex) * __frcp_rn(1.f + ex);
+    o[11] = Oc * op * (1.f - op);
   }
-  // Gram-Schmidt backward (splats.py:154-163), float32
-  const float a[3] = {sp.raw_ta[3 * i], sp.raw_ta[3 * i + 1], sp.raw_ta[3 * i + 2]};
-  const float b[3] = {sp.raw_tb[3 * i], sp.raw_tb[3 * i + 1], sp.raw_tb[3 * i + 2]};
-  const float na = sqrtf(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-  const float u[3] = {a[0] / na, a[1] / na, a[2] / na};
-  const float ub = u[0] * b[0] + u[1] * b[1] + u[2] * b[2];
-  const float w[3] = {b[0] - ub * u[0], b[1] - ub * u[1], b[2] - ub * u[2]};
-  const float nw = sqrtf(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
-  const float v[3] = {w[0] / nw, w[1] / nw, w[2] / nw};
-  const float gu[3] = {dta[0] + (v[1] * dn[2] - v[2] * dn[1]), dta[1] + (v[2] * dn[0] - v[0] * dn[2]),
-                       dta[2] + (v[0] * dn[1] - v[1] * dn[0])};
-  const float gv[3] = {dtb[0] + (dn[1] * u[2] - dn[2] * u[1]), dtb[1] + (dn[2] * u[0] - dn[0] * u[2]),
-                       dtb[2] + (dn[0] * u[1] - dn[1] * u[0])};
-  const float vg = v[0] * gv[0] + v[1] * gv[1] + v[2] * gv[2];
-  const float q[3] = {(gv[0] - vg * v[0]) / nw, (gv[1] - vg * v[1]) / nw, (gv[2] - vg * v[2]) / nw};
-  const float qu = q[0] * u[0] + q[1] * u[1] + q[2] * u[2];
-  float inner[3], gb_[3];
-  for (int c = 0; c < 3; ++c) {
-    gb_[c] = q[c] - qu * u[c];
-    inner[c] = gu[c] - ub * q[c] - qu * b[c];
   }
-  const float ui = u[0] * inner[0] + u[1] * inner[1] + u[2] * inner[2];
-  float* o = out + (size_t)i * 12;
-  for (int c = 0; c < 3; ++c) {
-    o[c] = dmu[c];
-    o[3 + c] = (inner[c] - ui * u[c]) / na;
-    o[6 + c] = gb_[c];
+  __syncthreads();
+  float* g = out + (size_t)base * nout;
+  if (cnt == kFinBlock && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    for (int q = tid; q < kFinBlock * nout / 4; q += kFinBlock)
+      reinterpret_cast<float4*>(g)[q] = reinterpret_cast<const float4*>(s_out)[q];
+  } else {
+    for (int q = tid; q < cnt * nout; q += kFinBlock) g[q] = s_out[q];
   }
-  const float e0 = d_scales_extra ? d_scales_extra[2 * i] : 0.f;
-  const float e1 = d_scales_extra ? d_scales_extra[2 * i + 1] : 0.f;
-  o[9] = (ds0 + e0) * s0;
-  o[10] = (ds1 + e1) * s1;
-  const float xo = sp.logit_opacity[i];
-  const float ex = __expf(-fabsf(xo));
-  const float op = xo >= 0.f ? 1.f / (1.f + ex) : ex / (1.f + ex);
-  o[11] = Oc * op * (1.f - op);
 }
 
 template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,

@@ -448,7 +448,7 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   }
   {
     StageTimer tm(rec, ST_FINALIZE, s);
-    k_finalize<<<(n + 255) / 256, 256, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc, d_scales_extra, grads,
+    k_finalize<<<(n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc, d_scales_extra, grads,
                                                 raw_space);
   }
   SS_CUDA_TRY(cudaGetLastError());
@@ -695,8 +695,8 @@ int ss_mapping_loss(int32_t width, int32_t height, const float* range, const flo
   if (width <= 0 || height <= 0) return SS_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   int P = width * height;
-  int blocks = (P + 1023) / 1024;
-  if (blocks > 148 * 2) blocks = 148 * 2;
+  int blocks = (P + 511) / 512;  // two pixels per thread
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   k_mapping_loss<<<blocks, 256, 0, s>>>(P, range, normal, opacity, kf_range, kf_valid, kf_normal, kf_nvalid,
                                         w_opacity, w_normal, range_floor, dD, dN, dO, parts4);
   SS_CUDA_TRY(cudaGetLastError());
