@@ -440,46 +440,68 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile
-constexpr int kTileSortIPL = kTileSortMax / 256;  // items per lane per warp segment
-constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> fallback
+constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile (8 warps)
+constexpr int kTileSortBig = 8192;                // long-list variant (32 warps, dynamic shared memory)
+constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> merge-sort fallback
+
+struct SortSmem {
+  uint16_t* sk[2];  // [MAX] 16-bit keys
+  uint32_t* sv[2];  // [MAX] splat ids
+  uint16_t* wcnt;   // [NW][256] per-warp digit counts
+  uint32_t* dtot;   // [256] digit offsets (and warp partials)
+  uint32_t* red;    // [2 * NW] min / max partials
+  int* bad;
+};
+
+template <int MAX, int NT>
+__host__ __device__ constexpr size_t sort_smem_bytes() {
+  return 2 * MAX * sizeof(uint16_t) + 2 * MAX * sizeof(uint32_t) + (NT / 32) * 256 * sizeof(uint16_t) +
+         256 * sizeof(uint32_t) + 2 * (NT / 32) * sizeof(uint32_t) + 16;
+}
+
+template <int MAX, int NT>
+__device__ __forceinline__ SortSmem carve_sort_smem(unsigned char* base) {
+  SortSmem m;
+  unsigned char* p = base;
+  m.sv[0] = reinterpret_cast<uint32_t*>(p); p += MAX * 4;
+  m.sv[1] = reinterpret_cast<uint32_t*>(p); p += MAX * 4;
+  m.dtot = reinterpret_cast<uint32_t*>(p); p += 256 * 4;
+  m.red = reinterpret_cast<uint32_t*>(p); p += 2 * (NT / 32) * 4;
+  m.bad = reinterpret_cast<int*>(p); p += 16;
+  m.sk[0] = reinterpret_cast<uint16_t*>(p); p += MAX * 2;
+  m.sk[1] = reinterpret_cast<uint16_t*>(p); p += MAX * 2;
+  m.wcnt = reinterpret_cast<uint16_t*>(p);
+  return m;
+}
 
 // Per-tile ordering in shared memory.  The 32-bit key (float64 range rounded
 // down to float32) is reduced to 16 bits relative to the tile's smallest key
 // (monotone), sorted by two 8-bit LSD passes with warp multisplit ranking,
 // and runs of equal 16-bit keys are then put in exact (float64 range, splat
-// index) order by insertion sort.  One block (8 warps) per tile.
-__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
-                                                   const uint32_t* __restrict__ key32,
-                                                   const unsigned long long* __restrict__ key64,
-                                                   int* __restrict__ long_list, int* __restrict__ n_long,
-                                                   const int* __restrict__ overflow) {
-  __shared__ uint16_t sk[2][kTileSortMax];
-  __shared__ uint32_t sv[2][kTileSortMax];
-  __shared__ uint16_t wcnt[8][256];
-  __shared__ uint32_t dtot[256];
-  __shared__ uint32_t red_min[8], red_max[8];
-  __shared__ int s_bad;
-  if (*overflow) return;
-  const int t = blockIdx.x;
-  const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
-  if (L <= 1) return;
-  if (L > kTileSortMax) {
-    if (threadIdx.x == 0) long_list[atomicAdd(n_long, 1)] = t;
-    return;
-  }
+// index) order by insertion sort.  One block of NT threads per tile, L <= MAX.
+// Returns false (nothing written) when a run of equal keys is too long.
+template <int MAX, int NT>
+__device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, int lo, int L,
+                               const uint32_t* __restrict__ key32, const unsigned long long* __restrict__ key64) {
+  constexpr int NW = NT / 32, IPL = MAX / NT;
+  static_assert(NT >= 256, "the digit scan needs 256 threads");
+  // every buffer is shared memory: let the compiler emit LDS/STS, not generic loads
+  uint16_t* const sk0 = m.sk[0];
+  uint16_t* const sk1 = m.sk[1];
+  uint32_t* const sv0 = m.sv[0];
+  uint32_t* const sv1 = m.sv[1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t kmin = 0xffffffffu, kmax = 0u;
-  uint32_t kk[kTileSortIPL];
+  uint32_t kk[IPL];
 #pragma unroll
-  for (int j = 0; j < kTileSortIPL; ++j) {
-    const int i = tid + 256 * j;
+  for (int j = 0; j < IPL; ++j) {
+    const int i = tid + NT * j;
     kk[j] = 0;
-    if (256 * j >= L) break;
+    if (NT * j >= L) break;
     if (i < L) {
       const uint32_t v = pairs[lo + i];
       kk[j] = key32[v];
-      sv[0][i] = v;
+      sv0[i] = v;
       kmin = min(kmin, kk[j]);
       kmax = max(kmax, kk[j]);
     }
@@ -489,116 +511,141 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
     kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
   }
   if (lane == 0) {
-    red_min[warp] = kmin;
-    red_max[warp] = kmax;
+    m.red[warp] = kmin;
+    m.red[NW + warp] = kmax;
   }
-  if (tid == 0) s_bad = 0;
+  if (tid == 0) *m.bad = 0;
   __syncthreads();
-  for (int w = 0; w < 8; ++w) {
-    kmin = min(kmin, red_min[w]);
-    kmax = max(kmax, red_max[w]);
+  for (int w = 0; w < NW; ++w) {
+    kmin = min(kmin, m.red[w]);
+    kmax = max(kmax, m.red[NW + w]);
   }
   const uint32_t span = kmax - kmin;
   const int shift = span >= 65536u ? (32 - __clz(span)) - 16 : 0;
 #pragma unroll
-  for (int j = 0; j < kTileSortIPL; ++j) {
-    const int i = tid + 256 * j;
-    if (256 * j >= L) break;
-    if (i < L) sk[0][i] = (uint16_t)((kk[j] - kmin) >> shift);
+  for (int j = 0; j < IPL; ++j) {
+    const int i = tid + NT * j;
+    if (NT * j >= L) break;
+    if (i < L) sk0[i] = (uint16_t)((kk[j] - kmin) >> shift);
   }
   __syncthreads();
-  const int seg = ((L + 255) / 256) * 32;  // warp w owns [w*seg, (w+1)*seg), lane-striped
+  const int seg = ((L + NT - 1) / NT) * 32;  // warp w owns [w*seg, (w+1)*seg), lane-striped
   const uint32_t lt = lanemask_lt();
   const uint32_t sspan = span >> shift;
+  uint16_t* wc = m.wcnt + warp * 256;
   int cur = 0;
   for (int p = 0; p < 2; ++p) {
     const int sh = 8 * p;
     if (p == 1 && sspan < 256u) break;  // high digit constant
-    for (int i = tid; i < 8 * 256; i += 256) (&wcnt[0][0])[i] = 0;
+    for (int i = tid; i < NW * 256; i += NT) m.wcnt[i] = 0;
     __syncthreads();
-    uint16_t lr[kTileSortIPL];
-    int dg[kTileSortIPL];
+    uint16_t lr[IPL];
+    int dg[IPL];
 #pragma unroll
-    for (int j = 0; j < kTileSortIPL; ++j) {
+    for (int j = 0; j < IPL; ++j) {
       dg[j] = 256;
       if (j * 32 >= seg) break;  // warp-uniform
       const int idx = warp * seg + j * 32 + lane;
       const bool ok = idx < L;
-      dg[j] = ok ? (int)((sk[cur][idx] >> sh) & 0xffu) : 256;
+      dg[j] = ok ? (int)(((cur ? sk1 : sk0)[idx] >> sh) & 0xffu) : 256;
       const uint32_t peers = __match_any_sync(0xffffffffu, dg[j]);
       const int leader = 31 - __clz(peers);
       uint16_t before = 0;
-      if (dg[j] < 256) before = wcnt[warp][dg[j]];
+      if (dg[j] < 256) before = wc[dg[j]];
       __syncwarp();
-      if (lane == leader && dg[j] < 256) wcnt[warp][dg[j]] = (uint16_t)(before + __popc(peers));
+      if (lane == leader && dg[j] < 256) wc[dg[j]] = (uint16_t)(before + __popc(peers));
       __syncwarp();
       lr[j] = (uint16_t)(before + __popc(peers & lt));
     }
     __syncthreads();
-    {
-      uint32_t s = 0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const uint32_t c = wcnt[w][tid];
-        wcnt[w][tid] = (uint16_t)s;
+    // digit offsets: per digit, exclusive over warps (in place) and the block-wide scan of the totals
+    uint32_t s = 0, inc = 0;
+    if (tid < 256) {
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t c = m.wcnt[w * 256 + tid];
+        m.wcnt[w * 256 + tid] = (uint16_t)s;
         s += c;
       }
-      uint32_t inc = s;
+      inc = s;
       for (int off = 1; off < 32; off <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
         if (lane >= off) inc += y;
       }
-      if (lane == 31) dtot[warp] = inc;
-      __syncthreads();
+      if (lane == 31) m.red[warp] = inc;
+    }
+    __syncthreads();
+    if (tid < 256) {
       uint32_t wex = 0;
-      for (int w = 0; w < warp; ++w) wex += dtot[w];
-      __syncthreads();
-      dtot[tid] = wex + inc - s;
+      for (int w = 0; w < warp; ++w) wex += m.red[w];
+      m.dtot[tid] = wex + inc - s;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kTileSortIPL; ++j) {
+    for (int j = 0; j < IPL; ++j) {
       if (j * 32 >= seg) break;
       if (dg[j] < 256) {
         const int idx = warp * seg + j * 32 + lane;
-        const uint32_t pos = dtot[dg[j]] + wcnt[warp][dg[j]] + lr[j];
-        sk[cur ^ 1][pos] = sk[cur][idx];
-        sv[cur ^ 1][pos] = sv[cur][idx];
+        const uint32_t pos = m.dtot[dg[j]] + wc[dg[j]] + lr[j];
+        (cur ? sk0 : sk1)[pos] = (cur ? sk1 : sk0)[idx];
+        (cur ? sv0 : sv1)[pos] = (cur ? sv1 : sv0)[idx];
       }
     }
     __syncthreads();
     cur ^= 1;
   }
   // exact (float64, index) order inside runs of equal sort keys
-  for (int i = tid; i < L; i += 256) {
-    const uint16_t k = sk[cur][i];
-    if (i > 0 && sk[cur][i - 1] == k) continue;
-    if (i + 1 >= L || sk[cur][i + 1] != k) continue;
+  const uint16_t* K = cur ? sk1 : sk0;
+  uint32_t* V = cur ? sv1 : sv0;
+  for (int i = tid; i < L; i += NT) {
+    const uint16_t k = K[i];
+    if (i > 0 && K[i - 1] == k) continue;
+    if (i + 1 >= L || K[i + 1] != k) continue;
     int j = i + 1;
-    while (j < L && sk[cur][j] == k) ++j;
+    while (j < L && K[j] == k) ++j;
     if (j - i > kMaxTieRun) {
-      s_bad = 1;
+      *m.bad = 1;
       continue;
     }
     for (int x = i + 1; x < j; ++x) {
-      const uint32_t v = sv[cur][x];
+      const uint32_t v = V[x];
       const unsigned long long kv = key64[v];
       int y = x - 1;
       while (y >= i) {
-        const uint32_t w = sv[cur][y];
+        const uint32_t w = V[y];
         if (key_less(key64[w], w, kv, v)) break;
-        sv[cur][y + 1] = w;
+        V[y + 1] = w;
         --y;
       }
-      sv[cur][y + 1] = v;
+      V[y + 1] = v;
     }
   }
   __syncthreads();
-  if (s_bad) {  // long run of near-equal ranges: exact merge sort instead
-    if (tid == 0) long_list[atomicAdd(n_long, 1)] = t;
+  const bool ok = !*m.bad;
+  if (ok)
+    for (int i = tid; i < L; i += NT) pairs[lo + i] = V[i];
+  __syncthreads();
+  return ok;
+}
+
+// Regular tiles (L <= kTileSortMax), one 256-thread block per tile; longer
+// lists go to long_list for k_tile_sort_big.
+__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
+                                                   const uint32_t* __restrict__ key32,
+                                                   const unsigned long long* __restrict__ key64,
+                                                   int* __restrict__ long_list, int* __restrict__ n_long,
+                                                   const int* __restrict__ overflow) {
+  __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, 256>()];
+  if (*overflow) return;
+  const int t = blockIdx.x;
+  const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+  if (L <= 1) return;
+  if (L > kTileSortMax) {
+    if (threadIdx.x == 0) long_list[atomicAdd(n_long, 1)] = t;
     return;
   }
-  for (int i = tid; i < L; i += 256) pairs[lo + i] = sv[cur][i];
+  const SortSmem m = carve_sort_smem<kTileSortMax, 256>(smem);
+  if (!sort_tile_smem<kTileSortMax, 256>(m, pairs, lo, L, key32, key64) && threadIdx.x == 0)
+    long_list[atomicAdd(n_long, 1)] = t;  // long run of equal keys: the big kernel's merge fallback
 }
 
 __device__ int count_less(const uint32_t* run, int len, const unsigned long long* key, unsigned long long k,
@@ -615,38 +662,53 @@ __device__ int count_less(const uint32_t* run, int len, const unsigned long long
   return lo;
 }
 
-// Fallback for lists longer than kTileSortMax: bottom-up merge sort in global
-// memory by the exact (float64 range, index) key, one block per long tile.
-__global__ void k_sort_long(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs, uint32_t* __restrict__ tmp,
-                            const unsigned long long* __restrict__ key, const int* __restrict__ long_list,
-                            const int* __restrict__ n_long) {
+// Fallback for lists longer than kTileSortBig (or with a long run of equal
+// sort keys): bottom-up merge sort in global memory by the exact (float64
+// range, index) key, by the whole block.
+__device__ void merge_sort_tile(uint32_t* __restrict__ pairs, uint32_t* __restrict__ tmp, int lo, int L,
+                                const unsigned long long* __restrict__ key) {
+  uint32_t* src = pairs + lo;
+  uint32_t* dst = tmp + lo;
+  for (int w = 1; w < L; w <<= 1) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      const int start = (i / (2 * w)) * (2 * w);
+      const int mid = min(start + w, L), end = min(start + 2 * w, L);
+      const uint32_t v = src[i];
+      const unsigned long long k = key[v];
+      int pos;
+      if (i < mid)
+        pos = (i - start) + count_less(src + mid, end - mid, key, k, v);
+      else
+        pos = (i - mid) + count_less(src + start, mid - start, key, k, v);
+      dst[start + pos] = v;
+    }
+    __syncthreads();
+    uint32_t* s = src;
+    src = dst;
+    dst = s;
+  }
+  if (src != pairs + lo)
+    for (int i = threadIdx.x; i < L; i += blockDim.x) pairs[lo + i] = src[i];
+  __syncthreads();
+}
+
+// Tiles k_tile_sort handed over (long_list): lists of up to kTileSortBig
+// entries sorted in shared memory by a 1024-thread block, anything else by
+// the global merge sort.
+__global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
+                                                        uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key32,
+                                                        const unsigned long long* __restrict__ key64,
+                                                        const int* __restrict__ long_list,
+                                                        const int* __restrict__ n_long) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  const SortSmem m = carve_sort_smem<kTileSortBig, 1024>(dsmem);
   const int nl = *n_long;
   for (int r = blockIdx.x; r < nl; r += gridDim.x) {
     const int t = long_list[r];
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
-    uint32_t* src = pairs + lo;
-    uint32_t* dst = tmp + lo;
-    for (int w = 1; w < L; w <<= 1) {
-      for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        const int start = (i / (2 * w)) * (2 * w);
-        const int mid = min(start + w, L), end = min(start + 2 * w, L);
-        const uint32_t v = src[i];
-        const unsigned long long k = key[v];
-        int pos;
-        if (i < mid)
-          pos = (i - start) + count_less(src + mid, end - mid, key, k, v);
-        else
-          pos = (i - mid) + count_less(src + start, mid - start, key, k, v);
-        dst[start + pos] = v;
-      }
-      __syncthreads();
-      uint32_t* s = src;
-      src = dst;
-      dst = s;
-    }
-    if (src != pairs + lo)
-      for (int i = threadIdx.x; i < L; i += blockDim.x) pairs[lo + i] = src[i];
-    __syncthreads();
+    bool ok = false;
+    if (L <= kTileSortBig) ok = sort_tile_smem<kTileSortBig, 1024>(m, pairs, lo, L, key32, key64);
+    if (!ok) merge_sort_tile(pairs, tmp, lo, L, key64);
   }
 }
 

@@ -123,3 +123,38 @@ def test_config_full_size_parity(cuda, index):
     rep = grad_report(got, plain)
     print("grad parity", rep)
     assert_grads(rep)
+
+
+def _crowded_params(n: int, n_tie: int, seed: int) -> dict:
+    """Splats crowded into a narrow cone ahead of the sensor (tile lists of thousands, past the
+    8-warp and 32-warp shared-memory sorts) plus a block of splats at exactly one range (runs of
+    equal sort keys longer than the insertion-sort limit)."""
+    rng = np.random.default_rng(seed)
+    az = rng.uniform(-0.15, 0.15, n)
+    el = rng.uniform(-0.1, 0.1, n)
+    r = rng.uniform(4.0, 12.0, n)
+    r[:n_tie] = 7.0
+    d = np.stack([np.cos(el) * np.cos(az), np.cos(el) * np.sin(az), np.sin(el)], 1)
+    c = d * r[:, None]
+    ta, tb = W.quat_tangents(rng.normal(size=(n, 4)))
+    ls = rng.normal(np.log(0.25), 0.3, (n, 2))
+    lo = rng.normal(0.0, 1.0, n)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    return {"centers": f(c), "raw_t_alpha": f(ta), "raw_t_beta": f(tb), "log_scales": f(ls), "logit_opacity": f(lo)}
+
+
+@pytest.mark.parametrize("n,n_tie", [(6000, 0), (30000, 400)])
+def test_long_lists_and_tie_runs_bit_exact(cuda, n, n_tie):
+    cam = W.synth_camera(512, 64)
+    params = _crowded_params(n, n_tie, 3)
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), params)
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), SplatModel.from_params(params))
+    lens = np.diff(ref["tile_ptr"])
+    print("max list", lens.max(), "lists > 2048:", int((lens > 2048).sum()), "> 8192:", int((lens > 8192).sum()))
+    assert lens.max() > 2048
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"])
+    assert np.array_equal(rec.pair_splats, ref["pair_splats"])
+    rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
+                       np.full(out.range.shape, 1.0))
+    assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
