@@ -231,11 +231,11 @@ def run_b200(args, ws, rank, local):
     rec = engine.Records()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def step(sp):
+    def step(sp, out=None):
         D, N, O = engine.forward(cam, pose12, sp, cfg, rec, sync=False)
         dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf_range, kf_valid, kf_normal, kf_nvalid, w_opacity=0.0,
                                                 w_normal=0.1)
-        g = engine.backward(rec, sp, dD, dN, dO, raw_space=True)
+        g = engine.backward(rec, sp, dD, dN, dO, raw_space=True, out=out)
         return g, parts
 
     engine.forward(cam, pose12, splats, cfg, rec)  # sizes the pair buffers (synchronous check)
@@ -309,7 +309,7 @@ def run_b200(args, ws, rank, local):
     dev_in = [{k: torch.empty_like(v, device=dev) for k, v in host.items()} for _ in range(2)]
     g_host = [torch.empty((500_000, 12), dtype=torch.float32).pin_memory() for _ in range(2)]
     loss_host = [torch.empty(4, dtype=torch.float64).pin_memory() for _ in range(2)]
-    g_dev = [None, None]
+    g_dev = [torch.empty((500_000, 12), dtype=torch.float32, device=dev) for _ in range(2)]
     parts_dev = [None, None]
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     d2h = g_host[0].numel() * 4 + 4 * 8
@@ -343,8 +343,8 @@ def run_b200(args, ws, rank, local):
             if i + 1 < n:
                 upload(i + 1)
             comp.wait_event(up_done[b_])
-            g, parts = step(dev_in[b_])
-            g_dev[b_], parts_dev[b_] = g, parts
+            _, parts = step(dev_in[b_], out=g_dev[b_])
+            parts_dev[b_] = parts
             step_done[b_].record(comp)
             download(i)
         copy_d.synchronize()

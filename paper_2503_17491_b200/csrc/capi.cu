@@ -100,6 +100,18 @@ __global__ void k_ffma_probe(float* out, int iters, float a, float b) {
   if (s == 12345.f) out[0] = s;
 }
 
+// totals[0..1] and status/overflow (misc[0..1]) into mapped host memory.
+__global__ void k_publish_totals(const long long* __restrict__ totals, const int* __restrict__ misc,
+                                 volatile long long* __restrict__ host) {
+  if (threadIdx.x == 0) {
+    host[0] = totals[0];
+    host[1] = totals[1];
+    const long long sm = (long long)(unsigned)misc[0] | ((long long)(unsigned)misc[1] << 32);
+    host[2] = sm;
+    __threadfence_system();
+  }
+}
+
 }  // namespace
 
 struct ss_records {
@@ -152,7 +164,8 @@ struct ss_records {
   size_t cap_last = 0;
   float* acc = nullptr;
   size_t cap_acc = 0;
-  long long* h_totals = nullptr;  // pinned: totals[2], status, overflow
+  long long* h_totals = nullptr;  // mapped pinned: totals[2], status, overflow
+  long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
   // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
   bool profiling = false;
@@ -222,7 +235,12 @@ const char* ss_version(void) { return "paper_2503_17491_b200 0.2 (sm_100a)"; }
 ss_records* ss_records_create(void) {
   ss_records* r = new (std::nothrow) ss_records();
   if (!r) return nullptr;
-  if (cudaMallocHost((void**)&r->h_totals, 4 * sizeof(long long)) != cudaSuccess) {
+  // mapped pinned memory: the forward publishes its totals with a kernel store,
+  // not a device-to-host copy (a copy would queue behind the caller's bulk
+  // downloads on the D2H copy engine and stall the compute stream)
+  if (cudaHostAlloc((void**)&r->h_totals, 4 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&r->d_h_totals, r->h_totals, 0) != cudaSuccess) {
+    if (r->h_totals) cudaFreeHost(r->h_totals);
     delete r;
     return nullptr;
   }
@@ -354,8 +372,8 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
                                                            rec->last, rec->bitmask, overflow, order, counters);
   }
   SS_CUDA_TRY(cudaGetLastError());
-  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals, rec->totals, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  SS_CUDA_TRY(cudaMemcpyAsync(rec->h_totals + 2, rec->misc, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  k_publish_totals<<<1, 32, 0, s>>>(rec->totals, rec->misc, rec->d_h_totals);
+  SS_CUDA_TRY(cudaGetLastError());
   SS_CUDA_TRY(cudaEventRecord(rec->done, s));
   return SS_OK;
 }

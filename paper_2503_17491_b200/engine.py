@@ -159,11 +159,16 @@ def forward(cam, pose_rt: np.ndarray, splats: dict, cfg, records: Records, sync:
     return D, N, O
 
 
-def backward(records: Records, splats: dict, dD, dN, dO, raw_space: bool, d_scales_extra=None):
-    """Splat gradients: (n, 15) plain-space or (n, 12) raw-space float32 device tensor."""
+def backward(records: Records, splats: dict, dD, dN, dO, raw_space: bool, d_scales_extra=None, out=None):
+    """Splat gradients: (n, 15) plain-space or (n, 12) raw-space float32 device tensor
+    (written into ``out`` when given: a contiguous float32 tensor of that shape)."""
     dev = require_cuda()
     n = int(splats["centers"].shape[0])
-    out = torch.empty((n, 12 if raw_space else 15), dtype=torch.float32, device=dev)
+    shape = (n, 12 if raw_space else 15)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=dev)
+    elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous float32 tensor of shape {shape}")
     dD = dD.contiguous().float()
     dN = dN.contiguous().float()
     dO = dO.contiguous().float()
