@@ -157,6 +157,8 @@ def secondary_metrics(dev):
                       "camera": "64x1024", "loss_first": first[0], "loss_last": losses[-1],
                       "note": "config 2: 200k surfels back-projected from 10 keyframes (workloads.config2_map)"}
     params, cam, scan, truth, initial = W.config3_problem()
+    from paper_2503_17491_b200 import engine
+    params = engine.as_device_params(params)  # the fixed map stays resident in HBM across registrations
     rcfg = REG.RegistrationConfig(mode="photometric", max_iters=20, tol=0.0)
     res = REG.register(params, scan, cam, initial, rcfg)  # warm-up (allocations)
     torch.cuda.synchronize()
@@ -173,7 +175,8 @@ def secondary_metrics(dev):
     out["registration"] = {"metric": "photometric registrations/s (2x render + 20 GN iterations)",
                            "value": 1.0 / dt, "unit": "registrations/s", "ms": dt * 1e3, "iterations": res.iterations,
                            "n_photo": res.n_photo, "initial_err_m": e0t, "final_err_m": err_t, "final_err_deg": err_r,
-                           "note": "config 3: 300k surfels on visible surfaces, host LM loop + device systems"}
+                           "note": "config 3: 300k surfels on visible surfaces (device-resident map); per registration: "
+                                   "2x render + anchors, scan range image, GN/LM loop in one cooperative kernel"}
     return out
 
 

@@ -23,6 +23,8 @@
  *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
  *                            the H/b accumulation of registration.py:470-477,
  *                            objective of registration.py:379-384)
+ *   ss_reg_photo_solve       registration.py:437-524 the GN/LM loop of register
+ *                            (photometric phase), se3.py:121-150 retract
  */
 #ifndef SPLAT_B200_H
 #define SPLAT_B200_H
@@ -42,7 +44,8 @@ typedef enum {
   SS_ERR_UNSUPPORTED = 3,      /* GeometryError: e.g. tile_size not 8 or 16    */
   SS_ERR_CUDA = 4,             /* RuntimeError: CUDA launch / allocation error */
   SS_ERR_CAPACITY = 5,         /* internal: pair capacity exceeded, retry      */
-  SS_ERR_DEGENERATE = 6        /* GeometryError: zero / parallel raw tangents  */
+  SS_ERR_DEGENERATE = 6,       /* GeometryError: zero / parallel raw tangents  */
+  SS_ERR_REGISTRATION = 7      /* RegistrationError: too few residuals survive */
 } ss_status;
 
 /* SphericalCamera (geometry.py:68-115) */
@@ -182,6 +185,27 @@ size_t ss_photo_workspace_bytes(int32_t M);
 int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
                     const ss_camera* cam, const double* T_Rt, double trim_floor, const ss_reg_cfg* cfg,
                     int32_t objective_only, double* out30, void* workspace, void* stream);
+
+/* RegistrationConfig fields of the photometric GN/LM loop (registration.py:41-61). */
+typedef struct {
+  double huber_photo, trim_factor, spread_gate, assoc_gate, trim_floor_photo, tol, damping_init, damping_max;
+  int32_t max_iters, min_residuals;
+} ss_reg_solve_cfg;
+
+/* The whole photometric Gauss-Newton / Levenberg loop of register()
+ * (registration.py:437-524, mode "photometric") on the device, one
+ * cooperative kernel: every evaluation of _photo_system (residuals, exact
+ * median trim, Huber-weighted 6x6 normal equations), the damped 6x6 solve,
+ * T <- T exp(delta), acceptance, damping and trim-floor schedule.  From
+ * initial pose T0_Rt; returns the final pose (before the host's SVD
+ * re-orthonormalisation) in T_out_Rt, info4 = {iterations, converged, m of
+ * the last full evaluation, evaluations run}, last_r2 = its sum of r^2.
+ * SS_ERR_REGISTRATION when fewer than min_residuals residuals survive.
+ * workspace: ss_reg_solve_workspace_bytes(M) bytes.  Synchronises the stream. */
+size_t ss_reg_solve_workspace_bytes(int32_t M);
+int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
+                       const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg, double* T_out_Rt,
+                       int32_t* info4, double* last_r2, void* workspace, void* stream);
 
 /* Measured FP32 FMA throughput of the current device (TFLOP/s), the roofline
  * denominator of the FP32-bound blend kernels.  Synchronises the stream. */

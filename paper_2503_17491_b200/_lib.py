@@ -45,6 +45,13 @@ class SsSplats(ctypes.Structure):
                 ("logit_opacity", ctypes.c_void_p)]
 
 
+class SsRegSolveCfg(ctypes.Structure):
+    _fields_ = [("huber_photo", ctypes.c_double), ("trim_factor", ctypes.c_double), ("spread_gate", ctypes.c_double),
+                ("assoc_gate", ctypes.c_double), ("trim_floor_photo", ctypes.c_double), ("tol", ctypes.c_double),
+                ("damping_init", ctypes.c_double), ("damping_max", ctypes.c_double), ("max_iters", ctypes.c_int32),
+                ("min_residuals", ctypes.c_int32)]
+
+
 class SsRegCfg(ctypes.Structure):
     _fields_ = [("huber_photo", ctypes.c_double), ("trim_factor", ctypes.c_double), ("spread_gate", ctypes.c_double)]
 
@@ -56,6 +63,7 @@ SS_ERR_UNSUPPORTED = 3
 SS_ERR_CUDA = 4
 SS_ERR_CAPACITY = 5
 SS_ERR_DEGENERATE = 6
+SS_ERR_REGISTRATION = 7
 
 _lib = None
 
@@ -99,6 +107,11 @@ def lib() -> ctypes.CDLL:
     L.ss_adam_step.restype = ctypes.c_int
     L.ss_range_image.argtypes = [ctypes.POINTER(SsCamera), vp, i32, vp, vp, vp]
     L.ss_range_image.restype = ctypes.c_int
+    L.ss_reg_solve_workspace_bytes.argtypes = [i32]
+    L.ss_reg_solve_workspace_bytes.restype = ctypes.c_size_t
+    L.ss_reg_photo_solve.argtypes = [vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp, ctypes.POINTER(SsRegSolveCfg), vp,
+                                     vp, vp, vp, vp]
+    L.ss_reg_photo_solve.restype = ctypes.c_int
     for name in ("ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_render_forward", "ss_records_counts", "ss_records_export", "ss_render_backward",
                  "ss_mapping_loss", "ss_photo_system"):
         getattr(L, name).restype = ctypes.c_int
@@ -110,14 +123,16 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
-            "ss_adam_step"]
+            "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_photo_solve"]
 
 
 def check(status: int, what: str = "") -> None:
     """Map a C-ABI status onto the reference's exception classes (errors.py)."""
-    from .errors import GeometryError
+    from .errors import GeometryError, RegistrationError
     if status == SS_OK:
         return
+    if status == SS_ERR_REGISTRATION:
+        raise RegistrationError(f"{what}: too few residuals survive association")
     msg = {SS_ERR_INVALID_ARGUMENT: "invalid argument", SS_ERR_STALE_RECORDS: "blend records are stale for this model",
            SS_ERR_UNSUPPORTED: "unsupported configuration", SS_ERR_CUDA: "CUDA error",
            SS_ERR_CAPACITY: "pair capacity exceeded", SS_ERR_DEGENERATE: "degenerate raw tangents"}.get(status, "error")

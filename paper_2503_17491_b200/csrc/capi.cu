@@ -10,7 +10,7 @@
 #include "binning.cu"
 #include "blend.cu"
 #include "loss.cu"
-#include "registration.cu"
+#include "reg_solve.cu"  // includes registration.cu
 
 using namespace ss;
 
@@ -671,6 +671,73 @@ int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, cons
   SS_CUDA_TRY(cudaMemcpyAsync(out30, dev_out, sizeof(double) * 30, cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaStreamSynchronize(s));
   return SS_OK;
+}
+
+size_t ss_reg_solve_workspace_bytes(int32_t M) {
+  const size_t m = (size_t)(M > 0 ? M : 1);
+  return m * sizeof(PhotoTmp) + m * 8 + (size_t)2 * kRsPasses * kRsBins * 4 + (size_t)1024 * 32 * 8 + 1024 * 4 +
+         sizeof(RegSolveState) + 256;
+}
+
+int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
+                       const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg, double* T_out_Rt,
+                       int32_t* info4, double* last_r2, void* workspace, void* stream) {
+  if (!X_w || M <= 0 || !scan_range || !scan_valid || !cam || !T0_Rt || !cfg || !T_out_Rt || !info4 || !last_r2 ||
+      !workspace)
+    return SS_ERR_INVALID_ARGUMENT;
+  if (cfg->max_iters < 0) return SS_ERR_INVALID_ARGUMENT;
+  RegCam rc;
+  int st = make_regcam(cam, rc);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  int occ = 0;
+  SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, 0));
+  if (occ < 1) return SS_ERR_CUDA;
+  const int G = std::min(num_sms(), 1024);
+  unsigned char* w = (unsigned char*)workspace;
+  PhotoTmp* tmp = (PhotoTmp*)w;
+  w += (size_t)M * sizeof(PhotoTmp);
+  unsigned long long* bits = (unsigned long long*)w;
+  w += (size_t)M * 8;
+  unsigned* hist = (unsigned*)w;
+  w += (size_t)2 * kRsPasses * kRsBins * 4;
+  double* part = (double*)w;
+  w += (size_t)1024 * 32 * 8;
+  int* pcnt = (int*)w;
+  w += 1024 * 4;
+  RegSolveState* state = (RegSolveState*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  // evaluation 0's histograms start zeroed; later evaluations zero the next set themselves
+  SS_CUDA_TRY(cudaMemsetAsync(hist, 0, (size_t)2 * kRsPasses * kRsBins * 4, s));
+  RegSolveState init{};
+  for (int q = 0; q < 12; ++q) init.T[q] = T0_Rt[q];
+  SS_CUDA_TRY(cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  RegSolveCfg k;
+  k.huber = cfg->huber_photo;
+  k.trim_factor = cfg->trim_factor;
+  k.spread_gate = cfg->spread_gate;
+  k.assoc_gate = cfg->assoc_gate;
+  k.trim_floor = cfg->trim_floor_photo;
+  k.tol = cfg->tol;
+  k.damping_init = cfg->damping_init;
+  k.damping_max = cfg->damping_max;
+  k.max_iters = cfg->max_iters;
+  k.min_residuals = cfg->min_residuals;
+  const double* Xp = X_w;
+  const double* sr = scan_range;
+  const uint8_t* sv = scan_valid;
+  void* args[] = {(void*)&Xp, (void*)&M, (void*)&rc, (void*)&sr, (void*)&sv, (void*)&k,
+                  (void*)&tmp, (void*)&bits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&state};
+  SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, 0, s));
+  RegSolveState out{};
+  SS_CUDA_TRY(cudaMemcpyAsync(&out, state, sizeof(out), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int q = 0; q < 12; ++q) T_out_Rt[q] = out.T[q];
+  info4[0] = out.it_total;
+  info4[1] = out.converged;
+  info4[2] = out.last_m;
+  info4[3] = out.n_eval;
+  *last_r2 = out.last_r2;
+  return out.status ? SS_ERR_REGISTRATION : SS_OK;
 }
 
 int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale, float* d_scales_extra,

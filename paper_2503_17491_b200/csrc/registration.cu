@@ -165,6 +165,43 @@ struct PhotoTmp {
   double r, du, dv, q[3];
 };
 
+// Residual of anchor i at pose T (registration.py:324-340); false when the
+// anchor has no valid bilinear sample.
+__device__ __forceinline__ bool photo_resid_one(const double* __restrict__ X, int i, const PoseK& T, const RegCam& cam,
+                                                const double* __restrict__ srange,
+                                                const uint8_t* __restrict__ svalid, double spread_gate,
+                                                PhotoTmp& t) {
+  // q = T^-1 X = R^T (X - t)
+  double d[3], q[3];
+  for (int c = 0; c < 3; ++c) d[c] = X[3 * i + c] - T.t[c];
+  for (int c = 0; c < 3; ++c) q[c] = T.R[c] * d[0] + T.R[3 + c] * d[1] + T.R[6 + c] * d[2];
+  const double rho2 = q[0] * q[0] + q[1] * q[1];
+  const double r2 = rho2 + q[2] * q[2];
+  const double az = atan2(q[1], q[0]), el = atan2(q[2], hypot(q[0], q[1]));
+  const double u = cam.fx * az + cam.cx - cam.off_u, v = cam.fy * el + cam.cy - cam.off_v;
+  const double fi = floor(u), fj = floor(v);
+  bool ok = rho2 > 1e-12 && fi >= 0.0 && fi + 1.0 < cam.W && fj >= 0.0 && fj + 1.0 < cam.H;
+  if (!ok) return false;
+  const int i0 = (int)fi, j0 = (int)fj;
+  const double fu = u - fi, fv = v - fj;
+  const size_t p00 = (size_t)j0 * cam.W + i0;
+  ok = svalid[p00] && svalid[p00 + 1] && svalid[p00 + cam.W] && svalid[p00 + cam.W + 1];
+  if (!ok) return false;
+  const double d00 = srange[p00], d10 = srange[p00 + 1], d01 = srange[p00 + cam.W], d11 = srange[p00 + cam.W + 1];
+  const double hi = fmax(fmax(d00, d10), fmax(d01, d11)), lo = fmin(fmin(d00, d10), fmin(d01, d11));
+  ok = hi - lo <= spread_gate;
+  const double top = d00 * (1 - fu) + d10 * fu;
+  const double bot = d01 * (1 - fu) + d11 * fu;
+  const double val = top * (1 - fv) + bot * fv;
+  t.r = sqrt(r2) - val;
+  t.du = (d10 - d00) * (1 - fv) + (d11 - d01) * fv;
+  t.dv = bot - top;
+  t.q[0] = q[0];
+  t.q[1] = q[1];
+  t.q[2] = q[2];
+  return ok;
+}
+
 // Residual of every anchor at pose T; |r| bits for the median of ok anchors.
 __global__ void k_photo_resid(const double* __restrict__ X, int M, PoseK T, RegCam cam,
                               const double* __restrict__ srange, const uint8_t* __restrict__ svalid,
@@ -172,43 +209,11 @@ __global__ void k_photo_resid(const double* __restrict__ X, int M, PoseK T, RegC
                               unsigned long long* __restrict__ absbits, int* __restrict__ n_ok) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool ok = false;
-  double rr = 0.0;
   if (i < M) {
-    // q = T^-1 X = R^T (X - t)
-    double d[3], q[3];
-    for (int c = 0; c < 3; ++c) d[c] = X[3 * i + c] - T.t[c];
-    for (int c = 0; c < 3; ++c) q[c] = T.R[c] * d[0] + T.R[3 + c] * d[1] + T.R[6 + c] * d[2];
-    const double rho2 = q[0] * q[0] + q[1] * q[1];
-    const double r2 = rho2 + q[2] * q[2];
-    const double az = atan2(q[1], q[0]), el = atan2(q[2], hypot(q[0], q[1]));
-    const double u = cam.fx * az + cam.cx - cam.off_u, v = cam.fy * el + cam.cy - cam.off_v;
-    const double fi = floor(u), fj = floor(v);
-    ok = rho2 > 1e-12 && fi >= 0.0 && fi + 1.0 < cam.W && fj >= 0.0 && fj + 1.0 < cam.H;
-    if (ok) {
-      const int i0 = (int)fi, j0 = (int)fj;
-      const double fu = u - fi, fv = v - fj;
-      const size_t p00 = (size_t)j0 * cam.W + i0;
-      ok = svalid[p00] && svalid[p00 + 1] && svalid[p00 + cam.W] && svalid[p00 + cam.W + 1];
-      if (ok) {
-        const double d00 = srange[p00], d10 = srange[p00 + 1], d01 = srange[p00 + cam.W],
-                     d11 = srange[p00 + cam.W + 1];
-        const double hi = fmax(fmax(d00, d10), fmax(d01, d11)), lo = fmin(fmin(d00, d10), fmin(d01, d11));
-        ok = hi - lo <= spread_gate;
-        const double top = d00 * (1 - fu) + d10 * fu;
-        const double bot = d01 * (1 - fu) + d11 * fu;
-        const double val = top * (1 - fv) + bot * fv;
-        PhotoTmp t;
-        t.r = sqrt(r2) - val;
-        rr = t.r;
-        t.du = (d10 - d00) * (1 - fv) + (d11 - d01) * fv;
-        t.dv = bot - top;
-        t.q[0] = q[0];
-        t.q[1] = q[1];
-        t.q[2] = q[2];
-        tmp[i] = t;
-      }
-    }
-    absbits[i] = ok ? (unsigned long long)__double_as_longlong(fabs(rr)) : ~0ull;
+    PhotoTmp t{};
+    ok = photo_resid_one(X, i, T, cam, srange, svalid, spread_gate, t);
+    if (ok) tmp[i] = t;
+    absbits[i] = ok ? (unsigned long long)__double_as_longlong(fabs(t.r)) : ~0ull;
   }
   const unsigned b = __ballot_sync(0xffffffffu, ok);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_ok, __popc(b));
@@ -281,6 +286,34 @@ __global__ void __launch_bounds__(1024) k_photo_median(const unsigned long long*
 
 // Trim, Huber-weight and reduce.  out: [0:21] sum w J^T J (upper, row-major),
 // [21:27] sum w J r, [27] Huber sum, [28] kept count, [29] sum r^2.
+// One kept anchor's contribution (registration.py:342-361, 219-228, 470-477):
+// [0:21] w J^T J upper, [21:27] w J r, [27] Huber, [28] count, [29] r^2.
+__device__ __forceinline__ void photo_accum_one(const PhotoTmp& t, const RegCam& cam, double thr, double huber,
+                                                int objective_only, double (&acc)[30]) {
+  const double ar = fabs(t.r);
+  if (!(ar <= thr)) return;
+  const double x = t.q[0], y = t.q[1], z = t.q[2];
+  const double rho2 = x * x + y * y, r2 = rho2 + z * z;
+  const double rho = sqrt(rho2), rq = sqrt(r2);
+  const double w = ar <= huber ? 1.0 : huber / fmax(ar, 1e-12);
+  acc[27] += ar <= huber ? 0.5 * t.r * t.r : huber * (ar - 0.5 * huber);
+  acc[28] += 1.0;
+  acc[29] += t.r * t.r;
+  if (objective_only) return;
+  const double dudq[3] = {cam.fx * (-y / rho2), cam.fx * (x / rho2), 0.0};
+  const double dvdq[3] = {cam.fy * (-x * z / (r2 * rho)), cam.fy * (-y * z / (r2 * rho)), cam.fy * (rho / r2)};
+  const double g[3] = {x / rq - t.du * dudq[0] - t.dv * dvdq[0], y / rq - t.du * dudq[1] - t.dv * dvdq[1],
+                       z / rq - t.du * dudq[2] - t.dv * dvdq[2]};
+  const double J[6] = {-g[0], -g[1], -g[2], g[1] * z - g[2] * y, g[2] * x - g[0] * z, g[0] * y - g[1] * x};
+  int k = 0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+#pragma unroll
+    for (int b = a; b < 6; ++b) acc[k++] += w * J[a] * J[b];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) acc[21 + a] += w * J[a] * t.r;
+}
+
 __global__ void __launch_bounds__(256) k_photo_accum(int M, RegCam cam, const PhotoTmp* __restrict__ tmp,
                                                      const unsigned long long* __restrict__ absbits,
                                                      const double* __restrict__ median, double trim_factor,
@@ -291,33 +324,7 @@ __global__ void __launch_bounds__(256) k_photo_accum(int M, RegCam cam, const Ph
 #pragma unroll
   for (int q = 0; q < 30; ++q) acc[q] = 0.0;
   const double thr = fmax(trim_factor * (*median), trim_floor);
-  if (i < M && absbits[i] != ~0ull) {
-    const PhotoTmp t = tmp[i];
-    const double ar = fabs(t.r);
-    if (ar <= thr) {
-      const double x = t.q[0], y = t.q[1], z = t.q[2];
-      const double rho2 = x * x + y * y, r2 = rho2 + z * z;
-      const double rho = sqrt(rho2), rq = sqrt(r2);
-      const double w = ar <= huber ? 1.0 : huber / fmax(ar, 1e-12);
-      acc[27] = ar <= huber ? 0.5 * t.r * t.r : huber * (ar - 0.5 * huber);
-      acc[28] = 1.0;
-      acc[29] = t.r * t.r;
-      if (!objective_only) {
-        const double dudq[3] = {cam.fx * (-y / rho2), cam.fx * (x / rho2), 0.0};
-        const double dvdq[3] = {cam.fy * (-x * z / (r2 * rho)), cam.fy * (-y * z / (r2 * rho)), cam.fy * (rho / r2)};
-        const double g[3] = {x / rq - t.du * dudq[0] - t.dv * dvdq[0], y / rq - t.du * dudq[1] - t.dv * dvdq[1],
-                             z / rq - t.du * dudq[2] - t.dv * dvdq[2]};
-        const double J[6] = {-g[0], -g[1], -g[2], g[1] * z - g[2] * y, g[2] * x - g[0] * z, g[0] * y - g[1] * x};
-        int k = 0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = a; b < 6; ++b) acc[k++] = w * J[a] * J[b];
-#pragma unroll
-        for (int a = 0; a < 6; ++a) acc[21 + a] = w * J[a] * t.r;
-      }
-    }
-  }
+  if (i < M && absbits[i] != ~0ull) photo_accum_one(tmp[i], cam, thr, huber, objective_only, acc);
   __shared__ double red[8][30];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll

@@ -6,7 +6,10 @@ line for line on the host (a 6x6 solve per step), while every residual,
 Jacobian, median trim and normal-equation reduction runs in the sm_100a
 kernels (libsplatb200.so, ``ss_photo_system``), the model render of
 ``sample_model`` is the B200 rasterizer and the scan range image is built on
-the device (``ss_range_image``).
+the device (``ss_range_image``).  By default the whole GN/LM loop runs in one
+cooperative kernel (``ss_reg_photo_solve``: no host round trip per
+evaluation); ``register(..., device_loop=False)`` runs it on the host over
+``ss_photo_system`` evaluations instead (the two agree to rounding).
 
 The geometric / joint / sequential modes need the PCA leaf tree and k-d tree
 association (registration.py:98-274), which SURVEY.md 8(f) lists as the next
@@ -21,7 +24,7 @@ import numpy as np
 import torch
 
 from . import engine
-from ._lib import SsRegCfg, check, lib
+from ._lib import SsRegCfg, SsRegSolveCfg, check, lib
 from .errors import RegistrationError
 from .geometry import SE3Pose, SphericalCamera, pose_rt
 from .rasterizer import RasterConfig
@@ -155,7 +158,7 @@ class PhotoProblem:
 
 
 def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, raster: RasterConfig | None = None,
-             rng=None) -> RegistrationResult:
+             rng=None, device_loop: bool = True) -> RegistrationResult:
     """Align a sensor-frame scan to the model (registration.py:387-524, photometric mode)."""
     cfg = cfg or RegistrationConfig()
     scan = np.asarray(scan, dtype=float).reshape(-1, 3)
@@ -174,8 +177,38 @@ def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, r
     X_w, n_model = sample_anchors(model, geo_cam, initial, cfg, raster, thin=s * s if s > 1 else 1)
     if n_model < cfg.min_residuals:
         raise RegistrationError("model renders to too few confident pixels")
-    prob = PhotoProblem(X_w, DeviceScan(cam, scan), cfg)
+    dscan = DeviceScan(cam, scan)
+    if device_loop:
+        return _solve_device(X_w, dscan, initial, cfg)
+    prob = PhotoProblem(X_w, dscan, cfg)
     return _solve(prob, initial, cfg)
+
+
+def _solve_device(X_w: torch.Tensor, scan: DeviceScan, initial, cfg: RegistrationConfig) -> RegistrationResult:
+    """The GN/LM loop (registration.py:437-524, photometric phase) as one device kernel."""
+    X = X_w.contiguous()
+    M = int(X.shape[0])
+    if M == 0:
+        raise RegistrationError("too few residuals survive association")
+    ws = torch.empty(int(lib().ss_reg_solve_workspace_bytes(M)), dtype=torch.uint8, device=X.device)
+    c = engine.ss_camera(scan.cam)
+    k = SsRegSolveCfg(float(cfg.huber_photo), float(cfg.trim_factor), float(cfg.spread_gate), float(cfg.assoc_gate),
+                      float(cfg.trim_floor_photo), float(cfg.tol), float(cfg.damping_init), float(cfg.damping_max),
+                      int(cfg.max_iters), int(cfg.min_residuals))
+    t0 = pose_rt(initial)
+    t_out = np.zeros(12)
+    info = np.zeros(4, dtype=np.int32)
+    r2 = ctypes.c_double(0.0)
+    check(lib().ss_reg_photo_solve(ctypes.c_void_p(X.data_ptr()), M, ctypes.c_void_p(scan.range.data_ptr()),
+                                   ctypes.c_void_p(scan.valid.data_ptr()), ctypes.byref(c),
+                                   t0.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k),
+                                   t_out.ctypes.data_as(ctypes.c_void_p), info.ctypes.data_as(ctypes.c_void_p),
+                                   ctypes.byref(r2), ctypes.c_void_p(ws.data_ptr()),
+                                   ctypes.c_void_p(engine.stream_ptr())), "register")
+    T = SE3Pose(t_out[:9].reshape(3, 3), t_out[9:]).orthonormalized()
+    m = int(info[2])
+    rms = float(np.sqrt(r2.value / m)) if m else 0.0
+    return RegistrationResult(T, bool(info[1]), int(info[0]), 0.0, rms, 0, m, cfg.mode)
 
 
 def _solve(prob: PhotoProblem, initial, cfg: RegistrationConfig) -> RegistrationResult:

@@ -57,10 +57,11 @@ def test_anchors_close_to_reference(cuda):
         assert np.abs(X.cpu().numpy() - G["X_w"]).max() < 1e-3
 
 
-def test_register_final_pose(cuda):
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_register_final_pose(cuda, device_loop):
     cfg = REG.RegistrationConfig(mode="photometric", max_iters=15)
     res = REG.register(SplatModel.from_params(PARAMS), G["scan"].astype(np.float64), _cam(),
-                       SE3Pose(G["initial_R"], G["initial_t"]), cfg)
+                       SE3Pose(G["initial_R"], G["initial_t"]), cfg, device_loop=device_loop)
     dt = np.abs(res.pose.translation - G["final_t"]).max()
     dR = np.abs(res.pose.rotation - G["final_R"]).max()
     print("register: dt", dt, "dR", dR, "iters", res.iterations, int(G["iterations"]), "n_photo", res.n_photo)
@@ -73,3 +74,52 @@ def test_non_photometric_mode_raises(cuda):
     with pytest.raises(Exception):
         REG.register(SplatModel.from_params(PARAMS), G["scan"].astype(np.float64), _cam(),
                      SE3Pose(G["initial_R"], G["initial_t"]), REG.RegistrationConfig(mode="sequential"))
+
+
+def _loops(X, scan, initial, cfg):
+    host = REG._solve(REG.PhotoProblem(X, scan, cfg), initial, cfg)
+    dev = REG._solve_device(X, scan, initial, cfg)
+    return host, dev
+
+
+def test_device_loop_matches_host_loop_golden(cuda):
+    """Same anchors and scan: the cooperative-kernel loop and the host loop over
+    ss_photo_system take the same accept/reject path and end at the same pose
+    (their 6x6 sums differ only in summation order)."""
+    scan = REG.DeviceScan(_cam(), G["scan"].astype(np.float64))
+    X = torch.tensor(G["X_w"], dtype=torch.float64, device="cuda")
+    for iters, tol in ((15, 1e-6), (30, 0.0)):
+        cfg = REG.RegistrationConfig(mode="photometric", max_iters=iters, tol=tol)
+        host, dev = _loops(X, scan, SE3Pose(G["initial_R"], G["initial_t"]), cfg)
+        assert dev.iterations == host.iterations and dev.converged == host.converged
+        assert dev.n_photo == host.n_photo
+        assert np.abs(dev.pose.translation - host.pose.translation).max() <= 1e-9
+        assert np.abs(dev.pose.rotation - host.pose.rotation).max() <= 1e-9
+        assert dev.photo_rms == pytest.approx(host.photo_rms, rel=1e-9)
+
+
+def test_device_loop_matches_host_loop_config3(cuda):
+    """BASELINE config 3 (300k-surfel map, 64x1024 scan, SE(3) offset, 20 iterations)."""
+    from paper_2503_17491_b200 import workloads as W
+    params, cam, scan_pts, truth, initial = W.config3_problem()
+    cfg = REG.RegistrationConfig(mode="photometric", max_iters=20, tol=0.0)
+    s = 2
+    geo = SphericalCamera(cam.width * s, cam.height * s, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    X, n = REG.sample_anchors(params, geo, initial, cfg, thin=s * s)
+    scan = REG.DeviceScan(cam, scan_pts)
+    host, dev = _loops(X, scan, initial, cfg)
+    print("config3 host", host.iterations, host.n_photo, "device", dev.iterations, dev.n_photo,
+          "err", np.abs(dev.pose.translation - truth.translation).max())
+    assert dev.iterations == host.iterations and dev.n_photo == host.n_photo
+    assert np.abs(dev.pose.translation - host.pose.translation).max() <= 1e-8
+    assert np.abs(dev.pose.rotation - host.pose.rotation).max() <= 1e-8
+    assert np.abs(dev.pose.translation - truth.translation).max() < 0.01
+
+
+def test_device_loop_too_few_residuals(cuda):
+    scan = REG.DeviceScan(_cam(), G["scan"].astype(np.float64))
+    X = torch.tensor(G["X_w"][:5], dtype=torch.float64, device="cuda")
+    from paper_2503_17491_b200.errors import RegistrationError
+    with pytest.raises(RegistrationError):
+        REG._solve_device(X, scan, SE3Pose(G["initial_R"], G["initial_t"]),
+                          REG.RegistrationConfig(mode="photometric"))
