@@ -20,6 +20,8 @@
  *   ss_adam_step             mapping.py:367-379     Adam of refine (+ :495-496 clamp)
  *   ss_reg_anchors           registration.py:190-213 sample_model (+ :430 thinning)
  *   ss_range_image           geometry.py:252-268     build_range_image
+ *   ss_smooth_range_image    geometry.py:271-287     smooth_range_image (size 3)
+ *   ss_range_image_normals   geometry.py:290-338     range_image_normals
  *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
  *                            the H/b accumulation of registration.py:470-477,
  *                            objective of registration.py:379-384)
@@ -172,6 +174,19 @@ int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, con
  * float64, device) -> nearest range per pixel (float64 H*W) and valid mask. */
 int ss_range_image(const ss_camera* cam, const double* pts, int32_t n, double* range_out, uint8_t* valid_out,
                    void* stream);
+
+/* smooth_range_image (geometry.py:271-287), size 3: 3x3 median of the valid
+ * ranges (invalid pixels count as +inf; columns wrap when `wrap`, else both
+ * axes clamp), pixels whose median is +inf keep their range.  range/out:
+ * H*W float64, valid: H*W bytes, all device.  Bit-exact. */
+int ss_smooth_range_image(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,
+                          double* out, void* stream);
+
+/* range_image_normals (geometry.py:290-338): central-difference unit normals
+ * (H*W*3 float64) oriented toward the sensor and their mask (four valid
+ * neighbours, azimuth seam wrapped for full-circle cameras). */
+int ss_range_image_normals(const ss_camera* cam, const double* range, const uint8_t* valid, double* normal_out,
+                           uint8_t* ok_out, void* stream);
 
 /* One evaluation of _photo_system (registration.py:316-362) with Huber
  * weights: residuals of anchors X_w (M x 3 float64) against the scan range

@@ -107,6 +107,10 @@ def lib() -> ctypes.CDLL:
     L.ss_adam_step.restype = ctypes.c_int
     L.ss_range_image.argtypes = [ctypes.POINTER(SsCamera), vp, i32, vp, vp, vp]
     L.ss_range_image.restype = ctypes.c_int
+    L.ss_smooth_range_image.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+    L.ss_smooth_range_image.restype = ctypes.c_int
+    L.ss_range_image_normals.argtypes = [ctypes.POINTER(SsCamera), vp, vp, vp, vp, vp]
+    L.ss_range_image_normals.restype = ctypes.c_int
     L.ss_reg_solve_workspace_bytes.argtypes = [i32]
     L.ss_reg_solve_workspace_bytes.restype = ctypes.c_size_t
     L.ss_reg_photo_solve.argtypes = [vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp, ctypes.POINTER(SsRegSolveCfg), vp,
@@ -123,7 +127,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
-            "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_photo_solve"]
+            "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_photo_solve",
+            "ss_smooth_range_image", "ss_range_image_normals"]
 
 
 def check(status: int, what: str = "") -> None:

@@ -9,6 +9,7 @@
 
 #include "binning.cu"
 #include "blend.cu"
+#include "keyframe.cu"
 #include "loss.cu"
 #include "reg_solve.cu"  // includes registration.cu
 
@@ -738,6 +739,28 @@ int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, c
   info4[3] = out.n_eval;
   *last_r2 = out.last_r2;
   return out.status ? SS_ERR_REGISTRATION : SS_OK;
+}
+
+int ss_smooth_range_image(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,
+                          double* out, void* stream) {
+  if (width < 1 || height < 1 || !range || !valid || !out) return SS_ERR_INVALID_ARGUMENT;
+  const int P = width * height;
+  k_smooth_range<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(width, height, wrap ? 1 : 0, range, valid, out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_range_image_normals(const ss_camera* cam, const double* range, const uint8_t* valid, double* normal_out,
+                           uint8_t* ok_out, void* stream) {
+  if (!cam || !range || !valid || !normal_out || !ok_out) return SS_ERR_INVALID_ARGUMENT;
+  CamK k;
+  const int st = make_camk(cam, 8, 0.5, k);
+  if (st) return st;
+  const int P = k.W * k.H;
+  k_range_normals<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(k, full_circle(cam) ? 1 : 0, range, valid,
+                                                                     normal_out, ok_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
 }
 
 int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale, float* d_scales_extra,

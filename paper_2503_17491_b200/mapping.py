@@ -76,6 +76,21 @@ class DeviceKeyframe:
         self.nvalid = torch.as_tensor(np.asarray(nvalid, np.uint8), device=dev).contiguous()
 
     @classmethod
+    def from_cloud(cls, cloud, pose, width: int, height: int, camera=None) -> "DeviceKeyframe":
+        """make_keyframe (mapping.py:106-114) on the device: the target images never leave HBM."""
+        from . import keyframe as KF
+        cam = camera if camera is not None else KF.estimate_camera(
+            cloud.cpu().numpy() if torch.is_tensor(cloud) else cloud, width, height)
+        im = KF.keyframe_images(cam, cloud)
+        kf = cls.__new__(cls)
+        kf.camera, kf.pose = cam, pose
+        kf.range = im["range"].float().contiguous()
+        kf.valid = im["valid"]
+        kf.normal = im["normal"].float().contiguous()
+        kf.nvalid = im["nvalid"]
+        return kf
+
+    @classmethod
     def from_reference(cls, kf) -> "DeviceKeyframe":
         return cls(kf.camera, kf.pose, kf.range_image.range, kf.range_image.valid, kf.normal_image.normals,
                    kf.normal_image.valid)

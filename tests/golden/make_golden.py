@@ -233,3 +233,40 @@ def make_refine_case():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "refine":
     make_refine_case()
+
+
+def make_keyframe_case():
+    """make_keyframe's images (mapping.py:106-114): range image, 3x3 median smoothing and
+    normals, for a full-circle scan (seam wrap) and a noisy partial-field-of-view crop."""
+    from splatscan.geometry import build_range_image, estimate_camera, range_image_normals, smooth_range_image
+    from splatscan.synth import ScanSpec, raycast_scan, room_with_boxes
+
+    rng = np.random.default_rng(5)
+    scene = room_with_boxes(n_boxes=5, seed=2)
+    spec = ScanSpec(width=256, height=32)
+    pose = SE3Pose(so3_exp(np.deg2rad([0.0, 0.0, 25.0])), np.array([0.5, -0.3, 0.2]))
+    full = f32(raycast_scan(scene, pose, spec).cloud)
+    noisy = full * (1.0 + 0.003 * rng.normal(size=(full.shape[0], 1)))
+    az = np.arctan2(noisy[:, 1], noisy[:, 0])
+    part = f32(noisy[(az > -1.2) & (az < 1.7)])
+    out = {}
+    for name, cloud, (W, H) in (("full", full, (256, 32)), ("part", part, (118, 32))):
+        cam = estimate_camera(cloud, W, H)
+        rimg = build_range_image(cam, cloud)
+        sm = smooth_range_image(rimg, cam.full_circle)
+        nimg = range_image_normals(cam, sm)
+        out[f"{name}_cloud"] = cloud
+        out[f"{name}_cam"] = np.array([cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max])
+        out[f"{name}_full_circle"] = np.array(cam.full_circle)
+        out[f"{name}_range"] = rimg.range
+        out[f"{name}_valid"] = rimg.valid
+        out[f"{name}_smooth"] = sm.range
+        out[f"{name}_normals"] = nimg.normals
+        out[f"{name}_nvalid"] = nimg.valid
+        print(name, "points", cloud.shape[0], "valid", int(rimg.valid.sum()), "normals", int(nimg.valid.sum()),
+              "full circle", cam.full_circle, "smoothed changed", int((sm.range != rimg.range).sum()))
+    np.savez_compressed(os.path.join(OUT, "golden_keyframe.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "keyframe":
+    make_keyframe_case()
