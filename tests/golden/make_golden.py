@@ -270,3 +270,47 @@ def make_keyframe_case():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "keyframe":
     make_keyframe_case()
+
+
+def make_geometric_case():
+    """The geometric half of registration (registration.py:98-164, 231-274, 387-524) on the
+    inputs of golden_register.npz: the leaf tree of the model points, one _geo_system
+    linearisation, and register() in the geometric, joint and sequential modes."""
+    from splatscan import registration as REG
+    from splatscan.registration import RegistrationConfig, register
+
+    G = np.load(os.path.join(OUT, "golden_register.npz"))
+    c = G["cam"]
+    cam = SphericalCamera(int(c[0]), int(c[1]), *[float(x) for x in c[2:]])
+    p = {k[2:]: G[k].astype(np.float64) for k in G.files if k.startswith("p_")}
+    model, _ = to_model(p)
+    scan = G["scan"].astype(np.float64)
+    initial = SE3Pose(G["initial_R"], G["initial_t"])
+    T0 = SE3Pose(G["T0_R"], G["T0_t"])
+    cfg = RegistrationConfig()
+    geo_cam = SphericalCamera(cam.width * 2, cam.height * 2, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    model_pts, _, _ = REG.sample_model(model, geo_cam, initial, cfg)
+    tree = REG.build_leaf_tree(model_pts, initial.translation, cfg.leaf_size, cfg.flatness_tau)
+    sel = np.random.default_rng(0).choice(scan.shape[0], cfg.max_geo_points, replace=False)
+    geo_scan = scan[sel]
+    r, J = REG._geo_system(tree, geo_scan, T0, cfg, max(cfg.trim_floor_geo, 0.5))
+    w = REG._huber_weights(r, cfg.huber_geo)
+    out = dict(model_pts=model_pts, point_leaf=tree.point_leaf, leaf_centroids=tree.centroids,
+               leaf_normals=tree.normals, leaf_sizes=tree.sizes, leaf_usable=tree.usable, geo_sel=sel,
+               geo_H0=(J.T * w) @ J, geo_b0=J.T @ (w * r), geo_m0=r.shape[0],
+               geo_huber0=REG._huber_value(r, cfg.huber_geo), geo_r0=r)
+    for mode, iters in (("geometric", 15), ("joint", 15), ("sequential", 30)):
+        res = register(model, scan, cam, initial, RegistrationConfig(mode=mode, max_iters=iters))
+        out.update({f"{mode}_R": res.pose.rotation, f"{mode}_t": res.pose.translation,
+                    f"{mode}_iterations": res.iterations, f"{mode}_converged": res.converged,
+                    f"{mode}_geo_rms": res.geo_rms, f"{mode}_photo_rms": res.photo_rms,
+                    f"{mode}_n_geo": res.n_geo, f"{mode}_n_photo": res.n_photo})
+        print(mode, "iters", res.iterations, "converged", res.converged, "n_geo", res.n_geo, "n_photo", res.n_photo,
+              "err_t", np.linalg.norm(res.pose.translation - G["truth_t"]))
+    print("model_pts", model_pts.shape[0], "leaves", tree.sizes.shape[0], "usable", int(tree.usable.sum()),
+          "geo m0", r.shape[0])
+    np.savez_compressed(os.path.join(OUT, "golden_register_geo.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "geometric":
+    make_geometric_case()
