@@ -25,8 +25,9 @@
  *   ss_photo_system          registration.py:316-362 _photo_system (+ Huber and
  *                            the H/b accumulation of registration.py:470-477,
  *                            objective of registration.py:379-384)
- *   ss_reg_photo_solve       registration.py:437-524 the GN/LM loop of register
- *                            (photometric phase), se3.py:121-150 retract
+ *   ss_leaf_tree_build       registration.py:98-164  build_leaf_tree
+ *   ss_reg_solve             registration.py:437-524 the GN/LM loop of register
+ *                            (every mode) + _geo_system :231-274, se3.py:121-150
  */
 #ifndef SPLAT_B200_H
 #define SPLAT_B200_H
@@ -201,26 +202,48 @@ int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, cons
                     const ss_camera* cam, const double* T_Rt, double trim_floor, const ss_reg_cfg* cfg,
                     int32_t objective_only, double* out30, void* workspace, void* stream);
 
-/* RegistrationConfig fields of the photometric GN/LM loop (registration.py:41-61). */
+/* build_leaf_tree (registration.py:98-164) of n device points (float64 n x 3):
+ * planar leaves of recursive PCA median splits, level-parallel on the device.
+ * Leaf arrays (host, capacity max_leaves): centroids, normals oriented toward
+ * viewpoint3 (zero when unusable), sizes, usable flags; point_leaf_out
+ * (device, n) maps every point to its leaf.  workspace:
+ * ss_leaf_tree_workspace_bytes(n).  Synchronises the stream (one small
+ * read-back per tree level). */
+size_t ss_leaf_tree_workspace_bytes(int32_t n);
+int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, int32_t leaf_size, double tau,
+                       int32_t max_leaves, double* centroids_out, double* normals_out, int32_t* sizes_out,
+                       uint8_t* usable_out, int32_t* point_leaf_out, int32_t* n_leaves_out, void* workspace,
+                       void* stream);
+
+/* RegistrationConfig fields of the GN/LM loop (registration.py:41-61);
+ * mode: 0 photometric, 1 geometric, 2 joint, 3 sequential. */
 typedef struct {
-  double huber_photo, trim_factor, spread_gate, assoc_gate, trim_floor_photo, tol, damping_init, damping_max;
-  int32_t max_iters, min_residuals;
+  double huber_photo, huber_geo, trim_factor, spread_gate, assoc_gate, trim_floor_photo, trim_floor_geo, tol,
+      damping_init, damping_max;
+  int32_t max_iters, min_residuals, assoc_k, mode;
 } ss_reg_solve_cfg;
 
-/* The whole photometric Gauss-Newton / Levenberg loop of register()
- * (registration.py:437-524, mode "photometric") on the device, one
- * cooperative kernel: every evaluation of _photo_system (residuals, exact
- * median trim, Huber-weighted 6x6 normal equations), the damped 6x6 solve,
- * T <- T exp(delta), acceptance, damping and trim-floor schedule.  From
- * initial pose T0_Rt; returns the final pose (before the host's SVD
- * re-orthonormalisation) in T_out_Rt, info4 = {iterations, converged, m of
- * the last full evaluation, evaluations run}, last_r2 = its sum of r^2.
+/* The whole Gauss-Newton / Levenberg loop of register() (registration.py:
+ * 437-524) on the device, one cooperative kernel, every mode: per
+ * evaluation the geometric system (k nearest usable leaves within
+ * assoc_gate, closest plane, median trim; registration.py:231-274) and / or
+ * the photometric one (_photo_system, :316-362), Huber-weighted 6x6 normal
+ * equations, the damped solve, T <- T exp(delta), acceptance with the
+ * reference's positional pairing of residual families and frozen terms
+ * (:379-384), damping and trim-floor schedules, sequential phases.
+ * Geometric inputs: usable leaf centroids / normals (n_leaves x 3 float64)
+ * and the subsampled scan (n_geo_scan x 3, sensor frame); photometric:
+ * world anchors X_w (M x 3) and the scan range image.  All device.
+ * Returns the final pose (before the host's SVD re-orthonormalisation),
+ * info6 = {iterations, converged, n_geo, n_photo, evaluations, status},
+ * r2_out2 = sum r^2 of the last geometric / photometric systems.
  * SS_ERR_REGISTRATION when fewer than min_residuals residuals survive.
- * workspace: ss_reg_solve_workspace_bytes(M) bytes.  Synchronises the stream. */
-size_t ss_reg_solve_workspace_bytes(int32_t M);
-int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
-                       const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg, double* T_out_Rt,
-                       int32_t* info4, double* last_r2, void* workspace, void* stream);
+ * workspace: ss_reg_solve_workspace_bytes(n_geo_scan, M).  Synchronises. */
+size_t ss_reg_solve_workspace_bytes(int32_t n_geo_scan, int32_t M);
+int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
+                 int32_t n_geo_scan, const double* X_w, int32_t M, const double* scan_range,
+                 const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,
+                 double* T_out_Rt, int32_t* info6, double* r2_out2, void* workspace, void* stream);
 
 /* Measured FP32 FMA throughput of the current device (TFLOP/s), the roofline
  * denominator of the FP32-bound blend kernels.  Synchronises the stream. */

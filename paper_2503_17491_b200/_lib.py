@@ -46,10 +46,11 @@ class SsSplats(ctypes.Structure):
 
 
 class SsRegSolveCfg(ctypes.Structure):
-    _fields_ = [("huber_photo", ctypes.c_double), ("trim_factor", ctypes.c_double), ("spread_gate", ctypes.c_double),
-                ("assoc_gate", ctypes.c_double), ("trim_floor_photo", ctypes.c_double), ("tol", ctypes.c_double),
+    _fields_ = [("huber_photo", ctypes.c_double), ("huber_geo", ctypes.c_double), ("trim_factor", ctypes.c_double),
+                ("spread_gate", ctypes.c_double), ("assoc_gate", ctypes.c_double),
+                ("trim_floor_photo", ctypes.c_double), ("trim_floor_geo", ctypes.c_double), ("tol", ctypes.c_double),
                 ("damping_init", ctypes.c_double), ("damping_max", ctypes.c_double), ("max_iters", ctypes.c_int32),
-                ("min_residuals", ctypes.c_int32)]
+                ("min_residuals", ctypes.c_int32), ("assoc_k", ctypes.c_int32), ("mode", ctypes.c_int32)]
 
 
 class SsRegCfg(ctypes.Structure):
@@ -111,11 +112,15 @@ def lib() -> ctypes.CDLL:
     L.ss_smooth_range_image.restype = ctypes.c_int
     L.ss_range_image_normals.argtypes = [ctypes.POINTER(SsCamera), vp, vp, vp, vp, vp]
     L.ss_range_image_normals.restype = ctypes.c_int
-    L.ss_reg_solve_workspace_bytes.argtypes = [i32]
+    L.ss_leaf_tree_workspace_bytes.argtypes = [i32]
+    L.ss_leaf_tree_workspace_bytes.restype = ctypes.c_size_t
+    L.ss_leaf_tree_build.argtypes = [vp, i32, vp, i32, d, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.ss_leaf_tree_build.restype = ctypes.c_int
+    L.ss_reg_solve_workspace_bytes.argtypes = [i32, i32]
     L.ss_reg_solve_workspace_bytes.restype = ctypes.c_size_t
-    L.ss_reg_photo_solve.argtypes = [vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp, ctypes.POINTER(SsRegSolveCfg), vp,
-                                     vp, vp, vp, vp]
-    L.ss_reg_photo_solve.restype = ctypes.c_int
+    L.ss_reg_solve.argtypes = [vp, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp,
+                               ctypes.POINTER(SsRegSolveCfg), vp, vp, vp, vp, vp]
+    L.ss_reg_solve.restype = ctypes.c_int
     for name in ("ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_render_forward", "ss_records_counts", "ss_records_export", "ss_render_backward",
                  "ss_mapping_loss", "ss_photo_system"):
         getattr(L, name).restype = ctypes.c_int
@@ -127,8 +132,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
-            "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_photo_solve",
-            "ss_smooth_range_image", "ss_range_image_normals"]
+            "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",
+            "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build"]
 
 
 def check(status: int, what: str = "") -> None:

@@ -10,6 +10,7 @@
 #include "binning.cu"
 #include "blend.cu"
 #include "keyframe.cu"
+#include "leaf_tree.cu"
 #include "loss.cu"
 #include "reg_solve.cu"  // includes registration.cu
 
@@ -674,19 +675,23 @@ int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, cons
   return SS_OK;
 }
 
-size_t ss_reg_solve_workspace_bytes(int32_t M) {
-  const size_t m = (size_t)(M > 0 ? M : 1);
-  return m * sizeof(PhotoTmp) + m * 8 + (size_t)2 * kRsPasses * kRsBins * 4 + (size_t)1024 * 32 * 8 + 1024 * 4 +
-         sizeof(RegSolveState) + 256;
+size_t ss_reg_solve_workspace_bytes(int32_t n_geo_scan, int32_t M) {
+  const size_t g = (size_t)(n_geo_scan > 0 ? n_geo_scan : 1), m = (size_t)(M > 0 ? M : 1);
+  return g * (sizeof(GeoTmp) + 8) + m * (sizeof(PhotoTmp) + 8) + (size_t)4 * kRsPasses * kRsBins * 4 +
+         (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + sizeof(RegSolveState) + 1024;
 }
 
-int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, const uint8_t* scan_valid,
-                       const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg, double* T_out_Rt,
-                       int32_t* info4, double* last_r2, void* workspace, void* stream) {
-  if (!X_w || M <= 0 || !scan_range || !scan_valid || !cam || !T0_Rt || !cfg || !T_out_Rt || !info4 || !last_r2 ||
-      !workspace)
+int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
+                 int32_t n_geo_scan, const double* X_w, int32_t M, const double* scan_range,
+                 const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,
+                 double* T_out_Rt, int32_t* info6, double* r2_out2, void* workspace, void* stream) {
+  if (!cam || !T0_Rt || !cfg || !T_out_Rt || !info6 || !r2_out2 || !workspace) return SS_ERR_INVALID_ARGUMENT;
+  if (cfg->mode < 0 || cfg->mode > 3 || cfg->max_iters < 0 || cfg->assoc_k < 1) return SS_ERR_INVALID_ARGUMENT;
+  const bool need_geo = cfg->mode != 0, need_photo = cfg->mode != 1;
+  if (need_geo && (n_leaves < 0 || n_geo_scan < 0 || (n_leaves > 0 && (!leaf_centroids || !leaf_normals)) ||
+                   (n_geo_scan > 0 && !geo_scan)))
     return SS_ERR_INVALID_ARGUMENT;
-  if (cfg->max_iters < 0) return SS_ERR_INVALID_ARGUMENT;
+  if (need_photo && (M < 0 || (M > 0 && (!X_w || !scan_range || !scan_valid)))) return SS_ERR_INVALID_ARGUMENT;
   RegCam rc;
   int st = make_regcam(cam, rc);
   if (st) return st;
@@ -695,49 +700,59 @@ int ss_reg_photo_solve(const double* X_w, int32_t M, const double* scan_range, c
   SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, 0));
   if (occ < 1) return SS_ERR_CUDA;
   const int G = std::min(num_sms(), 1024);
+  const int ng = need_geo ? n_geo_scan : 0, m = need_photo ? M : 0;
+  if (ng > G * kRsThreads) return SS_ERR_UNSUPPORTED;  // one scan point per thread
   unsigned char* w = (unsigned char*)workspace;
-  PhotoTmp* tmp = (PhotoTmp*)w;
-  w += (size_t)M * sizeof(PhotoTmp);
-  unsigned long long* bits = (unsigned long long*)w;
-  w += (size_t)M * 8;
-  unsigned* hist = (unsigned*)w;
-  w += (size_t)2 * kRsPasses * kRsBins * 4;
-  double* part = (double*)w;
-  w += (size_t)1024 * 32 * 8;
-  int* pcnt = (int*)w;
-  w += 1024 * 4;
-  RegSolveState* state = (RegSolveState*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
-  // evaluation 0's histograms start zeroed; later evaluations zero the next set themselves
-  SS_CUDA_TRY(cudaMemsetAsync(hist, 0, (size_t)2 * kRsPasses * kRsBins * 4, s));
+  auto take = [&](size_t bytes) {
+    unsigned char* p = (unsigned char*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+    w = p + bytes;
+    return p;
+  };
+  GeoTmp* gtmp = (GeoTmp*)take((size_t)std::max(ng, 1) * sizeof(GeoTmp));
+  unsigned long long* gbits = (unsigned long long*)take((size_t)std::max(ng, 1) * 8);
+  PhotoTmp* ptmp = (PhotoTmp*)take((size_t)std::max(m, 1) * sizeof(PhotoTmp));
+  unsigned long long* pbits = (unsigned long long*)take((size_t)std::max(m, 1) * 8);
+  unsigned* hist = (unsigned*)take((size_t)4 * kRsPasses * kRsBins * 4);
+  double* part = (double*)take((size_t)1024 * 2 * kRsAcc * 8);
+  int* pcnt = (int*)take(1024 * 4);
+  RegSolveState* state = (RegSolveState*)take(sizeof(RegSolveState));
+  // the first evaluation's histograms start zeroed; later evaluations zero the next set themselves
+  SS_CUDA_TRY(cudaMemsetAsync(hist, 0, (size_t)4 * kRsPasses * kRsBins * 4, s));
   RegSolveState init{};
   for (int q = 0; q < 12; ++q) init.T[q] = T0_Rt[q];
   SS_CUDA_TRY(cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   RegSolveCfg k;
-  k.huber = cfg->huber_photo;
+  k.huber_photo = cfg->huber_photo;
+  k.huber_geo = cfg->huber_geo;
   k.trim_factor = cfg->trim_factor;
   k.spread_gate = cfg->spread_gate;
   k.assoc_gate = cfg->assoc_gate;
-  k.trim_floor = cfg->trim_floor_photo;
+  k.floor_photo = cfg->trim_floor_photo;
+  k.floor_geo = cfg->trim_floor_geo;
   k.tol = cfg->tol;
   k.damping_init = cfg->damping_init;
   k.damping_max = cfg->damping_max;
   k.max_iters = cfg->max_iters;
   k.min_residuals = cfg->min_residuals;
-  const double* Xp = X_w;
-  const double* sr = scan_range;
-  const uint8_t* sv = scan_valid;
-  void* args[] = {(void*)&Xp, (void*)&M, (void*)&rc, (void*)&sr, (void*)&sv, (void*)&k,
-                  (void*)&tmp, (void*)&bits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&state};
+  k.assoc_k = cfg->assoc_k;
+  k.mode = cfg->mode;
+  RsGeo geo{leaf_centroids, leaf_normals, need_geo ? n_leaves : 0, geo_scan, ng};
+  RsPhoto ph{X_w, m, scan_range, scan_valid};
+  void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
+                  (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&state};
   SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, 0, s));
   RegSolveState out{};
   SS_CUDA_TRY(cudaMemcpyAsync(&out, state, sizeof(out), cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaStreamSynchronize(s));
   for (int q = 0; q < 12; ++q) T_out_Rt[q] = out.T[q];
-  info4[0] = out.it_total;
-  info4[1] = out.converged;
-  info4[2] = out.last_m;
-  info4[3] = out.n_eval;
-  *last_r2 = out.last_r2;
+  info6[0] = out.it_total;
+  info6[1] = out.converged;
+  info6[2] = out.last_m[0];
+  info6[3] = out.last_m[1];
+  info6[4] = out.n_eval;
+  info6[5] = out.status;
+  r2_out2[0] = out.last_r2[0];
+  r2_out2[1] = out.last_r2[1];
   return out.status ? SS_ERR_REGISTRATION : SS_OK;
 }
 
@@ -760,6 +775,71 @@ int ss_range_image_normals(const ss_camera* cam, const double* range, const uint
   k_range_normals<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(k, full_circle(cam) ? 1 : 0, range, valid,
                                                                      normal_out, ok_out);
   SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+size_t ss_leaf_tree_workspace_bytes(int32_t n) {
+  const size_t m = (size_t)(n > 0 ? n : 1);
+  return m * (4 + 4 + 8 + 8 + sizeof(LeafRec) + 8) + 1024;
+}
+
+int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, int32_t leaf_size, double tau,
+                       int32_t max_leaves, double* centroids_out, double* normals_out, int32_t* sizes_out,
+                       uint8_t* usable_out, int32_t* point_leaf_out, int32_t* n_leaves_out, void* workspace,
+                       void* stream) {
+  if (!pts || n <= 0 || !viewpoint3 || leaf_size < 0 || max_leaves <= 0 || !centroids_out || !normals_out ||
+      !sizes_out || !usable_out || !point_leaf_out || !n_leaves_out || !workspace)
+    return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* w = (unsigned char*)workspace;
+  int* idx = (int*)w;
+  w += (size_t)n * 4;
+  int* tmp = (int*)w;
+  w += (size_t)n * 4;
+  double* proj = (double*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+  w = (unsigned char*)(proj + n);
+  int2* nodes = (int2*)w;
+  w += (size_t)n * 8;
+  LeafRec* recs = (LeafRec*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+  w = (unsigned char*)(recs + n);
+  int2* leaves_d = (int2*)w;
+  k_iota<<<(n + 255) / 256, 256, 0, s>>>(n, idx);
+  const double3 vp = make_double3(viewpoint3[0], viewpoint3[1], viewpoint3[2]);
+  std::vector<int2> cur{make_int2(0, n)}, next, leaves;
+  std::vector<LeafRec> h;
+  int nl_total = 0;
+  while (!cur.empty()) {
+    const int L = (int)cur.size();
+    SS_CUDA_TRY(cudaMemcpyAsync(nodes, cur.data(), sizeof(int2) * L, cudaMemcpyHostToDevice, s));
+    k_leaf_level<<<L, kLtThreads, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
+    SS_CUDA_TRY(cudaGetLastError());
+    h.resize(L);
+    SS_CUDA_TRY(cudaMemcpyAsync(h.data(), recs, sizeof(LeafRec) * L, cudaMemcpyDeviceToHost, s));
+    SS_CUDA_TRY(cudaStreamSynchronize(s));
+    next.clear();
+    for (int i = 0; i < L; ++i) {
+      if (h[i].split) {
+        next.push_back(make_int2(cur[i].x, cur[i].x + h[i].nl));
+        next.push_back(make_int2(cur[i].x + h[i].nl, cur[i].y));
+        continue;
+      }
+      if (nl_total >= max_leaves) return SS_ERR_CAPACITY;
+      for (int k = 0; k < 3; ++k) {
+        centroids_out[3 * nl_total + k] = h[i].c[k];
+        normals_out[3 * nl_total + k] = h[i].n[k];
+      }
+      sizes_out[nl_total] = cur[i].y - cur[i].x;
+      usable_out[nl_total] = (uint8_t)h[i].usable;
+      leaves.push_back(cur[i]);
+      ++nl_total;
+    }
+    cur.swap(next);
+  }
+  SS_CUDA_TRY(cudaMemcpyAsync(leaves_d, leaves.data(), sizeof(int2) * nl_total, cudaMemcpyHostToDevice, s));
+  k_leaf_assign<<<nl_total, 256, 0, s>>>(idx, leaves_d, nl_total, point_leaf_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  *n_leaves_out = nl_total;
   return SS_OK;
 }
 

@@ -1,19 +1,19 @@
-"""Drop-in photometric registration (reference: pkg/src/splatscan/registration.py).
+"""Drop-in registration (reference: pkg/src/splatscan/registration.py).
 
-``register(model, scan, cam, initial, cfg)`` with ``cfg.mode == "photometric"``
-follows the reference's Gauss-Newton / Levenberg loop (registration.py:387-524)
-line for line on the host (a 6x6 solve per step), while every residual,
-Jacobian, median trim and normal-equation reduction runs in the sm_100a
-kernels (libsplatb200.so, ``ss_photo_system``), the model render of
-``sample_model`` is the B200 rasterizer and the scan range image is built on
-the device (``ss_range_image``).  By default the whole GN/LM loop runs in one
-cooperative kernel (``ss_reg_photo_solve``: no host round trip per
-evaluation); ``register(..., device_loop=False)`` runs it on the host over
-``ss_photo_system`` evaluations instead (the two agree to rounding).
-
-The geometric / joint / sequential modes need the PCA leaf tree and k-d tree
-association (registration.py:98-274), which SURVEY.md 8(f) lists as the next
-item and are not on this path: they raise ``RegistrationError``.
+``register(model, scan, cam, initial, cfg)`` runs the reference's
+Gauss-Newton / Levenberg loop (registration.py:387-524) in every mode --
+photometric, geometric, joint and the default sequential schedule -- as ONE
+cooperative sm_100a kernel (``ss_reg_solve``): per evaluation the geometric
+point-to-plane system (k nearest leaves, closest plane, median trim;
+:231-274) and / or the photometric range-warp system (:316-362), the damped
+6x6 solve, the SE(3) update and the acceptance test, with no host round trip.
+Around it: the model render of ``sample_model`` is the B200 rasterizer, the
+PCA leaf tree (:98-164) is built level-parallel on the device
+(``ss_leaf_tree_build``), the scan range image by ``ss_range_image``.  The
+host only draws the reference's geometric scan subsample (same numpy RNG
+call) and re-orthonormalises the final rotation (SVD).
+``register(..., device_loop=False)`` (photometric mode) runs the loop on the
+host over ``ss_photo_system`` evaluations instead (parity check of the kernel).
 """
 from __future__ import annotations
 
@@ -87,6 +87,49 @@ class DeviceScan:
               "build_range_image")
 
 
+@dataclass
+class LeafTree:
+    """registration.py:81-95 (the k-d tree over usable centroids is replaced by the
+    device association; ``kdtree`` stays None).  ``dev_centroids`` / ``dev_normals``
+    hold the usable leaves on the device for the association kernel."""
+    centroids: np.ndarray
+    normals: np.ndarray
+    sizes: np.ndarray
+    usable: np.ndarray
+    point_leaf: np.ndarray
+    kdtree: object = None
+    dev_centroids: torch.Tensor | None = None
+    dev_normals: torch.Tensor | None = None
+
+
+def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float = 0.02) -> LeafTree:
+    """registration.py:98-164 on the device (level-parallel PCA median splits)."""
+    dev = engine.require_cuda()
+    P = points if torch.is_tensor(points) else torch.as_tensor(np.asarray(points, np.float64).reshape(-1, 3))
+    P = P.to(dev, torch.float64).reshape(-1, 3).contiguous()
+    n = int(P.shape[0])
+    if n == 0:
+        raise RegistrationError("cannot build a leaf tree from an empty cloud")
+    vp = np.ascontiguousarray(np.asarray(viewpoint, np.float64).reshape(3))
+    cap = n
+    cent, nrm = np.zeros((cap, 3)), np.zeros((cap, 3))
+    sizes, usable = np.zeros(cap, np.int32), np.zeros(cap, np.uint8)
+    pl = torch.empty(n, dtype=torch.int32, device=dev)
+    nl = ctypes.c_int32(0)
+    ws = torch.empty(int(lib().ss_leaf_tree_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    check(lib().ss_leaf_tree_build(ctypes.c_void_p(P.data_ptr()), n, vp.ctypes.data_as(ctypes.c_void_p),
+                                   int(leaf_size), float(flatness_tau), cap, cent.ctypes.data_as(ctypes.c_void_p),
+                                   nrm.ctypes.data_as(ctypes.c_void_p), sizes.ctypes.data_as(ctypes.c_void_p),
+                                   usable.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(pl.data_ptr()),
+                                   ctypes.byref(nl), ctypes.c_void_p(ws.data_ptr()),
+                                   ctypes.c_void_p(engine.stream_ptr())), "build_leaf_tree")
+    k = nl.value
+    use = usable[:k].astype(bool)
+    return LeafTree(cent[:k].copy(), nrm[:k].copy(), sizes[:k].astype(int), use, pl.cpu().numpy().astype(int), None,
+                    torch.as_tensor(np.ascontiguousarray(cent[:k][use]), device=dev),
+                    torch.as_tensor(np.ascontiguousarray(nrm[:k][use]), device=dev))
+
+
 def sample_anchors(model_or_params, geo_cam, pose, cfg: RegistrationConfig, raster: RasterConfig | None = None,
                    thin: int = 1):
     """Device sample_model (registration.py:190-213): world anchors, thinned by ``thin``.
@@ -157,58 +200,80 @@ class PhotoProblem:
         return H, o[21:27].copy(), float(o[27]), m, float(o[29])
 
 
+_MODE = {"photometric": 0, "geometric": 1, "joint": 2, "sequential": 3}
+
+
 def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, raster: RasterConfig | None = None,
              rng=None, device_loop: bool = True) -> RegistrationResult:
-    """Align a sensor-frame scan to the model (registration.py:387-524, photometric mode)."""
+    """Align a sensor-frame scan to the model (registration.py:387-524)."""
     cfg = cfg or RegistrationConfig()
     scan = np.asarray(scan, dtype=float).reshape(-1, 3)
     if scan.shape[0] == 0:
         raise RegistrationError("empty scan")
-    if cfg.mode not in ("geometric", "photometric", "joint", "sequential"):
+    if cfg.mode not in _MODE:
         raise RegistrationError(f"unknown registration mode {cfg.mode!r}")
-    if cfg.mode != "photometric":
-        raise RegistrationError(f"mode {cfg.mode!r} needs the leaf-tree association, which is not on the B200 "
-                                "path (SURVEY 8(f)); use mode='photometric'")
     s = max(int(cfg.geo_supersample), 1)
     geo_cam = cam
     if s > 1:
         geo_cam = SphericalCamera(cam.width * s, cam.height * s, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
-    # anchors: the confident surface points thinned back to scan resolution
-    X_w, n_model = sample_anchors(model, geo_cam, initial, cfg, raster, thin=s * s if s > 1 else 1)
+    # model surface points (sample_model, :190-213) and the photometric anchors X_w = model_pts[::s*s] (:430)
+    model_pts, n_model = sample_anchors(model, geo_cam, initial, cfg, raster, thin=1)
     if n_model < cfg.min_residuals:
         raise RegistrationError("model renders to too few confident pixels")
+    X_w = model_pts[:: s * s].contiguous() if s > 1 else model_pts
     dscan = DeviceScan(cam, scan)
-    if device_loop:
-        return _solve_device(X_w, dscan, initial, cfg)
-    prob = PhotoProblem(X_w, dscan, cfg)
-    return _solve(prob, initial, cfg)
+    if not device_loop:
+        if cfg.mode != "photometric":
+            raise RegistrationError("the host loop covers the photometric mode only; use device_loop=True")
+        return _solve(PhotoProblem(X_w, dscan, cfg), initial, cfg)
+    tree, geo_scan = None, None
+    if cfg.mode != "photometric":
+        geo_scan = scan
+        if scan.shape[0] > cfg.max_geo_points:  # registration.py:419-421 (same numpy draw)
+            r = rng or np.random.default_rng(0)
+            geo_scan = scan[r.choice(scan.shape[0], cfg.max_geo_points, replace=False)]
+        tree = build_leaf_tree(model_pts, initial.translation, cfg.leaf_size, cfg.flatness_tau)
+        geo_scan = torch.as_tensor(np.ascontiguousarray(geo_scan), device=model_pts.device)
+    return solve_device(cfg, initial, dscan, X_w if cfg.mode != "geometric" else None, tree, geo_scan)
+
+
+def solve_device(cfg: RegistrationConfig, initial, scan: DeviceScan, X_w: torch.Tensor | None = None,
+                 tree: LeafTree | None = None, geo_scan: torch.Tensor | None = None) -> RegistrationResult:
+    """The GN/LM loop (registration.py:437-524) as one device kernel (``ss_reg_solve``)."""
+    dev = engine.require_cuda()
+    M = int(X_w.shape[0]) if X_w is not None else 0
+    nl = int(tree.dev_centroids.shape[0]) if tree is not None else 0
+    ng = int(geo_scan.shape[0]) if geo_scan is not None else 0
+    ws = torch.empty(int(lib().ss_reg_solve_workspace_bytes(ng, M)), dtype=torch.uint8, device=dev)
+    c = engine.ss_camera(scan.cam)
+    k = SsRegSolveCfg(float(cfg.huber_photo), float(cfg.huber_geo), float(cfg.trim_factor), float(cfg.spread_gate),
+                      float(cfg.assoc_gate), float(cfg.trim_floor_photo), float(cfg.trim_floor_geo), float(cfg.tol),
+                      float(cfg.damping_init), float(cfg.damping_max), int(cfg.max_iters), int(cfg.min_residuals),
+                      int(cfg.assoc_k), _MODE[cfg.mode])
+    t0 = pose_rt(initial)
+    t_out = np.zeros(12)
+    info = np.zeros(6, dtype=np.int32)
+    r2 = np.zeros(2)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else 0)  # noqa: E731
+    check(lib().ss_reg_solve(ptr(tree.dev_centroids if tree is not None else None),
+                             ptr(tree.dev_normals if tree is not None else None), nl, ptr(geo_scan), ng, ptr(X_w), M,
+                             ctypes.c_void_p(scan.range.data_ptr()), ctypes.c_void_p(scan.valid.data_ptr()),
+                             ctypes.byref(c), t0.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k),
+                             t_out.ctypes.data_as(ctypes.c_void_p), info.ctypes.data_as(ctypes.c_void_p),
+                             r2.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(ws.data_ptr()),
+                             ctypes.c_void_p(engine.stream_ptr())), "register")
+    T = SE3Pose(t_out[:9].reshape(3, 3), t_out[9:]).orthonormalized()
+    n_geo, n_photo = int(info[2]), int(info[3])
+    rms = lambda s2, m: float(np.sqrt(s2 / m)) if m else 0.0  # noqa: E731
+    return RegistrationResult(T, bool(info[1]), int(info[0]), rms(r2[0], n_geo), rms(r2[1], n_photo), n_geo,
+                              n_photo, cfg.mode)
 
 
 def _solve_device(X_w: torch.Tensor, scan: DeviceScan, initial, cfg: RegistrationConfig) -> RegistrationResult:
-    """The GN/LM loop (registration.py:437-524, photometric phase) as one device kernel."""
-    X = X_w.contiguous()
-    M = int(X.shape[0])
-    if M == 0:
+    """Photometric device loop on given anchors (kept for the parity tests)."""
+    if int(X_w.shape[0]) == 0:
         raise RegistrationError("too few residuals survive association")
-    ws = torch.empty(int(lib().ss_reg_solve_workspace_bytes(M)), dtype=torch.uint8, device=X.device)
-    c = engine.ss_camera(scan.cam)
-    k = SsRegSolveCfg(float(cfg.huber_photo), float(cfg.trim_factor), float(cfg.spread_gate), float(cfg.assoc_gate),
-                      float(cfg.trim_floor_photo), float(cfg.tol), float(cfg.damping_init), float(cfg.damping_max),
-                      int(cfg.max_iters), int(cfg.min_residuals))
-    t0 = pose_rt(initial)
-    t_out = np.zeros(12)
-    info = np.zeros(4, dtype=np.int32)
-    r2 = ctypes.c_double(0.0)
-    check(lib().ss_reg_photo_solve(ctypes.c_void_p(X.data_ptr()), M, ctypes.c_void_p(scan.range.data_ptr()),
-                                   ctypes.c_void_p(scan.valid.data_ptr()), ctypes.byref(c),
-                                   t0.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k),
-                                   t_out.ctypes.data_as(ctypes.c_void_p), info.ctypes.data_as(ctypes.c_void_p),
-                                   ctypes.byref(r2), ctypes.c_void_p(ws.data_ptr()),
-                                   ctypes.c_void_p(engine.stream_ptr())), "register")
-    T = SE3Pose(t_out[:9].reshape(3, 3), t_out[9:]).orthonormalized()
-    m = int(info[2])
-    rms = float(np.sqrt(r2.value / m)) if m else 0.0
-    return RegistrationResult(T, bool(info[1]), int(info[0]), 0.0, rms, 0, m, cfg.mode)
+    return solve_device(cfg, initial, scan, X_w.contiguous())
 
 
 def _solve(prob: PhotoProblem, initial, cfg: RegistrationConfig) -> RegistrationResult:

@@ -70,10 +70,15 @@ def test_register_final_pose(cuda, device_loop):
     assert abs(res.iterations - int(G["iterations"])) <= 2
 
 
-def test_non_photometric_mode_raises(cuda):
-    with pytest.raises(Exception):
-        REG.register(SplatModel.from_params(PARAMS), G["scan"].astype(np.float64), _cam(),
-                     SE3Pose(G["initial_R"], G["initial_t"]), REG.RegistrationConfig(mode="sequential"))
+def test_unknown_mode_and_host_loop_modes_raise(cuda):
+    from paper_2503_17491_b200.errors import RegistrationError
+    args = (SplatModel.from_params(PARAMS), G["scan"].astype(np.float64), _cam(), SE3Pose(G["initial_R"], G["initial_t"]))
+    with pytest.raises(RegistrationError):
+        REG.register(*args, REG.RegistrationConfig(mode="bogus"))
+    with pytest.raises(RegistrationError):  # the host loop is the photometric parity check only
+        REG.register(*args, REG.RegistrationConfig(mode="sequential"), device_loop=False)
+    with pytest.raises(RegistrationError):
+        REG.register(SplatModel.from_params(PARAMS), np.zeros((0, 3)), _cam(), SE3Pose(G["initial_R"], G["initial_t"]))
 
 
 def _loops(X, scan, initial, cfg):
