@@ -97,6 +97,14 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
  * so re-run), or the device-side status (e.g. SS_ERR_DEGENERATE). */
 int ss_records_check(ss_records* rec, int wait);
 
+/* Deterministic gradient reduction for the backward passes of these records
+ * (default off): every (tile, splat) entry is reduced across the warp in a
+ * fixed order and stored at its list position, then summed per splat over
+ * its tiles in row-major order -- bit-identical gradients run to run, at the
+ * cost of ~64 B per tile pair of extra traffic.  Without it the per-splat
+ * sums use float atomics (order-dependent rounding, ~1e-7 relative). */
+int ss_records_set_deterministic(ss_records* rec, int32_t deterministic);
+
 /* Number of (tile, splat) pairs and tiles of a finished forward. */
 int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y);
 /* Copy tile_ptr (tiles+1) and pair_splats (n_pairs) into caller device

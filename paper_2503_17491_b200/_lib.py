@@ -88,6 +88,8 @@ def lib() -> ctypes.CDLL:
     L.ss_render_backward.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, ctypes.c_int, vp]
     L.ss_fp32_peak_tflops.argtypes = [ctypes.POINTER(d), vp]
     L.ss_fp32_peak_tflops.restype = ctypes.c_int
+    L.ss_records_set_deterministic.argtypes = [vp, i32]
+    L.ss_records_set_deterministic.restype = ctypes.c_int
     L.ss_records_check.argtypes = [vp, ctypes.c_int]
     L.ss_records_check.restype = ctypes.c_int
     L.ss_records_work.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
@@ -133,7 +135,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",
-            "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build"]
+            "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build",
+            "ss_records_set_deterministic"]
 
 
 def check(status: int, what: str = "") -> None:

@@ -481,9 +481,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
                const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
                const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
                float* __restrict__ acc, const int* __restrict__ overflow, const int* __restrict__ order,
-               int* __restrict__ counter) {
+               int* __restrict__ counter, float* __restrict__ pacc) {
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
+  // deterministic mode (pacc != null): every entry is reduced by the fixed-order
+  // transpose and stored at its list position; k_det_gather sums them per splat
+  const bool det = pacc != nullptr;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
   __shared__ __align__(16) RawEntry raw_all[kWarpsPerBlock][2][32];
   extern __shared__ __align__(16) float4 bwd_dyn_smem[];  // kBwdDynSmem: the reduce-scatter transposes
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
         const unsigned lm = lm_next ? lm_next : __ballot_sync(0xffffffffu, (wl >> i) & 1u);
         lm_next = 0u;
         any &= ~(1u << i);
-        const bool direct = __popc(lm) <= kDirectLanes;
+        const bool direct = !det && __popc(lm) <= kDirectLanes;
         int mi = i;
         if (direct) {
           mi = ((lm >> lane) & 1u) ? i : -1;
@@ -654,7 +657,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
         for (int q = 0; q < 14; ++q) a16[q] = a[q];
         a16[14] = a16[15] = 0.f;
         const float tot = red_transpose16(a16, red, roff, lane);
-        if (lane < 14) atomicAdd(&acc[(size_t)x.sid * kAcc + lane], tot);
+        if (det) {
+          if (lane < 14) pacc[(size_t)(lo + base + i) * kAcc + lane] = tot;
+        } else if (lane < 14) {
+          atomicAdd(&acc[(size_t)x.sid * kAcc + lane], tot);
+        }
       }
       __syncwarp();
     }
@@ -853,9 +860,60 @@ template __global__ void k_forward<16>(BlendParams, int, const int*, const int*,
                                        const int*, int*);
 template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                       const float*, const float*, float*, const int*, const int*, int*);
+                                       const float*, const float*, float*, const int*, const int*, int*, float*);
 template __global__ void k_backward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
                                         const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                        const float*, const float*, float*, const int*, const int*, int*);
+                                        const float*, const float*, float*, const int*, const int*, int*, float*);
+
+// Deterministic mode: zero the per-position accumulators of the current pair count.
+__global__ void k_zero_pacc(float4* __restrict__ pacc, const long long* __restrict__ totals, long long cap) {
+  const long long n = min(totals[0], cap) * (kAcc / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    pacc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Deterministic mode: per splat, the entries it owns in its tiles' lists (tiles in
+// row-major order over its rectangle, its list position found by binary search on
+// the (float64 range, index) order) are summed in that fixed order.
+__global__ void __launch_bounds__(256) k_det_gather(int n, int tx, const int4* __restrict__ rect,
+                                                    const unsigned long long* __restrict__ key64,
+                                                    const int* __restrict__ tile_ptr, const int* __restrict__ pairs,
+                                                    const float* __restrict__ pacc, float* __restrict__ acc,
+                                                    const int* __restrict__ overflow) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n || *overflow) return;
+  float a[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) a[q] = 0.f;
+  const int4 r = rect[s];
+  const unsigned long long ks = key64[s];
+  for (int row = r.x; row <= r.y; ++row)
+    for (int k = 0; k < r.w; ++k) {
+      int c = r.z + k;
+      if (c >= tx) c -= tx;
+      const int t = row * tx + c;
+      int lo = tile_ptr[t], hi = tile_ptr[t + 1];
+      while (lo < hi) {  // first position not less than (ks, s)
+        const int mid = (lo + hi) >> 1;
+        const int v = pairs[mid];
+        const unsigned long long kv = key64[v];
+        if (kv < ks || (kv == ks && v < s))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      const float4* p4 = reinterpret_cast<const float4*>(pacc + (size_t)lo * kAcc);
+      const float4 x0 = p4[0], x1 = p4[1], x2 = p4[2], x3 = p4[3];
+      a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
+      a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
+      a[8] += x2.x; a[9] += x2.y; a[10] += x2.z; a[11] += x2.w;
+      a[12] += x3.x; a[13] += x3.y;
+    }
+  float4* o = reinterpret_cast<float4*>(acc + (size_t)s * kAcc);
+  o[0] = make_float4(a[0], a[1], a[2], a[3]);
+  o[1] = make_float4(a[4], a[5], a[6], a[7]);
+  o[2] = make_float4(a[8], a[9], a[10], a[11]);
+  o[3] = make_float4(a[12], a[13], 0.f, 0.f);
+}
 
 }  // namespace ss

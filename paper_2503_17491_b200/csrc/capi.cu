@@ -121,6 +121,9 @@ struct ss_records {
   PoseK pose{};
   BlendParams bp{};
   int n = 0, ntiles = 0, valid = 0, pending = 0;
+  int deterministic = 0;  // backward: fixed-order gradient reduction (ss_records_set_deterministic)
+  float* pacc = nullptr;  // deterministic mode: per list position accumulators
+  size_t cap_pacc = 0;
   uint32_t epoch = 0;
   long long n_pairs = 0, n_chunks = 0;
   long long cap_pairs = 0;  // speculative pair capacity of the current forward
@@ -255,7 +258,7 @@ void ss_records_destroy(ss_records* r, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   void* bufs[] = {r->rec,    r->rec64,   r->key64, r->key32,  r->rect, r->bsum, r->mat, r->tint,
                   r->tiles,  r->ptile,   r->psplat, r->pbucket, r->bitmask, r->misc, r->totals,
-                  r->Tf,     r->last,    r->acc};
+                  r->Tf,     r->last,    r->acc,     r->pacc};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, s);
   cudaStreamSynchronize(s);
@@ -384,6 +387,12 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
 // never raised before completion) for its counters.  Returns SS_ERR_CAPACITY
 // when the speculative pair capacity was too small (the next forward on
 // these records will allocate enough; re-run it), or the device status.
+int ss_records_set_deterministic(ss_records* rec, int32_t deterministic) {
+  if (!rec) return SS_ERR_INVALID_ARGUMENT;
+  rec->deterministic = deterministic ? 1 : 0;
+  return SS_OK;
+}
+
 int ss_records_check(ss_records* rec, int wait) {
   if (!rec) return SS_ERR_INVALID_ARGUMENT;
   if (!rec->pending) return rec->valid ? SS_OK : SS_ERR_STALE_RECORDS;
@@ -454,6 +463,12 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   const int* tile_ptr = rec->tiles;
   const int* chunk_ptr = rec->tiles + (ntiles + 1);
   set_smem_attrs();
+  float* pacc = nullptr;
+  if (rec->deterministic) {
+    if (grow(rec->pacc, rec->cap_pacc, (size_t)rec->cap_pairs * kAcc, s)) return SS_ERR_CUDA;
+    pacc = rec->pacc;
+    k_zero_pacc<<<num_sms() * 4, 256, 0, s>>>((float4*)pacc, rec->totals, rec->cap_pairs);
+  }
   {
     const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
     int* order = rec->tiles + 5 * (ntiles + 1);
@@ -462,12 +477,15 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
     if (rec->cam.T == 8)
       k_backward<8><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                           rec->acc, rec->misc + 1, order, counters + 1);
+                                                           rec->acc, rec->misc + 1, order, counters + 1, pacc);
     else
       k_backward<16><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1);
+                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1, pacc);
     SS_CUDA_TRY(cudaGetLastError());
+    if (pacc)
+      k_det_gather<<<(n + 255) / 256, 256, 0, s>>>(n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
+                                                   rec->acc, rec->misc + 1);
   }
   {
     StageTimer tm(rec, ST_FINALIZE, s);

@@ -145,6 +145,7 @@ def forward(cam, pose_rt: np.ndarray, splats: dict, cfg, records: Records, sync:
     sp = ss_splats(splats)
     k = ss_cfg(cfg)
     prt = np.ascontiguousarray(pose_rt, dtype=np.float64)
+    lib().ss_records_set_deterministic(records.ptr, int(bool(getattr(cfg, "deterministic", False))))
     for _attempt in range(4):
         st = lib().ss_render_forward(ctypes.byref(c), prt.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sp),
                                      ctypes.byref(k), ctypes.c_void_p(D.data_ptr()), ctypes.c_void_p(N.data_ptr()),

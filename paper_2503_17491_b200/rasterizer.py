@@ -39,6 +39,9 @@ class RasterConfig:
     denom_eps: float = 1e-12
     cutoff_sigma: float = engine.CUTOFF_SIGMA
     bbox_pad_px: float = 0.5
+    # not in the reference (rasterizer.py:69-78): fixed-order, run-to-run bit-identical
+    # gradient reduction in the backward of renders made with this config
+    deterministic: bool = False
 
 
 class _Lazy:

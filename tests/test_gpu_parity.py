@@ -158,3 +158,29 @@ def test_long_lists_and_tie_runs_bit_exact(cuda, n, n_tie):
     rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
                        np.full(out.range.shape, 1.0))
     assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
+
+
+def test_deterministic_backward_bit_identical(cuda):
+    """RasterConfig(deterministic=True): fixed-order reduction, bit-identical gradients run to run,
+    within the 1e-3 gate of the oracle; the default (atomic) path agrees to float rounding."""
+    c = W.config(0)
+    cam, params = c["camera"], c["splats"]
+    model = SplatModel.from_params(params)
+    rng = np.random.default_rng(3)
+    gD = rng.normal(size=(cam.height, cam.width))
+    gN = 0.1 * rng.normal(size=(cam.height, cam.width, 3))
+    gO = 0.05 * rng.normal(size=(cam.height, cam.width))
+    runs = []
+    for det in (True, True, False):
+        out, rec = rasterize_forward(cam, SE3Pose.identity(), model, RasterConfig(deterministic=det))
+        sg = rasterize_backward(model, rec, out, PixelGradients(gD, gN, gO))
+        runs.append(np.concatenate([sg.d_centers, sg.d_t_alpha, sg.d_t_beta, sg.d_normal, sg.d_scales,
+                                    sg.d_opacity[:, None]], axis=1))
+    assert np.array_equal(runs[0], runs[1])
+    ref = np.linalg.norm(runs[2])
+    assert np.linalg.norm(runs[0] - runs[2]) <= 1e-5 * ref
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    o = O.render(ct, np.eye(3), np.zeros(3), params)
+    plain = O.backward_lists(ct, o["arr"], np.eye(3), o["tile_ptr"], o["pair_splats"], o["range"], o["normal"],
+                             o["opacity"], gD, gN, gO)
+    assert_grads(grad_report(runs[0], plain))
