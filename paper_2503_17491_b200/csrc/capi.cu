@@ -829,7 +829,10 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   while (!cur.empty()) {
     const int L = (int)cur.size();
     SS_CUDA_TRY(cudaMemcpyAsync(nodes, cur.data(), sizeof(int2) * L, cudaMemcpyHostToDevice, s));
-    k_leaf_level<<<L, kLtThreads, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
+    if (L < num_sms())  // top levels: few large nodes, 1024 threads each
+      k_leaf_level<kLtThreadsBig><<<L, kLtThreadsBig, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
+    else
+      k_leaf_level<kLtThreads><<<L, kLtThreads, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
     SS_CUDA_TRY(cudaGetLastError());
     h.resize(L);
     SS_CUDA_TRY(cudaMemcpyAsync(h.data(), recs, sizeof(LeafRec) * L, cudaMemcpyDeviceToHost, s));

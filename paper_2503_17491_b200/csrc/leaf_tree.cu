@@ -24,7 +24,8 @@
 
 namespace ss {
 
-constexpr int kLtThreads = 256;
+constexpr int kLtThreads = 256;   // blocks of a level with many nodes
+constexpr int kLtThreadsBig = 1024;  // blocks of the top levels (few, large nodes)
 constexpr int kLtBins = 4096;
 constexpr int kLtCand = 256;
 
@@ -43,6 +44,7 @@ __device__ __forceinline__ double okey_inv(unsigned long long k) {
   return __longlong_as_double((long long)u);
 }
 
+template <int NT>
 __device__ double block_sum_d(double v, double* sred) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -50,7 +52,7 @@ __device__ double block_sum_d(double v, double* sred) {
   if (lane == 0) sred[warp] = v;
   __syncthreads();
   double s = 0.0;
-  for (int w = 0; w < kLtThreads / 32; ++w) s += sred[w];
+  for (int w = 0; w < NT / 32; ++w) s += sred[w];
   return s;
 }
 
@@ -103,6 +105,8 @@ __device__ void eig3(double a[3][3], double w[3], double V[3][3]) {
 }
 
 // Block-wide k-th smallest (0-based) of the keys of proj[0, n): returns the key.
+// sint: [NT/32] warp partials, then broadcast slots at sint[NT/32 + 0..4].
+template <int NT>
 __device__ unsigned long long block_select(const double* __restrict__ proj, int n, int k, unsigned* hist,
                                            unsigned long long* cand, int* sint) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -111,16 +115,17 @@ __device__ unsigned long long block_select(const double* __restrict__ proj, int 
   for (int p = 0; p < 6; ++p) {
     const int shift = p < 5 ? 52 - 12 * p : 0;
     const unsigned dmask = p < 5 ? 4095u : 15u;
-    for (int j = tid; j < kLtBins; j += kLtThreads) hist[j] = 0u;
+    for (int j = tid; j < kLtBins; j += NT) hist[j] = 0u;
     __syncthreads();
-    for (int j = tid; j < n; j += kLtThreads) {
+    for (int j = tid; j < n; j += NT) {
       const unsigned long long key = okey(proj[j]);
       if ((key & mask) == prefix) atomicAdd(&hist[(unsigned)(key >> shift) & dmask], 1u);
     }
     __syncthreads();
     // bin holding rank kk: per-thread runs of 16 bins, block scan
+    constexpr int PER = kLtBins / NT;
     unsigned loc = 0;
-    for (int j = 0; j < 16; ++j) loc += hist[tid * 16 + j];
+    for (int j = 0; j < PER; ++j) loc += hist[tid * PER + j];
     unsigned inc = loc;
     for (int off = 1; off < 32; off <<= 1) {
       const unsigned y = __shfl_up_sync(0xffffffffu, inc, off);
@@ -131,40 +136,40 @@ __device__ unsigned long long block_select(const double* __restrict__ proj, int 
     unsigned run = inc - loc;
     for (int w = 0; w < warp; ++w) run += (unsigned)sint[w];
     if ((unsigned)kk >= run && (unsigned)kk < run + loc) {
-      for (int j = 0; j < 16; ++j) {
-        const unsigned h = hist[tid * 16 + j];
+      for (int j = 0; j < PER; ++j) {
+        const unsigned h = hist[tid * PER + j];
         if ((unsigned)kk < run + h) {
-          sint[8] = tid * 16 + j;
-          sint[9] = (int)run;
-          sint[10] = (int)h;
+          sint[NT / 32] = tid * PER + j;
+          sint[NT / 32 + 1] = (int)run;
+          sint[NT / 32 + 2] = (int)h;
           break;
         }
         run += h;
       }
     }
     __syncthreads();
-    const int bin = sint[8], cnt = sint[10];
-    kk -= sint[9];
+    const int bin = sint[NT / 32], cnt = sint[NT / 32 + 2];
+    kk -= sint[NT / 32 + 1];
     prefix |= (unsigned long long)bin << shift;
     mask |= (unsigned long long)dmask << shift;
     __syncthreads();
     if (p == 5) return prefix;
     if (cnt <= kLtCand) {  // gather the few keys sharing the prefix and rank them
-      if (tid == 0) sint[11] = 0;
+      if (tid == 0) sint[NT / 32 + 3] = 0;
       __syncthreads();
-      for (int j = tid; j < n; j += kLtThreads) {
+      for (int j = tid; j < n; j += NT) {
         const unsigned long long key = okey(proj[j]);
-        if ((key & mask) == prefix) cand[atomicAdd(&sint[11], 1)] = key;
+        if ((key & mask) == prefix) cand[atomicAdd(&sint[NT / 32 + 3], 1)] = key;
       }
       __syncthreads();
-      for (int j = tid; j < cnt; j += kLtThreads) {
+      for (int j = tid; j < cnt; j += NT) {
         const unsigned long long c = cand[j];
         int rank = 0;
         for (int q = 0; q < cnt; ++q) rank += (cand[q] < c) | ((cand[q] == c) & (q < j));
-        if (rank == kk) sint[12] = j;
+        if (rank == kk) sint[NT / 32 + 4] = j;
       }
       __syncthreads();
-      const unsigned long long r = cand[sint[12]];
+      const unsigned long long r = cand[sint[NT / 32 + 4]];
       __syncthreads();
       return r;
     }
@@ -172,29 +177,30 @@ __device__ unsigned long long block_select(const double* __restrict__ proj, int 
   return prefix;
 }
 
-__global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restrict__ pts, int* __restrict__ idx,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pts, int* __restrict__ idx,
                                                            int* __restrict__ tmp, double* __restrict__ proj,
                                                            const int2* __restrict__ nodes, double3 viewpoint,
                                                            int leaf_size, double tau, LeafRec* __restrict__ out) {
-  __shared__ double sred[kLtThreads / 32];
+  __shared__ double sred[NT / 32];
   __shared__ double s_m[3], s_cov[6], s_axis[3], s_n[3], s_w[3], s_med;
   __shared__ unsigned hist[kLtBins];
   __shared__ unsigned long long cand[kLtCand];
-  __shared__ int sint[16];
+  __shared__ int sint[2 * (NT / 32) + 8];
   const int2 nd = nodes[blockIdx.x];
   const int b = nd.x, n = nd.y - nd.x;
   const int tid = threadIdx.x;
   // mean (registration.py:121)
   double sx = 0.0, sy = 0.0, sz = 0.0;
-  for (int j = tid; j < n; j += kLtThreads) {
+  for (int j = tid; j < n; j += NT) {
     const int i = idx[b + j];
     sx += pts[3 * i];
     sy += pts[3 * i + 1];
     sz += pts[3 * i + 2];
   }
-  sx = block_sum_d(sx, sred);
-  sy = block_sum_d(sy, sred);
-  sz = block_sum_d(sz, sred);
+  sx = block_sum_d<NT>(sx, sred);
+  sy = block_sum_d<NT>(sy, sred);
+  sz = block_sum_d<NT>(sz, sred);
   const double c[3] = {sx / n, sy / n, sz / n};
   LeafRec rec{};
   rec.c[0] = c[0];
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
   }
   // biased covariance (:125)
   double q[6] = {0, 0, 0, 0, 0, 0};
-  for (int j = tid; j < n; j += kLtThreads) {
+  for (int j = tid; j < n; j += NT) {
     const int i = idx[b + j];
     const double dx = pts[3 * i] - c[0], dy = pts[3 * i + 1] - c[1], dz = pts[3 * i + 2] - c[2];
     q[0] += dx * dx;
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
     q[4] += dy * dz;
     q[5] += dz * dz;
   }
-  for (int k = 0; k < 6; ++k) q[k] = block_sum_d(q[k], sred) / n;
+  for (int k = 0; k < 6; ++k) q[k] = block_sum_d<NT>(q[k], sred) / n;
   if (tid == 0) {
     const double a[3][3] = {{q[0], q[1], q[2]}, {q[1], q[3], q[4]}, {q[2], q[4], q[5]}};
     double w[3], V[3][3];
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
     return;
   }
   // projections on the principal axis and their median (:132-134)
-  for (int j = tid; j < n; j += kLtThreads) {
+  for (int j = tid; j < n; j += NT) {
     const int i = idx[b + j];
     proj[b + j] = (pts[3 * i] - c[0]) * s_axis[0] + (pts[3 * i + 1] - c[1]) * s_axis[1] +
                   (pts[3 * i + 2] - c[2]) * s_axis[2];
@@ -258,13 +264,13 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
   __syncthreads();
   const double* pr = proj + b;
   const int k1 = (n % 2 == 0) ? n / 2 - 1 : n / 2;
-  const unsigned long long key1 = block_select(pr, n, k1, hist, cand, sint);
+  const unsigned long long key1 = block_select<NT>(pr, n, k1, hist, cand, sint);
   double med = okey_inv(key1);
   if (n % 2 == 0) {
     // second middle value: key1 again if repeated, else the smallest larger key
     int le = 0;
     unsigned long long mn = ~0ull;
-    for (int j = tid; j < n; j += kLtThreads) {
+    for (int j = tid; j < n; j += NT) {
       const unsigned long long key = okey(pr[j]);
       le += key <= key1;
       if (key > key1) mn = min(mn, key);
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
     __syncthreads();
     le = 0;
     mn = ~0ull;
-    for (int w = 0; w < kLtThreads / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
       le += sint[w];
       mn = min(mn, cand[w]);
     }
@@ -291,13 +297,13 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
   }
   // left = proj <= med (:135); stable partition of the segment
   int nl = 0;
-  for (int j = tid; j < n; j += kLtThreads) nl += pr[j] <= med;
+  for (int j = tid; j < n; j += NT) nl += pr[j] <= med;
   for (int off = 16; off > 0; off >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, off);
   __syncthreads();
   if ((tid & 31) == 0) sint[tid >> 5] = nl;
   __syncthreads();
   nl = 0;
-  for (int w = 0; w < kLtThreads / 32; ++w) nl += sint[w];
+  for (int w = 0; w < NT / 32; ++w) nl += sint[w];
   __syncthreads();
   if (nl == 0 || nl == n) {  // (:136-139)
     emit_leaf(true);
@@ -305,24 +311,24 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
   }
   int base_l = 0, base_r = nl;
   const int lane = tid & 31, warp = tid >> 5;
-  for (int s0 = 0; s0 < n; s0 += kLtThreads) {
+  for (int s0 = 0; s0 < n; s0 += NT) {
     const int j = s0 + tid;
     const bool in = j < n;
     const bool left = in && pr[j] <= med;
     const unsigned bl = __ballot_sync(0xffffffffu, left), br = __ballot_sync(0xffffffffu, in && !left);
     if (lane == 0) {
       sint[warp] = __popc(bl);
-      sint[8 + warp] = __popc(br);
+      sint[NT / 32 + warp] = __popc(br);
     }
     __syncthreads();
     int ol = base_l, orr = base_r, tl = 0, tr = 0;
-    for (int w = 0; w < kLtThreads / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
       if (w < warp) {
         ol += sint[w];
-        orr += sint[8 + w];
+        orr += sint[NT / 32 + w];
       }
       tl += sint[w];
-      tr += sint[8 + w];
+      tr += sint[NT / 32 + w];
     }
     const unsigned lt = (1u << lane) - 1u;
     if (in) tmp[b + (left ? ol + __popc(bl & lt) : orr + __popc(br & lt))] = idx[b + j];
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kLtThreads) k_leaf_level(const double* __restr
     base_r += tr;
     __syncthreads();
   }
-  for (int j = tid; j < n; j += kLtThreads) idx[b + j] = tmp[b + j];
+  for (int j = tid; j < n; j += NT) idx[b + j] = tmp[b + j];
   if (tid == 0) {
     rec.split = 1;
     rec.nl = nl;

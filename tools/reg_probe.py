@@ -24,3 +24,8 @@ tl, res = t(lambda: REG._solve_device(X, scan, initial, cfg))
 tr, _ = t(lambda: REG.register(dp, scan_pts, cam, initial, cfg))
 tp, _ = t(lambda: engine.as_device_params(params))
 print(f"anchors {ta:.3f} ms  scan {ts:.3f} ms  device loop {tl:.3f} ms ({res.iterations} it)  register() {tr:.3f} ms  params upload {tp:.3f} ms")
+scfg = REG.RegistrationConfig()
+X1, n1 = REG.sample_anchors(dp, geo, initial, scfg, thin=1)
+tt, tree = t(lambda: REG.build_leaf_tree(X1, initial.translation))
+ts2, _ = t(lambda: REG.register(dp, scan_pts, cam, initial, scfg))
+print(f"model points {n1}: leaf tree {tt:.3f} ms ({tree.sizes.shape[0]} leaves); sequential register() {ts2:.3f} ms")
