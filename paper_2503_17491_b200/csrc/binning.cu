@@ -484,7 +484,7 @@ template <int MAX, int NT>
 __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, int lo, int L,
                                const uint32_t* __restrict__ key32, const unsigned long long* __restrict__ key64) {
   constexpr int NW = NT / 32, IPL = MAX / NT;
-  static_assert(NT >= 256, "the digit scan needs 256 threads");
+  static_assert(NT >= 64 && 256 % (NT < 256 ? NT : 256) == 0, "digit scan layout");
   // every buffer is shared memory: let the compiler emit LDS/STS, not generic loads
   uint16_t* const sk0 = m.sk[0];
   uint16_t* const sk1 = m.sk[1];
@@ -558,26 +558,42 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
       lr[j] = (uint16_t)(before + __popc(peers & lt));
     }
     __syncthreads();
-    // digit offsets: per digit, exclusive over warps (in place) and the block-wide scan of the totals
-    uint32_t s = 0, inc = 0;
-    if (tid < 256) {
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t c = m.wcnt[w * 256 + tid];
-        m.wcnt[w * 256 + tid] = (uint16_t)s;
-        s += c;
+    // digit offsets: per digit, exclusive over warps (in place) and the block-wide scan of the
+    // totals; thread t owns digits [t*DPT, (t+1)*DPT)
+    {
+      constexpr int DPT = NT >= 256 ? 1 : 256 / NT;
+      const bool act = tid * DPT < 256;  // warp-uniform
+      uint32_t sd[DPT], tsum = 0, inc = 0;
+      if (act) {
+#pragma unroll
+        for (int d = 0; d < DPT; ++d) {
+          const int dig = tid * DPT + d;
+          uint32_t sacc = 0;
+          for (int w = 0; w < NW; ++w) {
+            const uint32_t c = m.wcnt[w * 256 + dig];
+            m.wcnt[w * 256 + dig] = (uint16_t)sacc;
+            sacc += c;
+          }
+          sd[d] = sacc;
+          tsum += sacc;
+        }
+        inc = tsum;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= off) inc += y;
+        }
+        if (lane == 31) m.red[warp] = inc;
       }
-      inc = s;
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += y;
+      __syncthreads();
+      if (act) {
+        uint32_t run = inc - tsum;
+        for (int w = 0; w < warp; ++w) run += m.red[w];
+#pragma unroll
+        for (int d = 0; d < DPT; ++d) {
+          m.dtot[tid * DPT + d] = run;
+          run += sd[d];
+        }
       }
-      if (lane == 31) m.red[warp] = inc;
-    }
-    __syncthreads();
-    if (tid < 256) {
-      uint32_t wex = 0;
-      for (int w = 0; w < warp; ++w) wex += m.red[w];
-      m.dtot[tid] = wex + inc - s;
     }
     __syncthreads();
 #pragma unroll
@@ -629,12 +645,17 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
 
 // Regular tiles (L <= kTileSortMax), one 256-thread block per tile; longer
 // lists go to long_list for k_tile_sort_big.
-__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
+#ifndef SS_SORT_NT
+#define SS_SORT_NT 256
+#endif
+constexpr int kTileSortNT = SS_SORT_NT;
+
+__global__ void __launch_bounds__(kTileSortNT) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
                                                    const uint32_t* __restrict__ key32,
                                                    const unsigned long long* __restrict__ key64,
                                                    int* __restrict__ long_list, int* __restrict__ n_long,
                                                    const int* __restrict__ overflow) {
-  __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, 256>()];
+  __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, kTileSortNT>()];
   if (*overflow) return;
   const int t = blockIdx.x;
   const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
@@ -643,8 +664,8 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ tile_
     if (threadIdx.x == 0) long_list[atomicAdd(n_long, 1)] = t;
     return;
   }
-  const SortSmem m = carve_sort_smem<kTileSortMax, 256>(smem);
-  if (!sort_tile_smem<kTileSortMax, 256>(m, pairs, lo, L, key32, key64) && threadIdx.x == 0)
+  const SortSmem m = carve_sort_smem<kTileSortMax, kTileSortNT>(smem);
+  if (!sort_tile_smem<kTileSortMax, kTileSortNT>(m, pairs, lo, L, key32, key64) && threadIdx.x == 0)
     long_list[atomicAdd(n_long, 1)] = t;  // long run of equal keys: the big kernel's merge fallback
 }
 

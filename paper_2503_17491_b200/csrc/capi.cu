@@ -358,7 +358,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   }
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
-    k_tile_sort<<<ntiles, 256, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
+    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
     k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order, counters);
