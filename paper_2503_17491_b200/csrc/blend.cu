@@ -678,9 +678,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
 constexpr int kFinBlock = 128;
 
 __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, const SplatRec64* __restrict__ rec64,
-                                                        const float* __restrict__ acc,
+                                                        float* __restrict__ acc,
                                                         const float* __restrict__ d_scales_extra,
-                                                        float* __restrict__ out, int raw_space) {
+                                                        float* __restrict__ out, int raw_space,
+                                                        int* __restrict__ bwd_ticket) {
+  // the backward's persistent tile ticket restarts for the next backward pass
+  if (blockIdx.x == 0 && threadIdx.x == 0) *bwd_ticket = 0;
   // The block's records and accumulators are staged through shared memory
   // with coalesced 16-byte loads, its outputs leave the same way.
   __shared__ double2 s_rec[kFinBlock * 5];
@@ -843,6 +846,10 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   }
   }
   __syncthreads();
+  {  // consumed: leave the accumulators zeroed for the next backward pass
+    float4* a4 = reinterpret_cast<float4*>(acc + (size_t)base * kAcc);
+    for (int q = tid; q < cnt * 4; q += kFinBlock) a4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float* g = out + (size_t)base * nout;
   if (cnt == kFinBlock && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     for (int q = tid; q < kFinBlock * nout / 4; q += kFinBlock)

@@ -457,8 +457,13 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   cudaStream_t s = (cudaStream_t)stream;
   const int n = rec->n;
   if (n == 0) return SS_OK;
-  if (grow(rec->acc, rec->cap_acc, (size_t)n * kAcc, s)) return SS_ERR_CUDA;
-  SS_CUDA_TRY(cudaMemsetAsync(rec->acc, 0, sizeof(float) * (size_t)n * kAcc, s));
+  // acc is all-zero between backward passes: zeroed once when (re)allocated, and
+  // k_finalize clears every row it consumes (no per-call 32 MB memset)
+  {
+    float* before = rec->acc;
+    if (grow(rec->acc, rec->cap_acc, (size_t)n * kAcc, s)) return SS_ERR_CUDA;
+    if (rec->acc != before) SS_CUDA_TRY(cudaMemsetAsync(rec->acc, 0, sizeof(float) * rec->cap_acc, s));
+  }
   const int ntiles = rec->ntiles;
   const int* tile_ptr = rec->tiles;
   const int* chunk_ptr = rec->tiles + (ntiles + 1);
@@ -489,8 +494,9 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   }
   {
     StageTimer tm(rec, ST_FINALIZE, s);
-    k_finalize<<<(n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc, d_scales_extra, grads,
-                                                raw_space);
+    k_finalize<<<(n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc,
+                                                                    d_scales_extra, grads, raw_space,
+                                                                    rec->misc + 5);
   }
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;

@@ -184,3 +184,21 @@ def test_deterministic_backward_bit_identical(cuda):
     plain = O.backward_lists(ct, o["arr"], np.eye(3), o["tile_ptr"], o["pair_splats"], o["range"], o["normal"],
                              o["opacity"], gD, gN, gO)
     assert_grads(grad_report(runs[0], plain))
+
+
+def test_backward_twice_same_records(cuda):
+    """Two backward passes over one forward (different pixel gradients) are independent:
+    the device accumulators are cleared by each pass (rasterizer.py:534 allows repeated calls)."""
+    c = W.config(0)
+    cam, model = c["camera"], SplatModel.from_params(c["splats"])
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), model)
+    rng = np.random.default_rng(5)
+    g1 = PixelGradients(rng.normal(size=(cam.height, cam.width)), np.zeros((cam.height, cam.width, 3)),
+                        np.zeros((cam.height, cam.width)))
+    g2 = PixelGradients(np.zeros((cam.height, cam.width)), np.zeros((cam.height, cam.width, 3)),
+                        rng.normal(size=(cam.height, cam.width)))
+    a = rasterize_backward(model, rec, out, g1).d_centers
+    b = rasterize_backward(model, rec, out, g2).d_centers
+    a2 = rasterize_backward(model, rec, out, g1).d_centers
+    assert np.abs(a2 - a).max() <= 1e-6 * np.abs(a).max()
+    assert np.abs(b).max() > 0 and not np.allclose(a, b)
