@@ -51,8 +51,15 @@ __device__ __forceinline__ bool row_hit(const CamK& k, const double2* __restrict
 }
 
 // Per-tile-column and -row angular intervals (rasterizer.py:278-294).
-__global__ void k_tile_intervals(CamK k, double2* __restrict__ colt, double2* __restrict__ rowt) {
+// (also clears the forward's status / overflow / ticket words, the pair totals and
+// the tile counts: one launch instead of three memsets)
+__global__ void k_tile_intervals(CamK k, double2* __restrict__ colt, double2* __restrict__ rowt,
+                                 int* __restrict__ misc16, long long* __restrict__ totals2,
+                                 int* __restrict__ tile_count, int ntiles) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 16) misc16[i] = 0;
+  if (i < 2) totals2[i] = 0;
+  if (i < ntiles) tile_count[i] = 0;
   double c, h;
   if (i < k.tx) {
     tile_col_interval(k, i, c, h);

@@ -329,14 +329,13 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* n_long = rec->misc + 2;
   double2* colt = rec->tint;
   double2* rowt = rec->tint + k.tx;
-  SS_CUDA_TRY(cudaMemsetAsync(rec->misc, 0, sizeof(int) * 16, s));
-  SS_CUDA_TRY(cudaMemsetAsync(rec->totals, 0, sizeof(long long) * 2, s));
-  SS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(int) * ntiles, s));
+
   PoseK pk = rec->pose;
   SplatsK sk = to_k(splats);
   {
     StageTimer tm(rec, ST_PREPROCESS, s);
-    k_tile_intervals<<<(k.tx + k.ty + 127) / 128, 128, 0, s>>>(k, colt, rowt);
+    const int nti = std::max(std::max(k.tx + k.ty, ntiles), 16);
+    k_tile_intervals<<<(nti + 127) / 128, 128, 0, s>>>(k, colt, rowt, rec->misc, rec->totals, tile_count, ntiles);
     if (n > 0)
       k_preprocess<<<nb, 256, 0, s>>>(sk, pk, k, rk, colt, rowt, rec->rec, rec->rec64, rec->key64, rec->key32,
                                       rec->rect, rec->bsum, status);
