@@ -99,8 +99,10 @@ def _config0_loss_grads(out, tgt):
     return gD, gN, np.zeros_like(gD)
 
 
-@pytest.mark.parametrize("index", [0])
+@pytest.mark.parametrize("index", [0, 1])
 def test_config_full_size_parity(cuda, index):
+    """BASELINE configs 0 (64x1024, 50k splats) and 1 (the headline 128x2048, 500k splats)
+    against the float64 C oracle (all host threads; ~2 s per config-1 render on the box)."""
     c = W.config(index)
     cam, params = c["camera"], c["splats"]
     ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
