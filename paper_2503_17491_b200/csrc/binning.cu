@@ -174,22 +174,22 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
     const int c0 = (int)floor(uu / cam.T);
     for (int dc = 0; dc < 3 && h < 0; ++dc) {
       int c = c0 + (dc == 0 ? 0 : (dc == 1 ? -1 : 1));
-      c = ((c % tx) + tx) % tx;
+      c = ((c % tx) + tx) % tx;  // (c0 may lie anywhere: the only general modulo)
       if (col_hit(cam, colt, g, c)) h = c;
     }
   }
   if (h >= 0) {
     // the hit set is one circular run around h (interval overlap on a circle)
     int lo = h, cnt = 1;
-    while (cnt < tx) {
-      const int c = (lo - 1 + tx) % tx;
+    while (cnt < tx) {  // circular neighbours by compare-and-wrap (no integer division)
+      const int c = lo == 0 ? tx - 1 : lo - 1;
       if (!col_hit(cam, colt, g, c)) break;
       lo = c;
       ++cnt;
     }
     int hi = h;
     while (cnt < tx) {
-      const int c = (hi + 1) % tx;
+      const int c = hi + 1 == tx ? 0 : hi + 1;
       if (!col_hit(cam, colt, g, c)) break;
       hi = c;
       ++cnt;
@@ -208,7 +208,7 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
       ncols = tx;
     } else if (nhit > 0) {
       int c = first_miss;
-      while (!col_hit(cam, colt, g, c)) c = (c + 1) % tx;
+      while (!col_hit(cam, colt, g, c)) c = c + 1 == tx ? 0 : c + 1;
       c_start = c;
       ncols = nhit;
     }
