@@ -26,6 +26,8 @@
  *                            the H/b accumulation of registration.py:470-477,
  *                            objective of registration.py:379-384)
  *   ss_leaf_tree_build       registration.py:98-164  build_leaf_tree
+ *   ss_spawn_weights, ss_densify_mask, ss_spawn_splats, ss_prune_*
+ *                            mapping.py:202-311, 412-438 map growth
  *   ss_reg_solve             registration.py:437-524 the GN/LM loop of register
  *                            (every mode) + _geo_system :231-274, se3.py:121-150
  */
@@ -183,6 +185,31 @@ int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, con
  * float64, device) -> nearest range per pixel (float64 H*W) and valid mask. */
 int ss_range_image(const ss_camera* cam, const double* pts, int32_t n, double* range_out, uint8_t* valid_out,
                    void* stream);
+
+/* Map growth (mapping.py:202-311, 412-438).
+ * ss_spawn_weights: _range_gradient_weights (float64 H*W) of a keyframe range image.
+ * ss_densify_mask: densify_mask = valid & (rendered opacity <= densify_opacity |
+ *   |rendered range - keyframe range| >= densify_range_err).
+ * ss_spawn_splats: spawn_splats' splat construction for m drawn pixel indices
+ *   (row-major int64; the weighted draw itself is numpy's on the host), written
+ *   as float32 raw parameters at the given device pointers.
+ * ss_prune_flags + ss_prune_compact: SplatModel.prune / _Adam.prune -- keep splats
+ *   with sigmoid(logit) >= prune_opacity; flags and offsets live in `workspace`
+ *   (ss_prune_workspace_bytes(n)), then each per-splat array (rows of `width`
+ *   floats) is compacted stably into `dst`. */
+int ss_spawn_weights(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,
+                     double* w_out, void* stream);
+int ss_densify_mask(int32_t n_pixels, const double* kf_range, const uint8_t* kf_valid, const float* render_range,
+                    const float* render_opacity, double densify_opacity, double densify_range_err, uint8_t* mask_out,
+                    void* stream);
+int ss_spawn_splats(const ss_camera* cam, const double* kf_range, const double* kf_normal, const uint8_t* kf_nvalid,
+                    const double* pose_Rt, const int64_t* pixels, int32_t m, double footprint_gain,
+                    double scale_floor, double opacity_init, float* centers, float* raw_t_alpha, float* raw_t_beta,
+                    float* log_scales, float* logit_opacity, void* stream);
+size_t ss_prune_workspace_bytes(int32_t n);
+int ss_prune_flags(int32_t n, const float* logit_opacity, double prune_opacity, int32_t* n_keep_out, void* workspace,
+                   void* stream);
+int ss_prune_compact(int32_t n, int32_t width, const float* src, float* dst, const void* workspace, void* stream);
 
 /* smooth_range_image (geometry.py:271-287), size 3: 3x3 median of the valid
  * ranges (invalid pixels count as +inf; columns wrap when `wrap`, else both

@@ -118,6 +118,15 @@ def lib() -> ctypes.CDLL:
     L.ss_leaf_tree_workspace_bytes.restype = ctypes.c_size_t
     L.ss_leaf_tree_build.argtypes = [vp, i32, vp, i32, d, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     L.ss_leaf_tree_build.restype = ctypes.c_int
+    L.ss_spawn_weights.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+    L.ss_densify_mask.argtypes = [i32, vp, vp, vp, vp, d, d, vp, vp]
+    L.ss_spawn_splats.argtypes = [ctypes.POINTER(SsCamera), vp, vp, vp, vp, vp, i32, d, d, d, vp, vp, vp, vp, vp, vp]
+    L.ss_prune_workspace_bytes.argtypes = [i32]
+    L.ss_prune_workspace_bytes.restype = ctypes.c_size_t
+    L.ss_prune_flags.argtypes = [i32, vp, d, ctypes.POINTER(i32), vp, vp]
+    L.ss_prune_compact.argtypes = [i32, i32, vp, vp, vp, vp]
+    for name in ("ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats", "ss_prune_flags", "ss_prune_compact"):
+        getattr(L, name).restype = ctypes.c_int
     L.ss_reg_solve_workspace_bytes.argtypes = [i32, i32]
     L.ss_reg_solve_workspace_bytes.restype = ctypes.c_size_t
     L.ss_reg_solve.argtypes = [vp, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp,
@@ -136,7 +145,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",
             "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build",
-            "ss_records_set_deterministic"]
+            "ss_records_set_deterministic", "ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats",
+            "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact"]
 
 
 def check(status: int, what: str = "") -> None:

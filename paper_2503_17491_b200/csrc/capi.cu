@@ -10,6 +10,7 @@
 #include "binning.cu"
 #include "blend.cu"
 #include "keyframe.cu"
+#include "densify.cu"
 #include "leaf_tree.cu"
 #include "loss.cu"
 #include "reg_solve.cu"  // includes registration.cu
@@ -777,6 +778,101 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   r2_out2[0] = out.last_r2[0];
   r2_out2[1] = out.last_r2[1];
   return out.status ? SS_ERR_REGISTRATION : SS_OK;
+}
+
+int ss_spawn_weights(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,
+                     double* w_out, void* stream) {
+  if (width < 1 || height < 1 || !range || !valid || !w_out) return SS_ERR_INVALID_ARGUMENT;
+  const int P = width * height;
+  k_spawn_weights<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(width, height, wrap ? 1 : 0, range, valid, w_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_densify_mask(int32_t n_pixels, const double* kf_range, const uint8_t* kf_valid, const float* render_range,
+                    const float* render_opacity, double densify_opacity, double densify_range_err, uint8_t* mask_out,
+                    void* stream) {
+  if (n_pixels < 0 || (n_pixels > 0 && (!kf_range || !kf_valid || !render_range || !render_opacity || !mask_out)))
+    return SS_ERR_INVALID_ARGUMENT;
+  if (n_pixels == 0) return SS_OK;
+  k_densify_mask<<<(n_pixels + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      n_pixels, kf_range, kf_valid, render_range, render_opacity, densify_opacity, densify_range_err, mask_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_spawn_splats(const ss_camera* cam, const double* kf_range, const double* kf_normal, const uint8_t* kf_nvalid,
+                    const double* pose_Rt, const int64_t* pixels, int32_t m, double footprint_gain,
+                    double scale_floor, double opacity_init, float* centers, float* raw_t_alpha, float* raw_t_beta,
+                    float* log_scales, float* logit_opacity, void* stream) {
+  if (!cam || !pose_Rt || m < 0) return SS_ERR_INVALID_ARGUMENT;
+  if (m == 0) return SS_OK;
+  if (!kf_range || !kf_normal || !kf_nvalid || !pixels || !centers || !raw_t_alpha || !raw_t_beta || !log_scales ||
+      !logit_opacity || !(opacity_init > 0.0 && opacity_init < 1.0))
+    return SS_ERR_INVALID_ARGUMENT;
+  CamK ck;
+  const int st = make_camk(cam, 8, 0.5, ck);
+  if (st) return st;
+  SpawnK k;
+  k.W = ck.W;
+  k.fx = ck.fx;
+  k.fy = ck.fy;
+  k.cx = ck.cx;
+  k.cy = ck.cy;
+  k.off_u = ck.off_u;
+  k.off_v = ck.off_v;
+  for (int q = 0; q < 9; ++q) k.R[q] = pose_Rt[q];
+  for (int q = 0; q < 3; ++q) k.t[q] = pose_Rt[9 + q];
+  k.gain = footprint_gain;
+  k.floor_ = scale_floor;
+  k.opacity = opacity_init;
+  k_spawn<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(m, (const long long*)pixels, k, kf_range, kf_normal,
+                                                             kf_nvalid, centers, raw_t_alpha, raw_t_beta, log_scales,
+                                                             logit_opacity);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+size_t ss_prune_workspace_bytes(int32_t n) {
+  const size_t m = (size_t)(n > 0 ? n : 1);
+  return m * 4 + ((m + 255) / 256) * 4 + 64;
+}
+
+int ss_prune_flags(int32_t n, const float* logit_opacity, double prune_opacity, int32_t* n_keep_out, void* workspace,
+                   void* stream) {
+  if (n < 0 || !n_keep_out || (n > 0 && (!logit_opacity || !workspace))) return SS_ERR_INVALID_ARGUMENT;
+  if (n == 0) {
+    *n_keep_out = 0;
+    return SS_OK;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t* keep = (uint32_t*)workspace;
+  uint32_t* bsum = keep + n;
+  const int nb = (n + 255) / 256;
+  k_prune_flags<<<nb, 256, 0, s>>>(n, logit_opacity, prune_opacity, keep, bsum);
+  std::vector<uint32_t> h(nb);
+  SS_CUDA_TRY(cudaMemcpyAsync(h.data(), bsum, sizeof(uint32_t) * nb, cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  uint32_t run = 0;
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t c = h[b];
+    h[b] = run;
+    run += c;
+  }
+  SS_CUDA_TRY(cudaMemcpyAsync(bsum, h.data(), sizeof(uint32_t) * nb, cudaMemcpyHostToDevice, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  *n_keep_out = (int32_t)run;
+  return SS_OK;
+}
+
+int ss_prune_compact(int32_t n, int32_t width, const float* src, float* dst, const void* workspace, void* stream) {
+  if (n < 0 || width < 1 || (n > 0 && (!src || !dst || !workspace))) return SS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return SS_OK;
+  const uint32_t* keep = (const uint32_t*)workspace;
+  const uint32_t* boff = keep + n;
+  k_compact_f32<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, width, keep, boff, src, dst);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
 }
 
 int ss_smooth_range_image(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,

@@ -66,24 +66,29 @@ def sample_keyframe_index(n: int, p: float, rng) -> int:
 class DeviceKeyframe:
     """Camera, pose and target images of one keyframe on the device."""
 
-    def __init__(self, camera, pose, range_img, valid, normals, nvalid):
+    def __init__(self, camera, pose, range_img, valid, normals, nvalid, index: int = 0):
         dev = engine.require_cuda()
         self.camera = camera
         self.pose = pose
-        self.range = torch.as_tensor(np.asarray(range_img, np.float32), device=dev).contiguous()
+        self.index = index
+        # float64 images drive spawning (exact reference arithmetic); float32 copies feed the loss
+        self.range64 = torch.as_tensor(np.ascontiguousarray(range_img, np.float64), device=dev)
+        self.normal64 = torch.as_tensor(np.ascontiguousarray(normals, np.float64), device=dev)
+        self.range = self.range64.float().contiguous()
         self.valid = torch.as_tensor(np.asarray(valid, np.uint8), device=dev).contiguous()
-        self.normal = torch.as_tensor(np.asarray(normals, np.float32), device=dev).contiguous()
+        self.normal = self.normal64.float().contiguous()
         self.nvalid = torch.as_tensor(np.asarray(nvalid, np.uint8), device=dev).contiguous()
 
     @classmethod
-    def from_cloud(cls, cloud, pose, width: int, height: int, camera=None) -> "DeviceKeyframe":
+    def from_cloud(cls, cloud, pose, width: int, height: int, camera=None, index: int = 0) -> "DeviceKeyframe":
         """make_keyframe (mapping.py:106-114) on the device: the target images never leave HBM."""
         from . import keyframe as KF
         cam = camera if camera is not None else KF.estimate_camera(
             cloud.cpu().numpy() if torch.is_tensor(cloud) else cloud, width, height)
         im = KF.keyframe_images(cam, cloud)
         kf = cls.__new__(cls)
-        kf.camera, kf.pose = cam, pose
+        kf.camera, kf.pose, kf.index = cam, pose, index
+        kf.range64, kf.normal64 = im["range"], im["normal"]
         kf.range = im["range"].float().contiguous()
         kf.valid = im["valid"]
         kf.normal = im["normal"].float().contiguous()
@@ -93,7 +98,7 @@ class DeviceKeyframe:
     @classmethod
     def from_reference(cls, kf) -> "DeviceKeyframe":
         return cls(kf.camera, kf.pose, kf.range_image.range, kf.range_image.valid, kf.normal_image.normals,
-                   kf.normal_image.valid)
+                   kf.normal_image.valid, int(getattr(kf, "index", 0)))
 
 
 class DeviceMap:
@@ -114,6 +119,117 @@ class DeviceMap:
         self.rec = engine.Records()
         self.d_scales = torch.zeros((n, 2), dtype=torch.float32, device=dev)
         self.losses = torch.zeros((0, 4), dtype=torch.float64, device=dev)
+        self.epochs = torch.zeros(n, dtype=torch.int32, device=dev)  # keyframe that spawned each splat
+
+    # --- map growth (mapping.py:383-438) ---------------------------------------------
+    @classmethod
+    def start(cls, kf: DeviceKeyframe, cfg: MappingConfig, rng, raster: RasterConfig | None = None) -> "DeviceMap":
+        """LocalMap.start (mapping.py:392-400): an empty map seeded from one keyframe."""
+        ranges = kf.range64[kf.valid.bool()].cpu().numpy()
+        scale = float(np.median(ranges)) if ranges.size else 1.0
+        empty = {k: np.zeros((0, engine.PARAM_WIDTH[k]) if engine.PARAM_WIDTH[k] > 1 else 0, np.float32)
+                 for k in engine.PARAM_NAMES}
+        dm = cls(empty, [], max(scale, 1e-3))
+        dm.add_keyframe(kf, cfg, rng, raster)
+        return dm
+
+    def _resize(self, n_new: int, keep_prefix: int):
+        """Per-splat arrays grown to n_new rows (the first keep_prefix rows kept)."""
+        dev = self.m.device
+        for k in engine.PARAM_NAMES:
+            w = engine.PARAM_WIDTH[k]
+            t = torch.empty((n_new, w) if w > 1 else (n_new,), dtype=torch.float32, device=dev)
+            t[:keep_prefix] = self.params[k][:keep_prefix]
+            self.params[k] = t
+        for name in ("m", "v"):
+            t = torch.zeros((n_new, 12), dtype=torch.float32, device=dev)
+            t[:keep_prefix] = getattr(self, name)[:keep_prefix]
+            setattr(self, name, t)
+        e = torch.zeros(n_new, dtype=torch.int32, device=dev)
+        e[:keep_prefix] = self.epochs[:keep_prefix]
+        self.epochs = e
+        self.d_scales = torch.zeros((n_new, 2), dtype=torch.float32, device=dev)
+
+    def prune(self, prune_opacity: float) -> int:
+        """SplatModel.prune + _Adam.prune (splats.py:266-279, mapping.py:363-365) on the device."""
+        n = self.n
+        if n == 0:
+            return 0
+        dev = self.m.device
+        ws = torch.empty(int(lib().ss_prune_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+        kept = ctypes.c_int32(0)
+        check(lib().ss_prune_flags(n, ctypes.c_void_p(self.params["logit_opacity"].data_ptr()), float(prune_opacity),
+                                   ctypes.byref(kept), ctypes.c_void_p(ws.data_ptr()),
+                                   ctypes.c_void_p(engine.stream_ptr())), "prune")
+        k = kept.value
+        if k == n:
+            return 0
+        arrays = [(self.params, name, engine.PARAM_WIDTH[name]) for name in engine.PARAM_NAMES]
+        for holder, name, w in arrays + [(self.__dict__, "m", 12), (self.__dict__, "v", 12)]:
+            src = holder[name]
+            dst = torch.empty((k,) + tuple(src.shape[1:]), dtype=torch.float32, device=dev)
+            check(lib().ss_prune_compact(n, w, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                         ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(engine.stream_ptr())),
+                  "prune")
+            holder[name] = dst
+        e = torch.empty(k, dtype=torch.int32, device=dev)
+        check(lib().ss_prune_compact(n, 1, ctypes.c_void_p(self.epochs.data_ptr()), ctypes.c_void_p(e.data_ptr()),
+                                     ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(engine.stream_ptr())), "prune")
+        self.epochs = e
+        self.d_scales = torch.zeros((k, 2), dtype=torch.float32, device=dev)
+        return n - k
+
+    def spawn(self, kf: DeviceKeyframe, mask: torch.Tensor, n_max: int, cfg: MappingConfig, rng) -> int:
+        """spawn_splats (mapping.py:254-303): the weighted draw without replacement is numpy's own
+        call on the host; weights, back-projection and frames are computed on the device."""
+        cam = kf.camera
+        idx = np.flatnonzero((mask.bool() & kf.valid.bool()).cpu().numpy().ravel())
+        if idx.size == 0:
+            return 0
+        if idx.size > n_max:
+            w_img = torch.empty_like(kf.range64)
+            check(lib().ss_spawn_weights(cam.width, cam.height, int(bool(cam.full_circle)),
+                                         ctypes.c_void_p(kf.range64.data_ptr()), ctypes.c_void_p(kf.valid.data_ptr()),
+                                         ctypes.c_void_p(w_img.data_ptr()), ctypes.c_void_p(engine.stream_ptr())),
+                  "spawn weights")
+            w = w_img.cpu().numpy().ravel()[idx]
+            total = w.sum()
+            p = w / total if total > 0 else None
+            idx = rng.choice(idx, size=n_max, replace=False, p=p)
+        m = int(idx.size)
+        n0 = self.n
+        self._resize(n0 + m, n0)
+        pix = torch.as_tensor(np.ascontiguousarray(idx, np.int64), device=self.m.device)
+        c = engine.ss_camera(cam)
+        prt = pose_rt(kf.pose)
+        ptr = lambda name: ctypes.c_void_p(self.params[name][n0:].data_ptr())  # noqa: E731
+        check(lib().ss_spawn_splats(ctypes.byref(c), ctypes.c_void_p(kf.range64.data_ptr()),
+                                    ctypes.c_void_p(kf.normal64.data_ptr()), ctypes.c_void_p(kf.nvalid.data_ptr()),
+                                    prt.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(pix.data_ptr()), m,
+                                    float(cfg.footprint_gain), float(cfg.scale_floor), float(cfg.opacity_init),
+                                    ptr("centers"), ptr("raw_t_alpha"), ptr("raw_t_beta"), ptr("log_scales"),
+                                    ptr("logit_opacity"), ctypes.c_void_p(engine.stream_ptr())), "spawn")
+        self.epochs[n0:] = int(getattr(kf, "index", 0))
+        return m
+
+    def add_keyframe(self, kf: DeviceKeyframe, cfg: MappingConfig, rng, raster: RasterConfig | None = None) -> dict:
+        """add_keyframe (mapping.py:412-438): prune dead splats, densify where the keyframe is unexplained."""
+        stats = {"pruned": 0, "spawned": 0}
+        if self.n == 0:
+            mask = kf.valid
+        else:
+            raster = raster or RasterConfig()
+            D, N, O = engine.forward(kf.camera, pose_rt(kf.pose), self.params, raster, self.rec)
+            mask = torch.empty_like(kf.valid)
+            check(lib().ss_densify_mask(int(kf.valid.numel()), ctypes.c_void_p(kf.range64.data_ptr()),
+                                        ctypes.c_void_p(kf.valid.data_ptr()), ctypes.c_void_p(D.data_ptr()),
+                                        ctypes.c_void_p(O.data_ptr()), float(cfg.densify_opacity),
+                                        float(cfg.densify_range_err), ctypes.c_void_p(mask.data_ptr()),
+                                        ctypes.c_void_p(engine.stream_ptr())), "densify_mask")
+            stats["pruned"] = self.prune(cfg.prune_opacity)
+        stats["spawned"] = self.spawn(kf, mask, cfg.n_spawn, cfg, rng)
+        self.keyframes.append(kf)
+        return stats
 
     @property
     def n(self) -> int:

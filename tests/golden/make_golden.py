@@ -314,3 +314,46 @@ def make_geometric_case():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "geometric":
     make_geometric_case()
+
+
+def make_densify_case():
+    """Map growth (mapping.py:202-311, 383-438): LocalMap.start on keyframe 0 (spawn at every
+    valid pixel, capped: weighted draw without replacement), then add_keyframe with keyframe 1
+    (render, densify mask, prune, spawn), float64 keyframe images kept as they were used."""
+    from splatscan.mapping import LocalMap, MappingConfig, _range_gradient_weights, add_keyframe, densify_mask, \
+        make_keyframe
+    from splatscan.rasterizer import rasterize_forward as rf
+    from splatscan.synth import ScanSpec, raycast_scan, room_with_boxes
+
+    scene = room_with_boxes(n_boxes=4, seed=3)
+    spec = ScanSpec(width=128, height=16)
+    cfg = MappingConfig(n_spawn=1000)
+    poses = [SE3Pose.identity(), SE3Pose(so3_exp(np.deg2rad([0, 0, 6.0])), np.array([0.5, 0.2, 0.0]))]
+    kfs = [make_keyframe(i, raycast_scan(scene, p, spec).cloud, p, spec.width, spec.height) for i, p in enumerate(poses)]
+    rng = np.random.default_rng(21)
+    lmap = LocalMap.start(kfs[0], cfg, rng)
+    m0 = lmap.model
+    after_start = {k: getattr(m0, k).copy() for k in ("centers", "raw_t_alpha", "raw_t_beta", "log_scales",
+                                                         "logit_opacity")}
+    # make one splat prunable so add_keyframe exercises the compaction
+    lmap.model.logit_opacity[7] = -8.0
+    render, _ = rf(kfs[1].camera, kfs[1].pose, lmap.model)
+    mask1 = densify_mask(render, kfs[1], cfg)
+    stats = add_keyframe(lmap, kfs[1], cfg, rng)
+    out = {f"s_{k}": v for k, v in after_start.items()}
+    out.update({f"a_{k}": getattr(lmap.model, k).copy() for k in after_start})
+    for i, kf in enumerate(kfs):
+        c = kf.camera
+        out[f"kf{i}_cam"] = np.array([c.width, c.height, c.az_min, c.az_max, c.el_min, c.el_max])
+        out[f"kf{i}_R"], out[f"kf{i}_t"] = kf.pose.rotation, kf.pose.translation
+        out[f"kf{i}_range"], out[f"kf{i}_valid"] = kf.range_image.range, kf.range_image.valid
+        out[f"kf{i}_normal"], out[f"kf{i}_nvalid"] = kf.normal_image.normals, kf.normal_image.valid
+        out[f"kf{i}_gradw"] = _range_gradient_weights(kf)
+    out.update(scene_scale=lmap.scene_scale, mask1=mask1, pruned=stats["pruned"], spawned=stats["spawned"],
+               render1_range=render.range, render1_opacity=render.opacity, epochs=lmap.model.epochs)
+    np.savez_compressed(os.path.join(OUT, "golden_densify.npz"), **out)
+    print("densify: start", after_start["centers"].shape[0], "after add", len(lmap.model), stats)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "densify":
+    make_densify_case()
