@@ -743,8 +743,16 @@ __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ 
 // Tile processing order for the blend kernels: longest lists first (the
 // kernels fetch tiles dynamically, so this is longest-processing-time-first
 // scheduling).  Counting sort on min(L, 4095) / 4, one block.
+// Work slots of the blend kernels ((tile << 2) | part, see next_tile in
+// blend.cu), longest lists first: order_fwd holds one slot per tile
+// (counters[3] = ntiles); for the backward (order_bwd), when there are fewer
+// tiles than resident warps (split_target > 0), the split_target longest
+// tiles with at least 96 entries become two slots, one per pixel half
+// (counters[2] = slot count).  (Splitting the forward measured slower: both
+// halves re-stage every entry of the list.)
 __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_ptr,
-                                                     int* __restrict__ order, int* __restrict__ counters) {
+                                                     int* __restrict__ order_fwd, int* __restrict__ order,
+                                                     int* __restrict__ counters, int split_target) {
   __shared__ int hist[1024];
   const int tid = threadIdx.x;
   hist[tid] = 0;
@@ -770,9 +778,28 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   __syncthreads();
   hist[tid] = wex + inc - v;
   __syncthreads();
+  // tiles of >= 96 entries occupy the buckets 0 .. 1023 - 24 (bucket = 1023 - min(L, 4095) / 4)
+  __shared__ int s_nsplit;
+  if (tid == 0) {
+    const int n96 = hist[1023 - 23];  // exclusive prefix: tiles in buckets < 1000, i.e. L >= 96
+    s_nsplit = min(split_target, n96);
+  }
+  __syncthreads();
+  const int nsplit = s_nsplit;
   for (int t = tid; t < ntiles; t += 1024) {
     const int L = tile_ptr[t + 1] - tile_ptr[t];
-    order[atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1)] = t;
+    const int r = atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1);  // LPT rank
+    order_fwd[r] = t << 2;
+    if (r < nsplit) {
+      order[2 * r] = (t << 2) | 1;
+      order[2 * r + 1] = (t << 2) | 2;
+    } else {
+      order[nsplit + r] = t << 2;
+    }
+  }
+  if (tid == 0) {
+    counters[2] = ntiles + nsplit;
+    counters[3] = ntiles;
   }
 }
 

@@ -323,20 +323,25 @@ __device__ __forceinline__ float red_transpose16(const float (&a)[16], float* re
 }
 
 // Warp-uniform tile ticket (persistent warps, longest lists first).
-__device__ __forceinline__ int next_tile(int* counter, const int* order, int ntiles, int lane) {
+// Work slots: (tile << 2) | part, part 0 = the whole tile, 1 / 2 = only the
+// pixels of j = 0 / 1 (rows 0-3 / 4-7 of an 8x8 tile).  k_tile_order splits
+// the longest tiles in two when there are fewer tiles than resident warps, so
+// a few very long lists do not leave one warp per tile finishing alone.
+__device__ __forceinline__ int next_tile(int* counter, const int* order, const int* nslots, int lane) {
   int ti = 0;
   if (lane == 0) ti = atomicAdd(counter, 1);
   ti = __shfl_sync(0xffffffffu, ti, 0);
-  return ti < ntiles ? order[ti] : -1;
+  return ti < *nslots ? order[ti] : -1;
 }
 
-template <int TS>
+template <int TS, bool kSplit>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1)
     k_forward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
               const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
               float* __restrict__ out_D, float* __restrict__ out_N, float* __restrict__ out_O,
               float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask,
-              const int* __restrict__ overflow, const int* __restrict__ order, int* __restrict__ counter) {
+              const int* __restrict__ overflow, const int* __restrict__ order, int* __restrict__ counter,
+              const int* __restrict__ nslots) {
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;  // pair capacity exceeded: the host re-runs the render
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
@@ -344,21 +349,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CamK& k = bp.cam;
   float* st = stage[warp];
-  for (int t = next_tile(counter, order, ntiles, lane); t >= 0; t = next_tile(counter, order, ntiles, lane)) {
+  for (int code = next_tile(counter, order, nslots, lane); code >= 0; code = next_tile(counter, order, nslots, lane)) {
+    const int t = code >> 2, part = kSplit ? (code & 3) : 0;
     const int tr = t / k.tx, tc = t % k.tx;
     TileFrame f;
     tile_frame<TS>(k, tr, tc, f);
     Pix px[PPL];
     float T[PPL], D[PPL], O[PPL], N[PPL][3];
     int last[PPL];
-    bool live[PPL];
+    bool live[PPL], use[PPL];
     float xm = 0.f, ym = 0.f;
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
       pixel_geo<TS>(k, tr, tc, lane + 32 * j, f, px[j]);
+      use[j] = part == 0 || part == j + 1;  // (warp-uniform)
       T[j] = 1.f; D[j] = 0.f; O[j] = 0.f; N[j][0] = N[j][1] = N[j][2] = 0.f;
       last[j] = 0;
-      live[j] = px[j].ray_ok;
+      live[j] = px[j].ray_ok && use[j];
       if (px[j].ray_ok) {
         xm = fmaxf(xm, fabsf((float)px[j].x));
         ym = fmaxf(ym, fabsf((float)px[j].y));
@@ -401,6 +408,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
         const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
+          if (kSplit && !use[j]) continue;
           const float* p = px[j].p;
           const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
           // sign bit of q (q < 0 or -0; q = +0 only on the cone's safety margin):
@@ -439,14 +447,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
         }
       }
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
+      for (int j = 0; j < PPL; ++j)
+        if (use[j]) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
       __syncwarp();
     }
     __pipeline_wait_prior(0);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
-      if (!px[j].inside) continue;
+      if (!px[j].inside || !use[j]) continue;
       const size_t p = (size_t)px[j].row * k.W + px[j].col;
       out_D[p] = D[j];
       out_O[p] = O[j];
@@ -474,14 +483,14 @@ constexpr bool kBwdDF = false;
 constexpr bool kBwdDF = true;  // float-pair intersection in the backward (230 -> 209 us)
 #endif
 
-template <int TS>
+template <int TS, bool kSplit>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
     k_backward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
                const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
                const float* __restrict__ in_T, const int* __restrict__ in_last, const unsigned* __restrict__ bitmask,
                const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
                float* __restrict__ acc, const int* __restrict__ overflow, const int* __restrict__ order,
-               int* __restrict__ counter, float* __restrict__ pacc) {
+               int* __restrict__ counter, const int* __restrict__ nslots, float* __restrict__ pacc) {
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
   // deterministic mode (pacc != null): every entry is reduced by the fixed-order
@@ -496,7 +505,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
   float* red = reinterpret_cast<float*>(bwd_dyn_smem) + warp * 512;
   int roff[8];
   red_offsets(lane, roff);
-  for (int t = next_tile(counter, order, ntiles, lane); t >= 0; t = next_tile(counter, order, ntiles, lane)) {
+  for (int code = next_tile(counter, order, nslots, lane); code >= 0; code = next_tile(counter, order, nslots, lane)) {
+    const int t = code >> 2, part = kSplit ? (code & 3) : 0;
     const int tr = t / k.tx, tc = t % k.tx;
     TileFrame f;
     tile_frame<TS>(k, tr, tc, f);
@@ -510,7 +520,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       last[j] = 0;
       T[j] = 1.f;
       gD[j] = gO[j] = gN[j][0] = gN[j][1] = gN[j][2] = 0.f;
-      if (px[j].inside) {
+      if (px[j].inside && (part == 0 || part == j + 1)) {
         const size_t p = (size_t)px[j].row * k.W + px[j].col;
         last[j] = in_last[p];
         T[j] = in_T[p];
@@ -532,7 +542,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     // c-1 are copied (cp.async) while chunk c is processed.
     auto load_words = [&](int c, unsigned (&wd)[PPL], int& sid) {
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) wd[j] = c >= 0 ? bitmask[(size_t)(cbase + c) * (TS * TS) + lane + 32 * j] : 0u;
+      for (int j = 0; j < PPL; ++j)
+        wd[j] = (c >= 0 && (part == 0 || part == j + 1)) ? bitmask[(size_t)(cbase + c) * (TS * TS) + lane + 32 * j]
+                                                         : 0u;
       sid = (c >= 0 && c * 32 + lane < tile_ptr[t + 1] - lo) ? pairs[lo + c * 32 + lane] : -1;
     };
     auto or_words = [&](const unsigned (&wd)[PPL]) {
@@ -859,18 +871,21 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   }
 }
 
-template __global__ void k_forward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                      const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*,
-                                      const int*, int*);
-template __global__ void k_forward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                       const SplatRec64*, float*, float*, float*, float*, int*, unsigned*, const int*,
-                                       const int*, int*);
-template __global__ void k_backward<8>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                       const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                       const float*, const float*, float*, const int*, const int*, int*, float*);
-template __global__ void k_backward<16>(BlendParams, int, const int*, const int*, const int*, const SplatRec*,
-                                        const SplatRec64*, const float*, const int*, const unsigned*, const float*,
-                                        const float*, const float*, float*, const int*, const int*, int*, float*);
+#define SS_INST_FWD(TS, SPLIT)                                                                                  \
+  template __global__ void k_forward<TS, SPLIT>(BlendParams, int, const int*, const int*, const int*,               \
+                                                const SplatRec*, const SplatRec64*, float*, float*, float*, float*,  \
+                                                int*, unsigned*, const int*, const int*, int*, const int*);
+#define SS_INST_BWD(TS, SPLIT)                                                                                  \
+  template __global__ void k_backward<TS, SPLIT>(BlendParams, int, const int*, const int*, const int*,              \
+                                                 const SplatRec*, const SplatRec64*, const float*, const int*,       \
+                                                 const unsigned*, const float*, const float*, const float*, float*,  \
+                                                 const int*, const int*, int*, const int*, float*);
+SS_INST_FWD(8, false)
+
+SS_INST_FWD(16, false)
+SS_INST_BWD(8, false)
+SS_INST_BWD(8, true)
+SS_INST_BWD(16, false)
 
 // Deterministic mode: zero the per-position accumulators of the current pair count.
 __global__ void k_zero_pacc(float4* __restrict__ pacc, const long long* __restrict__ totals, long long cap) {

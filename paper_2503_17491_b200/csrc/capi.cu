@@ -123,6 +123,7 @@ struct ss_records {
   BlendParams bp{};
   int n = 0, ntiles = 0, valid = 0, pending = 0;
   int deterministic = 0;  // backward: fixed-order gradient reduction (ss_records_set_deterministic)
+  int split_target = 0;   // work slots beyond one per tile (k_tile_order)
   float* pacc = nullptr;  // deterministic mode: per list position accumulators
   size_t cap_pacc = 0;
   uint32_t epoch = 0;
@@ -226,10 +227,11 @@ void set_smem_attrs() {
   const int bytes = (int)(sizeof(uint32_t) * kMaxTiles);
   cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_backward<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sort_smem_bytes<kTileSortBig, 1024>());
-  cudaFuncSetAttribute(k_backward<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   done = true;
 }
 }  // namespace
@@ -312,7 +314,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) || grow(rec->bsum, rec->cap_bsum, (size_t)nb + 1, s) ||
       grow(rec->mat, rec->cap_mat, (size_t)pblocks * ntiles, s) ||
       grow(rec->tint, rec->cap_tint, (size_t)(k.tx + k.ty), s) ||
-      grow(rec->tiles, rec->cap_tiles, (size_t)6 * (ntiles + 1), s) ||
+      grow(rec->tiles, rec->cap_tiles, (size_t)8 * (ntiles + 1), s) ||
       grow(rec->ptile, rec->cap_ptile, (size_t)cap, s) || grow(rec->psplat, rec->cap_psplat, (size_t)cap, s) ||
       grow(rec->pbucket, rec->cap_pbucket, (size_t)cap, s) ||
       grow(rec->bitmask, rec->cap_bitmask, ((size_t)cap / 32 + ntiles + 1) * TT, s) ||
@@ -323,8 +325,12 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* chunk_ptr = rec->tiles + (ntiles + 1);
   int* tile_count = rec->tiles + 2 * (ntiles + 1);
   int* long_list = rec->tiles + 4 * (ntiles + 1);
-  int* order = rec->tiles + 5 * (ntiles + 1);
-  int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets
+  int* order = rec->tiles + 5 * (ntiles + 1);  // up to 2 * ntiles work slots
+  int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets, [2] work slots
+  // fewer tiles than resident blend warps (4 blocks x 4 warps per SM): split the longest in two
+  // (not in deterministic mode: both halves of a split tile would write one list position)
+  const int split_target = (k.T == 8 && !rec->deterministic) ? std::max(0, num_sms() * 16 - ntiles) : 0;
+  rec->split_target = split_target;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -361,20 +367,22 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
-    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order, counters);
+    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target);
   }
   rec->pairs = (int*)rec->pbucket;
   const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
   {
     StageTimer tmf(rec, ST_FORWARD, s);
     if (k.T == 8)
-      k_forward<8><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      k_forward<8, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                          rec->last, rec->bitmask, overflow, order, counters);
+                                                          rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
+                                                          counters, counters + 3);
     else
-      k_forward<16><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      k_forward<16, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-                                                           rec->last, rec->bitmask, overflow, order, counters);
+                                                           rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
+                                                          counters, counters + 3);
   }
   SS_CUDA_TRY(cudaGetLastError());
   k_publish_totals<<<1, 32, 0, s>>>(rec->totals, rec->misc, rec->d_h_totals);
@@ -475,18 +483,21 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
     k_zero_pacc<<<num_sms() * 4, 256, 0, s>>>((float4*)pacc, rec->totals, rec->cap_pairs);
   }
   {
-    const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
+    const int blocks =
+        std::min((ntiles + rec->split_target + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
     int* order = rec->tiles + 5 * (ntiles + 1);
     int* counters = rec->misc + 4;
     StageTimer tm(rec, ST_BACKWARD, s);
     if (rec->cam.T == 8)
-      k_backward<8><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      (rec->split_target ? k_backward<8, true> : k_backward<8, false>)<<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                           rec->acc, rec->misc + 1, order, counters + 1, pacc);
+                                                           rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
+                                                           pacc);
     else
-      k_backward<16><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
+      k_backward<16, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1, pacc);
+                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
+                                                           pacc);
     SS_CUDA_TRY(cudaGetLastError());
     if (pacc)
       k_det_gather<<<(n + 255) / 256, 256, 0, s>>>(n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
