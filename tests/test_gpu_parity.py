@@ -204,3 +204,27 @@ def test_backward_twice_same_records(cuda):
     a2 = rasterize_backward(model, rec, out, g1).d_centers
     assert np.abs(a2 - a).max() <= 1e-6 * np.abs(a).max()
     assert np.abs(b).max() > 0 and not np.allclose(a, b)
+
+
+def test_pair_capacity_overflow_rerun(cuda):
+    """A few huge splats near the sensor cover every tile: more (tile, splat) pairs than the
+    speculative capacity (max(8 n, 65536)), so the first forward overflows on the device and
+    rasterize_forward transparently re-runs with the exact capacity (ss_records_check)."""
+    rng = np.random.default_rng(8)
+    n = 120
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    params = {"centers": (d * rng.uniform(1.0, 3.0, (n, 1))).astype(np.float32),
+              "raw_t_alpha": rng.normal(size=(n, 3)).astype(np.float32),
+              "raw_t_beta": rng.normal(size=(n, 3)).astype(np.float32),
+              "log_scales": np.full((n, 2), np.log(1.5), np.float32),
+              "logit_opacity": rng.normal(size=n).astype(np.float32)}
+    cam = W.synth_camera(1024, 64)
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), params)
+    assert ref["pair_splats"].shape[0] > 65536
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), SplatModel.from_params(params))
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"]) and np.array_equal(rec.pair_splats, ref["pair_splats"])
+    rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
+                       np.full(out.range.shape, 1.0))
+    assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
