@@ -124,6 +124,7 @@ struct ss_records {
   int n = 0, ntiles = 0, valid = 0, pending = 0;
   int deterministic = 0;  // backward: fixed-order gradient reduction (ss_records_set_deterministic)
   int split_target = 0;   // work slots beyond one per tile (k_tile_order)
+  bool captured = false;  // last forward was recorded into a CUDA graph
   float* pacc = nullptr;  // deterministic mode: per list position accumulators
   size_t cap_pacc = 0;
   uint32_t epoch = 0;
@@ -387,7 +388,13 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   SS_CUDA_TRY(cudaGetLastError());
   k_publish_totals<<<1, 32, 0, s>>>(rec->totals, rec->misc, rec->d_h_totals);
   SS_CUDA_TRY(cudaGetLastError());
-  SS_CUDA_TRY(cudaEventRecord(rec->done, s));
+  // Under CUDA-graph capture the completion event cannot be waited on from the
+  // host: ss_records_check then synchronises the device instead (the totals
+  // still arrive through k_publish_totals on every replay).
+  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+  SS_CUDA_TRY(cudaStreamIsCapturing(s, &capst));
+  rec->captured = capst != cudaStreamCaptureStatusNone;
+  if (!rec->captured) SS_CUDA_TRY(cudaEventRecord(rec->done, s));
   return SS_OK;
 }
 
@@ -404,7 +411,10 @@ int ss_records_set_deterministic(ss_records* rec, int32_t deterministic) {
 int ss_records_check(ss_records* rec, int wait) {
   if (!rec) return SS_ERR_INVALID_ARGUMENT;
   if (!rec->pending) return rec->valid ? SS_OK : SS_ERR_STALE_RECORDS;
-  if (wait) {
+  if (rec->captured) {
+    if (!wait) return SS_OK;
+    SS_CUDA_TRY(cudaDeviceSynchronize());
+  } else if (wait) {
     SS_CUDA_TRY(cudaEventSynchronize(rec->done));
   } else if (cudaEventQuery(rec->done) != cudaSuccess) {
     return SS_OK;

@@ -228,3 +228,41 @@ def test_pair_capacity_overflow_rerun(cuda):
     rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
                        np.full(out.range.shape, 1.0))
     assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
+
+
+def test_cuda_graph_capture_replay(cuda):
+    """The forward / loss / backward sequence is stream-ordered with no host synchronisation,
+    so it captures into a CUDA graph; replays match eager execution (float-atomic rounding)."""
+    from paper_2503_17491_b200 import engine
+    c = W.config(0)
+    cam = c["camera"]
+    sp = {k: torch.from_numpy(v).cuda() for k, v in c["splats"].items()}
+    tgt = W.target_images(W.Scene(0), cam)
+    kr, kn = torch.from_numpy(tgt["range"]).cuda(), torch.from_numpy(tgt["normal"]).cuda()
+    kv = torch.from_numpy(tgt["valid"].astype(np.uint8)).cuda()
+    knv = torch.from_numpy(tgt["nvalid"].astype(np.uint8)).cuda()
+    rec, cfg = engine.Records(), RasterConfig()
+    pose = np.concatenate([np.eye(3).reshape(9), np.zeros(3)])
+
+    def step():
+        D, N, O = engine.forward(cam, pose, sp, cfg, rec, sync=False)
+        dD, dN, dO, parts = engine.mapping_loss(D, N, O, kr, kv, kn, knv, 0.0, 0.1)
+        return engine.backward(rec, sp, dD, dN, dO, raw_space=True)
+
+    engine.forward(cam, pose, sp, cfg, rec)  # sizes the pair buffers
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            eager = step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = eager.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        out = step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert rec.check(True) == 0
+    assert torch.allclose(out, eager, rtol=1e-4, atol=1e-6 * float(eager.abs().max()))
