@@ -920,7 +920,7 @@ int ss_range_image_normals(const ss_camera* cam, const double* range, const uint
 
 size_t ss_leaf_tree_workspace_bytes(int32_t n) {
   const size_t m = (size_t)(n > 0 ? n : 1);
-  return m * (4 + 4 + 8 + 8 + sizeof(LeafRec) + 8) + 1024;
+  return m * (4 + 4 + 8 + 2 * 8 + sizeof(LeafRec) + 8 + sizeof(LeafRec)) + 1024;
 }
 
 int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, int32_t leaf_size, double tau,
@@ -932,56 +932,71 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
     return SS_ERR_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned char* w = (unsigned char*)workspace;
-  int* idx = (int*)w;
-  w += (size_t)n * 4;
-  int* tmp = (int*)w;
-  w += (size_t)n * 4;
-  double* proj = (double*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
-  w = (unsigned char*)(proj + n);
-  int2* nodes = (int2*)w;
-  w += (size_t)n * 8;
-  LeafRec* recs = (LeafRec*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
-  w = (unsigned char*)(recs + n);
-  int2* leaves_d = (int2*)w;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = (unsigned char*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+    w = p + bytes;
+    return p;
+  };
+  // a node is split only when larger than leaf_size: a level holds at most 2n/(leaf_size+1) + 2 nodes
+  const int cap_nodes = std::min(n, 2 * (n / (leaf_size + 1)) + 2);
+  const int cap_leaves = std::min(max_leaves, n);
+  int* idx = (int*)take((size_t)n * 4);
+  int* tmp = (int*)take((size_t)n * 4);
+  double* proj = (double*)take((size_t)n * 8);
+  int2* nodes[2] = {(int2*)take((size_t)cap_nodes * 8), (int2*)take((size_t)cap_nodes * 8)};
+  LeafRec* recs = (LeafRec*)take((size_t)cap_nodes * sizeof(LeafRec));
+  int2* leaf_seg = (int2*)take((size_t)cap_leaves * 8);
+  LeafRec* leaf_rec = (LeafRec*)take((size_t)cap_leaves * sizeof(LeafRec));
+  int* counts = (int*)take(16);  // [0] nodes of level parity 0, [1] parity 1, [2] leaves, [3] overflow
   k_iota<<<(n + 255) / 256, 256, 0, s>>>(n, idx);
+  const int init[4] = {1, 0, 0, 0};
+  const int2 root = make_int2(0, n);
+  SS_CUDA_TRY(cudaMemcpyAsync(counts, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  SS_CUDA_TRY(cudaMemcpyAsync(nodes[0], &root, sizeof(root), cudaMemcpyHostToDevice, s));
   const double3 vp = make_double3(viewpoint3[0], viewpoint3[1], viewpoint3[2]);
-  std::vector<int2> cur{make_int2(0, n)}, next, leaves;
-  std::vector<LeafRec> h;
-  int nl_total = 0;
-  while (!cur.empty()) {
-    const int L = (int)cur.size();
-    SS_CUDA_TRY(cudaMemcpyAsync(nodes, cur.data(), sizeof(int2) * L, cudaMemcpyHostToDevice, s));
-    if (L < num_sms())  // top levels: few large nodes, 1024 threads each
-      k_leaf_level<kLtThreadsBig><<<L, kLtThreadsBig, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
-    else
-      k_leaf_level<kLtThreads><<<L, kLtThreads, 0, s>>>(pts, idx, tmp, proj, nodes, vp, leaf_size, tau, recs);
-    SS_CUDA_TRY(cudaGetLastError());
-    h.resize(L);
-    SS_CUDA_TRY(cudaMemcpyAsync(h.data(), recs, sizeof(LeafRec) * L, cudaMemcpyDeviceToHost, s));
-    SS_CUDA_TRY(cudaStreamSynchronize(s));
-    next.clear();
-    for (int i = 0; i < L; ++i) {
-      if (h[i].split) {
-        next.push_back(make_int2(cur[i].x, cur[i].x + h[i].nl));
-        next.push_back(make_int2(cur[i].x + h[i].nl, cur[i].y));
-        continue;
-      }
-      if (nl_total >= max_leaves) return SS_ERR_CAPACITY;
-      for (int k = 0; k < 3; ++k) {
-        centroids_out[3 * nl_total + k] = h[i].c[k];
-        normals_out[3 * nl_total + k] = h[i].n[k];
-      }
-      sizes_out[nl_total] = cur[i].y - cur[i].x;
-      usable_out[nl_total] = (uint8_t)h[i].usable;
-      leaves.push_back(cur[i]);
-      ++nl_total;
+  // Levels run back to back without host round trips: each level's grid is a
+  // bound on its node count (blocks past the actual count exit), the next
+  // level is laid out on the device; the host checks for leftovers at the end.
+  int level = 0;
+  for (int batch = 0;; ++batch) {
+    const int depth = batch == 0 ? 2 + (int)std::ceil(std::log2((double)n + 1.0)) : 8;
+    for (int q = 0; q < depth; ++q, ++level) {
+      const int par = level & 1;
+      const long long bound = std::min<long long>(level < 30 ? (1LL << level) : cap_nodes, cap_nodes);
+      if (bound < num_sms())  // top levels: few large nodes, 1024 threads each
+        k_leaf_level<kLtThreadsBig><<<(int)bound, kLtThreadsBig, 0, s>>>(pts, idx, tmp, proj, nodes[par],
+                                                                         counts + par, vp, leaf_size, tau, recs);
+      else
+        k_leaf_level<kLtThreads><<<(int)bound, kLtThreads, 0, s>>>(pts, idx, tmp, proj, nodes[par], counts + par,
+                                                                   vp, leaf_size, tau, recs);
+      k_next_level<<<1, 1024, 0, s>>>(nodes[par], counts + par, recs, nodes[par ^ 1], counts + (par ^ 1), leaf_seg,
+                                      leaf_rec, counts + 2, cap_leaves, counts + 3);
+      SS_CUDA_TRY(cudaGetLastError());
     }
-    cur.swap(next);
+    int h[4];
+    SS_CUDA_TRY(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[3]) return SS_ERR_CAPACITY;
+    if (h[level & 1] == 0) break;  // no node left at the next level
   }
-  SS_CUDA_TRY(cudaMemcpyAsync(leaves_d, leaves.data(), sizeof(int2) * nl_total, cudaMemcpyHostToDevice, s));
-  k_leaf_assign<<<nl_total, 256, 0, s>>>(idx, leaves_d, nl_total, point_leaf_out);
+  int nl_total = 0;
+  SS_CUDA_TRY(cudaMemcpyAsync(&nl_total, counts + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<LeafRec> hr(nl_total);
+  std::vector<int2> hs(nl_total);
+  SS_CUDA_TRY(cudaMemcpyAsync(hr.data(), leaf_rec, sizeof(LeafRec) * nl_total, cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaMemcpyAsync(hs.data(), leaf_seg, sizeof(int2) * nl_total, cudaMemcpyDeviceToHost, s));
+  k_leaf_assign<<<std::max(nl_total, 1), 256, 0, s>>>(idx, leaf_seg, nl_total, point_leaf_out);
   SS_CUDA_TRY(cudaGetLastError());
   SS_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int i = 0; i < nl_total; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      centroids_out[3 * i + k] = hr[i].c[k];
+      normals_out[3 * i + k] = hr[i].n[k];
+    }
+    sizes_out[i] = hs[i].y - hs[i].x;
+    usable_out[i] = (uint8_t)hr[i].usable;
+  }
   *n_leaves_out = nl_total;
   return SS_OK;
 }

@@ -180,8 +180,10 @@ __device__ unsigned long long block_select(const double* __restrict__ proj, int 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pts, int* __restrict__ idx,
                                                            int* __restrict__ tmp, double* __restrict__ proj,
-                                                           const int2* __restrict__ nodes, double3 viewpoint,
+                                                           const int2* __restrict__ nodes,
+                                                           const int* __restrict__ n_nodes, double3 viewpoint,
                                                            int leaf_size, double tau, LeafRec* __restrict__ out) {
+  if ((int)blockIdx.x >= *n_nodes) return;  // grid sized by a bound on the level's node count
   __shared__ double sred[NT / 32];
   __shared__ double s_m[3], s_cov[6], s_axis[3], s_n[3], s_w[3], s_med;
   __shared__ unsigned hist[kLtBins];
@@ -341,6 +343,57 @@ __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pt
     rec.split = 1;
     rec.nl = nl;
     out[blockIdx.x] = rec;
+  }
+}
+
+// Lay out the next level (children of split nodes, in node order) and append
+// this level's leaves (in node order): one block, counts scanned per thread run.
+__global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cur, const int* __restrict__ n_cur_p,
+                                                     const LeafRec* __restrict__ recs, int2* __restrict__ next,
+                                                     int* __restrict__ n_next_p, int2* __restrict__ leaf_seg,
+                                                     LeafRec* __restrict__ leaf_rec, int* __restrict__ n_leaves_p,
+                                                     int max_leaves, int* __restrict__ overflow) {
+  __shared__ int s_c[1024], s_l[1024];
+  const int n_cur = *n_cur_p, tid = threadIdx.x;
+  const int per = (n_cur + 1023) / 1024;
+  const int b = min(tid * per, n_cur), e = min(b + per, n_cur);
+  int nc = 0, nl = 0;
+  for (int i = b; i < e; ++i) {
+    if (recs[i].split)
+      nc += 2;
+    else
+      ++nl;
+  }
+  s_c[tid] = nc;
+  s_l[tid] = nl;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int vc = tid >= off ? s_c[tid - off] : 0, vl = tid >= off ? s_l[tid - off] : 0;
+    __syncthreads();
+    s_c[tid] += vc;
+    s_l[tid] += vl;
+    __syncthreads();
+  }
+  const int leaf0 = *n_leaves_p;
+  int oc = s_c[tid] - nc, ol = leaf0 + s_l[tid] - nl;
+  for (int i = b; i < e; ++i) {
+    const int2 nd = cur[i];
+    const LeafRec& r = recs[i];
+    if (r.split) {
+      next[oc++] = make_int2(nd.x, nd.x + r.nl);
+      next[oc++] = make_int2(nd.x + r.nl, nd.y);
+    } else if (ol < max_leaves) {
+      leaf_seg[ol] = nd;
+      leaf_rec[ol] = r;
+      ++ol;
+    } else {
+      *overflow = 1;
+    }
+  }
+  __syncthreads();
+  if (tid == 1023) {
+    *n_next_p = s_c[1023];
+    *n_leaves_p = leaf0 + s_l[1023];
   }
 }
 
