@@ -87,19 +87,25 @@ class DeviceScan:
               "build_range_image")
 
 
-@dataclass
 class LeafTree:
     """registration.py:81-95 (the k-d tree over usable centroids is replaced by the
     device association; ``kdtree`` stays None).  ``dev_centroids`` / ``dev_normals``
-    hold the usable leaves on the device for the association kernel."""
-    centroids: np.ndarray
-    normals: np.ndarray
-    sizes: np.ndarray
-    usable: np.ndarray
-    point_leaf: np.ndarray
-    kdtree: object = None
-    dev_centroids: torch.Tensor | None = None
-    dev_normals: torch.Tensor | None = None
+    hold the usable leaves on the device for the association kernel; ``point_leaf``
+    is copied to the host on first access."""
+
+    kdtree = None
+
+    def __init__(self, centroids, normals, sizes, usable, point_leaf_dev, dev_centroids, dev_normals):
+        self.centroids, self.normals, self.sizes, self.usable = centroids, normals, sizes, usable
+        self.point_leaf_dev = point_leaf_dev
+        self.dev_centroids, self.dev_normals = dev_centroids, dev_normals
+        self._point_leaf = None
+
+    @property
+    def point_leaf(self) -> np.ndarray:
+        if self._point_leaf is None:
+            self._point_leaf = self.point_leaf_dev.cpu().numpy().astype(int)
+        return self._point_leaf
 
 
 def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float = 0.02) -> LeafTree:
@@ -125,7 +131,7 @@ def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float 
                                    ctypes.c_void_p(engine.stream_ptr())), "build_leaf_tree")
     k = nl.value
     use = usable[:k].astype(bool)
-    return LeafTree(cent[:k].copy(), nrm[:k].copy(), sizes[:k].astype(int), use, pl.cpu().numpy().astype(int), None,
+    return LeafTree(cent[:k].copy(), nrm[:k].copy(), sizes[:k].astype(int), use, pl,
                     torch.as_tensor(np.ascontiguousarray(cent[:k][use]), device=dev),
                     torch.as_tensor(np.ascontiguousarray(nrm[:k][use]), device=dev))
 
