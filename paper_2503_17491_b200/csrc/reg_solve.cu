@@ -647,8 +647,9 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         }
       }
     }
-    // --- per-block partial sums (both families), block 0 reduces them in block order
+    // --- per-block partial sums (families of this evaluation), block 0 reduces them in block order
     for (int f = 0; f < 2; ++f) {
+      if (!fam_on[f]) continue;  // (uniform)
 #pragma unroll
       for (int q = 0; q < 31; ++q) {
         double v = acc[f][q];
@@ -666,6 +667,10 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
     grid.sync();
     if (blockIdx.x == 0) {
       for (int f = 0; f < 2; ++f) {
+        if (!fam_on[f]) {
+          if (tid < kRsAcc) sfin[f * kRsAcc + tid] = 0.0;
+          continue;
+        }
         const int q = tid & 31, g = tid >> 5;
         double s = 0.0;
         if (q < 31)
