@@ -175,6 +175,8 @@ struct ss_records {
   long long* h_totals = nullptr;  // mapped pinned: totals[2], status, overflow
   long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
+  cudaEvent_t fwd_end = nullptr;  // forward kernels finished (side-stream fork point)
+  cudaStream_t side = nullptr;    // publishes the totals off the compute stream
   // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -254,6 +256,8 @@ ss_records* ss_records_create(void) {
     return nullptr;
   }
   cudaEventCreateWithFlags(&r->done, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&r->fwd_end, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
   return r;
 }
 
@@ -272,6 +276,8 @@ void ss_records_destroy(ss_records* r, void* stream) {
   }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->done) cudaEventDestroy(r->done);
+  if (r->fwd_end) cudaEventDestroy(r->fwd_end);
+  if (r->side) cudaStreamDestroy(r->side);
   if (r->h_totals) cudaFreeHost(r->h_totals);
   delete r;
 }
@@ -386,15 +392,23 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
                                                           counters, counters + 3);
   }
   SS_CUDA_TRY(cudaGetLastError());
-  k_publish_totals<<<1, 32, 0, s>>>(rec->totals, rec->misc, rec->d_h_totals);
-  SS_CUDA_TRY(cudaGetLastError());
-  // Under CUDA-graph capture the completion event cannot be waited on from the
-  // host: ss_records_check then synchronises the device instead (the totals
-  // still arrive through k_publish_totals on every replay).
+  // The totals go to mapped host memory from a side stream: that kernel's
+  // store crosses PCIe and would otherwise hold the compute stream behind the
+  // caller's bulk copies.  Under CUDA-graph capture the completion event cannot
+  // be waited on from the host: the kernel stays on the captured stream and
+  // ss_records_check synchronises the device instead.
   cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
   SS_CUDA_TRY(cudaStreamIsCapturing(s, &capst));
   rec->captured = capst != cudaStreamCaptureStatusNone;
-  if (!rec->captured) SS_CUDA_TRY(cudaEventRecord(rec->done, s));
+  if (rec->captured) {
+    k_publish_totals<<<1, 32, 0, s>>>(rec->totals, rec->misc, rec->d_h_totals);
+  } else {
+    SS_CUDA_TRY(cudaEventRecord(rec->fwd_end, s));
+    SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->fwd_end, 0));
+    k_publish_totals<<<1, 32, 0, rec->side>>>(rec->totals, rec->misc, rec->d_h_totals);
+    SS_CUDA_TRY(cudaEventRecord(rec->done, rec->side));
+  }
+  SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
 
