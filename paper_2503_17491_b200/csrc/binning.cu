@@ -750,14 +750,18 @@ __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ 
 // tiles with at least 96 entries become two slots, one per pixel half
 // (counters[2] = slot count).  (Splitting the forward measured slower: both
 // halves re-stage every entry of the list.)
+// long_target > 0: up to long_target of the longest tiles with >= 768 entries go
+// to the block-per-tile forward (k_forward_long, tickets counters[4] < counters[5]);
+// the warp-per-tile forward starts its tickets after them (counters[0] = nlong).
 __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_ptr,
                                                      int* __restrict__ order_fwd, int* __restrict__ order,
-                                                     int* __restrict__ counters, int split_target) {
+                                                     int* __restrict__ counters, int split_target,
+                                                     int long_target) {
   __shared__ int hist[1024];
   const int tid = threadIdx.x;
   hist[tid] = 0;
   if (tid < 4) counters[tid] = 0;
-  __syncthreads();
+  __syncthreads();  // (counters[0] is set to the long-tile count below, after the scan)
   for (int t = tid; t < ntiles; t += 1024) {
     const int L = tile_ptr[t + 1] - tile_ptr[t];
     atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1);
@@ -783,6 +787,11 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   if (tid == 0) {
     const int n96 = hist[1023 - 23];  // exclusive prefix: tiles in buckets < 1000, i.e. L >= 96
     s_nsplit = min(split_target, n96);
+    const int n768 = hist[1023 - 191];  // L >= 768
+    const int nlong = min(long_target, n768);
+    counters[0] = nlong;
+    counters[4] = 0;
+    counters[5] = nlong;
   }
   __syncthreads();
   const int nsplit = s_nsplit;

@@ -468,6 +468,155 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
   }
 }
 
+// Long lists, forward (config 2: fewer tiles than resident warps, lists of
+// thousands): one 128-thread block per tile instead of one warp.  Per round of
+// 128 entries all four warps run the cone test of one 32-entry chunk each;
+// then warps 0-1 composite (one pixel per lane, front to back over the four
+// chunks) while warps 2-3 stage the next round's entries -- the sequential
+// compositing of a tile overlaps the float64 staging of its next entries
+// instead of alternating with it in one warp.
+constexpr int kLongRound = 128;
+
+__global__ void __launch_bounds__(128) k_forward_long(
+    BlendParams bp, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
+    const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
+    float* __restrict__ out_D, float* __restrict__ out_N, float* __restrict__ out_O, float* __restrict__ out_T,
+    int* __restrict__ out_last, unsigned* __restrict__ bitmask, const int* __restrict__ overflow,
+    const int* __restrict__ order, int* __restrict__ counter, const int* __restrict__ nlong) {
+  constexpr int TS = 8;
+  if (*overflow) return;
+  extern __shared__ __align__(16) float lsm[];  // 2 x kLongRound x kStride staged entries
+  __shared__ unsigned cwbuf[4][64];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const CamK& k = bp.cam;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      const int ti = atomicAdd(counter, 1);
+      s_tile = ti < *nlong ? (order[ti] >> 2) : -1;
+    }
+    __syncthreads();
+    const int t = s_tile;
+    if (t < 0) break;
+    const int tr = t / k.tx, tc = t % k.tx;
+    TileFrame f;
+    tile_frame<TS>(k, tr, tc, f);
+    // every warp: geometry of all 64 pixels (two per lane) for its cone tests
+    Pix px[2];
+    float xm = 0.f, ym = 0.f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      pixel_geo<TS>(k, tr, tc, lane + 32 * j, f, px[j]);
+      if (px[j].ray_ok) {
+        xm = fmaxf(xm, fabsf((float)px[j].x));
+        ym = fmaxf(ym, fabsf((float)px[j].y));
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, off));
+      ym = fmaxf(ym, __shfl_xor_sync(0xffffffffu, ym, off));
+    }
+    xm *= 1.0001f;
+    ym *= 1.0001f;
+    // compositing threads (warps 0-1): pixel tid
+    const bool comp = warp < 2;
+    const Pix pc = warp == 0 ? px[0] : px[1];  // (warps 0-1: pixel lane + 32 * warp == tid)
+    float T = 1.f, D = 0.f, O = 0.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
+    int last = 0;
+    bool live = comp && pc.ray_ok;
+    const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
+    const int cbase = chunk_ptr[t];
+    auto stage_range = [&](int round, int buf, int e0, int stride) {
+      for (int e = e0; e < kLongRound; e += stride) {
+        const int idx = round * kLongRound + e;
+        if (idx >= L) break;
+        const int sid = pairs[lo + idx];
+        RawEntry raw;
+        raw.r0 = rec[sid].r0;
+        raw.r1 = rec[sid].r1;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) raw.v[q] = rec64[sid].v[q];
+        stage_entry<true>(lsm + ((size_t)buf * kLongRound + e) * kStride, sid, raw, f, xm, ym);
+      }
+    };
+    stage_range(0, 0, tid, 128);
+    __syncthreads();
+    for (int round = 0; round * kLongRound < L; ++round) {
+      const int buf = round & 1;
+      const float* stg = lsm + (size_t)buf * kLongRound * kStride;
+      // cone test: warp w, chunk w of the round, all 64 pixels
+      {
+        const int cnt = min(32, L - round * kLongRound - 32 * warp);
+        unsigned cw0 = 0u, cw1 = 0u;
+        for (int i = 0; i < cnt; ++i) {
+          const float* e = stg + (32 * warp + i) * kStride;
+          const float4 c0 = *reinterpret_cast<const float4*>(e);
+          const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
+          const float* p0 = px[0].p;
+          const float* p1 = px[1].p;
+          const float q0 = c0.x * p0[0] + c0.y * p0[1] + c0.z * p0[2] + c0.w * p0[3] + c1.x * p0[4] + c1.y * p0[5];
+          const float q1 = c0.x * p1[0] + c0.y * p1[1] + c0.z * p1[2] + c0.w * p1[3] + c1.x * p1[4] + c1.y * p1[5];
+          cw0 = (cw0 << 1) | (__float_as_uint(q0) >> 31);
+          cw1 = (cw1 << 1) | (__float_as_uint(q1) >> 31);
+        }
+        if (cnt > 0) {
+          cw0 = __brev(cw0) >> (32 - cnt);
+          cw1 = __brev(cw1) >> (32 - cnt);
+        }
+        cwbuf[warp][lane] = cnt > 0 ? cw0 : 0u;
+        cwbuf[warp][lane + 32] = cnt > 0 ? cw1 : 0u;
+      }
+      __syncthreads();
+      if (comp) {
+        for (int w = 0; w < 4; ++w) {
+          const int base = round * kLongRound + 32 * w;
+          if (base >= L) break;
+          unsigned m = live ? cwbuf[w][tid] : 0u;
+          unsigned word = 0u;
+          while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            Entry x;
+            load_entry(stg + (32 * w + i) * kStride, x);
+            Hit h;
+            intersect(x, pc, bp, h);
+            if (!h.use) continue;
+            const float wgt = h.alpha * T;
+            D += wgt * h.lam;
+            O += wgt;
+            N0 += wgt * x.n[0];
+            N1 += wgt * x.n[1];
+            N2 += wgt * x.n[2];
+            T *= (1.f - h.alpha);
+            word |= 1u << i;
+            last = base + i + 1;
+            if (T < bp.min_T) {
+              live = false;
+              m = 0u;
+            }
+          }
+          bitmask[(size_t)(cbase + round * 4 + w) * (TS * TS) + tid] = word;
+        }
+      } else if ((round + 1) * kLongRound < L) {
+        stage_range(round + 1, buf ^ 1, tid - 64, 64);  // the next round, under the compositing
+      }
+      if (!__syncthreads_or(live)) break;
+    }
+    if (comp && pc.inside) {
+      const size_t p = (size_t)pc.row * k.W + pc.col;
+      out_D[p] = D;
+      out_O[p] = O;
+      out_N[3 * p] = N0;
+      out_N[3 * p + 1] = N1;
+      out_N[3 * p + 2] = N2;
+      out_T[p] = T;
+      out_last[p] = last;
+    }
+  }
+}
+constexpr int kLongSmem = 2 * kLongRound * kStride * 4;
+
 constexpr int kAcc = 16;  // floats per splat accumulator (14 used)
 // Entries that at most this many lanes contributed to skip the warp
 // transpose: those lanes add their 14 values with vector atomics (A/B at

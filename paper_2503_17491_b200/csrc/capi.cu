@@ -176,6 +176,7 @@ struct ss_records {
   long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
   cudaEvent_t fwd_end = nullptr;  // forward kernels finished (side-stream fork point)
+  cudaEvent_t long_fork = nullptr, long_join = nullptr;  // block-per-tile forward on `side`
   cudaStream_t side = nullptr;    // publishes the totals off the compute stream
   // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
   bool profiling = false;
@@ -257,6 +258,8 @@ ss_records* ss_records_create(void) {
   }
   cudaEventCreateWithFlags(&r->done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&r->fwd_end, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&r->long_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&r->long_join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
   return r;
 }
@@ -277,6 +280,8 @@ void ss_records_destroy(ss_records* r, void* stream) {
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->done) cudaEventDestroy(r->done);
   if (r->fwd_end) cudaEventDestroy(r->fwd_end);
+  if (r->long_fork) cudaEventDestroy(r->long_fork);
+  if (r->long_join) cudaEventDestroy(r->long_join);
   if (r->side) cudaStreamDestroy(r->side);
   if (r->h_totals) cudaFreeHost(r->h_totals);
   delete r;
@@ -338,6 +343,8 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   // (not in deterministic mode: both halves of a split tile would write one list position)
   const int split_target = (k.T == 8 && !rec->deterministic) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
+  // ... and hand the longest lists (>= 768 entries) to the block-per-tile forward
+  const int long_target = (k.T == 8 && num_sms() * 16 > ntiles) ? num_sms() : 0;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -374,12 +381,21 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
-    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target);
+    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target,
+                                    long_target);
   }
   rec->pairs = (int*)rec->pbucket;
   const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
   {
     StageTimer tmf(rec, ST_FORWARD, s);
+    if (long_target) {  // the longest tiles, one block each, concurrently on the side stream
+      SS_CUDA_TRY(cudaEventRecord(rec->long_fork, s));
+      SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->long_fork, 0));
+      k_forward_long<<<long_target, 128, kLongSmem, rec->side>>>(
+          rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity,
+          rec->Tf, rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1), counters + 4, counters + 5);
+      SS_CUDA_TRY(cudaEventRecord(rec->long_join, rec->side));
+    }
     if (k.T == 8)
       k_forward<8, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
@@ -390,6 +406,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
                                                            rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                            rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
                                                           counters, counters + 3);
+    if (long_target) SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->long_join, 0));
   }
   SS_CUDA_TRY(cudaGetLastError());
   // The totals go to mapped host memory from a side stream: that kernel's
