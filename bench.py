@@ -144,6 +144,7 @@ def secondary_metrics(dev):
     cfg = MP.MappingConfig(w_opacity=0.05, w_normal=0.1)
     MP.DeviceMap(params, dkf, scale).refine(cfg, 5, np.random.default_rng(1))  # warm-up on a throwaway map
     dm = MP.DeviceMap(params, dkf, scale)
+    dm.capture_graphs(cfg)  # one CUDA graph per keyframe step (capture executes nothing)
     rng = np.random.default_rng(0)
 
     def depth_rmse():

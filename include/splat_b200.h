@@ -107,6 +107,13 @@ int ss_records_check(ss_records* rec, int wait);
  * sums use float atomics (order-dependent rounding, ~1e-7 relative). */
 int ss_records_set_deterministic(ss_records* rec, int32_t deterministic);
 
+/* Reserve pair capacity for the next forwards on `rec` (at least n_pairs). */
+int ss_records_reserve(ss_records* rec, int64_t n_pairs);
+
+/* *sticky = 1 (device int) if the last forward on `rec` overflowed its pair
+ * capacity: lets a CUDA-graph replay loop detect an overflow after the fact. */
+int ss_records_sticky_overflow(const ss_records* rec, int32_t* sticky, void* stream);
+
 /* Number of (tile, splat) pairs and tiles of a finished forward. */
 int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y);
 /* Copy tile_ptr (tiles+1) and pair_splats (n_pairs) into caller device
@@ -163,6 +170,17 @@ int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale
 int ss_adam_step(float* centers, float* raw_t_alpha, float* raw_t_beta, float* log_scales, float* logit_opacity,
                  const float* grads, float* m, float* v, int32_t n, int32_t t, const double* lrs5, double beta1,
                  double beta2, double eps, double log_scale_lo, double log_scale_hi, void* stream);
+
+/* The same Adam step with the step counter on the device (t_dev += 1, bias
+ * corrections computed there into bias_ws[2]): no per-step host argument, so
+ * the whole refine step replays as one CUDA graph. */
+int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, float* log_scales, float* logit_opacity,
+                     const float* grads, float* m, float* v, int32_t n, int32_t* t_dev, float* bias_ws,
+                     const double* lrs5, double beta1, double beta2, double eps, double log_scale_lo,
+                     double log_scale_hi, void* stream);
+
+/* history[*it_dev] = parts4 (the four mapping-loss parts of a step), *it_dev += 1. */
+int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream);
 
 /* ---- photometric registration (registration.py:170-384) -------------- */
 typedef struct {

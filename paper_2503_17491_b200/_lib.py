@@ -90,6 +90,10 @@ def lib() -> ctypes.CDLL:
     L.ss_fp32_peak_tflops.restype = ctypes.c_int
     L.ss_records_set_deterministic.argtypes = [vp, i32]
     L.ss_records_set_deterministic.restype = ctypes.c_int
+    L.ss_records_reserve.argtypes = [vp, i64]
+    L.ss_records_reserve.restype = ctypes.c_int
+    L.ss_records_sticky_overflow.argtypes = [vp, vp, vp]
+    L.ss_records_sticky_overflow.restype = ctypes.c_int
     L.ss_records_check.argtypes = [vp, ctypes.c_int]
     L.ss_records_check.restype = ctypes.c_int
     L.ss_records_work.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
@@ -108,6 +112,10 @@ def lib() -> ctypes.CDLL:
     L.ss_scale_loss.restype = ctypes.c_int
     L.ss_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, d, d, d, d, d, vp]
     L.ss_adam_step.restype = ctypes.c_int
+    L.ss_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, d, d, d, d, d, vp]
+    L.ss_adam_step_dev.restype = ctypes.c_int
+    L.ss_store_loss_parts.argtypes = [vp, vp, vp, i32, vp]
+    L.ss_store_loss_parts.restype = ctypes.c_int
     L.ss_range_image.argtypes = [ctypes.POINTER(SsCamera), vp, i32, vp, vp, vp]
     L.ss_range_image.restype = ctypes.c_int
     L.ss_smooth_range_image.argtypes = [i32, i32, i32, vp, vp, vp, vp]
@@ -146,7 +154,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",
             "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build",
             "ss_records_set_deterministic", "ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats",
-            "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact"]
+            "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact", "ss_adam_step_dev",
+            "ss_store_loss_parts", "ss_records_sticky_overflow", "ss_records_reserve"]
 
 
 def check(status: int, what: str = "") -> None:

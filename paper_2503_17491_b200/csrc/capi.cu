@@ -201,15 +201,19 @@ struct StageTimer {
   int stage;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
+  bool on = false;
   StageTimer(ss_records* r_, int st, cudaStream_t s_) : r(r_), stage(st), s(s_) {
-    if (r->profiling) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    on = r->profiling && cs == cudaStreamCaptureStatusNone;  // (no timing events inside a graph)
+    if (on) {
       a = r->take_event();
       b = r->take_event();
       cudaEventRecord(a, s);
     }
   }
   ~StageTimer() {
-    if (r->profiling) {
+    if (on) {
       cudaEventRecord(b, s);
       r->ev_used.push_back({stage, {a, b}});
     }
@@ -433,6 +437,23 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
 // never raised before completion) for its counters.  Returns SS_ERR_CAPACITY
 // when the speculative pair capacity was too small (the next forward on
 // these records will allocate enough; re-run it), or the device status.
+__global__ void k_sticky_or(const int* __restrict__ flag, int* __restrict__ sticky) {
+  if (*flag) *sticky = 1;
+}
+
+int ss_records_sticky_overflow(const ss_records* rec, int32_t* sticky, void* stream) {
+  if (!rec || !sticky || !rec->misc) return SS_ERR_INVALID_ARGUMENT;
+  k_sticky_or<<<1, 1, 0, (cudaStream_t)stream>>>(rec->misc + 1, sticky);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_records_reserve(ss_records* rec, int64_t n_pairs) {
+  if (!rec || n_pairs < 0) return SS_ERR_INVALID_ARGUMENT;
+  rec->want_pairs = std::max<long long>(rec->want_pairs, n_pairs);
+  return SS_OK;
+}
+
 int ss_records_set_deterministic(ss_records* rec, int32_t deterministic) {
   if (!rec) return SS_ERR_INVALID_ARGUMENT;
   rec->deterministic = deterministic ? 1 : 0;
@@ -1038,6 +1059,40 @@ int ss_scale_loss(const float* log_scales, int32_t n, double cap, double w_scale
   if (n == 0) return SS_OK;
   cudaStream_t s = (cudaStream_t)stream;
   k_scale_loss<<<(n + 255) / 256, 256, 0, s>>>(n, log_scales, cap, w_scale, d_scales_extra, loss_out);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, float* log_scales, float* logit_opacity,
+                     const float* grads, float* m, float* v, int32_t n, int32_t* t_dev, float* bias_ws,
+                     const double* lrs5, double beta1, double beta2, double eps, double log_scale_lo,
+                     double log_scale_hi, void* stream) {
+  if (n < 0 || !t_dev || !bias_ws || !lrs5) return SS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return SS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  AdamK a;
+  a.p[0] = centers;
+  a.p[1] = raw_t_alpha;
+  a.p[2] = raw_t_beta;
+  a.p[3] = log_scales;
+  a.p[4] = logit_opacity;
+  for (int q = 0; q < 5; ++q) a.lr[q] = (float)lrs5[q];
+  a.b1 = (float)beta1;
+  a.b2 = (float)beta2;
+  a.eps = (float)eps;
+  a.b1c = a.b2c = 1.f;
+  a.lo = (float)log_scale_lo;
+  a.hi = (float)log_scale_hi;
+  k_adam_tick<<<1, 1, 0, s>>>(t_dev, beta1, beta2, bias_ws);
+  const long long tot = 12LL * n;
+  k_adam_dev<<<(int)((tot + 255) / 256), 256, 0, s>>>(n, a, bias_ws, grads, m, v);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream) {
+  if (!parts4 || !history || !it_dev || cap < 0) return SS_ERR_INVALID_ARGUMENT;
+  k_store_parts<<<1, 1, 0, (cudaStream_t)stream>>>(parts4, history, it_dev, cap);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }

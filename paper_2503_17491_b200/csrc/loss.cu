@@ -129,4 +129,53 @@ __global__ void k_adam(int n, AdamK a, const float* __restrict__ g, float* __res
   *pp = x;
 }
 
+// Device-resident step counter for CUDA-graph replays of the refine step:
+// t += 1 and the bias corrections 1 - beta^t (what the host computes for ss_adam_step).
+__global__ void k_adam_tick(int* __restrict__ t_dev, double b1, double b2, float* __restrict__ bias) {
+  const int t = *t_dev + 1;
+  *t_dev = t;
+  bias[0] = (float)(1.0 - pow(b1, (double)t));
+  bias[1] = (float)(1.0 - pow(b2, (double)t));
+}
+
+__global__ void k_adam_dev(int n, AdamK a, const float* __restrict__ bias, const float* __restrict__ g,
+                           float* __restrict__ m, float* __restrict__ v) {
+  a.b1c = bias[0];
+  a.b2c = bias[1];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= 12 * n) return;
+  const int i = k / 12, c = k % 12;
+  int grp, off, w;
+  if (c < 3) {
+    grp = 0; off = c; w = 3;
+  } else if (c < 6) {
+    grp = 1; off = c - 3; w = 3;
+  } else if (c < 9) {
+    grp = 2; off = c - 6; w = 3;
+  } else if (c < 11) {
+    grp = 3; off = c - 9; w = 2;
+  } else {
+    grp = 4; off = 0; w = 1;
+  }
+  const float gk = g[k];
+  const float mk = a.b1 * m[k] + (1.f - a.b1) * gk;
+  const float vk = a.b2 * v[k] + (1.f - a.b2) * gk * gk;
+  m[k] = mk;
+  v[k] = vk;
+  const float upd = a.lr[grp] * (mk / a.b1c) / (sqrtf(vk / a.b2c) + a.eps);
+  float* pp = a.p[grp] + (size_t)i * w + off;
+  float x = *pp - upd;
+  if (grp == 3) x = fminf(fmaxf(x, a.lo), a.hi);
+  *pp = x;
+}
+
+// history[it] = the 4 loss parts of this step; it += 1 (graph-replayed refine).
+__global__ void k_store_parts(const double* __restrict__ parts, double* __restrict__ hist, int* __restrict__ it,
+                              int cap) {
+  const int i = *it;
+  if (i < cap)
+    for (int q = 0; q < 4; ++q) hist[4 * i + q] = parts[q];
+  *it = i + 1;
+}
+
 }  // namespace ss

@@ -239,13 +239,14 @@ class DeviceMap:
         return np.array([cfg.lr_centers * self.scene_scale, cfg.lr_tangents, cfg.lr_tangents, cfg.lr_log_scales,
                          cfg.lr_logit_opacity], dtype=np.float64)
 
-    def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None):
+    def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None,
+                     sync: bool = True):
         """Render keyframe ``kf_index``, mapping loss, backward: (n x 12 raw gradient, loss parts
         [range, opacity, normal, scale] float64) on the device."""
         raster = raster or RasterConfig()
         kf = self.keyframes[kf_index]
         sp = self.params
-        D, N, O = engine.forward(kf.camera, pose_rt(kf.pose), sp, raster, self.rec)
+        D, N, O = engine.forward(kf.camera, pose_rt(kf.pose), sp, raster, self.rec, sync=sync)
         dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf.range, kf.valid, kf.normal, kf.nvalid,
                                                 w_opacity=cfg.w_opacity, w_normal=cfg.w_normal,
                                                 range_floor=cfg.range_weight_floor)
@@ -273,15 +274,118 @@ class DeviceMap:
         self.apply_adam(g, cfg)
         return parts
 
-    def refine(self, cfg: MappingConfig, iters: int, rng, raster: RasterConfig | None = None) -> list:
-        """mapping.py:455-498 on the device; returns the per-iteration loss totals."""
+    def refine(self, cfg: MappingConfig, iters: int, rng, raster: RasterConfig | None = None,
+               graphs: bool = True) -> list:
+        """mapping.py:455-498 on the device; returns the per-iteration loss totals.
+
+        With ``graphs`` (default) each keyframe's whole step (render, loss,
+        backward, Adam) is captured once as a CUDA graph and replayed, so the
+        host only draws the keyframe index: the eager loop is host-bound
+        (~0.7 ms of Python and launches per iteration at config 2)."""
         if self.n == 0 or not self.keyframes:
             return []
+        if graphs:
+            out = self._refine_graphs(cfg, iters, rng, raster or RasterConfig())
+            if out is not None:
+                return out
         parts = []
         for _ in range(iters):
             idx = sample_keyframe_index(len(self.keyframes), cfg.kf_sample_p, rng)
             parts.append(self.step(idx, cfg, raster))
         P = torch.stack(parts).cpu().numpy()
+        w = np.array([1.0, cfg.w_opacity, cfg.w_normal, cfg.w_scale])
+        return [float(x) for x in P @ w]
+
+    # --- CUDA-graph refine -----------------------------------------------------------
+    _HIST = 4096
+
+    def _graph_key(self, cfg, raster):
+        return (self.n, len(self.keyframes), tuple(self.params[k].data_ptr() for k in engine.PARAM_NAMES),
+                self.m.data_ptr(), self.v.data_ptr(), tuple(sorted(vars(cfg).items())),
+                tuple(sorted(vars(raster).items())), self.scene_scale)
+
+    def _graph_step(self, kf_index, cfg, raster):
+        g, parts = self.raw_gradient(kf_index, cfg, raster, sync=False)
+        check(lib().ss_records_sticky_overflow(self.rec.ptr, ctypes.c_void_p(self._sticky.data_ptr()),
+                                               ctypes.c_void_p(engine.stream_ptr())), "overflow flag")
+        lrs = self.lrs(cfg)
+        check(lib().ss_adam_step_dev(*(ctypes.c_void_p(self.params[k].data_ptr()) for k in engine.PARAM_NAMES),
+                                     ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
+                                     ctypes.c_void_p(self.v.data_ptr()), self.n, ctypes.c_void_p(self._t_dev.data_ptr()),
+                                     ctypes.c_void_p(self._bias.data_ptr()), lrs.ctypes.data_as(ctypes.c_void_p), 0.9,
+                                     0.999, 1e-8, float(np.log(cfg.scale_floor)),
+                                     float(np.log(10.0 * cfg.scale_cap)), ctypes.c_void_p(engine.stream_ptr())),
+              "adam_step")
+        check(lib().ss_store_loss_parts(ctypes.c_void_p(parts.data_ptr()), ctypes.c_void_p(self._hist.data_ptr()),
+                                        ctypes.c_void_p(self._it.data_ptr()), self._HIST,
+                                        ctypes.c_void_p(engine.stream_ptr())), "loss history")
+
+    def capture_graphs(self, cfg: MappingConfig, raster: RasterConfig | None = None) -> None:
+        """Capture the refine step of every keyframe as a CUDA graph now (capture runs nothing:
+        no side effect on the map), so that refine() replays only."""
+        raster = raster or RasterConfig()
+        self._prepare_graphs(cfg, raster)
+        for idx in range(len(self.keyframes)):
+            self._graph_for(idx, cfg, raster)
+
+    def _graph_for(self, idx, cfg, raster):
+        gr = self._graphs.get(idx)
+        if gr is None:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(gr, stream=side):
+                    self._graph_step(idx, cfg, raster)
+            torch.cuda.current_stream().wait_stream(side)
+            self._graphs[idx] = gr
+        return gr
+
+    def _prepare_graphs(self, cfg, raster):
+        dev = self.m.device
+        key = self._graph_key(cfg, raster)
+        if getattr(self, "_gkey", None) != key:
+            # size the shared records for every keyframe (2x headroom: the step moves the splats)
+            most = 0
+            for kf in self.keyframes:
+                engine.forward(kf.camera, pose_rt(kf.pose), self.params, raster, self.rec)
+                most = max(most, self.rec.counts()[0])
+            lib().ss_records_reserve(self.rec.ptr, 2 * most + 65536)
+            # allocate at that size, backward buffers included (nothing may be allocated under capture)
+            self.raw_gradient(len(self.keyframes) - 1, cfg, raster)
+            self._graphs = {}
+            self._gkey = key
+            self._t_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._bias = torch.ones(2, dtype=torch.float32, device=dev)
+            self._it = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._sticky = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._hist = torch.zeros((self._HIST, 4), dtype=torch.float64, device=dev)
+
+    def _refine_graphs(self, cfg, iters, rng, raster):
+        """Graph-replayed refine; None when it cannot be used (the eager loop runs instead)."""
+        if iters > self._HIST or bool(getattr(raster, "deterministic", False)):
+            return None
+        self._prepare_graphs(cfg, raster)
+        snapshot = ({k: v.clone() for k, v in self.params.items()}, self.m.clone(), self.v.clone(), self.t,
+                    rng.bit_generator.state)
+        self._t_dev.fill_(self.t)
+        self._it.zero_()
+        self._sticky.zero_()
+        for _ in range(iters):
+            idx = sample_keyframe_index(len(self.keyframes), cfg.kf_sample_p, rng)
+            self._graph_for(idx, cfg, raster).replay()
+        if int(self._sticky.item()):  # a replay overflowed its pair capacity: redo eagerly
+            params, m, v, t, state = snapshot
+            for k in engine.PARAM_NAMES:
+                self.params[k].copy_(params[k])
+            self.m.copy_(m)
+            self.v.copy_(v)
+            self.t = t
+            rng.bit_generator.state = state
+            self._gkey = None
+            return None
+        self.t = int(self._t_dev.item())
+        P = self._hist[:iters].cpu().numpy()
         w = np.array([1.0, cfg.w_opacity, cfg.w_normal, cfg.w_scale])
         return [float(x) for x in P @ w]
 
