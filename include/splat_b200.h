@@ -279,7 +279,8 @@ typedef struct {
 /* The whole Gauss-Newton / Levenberg loop of register() (registration.py:
  * 437-524) on the device, one cooperative kernel, every mode: per
  * evaluation the geometric system (k nearest usable leaves within
- * assoc_gate, closest plane, median trim; registration.py:231-274) and / or
+ * assoc_gate -- found through a hash grid of gate-sized cells built on the
+ * stream first --, closest plane, median trim; registration.py:231-274) and / or
  * the photometric one (_photo_system, :316-362), Huber-weighted 6x6 normal
  * equations, the damped solve, T <- T exp(delta), acceptance with the
  * reference's positional pairing of residual families and frozen terms
@@ -291,8 +292,8 @@ typedef struct {
  * info6 = {iterations, converged, n_geo, n_photo, evaluations, status},
  * r2_out2 = sum r^2 of the last geometric / photometric systems.
  * SS_ERR_REGISTRATION when fewer than min_residuals residuals survive.
- * workspace: ss_reg_solve_workspace_bytes(n_geo_scan, M).  Synchronises. */
-size_t ss_reg_solve_workspace_bytes(int32_t n_geo_scan, int32_t M);
+ * workspace: ss_reg_solve_workspace_bytes(n_leaves, n_geo_scan, M).  Synchronises. */
+size_t ss_reg_solve_workspace_bytes(int32_t n_leaves, int32_t n_geo_scan, int32_t M);
 int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
                  int32_t n_geo_scan, const double* X_w, int32_t M, const double* scan_range,
                  const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,

@@ -92,7 +92,7 @@ def geo_system(tree: Tree, scan, R, t, trim_floor, k=3, gate=1.0, trim_factor=5.
 
 def register(mode, tree: Tree, geo_scan, X, rimg, valid, cam, R0, t0, max_iters=30, tol=1e-6, huber_geo=0.1,
              huber_photo=0.2, floor_geo=0.02, floor_photo=0.02, gate=1.0, damping_init=1e-6, damping_max=1e6,
-             min_residuals=10):
+             min_residuals=10, k=3):
     """register()'s loop for every mode.  Returns (R, t, iters, converged, geo_rms, photo_rms, n_geo, n_photo)."""
     phases = [("geometric", max_iters // 2), ("joint", max_iters)] if mode == "sequential" else [(mode, max_iters)]
     R, t = np.array(R0, float), np.array(t0, float)
@@ -111,7 +111,7 @@ def register(mode, tree: Tree, geo_scan, X, rimg, valid, cam, R0, t0, max_iters=
             for fam, use in (("geo", use_geo), ("photo", use_photo)):
                 sysr = None
                 if use:
-                    sysr = geo_system(tree, geo_scan, R, t, fg) if fam == "geo" else \
+                    sysr = geo_system(tree, geo_scan, R, t, fg, k=k, gate=gate) if fam == "geo" else \
                         RO.photo_system(X, rimg, valid, cam, R, t, fp)
                 if sysr is not None:
                     r, J = sysr
@@ -140,7 +140,7 @@ def register(mode, tree: Tree, geo_scan, X, rimg, valid, cam, R0, t0, max_iters=
                 Rt, tt = R @ dR, R @ dt + t
                 trial = []
                 if use_geo:
-                    g2 = geo_system(tree, geo_scan, Rt, tt, fg)
+                    g2 = geo_system(tree, geo_scan, Rt, tt, fg, k=k, gate=gate)
                     if g2 is not None:
                         trial.append(g2[0])
                 if use_photo:

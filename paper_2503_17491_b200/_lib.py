@@ -135,7 +135,7 @@ def lib() -> ctypes.CDLL:
     L.ss_prune_compact.argtypes = [i32, i32, vp, vp, vp, vp]
     for name in ("ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats", "ss_prune_flags", "ss_prune_compact"):
         getattr(L, name).restype = ctypes.c_int
-    L.ss_reg_solve_workspace_bytes.argtypes = [i32, i32]
+    L.ss_reg_solve_workspace_bytes.argtypes = [i32, i32, i32]
     L.ss_reg_solve_workspace_bytes.restype = ctypes.c_size_t
     L.ss_reg_solve.argtypes = [vp, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp,
                                ctypes.POINTER(SsRegSolveCfg), vp, vp, vp, vp, vp]

@@ -772,10 +772,12 @@ int ss_photo_system(const double* X_w, int32_t M, const double* scan_range, cons
   return SS_OK;
 }
 
-size_t ss_reg_solve_workspace_bytes(int32_t n_geo_scan, int32_t M) {
+size_t ss_reg_solve_workspace_bytes(int32_t n_leaves, int32_t n_geo_scan, int32_t M) {
   const size_t g = (size_t)(n_geo_scan > 0 ? n_geo_scan : 1), m = (size_t)(M > 0 ? M : 1);
+  const size_t l = (size_t)(n_leaves > 0 ? n_leaves : 1);
   return g * (sizeof(GeoTmp) + 8) + m * (sizeof(PhotoTmp) + 8) + (size_t)4 * kRsPasses * kRsBins * 4 +
-         (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + sizeof(RegSolveState) + 1024;
+         (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + sizeof(RegSolveState) + (kRsGridBuckets + 1) * 4 +
+         l * (sizeof(RsLeafEntry) + 4) + 1024;
 }
 
 int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
@@ -793,8 +795,28 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   int st = make_regcam(cam, rc);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  // leaf grid buckets: a power of two >= 2 n_leaves in [64, kRsGridBuckets]; staged in
+  // shared memory when it fits beside the kernel's static shared memory
+  const int nl = need_geo ? n_leaves : 0;
+  int nbk = 64;
+  while (nbk < kRsGridBuckets && nbk < 2 * nl) nbk *= 2;
+  const int gmask = nbk - 1;
+  const size_t gsmem = rs_grid_smem_bytes(nl, gmask);
+  const bool staged = nl > 0 && gsmem <= (size_t)96 * 1024;
+  // then the |r| patterns of the larger family, for the per-block median select
+  int dev = 0, optin = 0;
+  SS_CUDA_TRY(cudaGetDevice(&dev));
+  SS_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa{};
+  SS_CUDA_TRY(cudaFuncGetAttributes(&fa, k_reg_solve));
+  const size_t budget = (size_t)std::max(0, optin - (int)fa.sharedSizeBytes - 1024);
+  const size_t sel_off = staged ? (gsmem + 15) / 16 * 16 : 0;
+  const int nfam = std::max(need_geo ? n_geo_scan : 0, need_photo ? M : 0);
+  const bool sel_fits = sel_off + (size_t)nfam * 8 <= budget;
+  const size_t dyn = sel_fits ? sel_off + (size_t)nfam * 8 : (staged ? gsmem : 0);
+  if (dyn > 0) SS_CUDA_TRY(cudaFuncSetAttribute(k_reg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int occ = 0;
-  SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, 0));
+  SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, dyn));
   if (occ < 1) return SS_ERR_CUDA;
   const int G = std::min(num_sms(), 1024);
   const int ng = need_geo ? n_geo_scan : 0, m = need_photo ? M : 0;
@@ -813,6 +835,14 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   double* part = (double*)take((size_t)1024 * 2 * kRsAcc * 8);
   int* pcnt = (int*)take(1024 * 4);
   RegSolveState* state = (RegSolveState*)take(sizeof(RegSolveState));
+  int* bstart = (int*)take((size_t)(kRsGridBuckets + 1) * 4);
+  RsLeafEntry* ent = (RsLeafEntry*)take((size_t)std::max(nl, 1) * sizeof(RsLeafEntry));
+  int* lbucket = (int*)take((size_t)std::max(nl, 1) * 4);
+  const double inv_cs = rs_inv_cell(cfg->assoc_gate);
+  if (nl > 0) {
+    k_leaf_grid<<<1, 1024, 0, s>>>(leaf_centroids, nl, inv_cs, gmask, bstart, ent, lbucket);
+    SS_CUDA_TRY(cudaGetLastError());
+  }
   // the first evaluation's histograms start zeroed; later evaluations zero the next set themselves
   SS_CUDA_TRY(cudaMemsetAsync(hist, 0, (size_t)4 * kRsPasses * kRsBins * 4, s));
   RegSolveState init{};
@@ -833,11 +863,13 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   k.min_residuals = cfg->min_residuals;
   k.assoc_k = cfg->assoc_k;
   k.mode = cfg->mode;
-  RsGeo geo{leaf_centroids, leaf_normals, need_geo ? n_leaves : 0, geo_scan, ng};
+  k.sel_off = (int)sel_off;
+  k.sel_cap = sel_fits ? nfam : -1;
+  RsGeo geo{leaf_centroids, leaf_normals, nl, geo_scan, ng, bstart, ent, inv_cs, gmask, staged ? 1 : 0};
   RsPhoto ph{X_w, m, scan_range, scan_valid};
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
                   (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&state};
-  SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, 0, s));
+  SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, dyn, s));
   RegSolveState out{};
   SS_CUDA_TRY(cudaMemcpyAsync(&out, state, sizeof(out), cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaStreamSynchronize(s));

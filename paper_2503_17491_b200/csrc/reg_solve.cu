@@ -36,6 +36,7 @@ struct RegSolveCfg {
   double huber_photo, huber_geo, trim_factor, spread_gate, assoc_gate, floor_photo, floor_geo, tol, damping_init,
       damping_max;
   int max_iters, min_residuals, assoc_k, mode;
+  int sel_off, sel_cap;  // families with n <= sel_cap select their median per block, |r| staged at dyn smem + sel_off
 };
 
 constexpr int kRsThreads = 256;
@@ -44,7 +45,29 @@ constexpr int kRsPasses = 6;   // bits 63-52, 51-40, 39-28, 27-16, 15-4, 3-0
 constexpr int kRsCand = 256;   // a selected bin this small is finished by an exact in-block rank
 constexpr int kRsAcc = 32;     // per family: [0:21] H upper, [21:27] b, [27] Huber(huber_geo),
                                // [28] m, [29] sum r^2, [30] Huber(huber_photo)
-constexpr int kRsLeafChunk = 256;
+
+// -DSS_RS_PROF: block 0 / thread 0 accumulates %globaltimer deltas between
+// marks and prints them when the loop ends (tools/reg_stages.sh).
+#ifdef SS_RS_PROF
+#define RS_MARK(k)                                                                   \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                                         \
+    unsigned long long t_;                                                           \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+    rs_prof[k] += t_ - rs_last;                                                      \
+    rs_last = t_;                                                                    \
+  }
+__device__ unsigned long long g_rs_sub[8], g_rs_sub_last;
+#define RS_SUB(k)                                                                    \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                                         \
+    unsigned long long t_;                                                           \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+    if (k >= 0) g_rs_sub[k < 0 ? 0 : k] += t_ - g_rs_sub_last;                       \
+    g_rs_sub_last = t_;                                                              \
+  }
+#else
+#define RS_MARK(k)
+#define RS_SUB(k)
+#endif
 
 enum { RS_EVAL = 0, RS_DONE = 1 };
 
@@ -151,6 +174,24 @@ __device__ bool solve6(double* A, double* y) {
     y[k] = s / A[6 * k + k];
   }
   return true;
+}
+
+// Insert (d, id) into a k-best list sorted by (d, id), dropping the last slot.
+// Fully unrolled so the list stays in registers.
+template <int K>
+__device__ __forceinline__ void rs_kbest_insert(double (&kd)[K], int (&ki)[K], double d, int id) {
+#pragma unroll
+  for (int a = K - 1; a >= 0; --a) {
+    const bool before_a = d < kd[a] || (d == kd[a] && id < ki[a]);
+    if (a > 0) {
+      const bool before_prev = d < kd[a - 1] || (d == kd[a - 1] && id < ki[a - 1]);
+      kd[a] = before_prev ? kd[a - 1] : (before_a ? d : kd[a]);
+      ki[a] = before_prev ? ki[a - 1] : (before_a ? id : ki[a]);
+    } else {
+      kd[0] = before_a ? d : kd[0];
+      ki[0] = before_a ? id : ki[0];
+    }
+  }
 }
 
 __device__ int rs_phase_mode(const RegSolveCfg& cfg, int phase) {
@@ -292,6 +333,18 @@ __device__ void rs_step(RegSolveState* st, const RegSolveCfg& cfg, const double*
   rs_try(st, cfg);
 }
 
+// One radix-select histogram step for a warp: pattern b (~0 = invalid) counts in
+// its digit's bin when it matches the prefix.  Lanes sharing a bin add once
+// (the top digits cluster: |r| share few exponents).  Returns whether b counted.
+__device__ __forceinline__ int rs_hist_add(unsigned long long b, unsigned long long prefix, unsigned long long mask,
+                                           int shift, unsigned dmask, unsigned* sh, int lane) {
+  const bool in = b != ~0ull && (b & mask) == prefix;
+  const unsigned d = in ? (unsigned)(b >> shift) & dmask : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, d);
+  if (in && lane == __ffs(peers) - 1) atomicAdd(&sh[d], (unsigned)__popc(peers));
+  return in;
+}
+
 // Block-wide: find the bin of hist[0, nbins) holding rank kk; returns (bin, count before it).
 __device__ void rs_find_bin(const unsigned* __restrict__ hist, int nbins, int kk, int* s_bin, int* s_before,
                             unsigned* s_part) {
@@ -355,10 +408,8 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
     const unsigned dmask = (1u << nb) - 1u;
     for (int j = tid; j < kRsBins; j += kRsThreads) sh[j] = 0u;
     __syncthreads();
-    for (int i = gtid; i < n; i += nthr) {
-      const unsigned long long b = bits[i];
-      if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> shift) & dmask], 1u);
-    }
+    for (int i0 = gtid - lane; i0 < n; i0 += nthr)  // warp-uniform trip count
+      rs_hist_add(i0 + lane < n ? bits[i0 + lane] : ~0ull, prefix, mask, shift, dmask, sh, lane);
     __syncthreads();
     unsigned* Hp = Hc + p * kRsBins;
     for (int j = tid; j <= (int)dmask; j += kRsThreads)
@@ -427,6 +478,130 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
   return (v1 + __longlong_as_double((long long)*((volatile unsigned long long*)vmin))) / 2.0;
 }
 
+// Exact median of the valid patterns in sv[0, n) (shared memory), one block, no
+// grid barrier.  A first sweep finds the count and the smallest / largest
+// pattern; the radix passes then start at the highest bit in which those two
+// differ (12-bit digits downwards), so the first histogram already splits the
+// occupied range instead of the mostly shared exponent bits.  *s_m gets the
+// number of valid entries (the median is 0 when there are none).
+__device__ double rs_median_block(const unsigned long long* sv, int n, unsigned* sh, unsigned* s_part, int* s_bin,
+                                  int* s_before, unsigned long long* s_min, int* s_m) {
+  __shared__ int s_ng;
+  __shared__ unsigned long long s_max[kRsThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  RS_SUB(-1);
+  int cnt = 0;
+  unsigned long long mn = ~0ull, mx = 0ull;
+  for (int i = tid; i < n; i += kRsThreads) {
+    const unsigned long long b = sv[i];
+    if (b != ~0ull) {
+      ++cnt;
+      mn = min(mn, b);
+      mx = max(mx, b);
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  }
+  if (lane == 0) {
+    s_part[warp] = (unsigned)cnt;
+    s_min[warp] = mn;
+    s_max[warp] = mx;
+  }
+  __syncthreads();
+  int m = 0;
+  for (int w = 0; w < kRsThreads / 32; ++w) {
+    m += (int)s_part[w];
+    mn = min(mn, s_min[w]);
+    mx = max(mx, s_max[w]);
+  }
+  *s_m = m;  // (every thread writes the same value)
+  __syncthreads();
+  RS_SUB(0);
+  if (m == 0) return 0.0;
+  if (mn == mx) return __longlong_as_double((long long)mn);  // all equal
+  const int k1 = (m % 2 == 0) ? m / 2 - 1 : m / 2;
+  int kk = k1, cnt_eq = 0, top = 63 - __clzll(mn ^ mx);  // <= 62: valid patterns are non-negative doubles
+  unsigned long long mask = ~((2ull << top) - 1ull), prefix = mn & mask;
+  bool exact = false;
+  unsigned long long v2c = ~0ull;
+  for (;;) {
+    const int lo = max(top - 11, 0);
+    const unsigned dmask = (1u << (top - lo + 1)) - 1u;
+    for (int j = tid; j <= (int)dmask; j += kRsThreads) sh[j] = 0u;
+    __syncthreads();
+    for (int i = tid; i < n; i += kRsThreads) {
+      const unsigned long long b = sv[i];
+      if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
+    }
+    __syncthreads();
+    RS_SUB(1);
+    rs_find_bin(sh, (int)dmask + 1, kk, s_bin, s_before, s_part);
+    RS_SUB(2);
+    const int bin = *s_bin;
+    kk -= *s_before;
+    const int cnt_bin = (int)sh[bin];
+    prefix |= (unsigned long long)bin << lo;
+    mask |= (unsigned long long)dmask << lo;
+    __syncthreads();
+    if (lo == 0) {
+      cnt_eq = cnt_bin;
+      exact = true;
+      break;
+    }
+    top = lo - 1;
+    if (cnt_bin <= kRsCand) {
+      // few values share the prefix: gather and rank them exactly
+      unsigned long long* sc = reinterpret_cast<unsigned long long*>(sh);  // kRsCand x 8 B fits
+      if (tid == 0) s_ng = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += kRsThreads) {
+        const unsigned long long b = sv[i];
+        if (b != ~0ull && (b & mask) == prefix) sc[atomicAdd(&s_ng, 1)] = b;
+      }
+      __syncthreads();
+      RS_SUB(3);
+      for (int j = tid; j < cnt_bin; j += kRsThreads) {
+        const unsigned long long c = sc[j];
+        int lt = 0, eqb = 0;
+        for (int q = 0; q < cnt_bin; ++q) {
+          lt += sc[q] < c;
+          eqb += (sc[q] == c) & (q < j);
+        }
+        const int rank = lt + eqb;  // distinct ranks 0..cnt_bin-1
+        if (rank == kk) sh[2 * kRsCand] = (unsigned)j;
+        if (rank == kk + 1) sh[2 * kRsCand + 1] = (unsigned)j;
+      }
+      if (tid == 0 && kk + 1 >= cnt_bin) sh[2 * kRsCand + 1] = 0xffffffffu;
+      __syncthreads();
+      prefix = sc[sh[2 * kRsCand]];
+      const unsigned j2 = sh[2 * kRsCand + 1];
+      v2c = j2 == 0xffffffffu ? ~0ull : sc[j2];
+      __syncthreads();
+      RS_SUB(4);
+      break;
+    }
+  }
+  const double v1 = __longlong_as_double((long long)prefix);
+  if (m % 2 != 0) return v1;
+  if (!exact && v2c != ~0ull) return (v1 + __longlong_as_double((long long)v2c)) / 2.0;
+  if (exact && k1 + 1 < (k1 - kk) + cnt_eq) return v1;
+  RS_SUB(5);
+  unsigned long long nx = ~0ull;
+  for (int i = tid; i < n; i += kRsThreads) {
+    const unsigned long long b = sv[i];
+    if (b != ~0ull && b > prefix) nx = min(nx, b);
+  }
+  for (int off = 16; off > 0; off >>= 1) nx = min(nx, __shfl_xor_sync(0xffffffffu, nx, off));
+  if (lane == 0) s_min[warp] = nx;
+  __syncthreads();
+  for (int w = 0; w < kRsThreads / 32; ++w) nx = min(nx, s_min[w]);
+  __syncthreads();
+  return (v1 + __longlong_as_double((long long)nx)) / 2.0;
+}
+
 // Block count of valid entries -> grid total (pcnt: per-block slots).
 __device__ int rs_count(cg::grid_group& grid, int okc, int* __restrict__ pcnt, unsigned* s_part, int* s_m) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -449,13 +624,167 @@ __device__ int rs_count(cg::grid_group& grid, int okc, int* __restrict__ pcnt, u
   return *s_m;
 }
 
+// Leaf hash grid for the association: cells of edge >= assoc_gate, so every
+// leaf within the gate of a point lies in the point's 27-cell neighbourhood
+// (and the k nearest within the gate -- the only ones the residual uses -- are
+// exactly the k nearest among those).  Cells hash into kRsGridBuckets buckets;
+// a bucket's entries carry their cell key so each leaf is seen once.
+constexpr int kRsGridBuckets = 4096;
+constexpr int kRsCellBias = 1 << 20;  // cell coordinates clamped to [-2^20, 2^20)
+
+struct RsLeafEntry {
+  double c[3];
+  unsigned long long key;
+  int id, pad;
+};
+
+__device__ __forceinline__ int rs_cell(double x, double inv_cs) {
+  const double f = floor(x * inv_cs);
+  return (int)fmin(fmax(f, -(double)kRsCellBias), (double)(kRsCellBias - 1));  // NaN -> lower bound
+}
+__device__ __forceinline__ unsigned long long rs_cell_key(int ix, int iy, int iz) {
+  return ((unsigned long long)(ix + kRsCellBias) << 42) | ((unsigned long long)(iy + kRsCellBias) << 21) |
+         (unsigned long long)(iz + kRsCellBias);
+}
+__device__ __forceinline__ int rs_bucket(unsigned long long k, int mask) {
+  k ^= k >> 31;
+  k *= 0x7fb5d329728ea185ull;
+  k ^= k >> 27;
+  k *= 0x81dadef4bc2dd44dull;
+  k ^= k >> 33;
+  return (int)k & mask;
+}
+// 1 / cell edge; 0 (one cell) when the gate is not a positive finite number
+__host__ __device__ inline double rs_inv_cell(double gate) {
+  const double g = gate < 0 ? -gate : gate;
+  return (g > 0 && g < 1e300) ? 1.0 / (g * (1.0 + 1e-9)) : 0.0;
+}
+
+// One block: counting sort of the leaves into mask + 1 (<= kRsGridBuckets) hash buckets.
+__global__ void __launch_bounds__(1024) k_leaf_grid(const double* __restrict__ cent, int nl, double inv_cs, int mask,
+                                                    int* __restrict__ bstart, RsLeafEntry* __restrict__ ent,
+                                                    int* __restrict__ lbucket) {
+  __shared__ int cnt[kRsGridBuckets];
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x;
+  for (int b = tid; b < kRsGridBuckets; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  for (int l = tid; l < nl; l += blockDim.x) {
+    const int b = rs_bucket(rs_cell_key(rs_cell(cent[3 * l], inv_cs), rs_cell(cent[3 * l + 1], inv_cs),
+                                        rs_cell(cent[3 * l + 2], inv_cs)), mask);
+    lbucket[l] = b;
+    atomicAdd(&cnt[b], 1);
+  }
+  __syncthreads();
+  // exclusive scan, 4 buckets per thread (blockDim.x == 1024)
+  int v[4], run = 0;
+  for (int q = 0; q < 4; ++q) {
+    v[q] = run;
+    run += cnt[4 * tid + q];
+  }
+  int incl = run;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, off);
+    if ((tid & 31) >= off) incl += t;
+  }
+  if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = wsum[tid], wi = w;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, off);
+      if (tid >= off) wi += t;
+    }
+    wsum[tid] = wi - w;
+  }
+  __syncthreads();
+  const int base = wsum[tid >> 5] + incl - run;
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    bstart[4 * tid + q] = base + v[q];
+    cnt[4 * tid + q] = base + v[q];  // fill cursor
+  }
+  if (tid == 0) bstart[kRsGridBuckets] = nl;
+  __syncthreads();
+  for (int l = tid; l < nl; l += blockDim.x) {
+    const int pos = atomicAdd(&cnt[lbucket[l]], 1);  // order inside a bucket is irrelevant
+    RsLeafEntry e;
+    for (int c = 0; c < 3; ++c) e.c[c] = cent[3 * l + c];
+    e.key = rs_cell_key(rs_cell(e.c[0], inv_cs), rs_cell(e.c[1], inv_cs), rs_cell(e.c[2], inv_cs));
+    e.id = l;
+    e.pad = 0;
+    ent[pos] = e;
+  }
+}
+
 struct RsGeo {  // geometric inputs: usable leaves and the (subsampled) scan, sensor frame
   const double* cent;
   const double* nrm;
   int n_leaves;
   const double* scan;
   int n_scan;
+  const int* bstart;  // leaf hash grid (k_leaf_grid): mask + 1 buckets
+  const RsLeafEntry* ent;
+  double inv_cs;
+  int mask;
+  int staged;  // the grid fits the dynamic shared memory: copied there once per launch
 };
+
+__host__ __device__ inline size_t rs_grid_smem_bytes(int nl, int mask) {
+  return ((size_t)(mask + 2) * 4 + 15) / 16 * 16 + (size_t)nl * sizeof(RsLeafEntry);
+}
+
+// k nearest leaves (sorted by (d2, leaf index)) of p among the leaves of its
+// 27-cell neighbourhood; S consecutive lanes share p, each visiting every S-th
+// cell, and merge their lists by butterfly shuffles (all lanes of the warp call
+// this).  Results land in kd/ki[0, K), +inf beyond.
+template <int K>
+__device__ __forceinline__ void rs_knn(const double* p, bool active, int sub, int S, const int* bst,
+                                       const RsLeafEntry* ent, int mask, double inv_cs, double (&kd8)[8],
+                                       int (&ki8)[8]) {
+  double kd[K];
+  int ki[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    kd[a] = __longlong_as_double(0x7ff0000000000000LL);
+    ki[a] = 0x7fffffff;
+  }
+  if (active) {
+    const int cx = rs_cell(p[0], inv_cs), cy = rs_cell(p[1], inv_cs), cz = rs_cell(p[2], inv_cs);
+    for (int nb = sub; nb < 27; nb += S) {
+      const int ix = cx + nb / 9 - 1, iy = cy + (nb / 3) % 3 - 1, iz = cz + nb % 3 - 1;
+      if (ix < -kRsCellBias || ix >= kRsCellBias || iy < -kRsCellBias || iy >= kRsCellBias || iz < -kRsCellBias ||
+          iz >= kRsCellBias)
+        continue;
+      const unsigned long long key = rs_cell_key(ix, iy, iz);
+      const int b = rs_bucket(key, mask);
+      const int e1 = bst[b + 1];
+      for (int e = bst[b]; e < e1; ++e) {
+        const RsLeafEntry& le = ent[e];
+        if (le.key != key) continue;
+        const double dx = p[0] - le.c[0], dy = p[1] - le.c[1], dz = p[2] - le.c[2];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 <= kd[K - 1]) rs_kbest_insert<K>(kd, ki, d2, le.id);  // a tie may still win on the index
+      }
+    }
+  }
+  for (int off = 1; off < S; off <<= 1) {
+    double od[K];
+    int oi[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      od[a] = __shfl_xor_sync(0xffffffffu, kd[a], off);
+      oi[a] = __shfl_xor_sync(0xffffffffu, ki[a], off);
+    }
+#pragma unroll
+    for (int a = 0; a < K; ++a) rs_kbest_insert<K>(kd, ki, od[a], oi[a]);
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    kd8[a] = a < K ? kd[a] : __longlong_as_double(0x7ff0000000000000LL);
+    ki8[a] = a < K ? ki[a] : 0x7fffffff;
+  }
+}
 struct RsPhoto {  // photometric inputs: world anchors and the scan range image
   const double* X;
   int M;
@@ -470,16 +799,30 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
                                                          unsigned* __restrict__ hist, double* __restrict__ part,
                                                          int* __restrict__ pcnt, RegSolveState* st) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned sh[kRsBins];
+  __shared__ __align__(16) unsigned sh[kRsBins];
   __shared__ double sred[kRsThreads / 32][kRsAcc];
   __shared__ double sfin[2 * kRsAcc];
-  __shared__ double s_lc[3 * kRsLeafChunk], s_ln[3 * kRsLeafChunk];
   __shared__ unsigned s_part[kRsThreads / 32];
   __shared__ int s_bin, s_before, s_m;
   __shared__ unsigned long long s_min[kRsThreads / 32];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = G * kRsThreads;
   const int kmax = min(min(cfg.assoc_k, geo.n_leaves), 8);
+  // the leaf grid is constant for the launch: stage it in shared memory when it fits
+  extern __shared__ __align__(16) unsigned char rs_dyn[];
+  const int* s_bst = geo.bstart;
+  const RsLeafEntry* s_ent = geo.ent;
+  if (geo.staged) {
+    int* b = reinterpret_cast<int*>(rs_dyn);
+    RsLeafEntry* en = reinterpret_cast<RsLeafEntry*>(rs_dyn + ((size_t)(geo.mask + 2) * 4 + 15) / 16 * 16);
+    for (int q = threadIdx.x; q <= geo.mask + 1; q += kRsThreads) b[q] = geo.bstart[q];
+    const double* src = reinterpret_cast<const double*>(geo.ent);
+    double* dst = reinterpret_cast<double*>(en);
+    for (int q = threadIdx.x; q < geo.n_leaves * (int)(sizeof(RsLeafEntry) / 8); q += kRsThreads) dst[q] = src[q];
+    s_bst = b;
+    s_ent = en;
+    __syncthreads();
+  }
   if (blockIdx.x == 0 && tid == 0) {
     st->it_total = 0;
     st->status = 0;
@@ -493,10 +836,26 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
       }
     rs_begin_phase(st, cfg, 0);
   }
+#ifdef SS_RS_PROF
+  unsigned long long rs_prof[10] = {}, rs_last = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(rs_last));
+#endif
   for (int e = 0;; ++e) {
     grid.sync();
+    RS_MARK(0);
     volatile RegSolveState* vs = st;
-    if (vs->action == RS_DONE) break;
+    if (vs->action == RS_DONE) {
+#ifdef SS_RS_PROF
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("RSPROF evals %d step+sync %llu resid %llu count %llu median %llu accum %llu part %llu sync %llu final %llu"
+               " | sel zero %llu hist %llu find %llu gather %llu rank %llu\n",
+               e, rs_prof[0], rs_prof[1], rs_prof[2], rs_prof[3], rs_prof[4], rs_prof[5], rs_prof[6], rs_prof[7],
+               g_rs_sub[0], g_rs_sub[1], g_rs_sub[2], g_rs_sub[3], g_rs_sub[4]);
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q = 0; q < 8; ++q) g_rs_sub[q] = 0;
+#endif
+      break;
+    }
     PoseK P;
     for (int q = 0; q < 9; ++q) P.R[q] = vs->P[q];
     for (int q = 0; q < 3; ++q) P.t[q] = vs->P[9 + q];
@@ -512,13 +871,11 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         st->vmin[par ^ 1][f] = ~0ull;
         st->ncand[par ^ 1][f] = 0;
       }
-    double acc[2][kRsAcc];
-#pragma unroll
-    for (int f = 0; f < 2; ++f)
-#pragma unroll
-      for (int q = 0; q < kRsAcc; ++q) acc[f][q] = 0.0;
     for (int f = 0; f < 2; ++f) {
       if (!fam_on[f]) continue;  // uniform across the grid
+      double acc[kRsAcc];
+#pragma unroll
+      for (int q = 0; q < kRsAcc; ++q) acc[q] = 0.0;
       unsigned* Hc = hist + ((size_t)par * 2 + f) * kRsPasses * kRsBins;
       unsigned long long* bits = f == 0 ? gbits : pbits;
       const int n = f == 0 ? geo.n_scan : ph.M;
@@ -527,7 +884,14 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
       if (f == 0) {
         // k nearest usable leaf centroids within the gate, then the leaf whose plane
         // is closest (registration.py:249-265); leaves staged through shared memory
-        const int i = gtid;  // one scan point per thread (n_scan <= grid threads, checked by the host)
+        // S consecutive lanes share one scan point (n_scan <= grid threads, checked by
+        // the host), each visiting every S-th cell of the point's 27-cell
+        // neighbourhood in the leaf grid; their sorted k-best lists merge by
+        // butterfly shuffles.  The lists live in registers (static indexing) and
+        // order by (d2, leaf index), so the result does not depend on visit order.
+        int S = 1;
+        while (S < 32 && 2 * S * n <= nthr) S *= 2;
+        const int i = gtid / S, sub = gtid & (S - 1);
         double p[3] = {0, 0, 0}, q3[3] = {0, 0, 0};
         if (i < n) {
           for (int c = 0; c < 3; ++c) q3[c] = geo.scan[3 * i + c];
@@ -536,42 +900,31 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         }
         double kd[8];
         int ki[8];
-        for (int a = 0; a < 8; ++a) {
-          kd[a] = __longlong_as_double(0x7ff0000000000000LL);
-          ki[a] = -1;
-        }
-        for (int c0 = 0; c0 < geo.n_leaves; c0 += kRsLeafChunk) {
-          const int cn = min(kRsLeafChunk, geo.n_leaves - c0);
-          __syncthreads();
-          for (int j = tid; j < 3 * cn; j += kRsThreads) {
-            s_lc[j] = geo.cent[3 * c0 + j];
-            s_ln[j] = geo.nrm[3 * c0 + j];
-          }
-          __syncthreads();
-          if (i < n)
-            for (int j = 0; j < cn; ++j) {
-              const double dx = p[0] - s_lc[3 * j], dy = p[1] - s_lc[3 * j + 1], dz = p[2] - s_lc[3 * j + 2];
-              const double d2 = dx * dx + dy * dy + dz * dz;
-              if (d2 < kd[kmax - 1]) {  // insertion into the sorted k best
-                int a = kmax - 1;
-                while (a > 0 && kd[a - 1] > d2) {
-                  kd[a] = kd[a - 1];
-                  ki[a] = ki[a - 1];
-                  --a;
-                }
-                kd[a] = d2;
-                ki[a] = c0 + j;
-              }
-            }
+        switch (kmax) {  // (uniform)
+#define RS_KNN_CASE(K) \
+  case K:              \
+    rs_knn<K>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki); \
+    break;
+          RS_KNN_CASE(1)
+          RS_KNN_CASE(2)
+          RS_KNN_CASE(3)
+          RS_KNN_CASE(4)
+          RS_KNN_CASE(5)
+          RS_KNN_CASE(6)
+          RS_KNN_CASE(7)
+          default:
+            rs_knn<8>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki);
+#undef RS_KNN_CASE
         }
         bool ok = false;
         GeoTmp g{};
-        if (i < n) {
+        if (i < n && sub == 0) {
           const double gate2 = cfg.assoc_gate * cfg.assoc_gate;
           double best = __longlong_as_double(0x7ff0000000000000LL);
           int bl = -1;
-          for (int a = 0; a < kmax; ++a) {
-            if (ki[a] < 0 || !(kd[a] < gate2)) continue;  // beyond distance_upper_bound
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            if (a >= kmax || !(kd[a] < gate2)) continue;  // beyond distance_upper_bound
             const double* nn = geo.nrm + 3 * ki[a];
             const double* cc = geo.cent + 3 * ki[a];
             const double pd = fabs(nn[0] * (p[0] - cc[0]) + nn[1] * (p[1] - cc[1]) + nn[2] * (p[2] - cc[2]));
@@ -580,7 +933,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
               bl = ki[a];
             }
           }
-          ok = ki[0] >= 0 && kd[0] < gate2;
+          ok = kd[0] < gate2;
           if (ok) {
             const double* nn = geo.nrm + 3 * bl;
             const double* cc = geo.cent + 3 * bl;
@@ -603,10 +956,28 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
           okc += ok;
         }
       }
-      const int m = rs_count(grid, okc, pcnt, s_part, &s_m);
-      if (m == 0) continue;  // the family returns None (uniform)
-      const double med = rs_median(grid, bits, n, m, Hc, st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f],
-                                   sh, s_part, &s_bin, &s_before, s_min);
+      RS_MARK(1);
+      int m;
+      double med = 0.0;
+      if (n <= cfg.sel_cap) {
+        // every block stages all |r| patterns in shared memory and selects the
+        // median itself: one grid barrier instead of one per radix pass
+        grid.sync();
+        RS_MARK(2);
+        unsigned long long* sv = reinterpret_cast<unsigned long long*>(rs_dyn + cfg.sel_off);
+        for (int q = tid; q < n; q += kRsThreads) sv[q] = bits[q];
+        __syncthreads();
+        med = rs_median_block(sv, n, sh, s_part, &s_bin, &s_before, s_min, &s_m);
+        m = s_m;
+      } else {
+        m = rs_count(grid, okc, pcnt, s_part, &s_m);
+        RS_MARK(2);
+        if (m > 0)
+          med = rs_median(grid, bits, n, m, Hc, st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part,
+                          &s_bin, &s_before, s_min);
+      }
+      RS_MARK(3);
+      if (m > 0) {  // else the family returns None (uniform); its partial sums stay zero
       // --- trim, Huber, normal equations
       if (f == 0) {
         const double thr = fmax(cfg.trim_factor * med, fgeo);
@@ -621,38 +992,30 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
           const double J[6] = {nR[0], nR[1], nR[2], g.q[1] * nR[2] - g.q[2] * nR[1], g.q[2] * nR[0] - g.q[0] * nR[2],
                                g.q[0] * nR[1] - g.q[1] * nR[0]};
           const double w = ar <= cfg.huber_geo ? 1.0 : cfg.huber_geo / fmax(ar, 1e-12);
-          acc[0][27] += hub_value(g.r, cfg.huber_geo);
-          acc[0][30] += hub_value(g.r, cfg.huber_photo);
-          acc[0][28] += 1.0;
-          acc[0][29] += g.r * g.r;
+          acc[27] += hub_value(g.r, cfg.huber_geo);
+          acc[30] += hub_value(g.r, cfg.huber_photo);
+          acc[28] += 1.0;
+          acc[29] += g.r * g.r;
           if (objective_only) continue;
           int k = 0;
           for (int a = 0; a < 6; ++a)
-            for (int b2 = a; b2 < 6; ++b2) acc[0][k++] += w * J[a] * J[b2];
-          for (int a = 0; a < 6; ++a) acc[0][21 + a] += w * J[a] * g.r;
+            for (int b2 = a; b2 < 6; ++b2) acc[k++] += w * J[a] * J[b2];
+          for (int a = 0; a < 6; ++a) acc[21 + a] += w * J[a] * g.r;
         }
       } else {
         const double thr = fmax(cfg.trim_factor * med, fph);
         for (int i = gtid; i < n; i += nthr) {
           if (bits[i] == ~0ull) continue;
-          const PhotoTmp& t = ptmp[i];
-          double a30[30];
-          for (int q = 0; q < 30; ++q) a30[q] = 0.0;
-          photo_accum_one(t, cam, thr, cfg.huber_photo, objective_only, a30);
-          if (a30[28] == 0.0) continue;
-          for (int q = 0; q < 30; ++q) acc[1][q] += a30[q];
-          acc[1][30] += a30[27];                       // Huber with huber_photo
-          acc[1][27] += hub_value(t.r, cfg.huber_geo);  // ... and with huber_geo (positional pairing)
-          acc[1][27] -= a30[27];
+          // slot 30: Huber with huber_photo; slot 27: with huber_geo (positional pairing)
+          photo_accum_one(ptmp[i], cam, thr, cfg.huber_photo, cfg.huber_geo, objective_only, acc);
         }
       }
-    }
-    // --- per-block partial sums (families of this evaluation), block 0 reduces them in block order
-    for (int f = 0; f < 2; ++f) {
-      if (!fam_on[f]) continue;  // (uniform)
+      }
+      RS_MARK(4);
+      // --- per-block partial sums of this family; block 0 reduces them in block order
 #pragma unroll
       for (int q = 0; q < 31; ++q) {
-        double v = acc[f][q];
+        double v = acc[q];
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if (lane == 0) sred[warp][q] = v;
       }
@@ -663,8 +1026,10 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         part[((size_t)blockIdx.x * 2 + f) * kRsAcc + tid] = s;
       }
       __syncthreads();
+      RS_MARK(5);
     }
     grid.sync();
+    RS_MARK(6);
     if (blockIdx.x == 0) {
       for (int f = 0; f < 2; ++f) {
         if (!fam_on[f]) {
@@ -684,6 +1049,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         }
         __syncthreads();
       }
+      RS_MARK(7);
       if (tid == 0) rs_step(st, cfg, sfin);
     }
   }

@@ -314,6 +314,35 @@ __device__ __forceinline__ void photo_accum_one(const PhotoTmp& t, const RegCam&
   for (int a = 0; a < 6; ++a) acc[21 + a] += w * J[a] * t.r;
 }
 
+// As above into the registration kernel's 32-slot layout: Huber(huber) in
+// slot 30 and Huber(huber_geo) in slot 27.
+__device__ __forceinline__ void photo_accum_one(const PhotoTmp& t, const RegCam& cam, double thr, double huber,
+                                                double huber_geo, int objective_only, double (&acc)[32]) {
+  const double ar = fabs(t.r);
+  if (!(ar <= thr)) return;
+  const double x = t.q[0], y = t.q[1], z = t.q[2];
+  const double rho2 = x * x + y * y, r2 = rho2 + z * z;
+  const double rho = sqrt(rho2), rq = sqrt(r2);
+  const double w = ar <= huber ? 1.0 : huber / fmax(ar, 1e-12);
+  acc[30] += ar <= huber ? 0.5 * t.r * t.r : huber * (ar - 0.5 * huber);
+  acc[27] += ar <= huber_geo ? 0.5 * t.r * t.r : huber_geo * (ar - 0.5 * huber_geo);
+  acc[28] += 1.0;
+  acc[29] += t.r * t.r;
+  if (objective_only) return;
+  const double dudq[3] = {cam.fx * (-y / rho2), cam.fx * (x / rho2), 0.0};
+  const double dvdq[3] = {cam.fy * (-x * z / (r2 * rho)), cam.fy * (-y * z / (r2 * rho)), cam.fy * (rho / r2)};
+  const double g[3] = {x / rq - t.du * dudq[0] - t.dv * dvdq[0], y / rq - t.du * dudq[1] - t.dv * dvdq[1],
+                       z / rq - t.du * dudq[2] - t.dv * dvdq[2]};
+  const double J[6] = {-g[0], -g[1], -g[2], g[1] * z - g[2] * y, g[2] * x - g[0] * z, g[0] * y - g[1] * x};
+  int k = 0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+#pragma unroll
+    for (int b = a; b < 6; ++b) acc[k++] += w * J[a] * J[b];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) acc[21 + a] += w * J[a] * t.r;
+}
+
 __global__ void __launch_bounds__(256) k_photo_accum(int M, RegCam cam, const PhotoTmp* __restrict__ tmp,
                                                      const unsigned long long* __restrict__ absbits,
                                                      const double* __restrict__ median, double trim_factor,

@@ -250,7 +250,7 @@ def solve_device(cfg: RegistrationConfig, initial, scan: DeviceScan, X_w: torch.
     M = int(X_w.shape[0]) if X_w is not None else 0
     nl = int(tree.dev_centroids.shape[0]) if tree is not None else 0
     ng = int(geo_scan.shape[0]) if geo_scan is not None else 0
-    ws = torch.empty(int(lib().ss_reg_solve_workspace_bytes(ng, M)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(lib().ss_reg_solve_workspace_bytes(nl, ng, M)), dtype=torch.uint8, device=dev)
     c = engine.ss_camera(scan.cam)
     k = SsRegSolveCfg(float(cfg.huber_photo), float(cfg.huber_geo), float(cfg.trim_factor), float(cfg.spread_gate),
                       float(cfg.assoc_gate), float(cfg.trim_floor_photo), float(cfg.trim_floor_geo), float(cfg.tol),
@@ -271,8 +271,10 @@ def solve_device(cfg: RegistrationConfig, initial, scan: DeviceScan, X_w: torch.
     T = SE3Pose(t_out[:9].reshape(3, 3), t_out[9:]).orthonormalized()
     n_geo, n_photo = int(info[2]), int(info[3])
     rms = lambda s2, m: float(np.sqrt(s2 / m)) if m else 0.0  # noqa: E731
-    return RegistrationResult(T, bool(info[1]), int(info[0]), rms(r2[0], n_geo), rms(r2[1], n_photo), n_geo,
-                              n_photo, cfg.mode)
+    res = RegistrationResult(T, bool(info[1]), int(info[0]), rms(r2[0], n_geo), rms(r2[1], n_photo), n_geo,
+                             n_photo, cfg.mode)
+    res.n_evaluations = int(info[4])  # residual evaluations the device loop ran (diagnostic)
+    return res
 
 
 def _solve_device(X_w: torch.Tensor, scan: DeviceScan, initial, cfg: RegistrationConfig) -> RegistrationResult:

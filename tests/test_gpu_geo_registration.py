@@ -97,3 +97,33 @@ def test_device_loop_matches_reference_on_reference_inputs(cuda, mode, iters):
     assert res.iterations == int(GG[f"{mode}_iterations"]) and res.converged == bool(GG[f"{mode}_converged"])
     assert res.n_geo == int(GG[f"{mode}_n_geo"]) and res.n_photo == int(GG[f"{mode}_n_photo"])
     assert dt <= 1e-7 and np.abs(res.pose.rotation - GG[f"{mode}_R"]).max() <= 1e-7
+
+
+class _Leaves:
+    """The oracle's usable leaves in the device layout solve_device reads."""
+
+    def __init__(self, t):
+        self.dev_centroids = torch.as_tensor(np.ascontiguousarray(t.c[t.usable]), device="cuda")
+        self.dev_normals = torch.as_tensor(np.ascontiguousarray(t.n[t.usable]), device="cuda")
+
+
+@pytest.mark.parametrize("gate,k", [(0.12, 3), (0.4, 1), (0.4, 5), (2.5, 8), (1e4, 3), (-0.4, 3)])
+def test_association_gate_and_k_vs_oracle(cuda, gate, k):
+    """The hashed-grid association (cells of edge |assoc_gate|) against the oracle's
+    cKDTree query with distance_upper_bound, over gates from a few leaves per query to
+    one cell holding every leaf, and k from 1 to the device maximum of 8."""
+    from oracle import geo_registration_oracle as GO
+    from paper_2503_17491_b200 import SE3Pose, SphericalCamera
+    c = G["cam"]
+    cam = SphericalCamera(int(c[0]), int(c[1]), *[float(x) for x in c[2:]])
+    ot = GO.Tree(GG["model_pts"], G["initial_t"])
+    scan_np = G["scan"].astype(np.float64)[GG["geo_sel"]]
+    R, t, it, conv, grms, _, ng, _ = GO.register("geometric", ot, scan_np, None, None, None, None, G["initial_R"],
+                                                 G["initial_t"], max_iters=6, gate=gate, k=k)
+    cfg = REG.RegistrationConfig(mode="geometric", max_iters=6, assoc_gate=gate, assoc_k=k)
+    res = REG.solve_device(cfg, SE3Pose(G["initial_R"], G["initial_t"]), REG.DeviceScan(cam, G["scan"].astype(np.float64)),
+                           None, _Leaves(ot), torch.as_tensor(scan_np, device="cuda"))
+    print(gate, k, "iters", res.iterations, it, "n_geo", res.n_geo, ng, "dt", np.abs(res.pose.translation - t).max())
+    assert res.iterations == it and res.converged == conv and res.n_geo == ng
+    assert np.abs(res.pose.translation - t).max() <= 1e-9 and np.abs(res.pose.rotation - R).max() <= 1e-9
+    assert abs(res.geo_rms - grms) <= 1e-9

@@ -103,14 +103,17 @@ def test_device_loop_matches_host_loop_golden(cuda):
         assert dev.photo_rms == pytest.approx(host.photo_rms, rel=1e-9)
 
 
-def test_device_loop_matches_host_loop_config3(cuda):
-    """BASELINE config 3 (300k-surfel map, 64x1024 scan, SE(3) offset, 20 iterations)."""
+@pytest.mark.parametrize("thin", [4, 1])
+def test_device_loop_matches_host_loop_config3(cuda, thin):
+    """BASELINE config 3 (300k-surfel map, 64x1024 scan, SE(3) offset, 20 iterations).
+    thin=4 (~11k anchors) selects the trim median per block from shared memory;
+    thin=1 (~176k anchors, beyond shared memory) takes the grid-wide radix select."""
     from paper_2503_17491_b200 import workloads as W
     params, cam, scan_pts, truth, initial = W.config3_problem()
     cfg = REG.RegistrationConfig(mode="photometric", max_iters=20, tol=0.0)
     s = 2
     geo = SphericalCamera(cam.width * s, cam.height * s, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
-    X, n = REG.sample_anchors(params, geo, initial, cfg, thin=s * s)
+    X, n = REG.sample_anchors(params, geo, initial, cfg, thin=thin)
     scan = REG.DeviceScan(cam, scan_pts)
     host, dev = _loops(X, scan, initial, cfg)
     print("config3 host", host.iterations, host.n_photo, "device", dev.iterations, dev.n_photo,

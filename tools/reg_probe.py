@@ -29,3 +29,13 @@ X1, n1 = REG.sample_anchors(dp, geo, initial, scfg, thin=1)
 tt, tree = t(lambda: REG.build_leaf_tree(X1, initial.translation))
 ts2, _ = t(lambda: REG.register(dp, scan_pts, cam, initial, scfg))
 print(f"model points {n1}: leaf tree {tt:.3f} ms ({tree.sizes.shape[0]} leaves); sequential register() {ts2:.3f} ms")
+X1, n1 = REG.sample_anchors(dp, geo, initial, scfg, thin=1)
+tree = REG.build_leaf_tree(X1, initial.translation)
+scan = REG.DeviceScan(cam, scan_pts)
+sel = np.random.default_rng(0).choice(scan_pts.shape[0], scfg.max_geo_points, replace=False) if scan_pts.shape[0] > scfg.max_geo_points else np.arange(scan_pts.shape[0])
+gs = torch.as_tensor(np.ascontiguousarray(scan_pts[sel]), device="cuda")
+Xw = X1[::4].contiguous()
+for mode in ("geometric", "photometric", "joint", "sequential"):
+    c = REG.RegistrationConfig(mode=mode, max_iters=20, tol=0.0)
+    tm, res = t(lambda: REG.solve_device(c, initial, scan, Xw if mode != "geometric" else None, tree if mode != "photometric" else None, gs if mode != "photometric" else None))
+    print(f"{mode}: loop {tm:.3f} ms, {res.iterations} it, {res.n_evaluations} evals, {tm / max(res.iterations, 1) * 1e3:.0f} us/it, {tm / max(res.n_evaluations, 1) * 1e3:.0f} us/eval")
