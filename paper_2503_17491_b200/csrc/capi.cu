@@ -776,7 +776,7 @@ size_t ss_reg_solve_workspace_bytes(int32_t n_leaves, int32_t n_geo_scan, int32_
   const size_t g = (size_t)(n_geo_scan > 0 ? n_geo_scan : 1), m = (size_t)(M > 0 ? M : 1);
   const size_t l = (size_t)(n_leaves > 0 ? n_leaves : 1);
   return g * (sizeof(GeoTmp) + 8) + m * (sizeof(PhotoTmp) + 8) + (size_t)4 * kRsPasses * kRsBins * 4 +
-         (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + sizeof(RegSolveState) + (kRsGridBuckets + 1) * 4 +
+         (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + 1024 * 16 + sizeof(RegSolveState) + (kRsGridBuckets + 1) * 4 +
          l * (sizeof(RsLeafEntry) + 4) + 1024;
 }
 
@@ -834,6 +834,7 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   unsigned* hist = (unsigned*)take((size_t)4 * kRsPasses * kRsBins * 4);
   double* part = (double*)take((size_t)1024 * 2 * kRsAcc * 8);
   int* pcnt = (int*)take(1024 * 4);
+  unsigned long long* pmm = (unsigned long long*)take(1024 * 16);
   RegSolveState* state = (RegSolveState*)take(sizeof(RegSolveState));
   int* bstart = (int*)take((size_t)(kRsGridBuckets + 1) * 4);
   RsLeafEntry* ent = (RsLeafEntry*)take((size_t)std::max(nl, 1) * sizeof(RsLeafEntry));
@@ -868,7 +869,7 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   RsGeo geo{leaf_centroids, leaf_normals, nl, geo_scan, ng, bstart, ent, inv_cs, gmask, staged ? 1 : 0};
   RsPhoto ph{X_w, m, scan_range, scan_valid};
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
-                  (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&state};
+                  (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&pmm, (void*)&state};
   SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, dyn, s));
   RegSolveState out{};
   SS_CUDA_TRY(cudaMemcpyAsync(&out, state, sizeof(out), cudaMemcpyDeviceToHost, s));

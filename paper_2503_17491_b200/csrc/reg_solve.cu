@@ -333,18 +333,6 @@ __device__ void rs_step(RegSolveState* st, const RegSolveCfg& cfg, const double*
   rs_try(st, cfg);
 }
 
-// One radix-select histogram step for a warp: pattern b (~0 = invalid) counts in
-// its digit's bin when it matches the prefix.  Lanes sharing a bin add once
-// (the top digits cluster: |r| share few exponents).  Returns whether b counted.
-__device__ __forceinline__ int rs_hist_add(unsigned long long b, unsigned long long prefix, unsigned long long mask,
-                                           int shift, unsigned dmask, unsigned* sh, int lane) {
-  const bool in = b != ~0ull && (b & mask) == prefix;
-  const unsigned d = in ? (unsigned)(b >> shift) & dmask : 0xffffffffu;
-  const unsigned peers = __match_any_sync(0xffffffffu, d);
-  if (in && lane == __ffs(peers) - 1) atomicAdd(&sh[d], (unsigned)__popc(peers));
-  return in;
-}
-
 // Block-wide: find the bin of hist[0, nbins) holding rank kk; returns (bin, count before it).
 __device__ void rs_find_bin(const unsigned* __restrict__ hist, int nbins, int kk, int* s_bin, int* s_before,
                             unsigned* s_part) {
@@ -392,48 +380,60 @@ __device__ __forceinline__ double hub_value(double r, double d) {
 // m: number of valid entries (> 0).  Hc: this evaluation's kRsPasses x kRsBins
 // histograms (zeroed); cand / ncand / vmin: this evaluation's scratch.
 __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __restrict__ bits, int n, int m,
-                            unsigned* __restrict__ Hc, unsigned long long* cand, int* ncand,
-                            unsigned long long* vmin, unsigned* sh, unsigned* s_part, int* s_bin, int* s_before,
-                            unsigned long long* s_min) {
+                            unsigned long long vlo, unsigned long long vhi, unsigned* __restrict__ Hc,
+                            unsigned long long* cand, int* ncand, unsigned long long* vmin, unsigned* sh,
+                            unsigned* s_part, int* s_bin, int* s_before, unsigned long long* s_min) {
+  // vlo / vhi: smallest / largest valid pattern (rs_count).  The radix passes start at
+  // the highest bit in which they differ (12-bit digits downwards).
+  if (vlo == vhi) return __longlong_as_double((long long)vlo);  // all equal
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = gridDim.x * kRsThreads;
   const int k1 = (m % 2 == 0) ? m / 2 - 1 : m / 2;
-  unsigned long long prefix = 0ull, mask = 0ull;
+  int top = 63 - __clzll(vlo ^ vhi);  // <= 62: valid patterns are non-negative doubles
+  unsigned long long mask = ~((2ull << top) - 1ull), prefix = vlo & mask;
   int kk = k1, cnt_eq = 0;
   bool exact = false;
   unsigned long long v2c = ~0ull;
-  for (int p = 0; p < kRsPasses; ++p) {
-    const int shift = p < 5 ? 52 - 12 * p : 0;
-    const int nb = p < 5 ? 12 : 4;
-    const unsigned dmask = (1u << nb) - 1u;
-    for (int j = tid; j < kRsBins; j += kRsThreads) sh[j] = 0u;
+  RS_SUB(-1);
+  for (int p = 0;; ++p) {
+    const int lo = max(top - 11, 0);
+    const unsigned dmask = (1u << (top - lo + 1)) - 1u;
+    for (int j = tid; j <= (int)dmask; j += kRsThreads) sh[j] = 0u;
     __syncthreads();
-    for (int i0 = gtid - lane; i0 < n; i0 += nthr)  // warp-uniform trip count
-      rs_hist_add(i0 + lane < n ? bits[i0 + lane] : ~0ull, prefix, mask, shift, dmask, sh, lane);
+    for (int i = gtid; i < n; i += nthr) {
+      const unsigned long long b = bits[i];
+      if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
+    }
     __syncthreads();
-    unsigned* Hp = Hc + p * kRsBins;
+    unsigned* Hp = Hc + p * kRsBins;  // p < kRsPasses: at most ceil(63 / 12) passes
     for (int j = tid; j <= (int)dmask; j += kRsThreads)
       if (sh[j]) atomicAdd(&Hp[j], sh[j]);
+    RS_SUB(0);
     grid.sync();
+    RS_SUB(1);
     rs_find_bin(Hp, (int)dmask + 1, kk, s_bin, s_before, s_part);
+    RS_SUB(2);
     const int bin = *s_bin;
     kk -= *s_before;
     const int cnt_bin = (int)Hp[bin];
-    if (p == kRsPasses - 1) cnt_eq = cnt_bin;
-    prefix |= (unsigned long long)bin << shift;
-    mask |= (unsigned long long)dmask << shift;
+    prefix |= (unsigned long long)bin << lo;
+    mask |= (unsigned long long)dmask << lo;
     __syncthreads();
-    if (p == kRsPasses - 1) {
+    if (lo == 0) {
+      cnt_eq = cnt_bin;
       exact = true;
       break;
     }
+    top = lo - 1;
     if (cnt_bin <= kRsCand) {
       // few values share the prefix: gather them and rank them exactly in every block
       for (int i = gtid; i < n; i += nthr) {
         const unsigned long long b = bits[i];
         if (b != ~0ull && (b & mask) == prefix) cand[atomicAdd(ncand, 1)] = b;
       }
+      RS_SUB(3);
       grid.sync();
+      RS_SUB(1);
       unsigned long long* sc = reinterpret_cast<unsigned long long*>(sh);  // kRsCand x 8 B fits
       for (int j = tid; j < cnt_bin; j += kRsThreads) sc[j] = ((volatile unsigned long long*)cand)[j];
       __syncthreads();
@@ -454,6 +454,7 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
       const unsigned j2 = sh[2 * kRsCand + 1];
       v2c = j2 == 0xffffffffu ? ~0ull : sc[j2];
       __syncthreads();
+      RS_SUB(4);
       break;
     }
   }
@@ -474,7 +475,9 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
     for (int w = 1; w < kRsThreads / 32; ++w) mn = min(mn, s_min[w]);
     if (mn != ~0ull) atomicMin(vmin, mn);
   }
+  RS_SUB(5);
   grid.sync();
+  RS_SUB(1);
   return (v1 + __longlong_as_double((long long)*((volatile unsigned long long*)vmin))) / 2.0;
 }
 
@@ -602,23 +605,54 @@ __device__ double rs_median_block(const unsigned long long* sv, int n, unsigned*
   return (v1 + __longlong_as_double((long long)nx)) / 2.0;
 }
 
-// Block count of valid entries -> grid total (pcnt: per-block slots).
-__device__ int rs_count(cg::grid_group& grid, int okc, int* __restrict__ pcnt, unsigned* s_part, int* s_m) {
+// Block count of valid entries -> grid total (pcnt: per-block slots), and the
+// grid's smallest / largest valid pattern (pmm: per-block pairs) -> s_mm[0..1].
+__device__ int rs_count(cg::grid_group& grid, int okc, unsigned long long mn, unsigned long long mx,
+                        int* __restrict__ pcnt, unsigned long long* __restrict__ pmm, unsigned* s_part,
+                        unsigned long long* s_mm, int* s_m) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   okc = __reduce_add_sync(0xffffffffu, okc);
-  if (lane == 0) s_part[warp] = (unsigned)okc;
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  }
+  if (lane == 0) {
+    s_part[warp] = (unsigned)okc;
+    s_mm[2 * warp] = mn;
+    s_mm[2 * warp + 1] = mx;
+  }
   __syncthreads();
   if (tid == 0) {
     int c = 0;
-    for (int w = 0; w < kRsThreads / 32; ++w) c += (int)s_part[w];
+    for (int w = 0; w < kRsThreads / 32; ++w) {
+      c += (int)s_part[w];
+      mn = min(mn, s_mm[2 * w]);
+      mx = max(mx, s_mm[2 * w + 1]);
+    }
     pcnt[blockIdx.x] = c;
+    pmm[2 * blockIdx.x] = mn;
+    pmm[2 * blockIdx.x + 1] = mx;
   }
   grid.sync();
   if (tid < 32) {
     int c = 0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) c += pcnt[b];
+    mn = ~0ull;
+    mx = 0ull;
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      c += pcnt[b];
+      mn = min(mn, pmm[2 * b]);
+      mx = max(mx, pmm[2 * b + 1]);
+    }
     c = __reduce_add_sync(0xffffffffu, c);
-    if (lane == 0) *s_m = c;
+    for (int off = 16; off > 0; off >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if (lane == 0) {
+      *s_m = c;
+      s_mm[2 * (kRsThreads / 32)] = mn;
+      s_mm[2 * (kRsThreads / 32) + 1] = mx;
+    }
   }
   __syncthreads();
   return *s_m;
@@ -797,7 +831,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
                                                          unsigned long long* __restrict__ gbits,
                                                          unsigned long long* __restrict__ pbits,
                                                          unsigned* __restrict__ hist, double* __restrict__ part,
-                                                         int* __restrict__ pcnt, RegSolveState* st) {
+                                                         int* __restrict__ pcnt, unsigned long long* __restrict__ pmm,
+                                                         RegSolveState* st) {
   cg::grid_group grid = cg::this_grid();
   __shared__ __align__(16) unsigned sh[kRsBins];
   __shared__ double sred[kRsThreads / 32][kRsAcc];
@@ -805,6 +840,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
   __shared__ unsigned s_part[kRsThreads / 32];
   __shared__ int s_bin, s_before, s_m;
   __shared__ unsigned long long s_min[kRsThreads / 32];
+  __shared__ unsigned long long s_mm[2 * (kRsThreads / 32) + 2];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = G * kRsThreads;
   const int kmax = min(min(cfg.assoc_k, geo.n_leaves), 8);
@@ -848,9 +884,9 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
 #ifdef SS_RS_PROF
       if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("RSPROF evals %d step+sync %llu resid %llu count %llu median %llu accum %llu part %llu sync %llu final %llu"
-               " | sel zero %llu hist %llu find %llu gather %llu rank %llu\n",
+               " | sub %llu %llu %llu %llu %llu %llu\n",
                e, rs_prof[0], rs_prof[1], rs_prof[2], rs_prof[3], rs_prof[4], rs_prof[5], rs_prof[6], rs_prof[7],
-               g_rs_sub[0], g_rs_sub[1], g_rs_sub[2], g_rs_sub[3], g_rs_sub[4]);
+               g_rs_sub[0], g_rs_sub[1], g_rs_sub[2], g_rs_sub[3], g_rs_sub[4], g_rs_sub[5]);
       if (blockIdx.x == 0 && threadIdx.x == 0)
         for (int q = 0; q < 8; ++q) g_rs_sub[q] = 0;
 #endif
@@ -881,6 +917,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
       const int n = f == 0 ? geo.n_scan : ph.M;
       // --- residuals
       int okc = 0;
+      unsigned long long vlo = ~0ull, vhi = 0ull;  // this thread's smallest / largest valid |r| pattern
       if (f == 0) {
         // k nearest usable leaf centroids within the gate, then the leaf whose plane
         // is closest (registration.py:249-265); leaves staged through shared memory
@@ -944,7 +981,9 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
             }
           }
           gtmp[i] = g;
-          bits[i] = ok ? (unsigned long long)__double_as_longlong(fabs(g.r)) : ~0ull;
+          const unsigned long long bv = ok ? (unsigned long long)__double_as_longlong(fabs(g.r)) : ~0ull;
+          bits[i] = bv;
+          if (ok) vlo = vhi = bv;
         }
         okc = ok;
       } else {
@@ -952,7 +991,12 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
           PhotoTmp t{};
           const bool ok = photo_resid_one(ph.X, i, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t);
           ptmp[i] = t;
-          bits[i] = ok ? (unsigned long long)__double_as_longlong(fabs(t.r)) : ~0ull;
+          const unsigned long long bv = ok ? (unsigned long long)__double_as_longlong(fabs(t.r)) : ~0ull;
+          bits[i] = bv;
+          if (ok) {
+            vlo = min(vlo, bv);
+            vhi = max(vhi, bv);
+          }
           okc += ok;
         }
       }
@@ -970,11 +1014,12 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         med = rs_median_block(sv, n, sh, s_part, &s_bin, &s_before, s_min, &s_m);
         m = s_m;
       } else {
-        m = rs_count(grid, okc, pcnt, s_part, &s_m);
+        m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
         RS_MARK(2);
         if (m > 0)
-          med = rs_median(grid, bits, n, m, Hc, st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part,
-                          &s_bin, &s_before, s_min);
+          med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
+                          st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
+                          s_min);
       }
       RS_MARK(3);
       if (m > 0) {  // else the family returns None (uniform); its partial sums stay zero
