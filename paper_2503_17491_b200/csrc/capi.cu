@@ -12,6 +12,7 @@
 #include "keyframe.cu"
 #include "densify.cu"
 #include "leaf_tree.cu"
+#include "leaf_top.cu"
 #include "loss.cu"
 #include "reg_solve.cu"  // includes registration.cu
 
@@ -1005,7 +1006,7 @@ int ss_range_image_normals(const ss_camera* cam, const double* range, const uint
 
 size_t ss_leaf_tree_workspace_bytes(int32_t n) {
   const size_t m = (size_t)(n > 0 ? n : 1);
-  return m * (4 + 4 + 8 + 2 * 8 + sizeof(LeafRec) + 8 + sizeof(LeafRec)) + 1024;
+  return m * (4 + 4 + 8 + 2 * 8 + sizeof(LeafRec) + 8 + sizeof(LeafRec)) + lt_top_ws_bytes(num_sms()) + 1024;
 }
 
 int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, int32_t leaf_size, double tau,
@@ -1033,6 +1034,21 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   int2* leaf_seg = (int2*)take((size_t)cap_leaves * 8);
   LeafRec* leaf_rec = (LeafRec*)take((size_t)cap_leaves * sizeof(LeafRec));
   int* counts = (int*)take(16);  // [0] nodes of level parity 0, [1] parity 1, [2] leaves, [3] overflow
+  // top levels (node bound 2^level below the grid): one cooperative kernel, all SMs per level
+  const int G = num_sms();
+  int top_levels = 0;
+  // (measured at config 3: levels 0-4 here, 1.73 -> 0.73 ms; deeper levels have enough
+  // nodes for the per-node kernel, whose cost falls with the node size)
+  while (top_levels < 5 && (1 << top_levels) <= std::min(kLtTopMaxNodes, G - 1)) ++top_levels;
+  LtTopWs tws{};
+  tws.part = (double*)take((size_t)G * 9 * 8);
+  tws.pmm = (unsigned long long*)take((size_t)G * 16);
+  tws.pcnt = (int*)take((size_t)G * 4);
+  tws.hist = (unsigned*)take((size_t)3 * kLtTopMaxNodes * kLtBins * 4);
+  tws.cand = (unsigned long long*)take((size_t)kLtTopMaxNodes * kLtCand * 8);
+  tws.ncand = (int*)take((size_t)kLtTopMaxNodes * 4);
+  tws.vmin = (unsigned long long*)take((size_t)kLtTopMaxNodes * 8);
+  tws.more = (int*)take(8);
   k_iota<<<(n + 255) / 256, 256, 0, s>>>(n, idx);
   const int init[4] = {1, 0, 0, 0};
   const int2 root = make_int2(0, n);
@@ -1043,8 +1059,26 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   // bound on its node count (blocks past the actual count exit), the next
   // level is laid out on the device; the host checks for leftovers at the end.
   int level = 0;
+  if (top_levels > 0) {
+    int occ = 0;
+    SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_leaf_top, kLtTopThreads, 0));
+    if (occ < 1) return SS_ERR_CUDA;
+    const double* a_pts = pts;
+    int *a_idx = idx, *a_tmp = tmp, *a_counts = counts;
+    double* a_proj = proj;
+    int2 *a_n0 = nodes[0], *a_n1 = nodes[1], *a_seg = leaf_seg;
+    LeafRec *a_recs = recs, *a_lrec = leaf_rec;
+    int a_cap = cap_leaves, a_ls = leaf_size, a_lv = top_levels;
+    double a_tau = tau;
+    double3 a_vp = vp;
+    void* args[] = {(void*)&a_pts, (void*)&a_idx, (void*)&a_tmp, (void*)&a_proj, (void*)&a_n0, (void*)&a_n1,
+                    (void*)&a_counts, (void*)&a_recs, (void*)&a_seg, (void*)&a_lrec, (void*)&a_cap, (void*)&a_vp,
+                    (void*)&a_ls, (void*)&a_tau, (void*)&a_lv, (void*)&tws};
+    SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_leaf_top, dim3(G), dim3(kLtTopThreads), args, 0, s));
+    level = top_levels;
+  }
   for (int batch = 0;; ++batch) {
-    const int depth = batch == 0 ? 2 + (int)std::ceil(std::log2((double)n + 1.0)) : 8;
+    const int depth = batch == 0 ? std::max(1, 2 + (int)std::ceil(std::log2((double)n + 1.0)) - level) : 8;
     for (int q = 0; q < depth; ++q, ++level) {
       const int par = level & 1;
       const long long bound = std::min<long long>(level < 30 ? (1LL << level) : cap_nodes, cap_nodes);
@@ -1071,7 +1105,11 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   std::vector<int2> hs(nl_total);
   SS_CUDA_TRY(cudaMemcpyAsync(hr.data(), leaf_rec, sizeof(LeafRec) * nl_total, cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaMemcpyAsync(hs.data(), leaf_seg, sizeof(int2) * nl_total, cudaMemcpyDeviceToHost, s));
-  k_leaf_assign<<<std::max(nl_total, 1), 256, 0, s>>>(idx, leaf_seg, nl_total, point_leaf_out);
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  int max_seg = 1;
+  for (int i = 0; i < nl_total; ++i) max_seg = std::max(max_seg, hs[i].y - hs[i].x);
+  k_leaf_assign<<<dim3(std::max(nl_total, 1), (max_seg + 1023) / 1024), 256, 0, s>>>(idx, leaf_seg, nl_total,
+                                                                                     point_leaf_out);
   SS_CUDA_TRY(cudaGetLastError());
   SS_CUDA_TRY(cudaStreamSynchronize(s));
   for (int i = 0; i < nl_total; ++i) {

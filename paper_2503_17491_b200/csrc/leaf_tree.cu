@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pt
                                                            int leaf_size, double tau, LeafRec* __restrict__ out) {
   if ((int)blockIdx.x >= *n_nodes) return;  // grid sized by a bound on the level's node count
   __shared__ double sred[NT / 32];
-  __shared__ double s_m[3], s_cov[6], s_axis[3], s_n[3], s_w[3], s_med;
+  __shared__ double s_axis[3], s_n[3], s_w[3];
   __shared__ unsigned hist[kLtBins];
   __shared__ unsigned long long cand[kLtCand];
   __shared__ int sint[2 * (NT / 32) + 8];
@@ -397,12 +397,15 @@ __global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cu
   }
 }
 
+// point -> leaf: blockIdx.x = leaf, blockIdx.y = 1024-point chunk of its segment
+// (flat leaves stop splitting early and can hold tens of thousands of points)
 __global__ void k_leaf_assign(const int* __restrict__ idx, const int2* __restrict__ leaves, int nleaves,
                               int* __restrict__ point_leaf) {
   const int l = blockIdx.x;
   if (l >= nleaves) return;
   const int2 s = leaves[l];
-  for (int j = s.x + threadIdx.x; j < s.y; j += blockDim.x) point_leaf[idx[j]] = l;
+  const int j0 = s.x + blockIdx.y * 1024;
+  for (int j = j0 + threadIdx.x; j < min(s.y, j0 + 1024); j += blockDim.x) point_leaf[idx[j]] = l;
 }
 
 __global__ void k_iota(int n, int* __restrict__ v) {

@@ -108,6 +108,16 @@ class LeafTree:
         return self._point_leaf
 
 
+_TREE_HOST: list = []
+
+
+def _tree_host_buffers(cap: int):
+    """Reused host output buffers of ss_leaf_tree_build (fresh multi-MB arrays per call cost page faults)."""
+    if not _TREE_HOST or _TREE_HOST[0][0].shape[0] < cap:
+        _TREE_HOST[:] = [(np.zeros((cap, 3)), np.zeros((cap, 3)), np.zeros(cap, np.int32), np.zeros(cap, np.uint8))]
+    return _TREE_HOST[0]
+
+
 def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float = 0.02) -> LeafTree:
     """registration.py:98-164 on the device (level-parallel PCA median splits)."""
     dev = engine.require_cuda()
@@ -118,8 +128,7 @@ def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float 
         raise RegistrationError("cannot build a leaf tree from an empty cloud")
     vp = np.ascontiguousarray(np.asarray(viewpoint, np.float64).reshape(3))
     cap = n
-    cent, nrm = np.zeros((cap, 3)), np.zeros((cap, 3))
-    sizes, usable = np.zeros(cap, np.int32), np.zeros(cap, np.uint8)
+    cent, nrm, sizes, usable = _tree_host_buffers(cap)
     pl = torch.empty(n, dtype=torch.int32, device=dev)
     nl = ctypes.c_int32(0)
     ws = torch.empty(int(lib().ss_leaf_tree_workspace_bytes(n)), dtype=torch.uint8, device=dev)
