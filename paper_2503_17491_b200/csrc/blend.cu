@@ -59,7 +59,58 @@ constexpr int kBwdDynSmem = kWarpsPerBlock * 32 * 16 * 4;
 struct BlendParams {
   CamK cam;
   float alpha_cutoff, alpha_clamp, min_T, denom_eps;
+  // Segment-parallel backward (few tiles, long lists): the forward records every
+  // pixel's running state (T, D, O, N) before each kSegChunks-chunk boundary of
+  // its tile's list, and the final D, O, N, so that the backward can walk each
+  // segment of a list independently (segst == nullptr: off).
+  float* segst;  // [global chunk / kSegChunks][6][64]
+  float* fin;    // [5][W * H]: final D, O, N0, N1, N2
 };
+
+#ifndef SS_SEG_CHUNKS
+#define SS_SEG_CHUNKS 4
+#endif
+// chunks of 32 entries per backward segment (A/B at config 2, backward us:
+// halves-split tiles 240, segments of 16 chunks 189, 8 -> 135, 4 -> 121)
+constexpr int kSegChunks = SS_SEG_CHUNKS;
+static_assert(kSegChunks % 4 == 0, "k_forward_long records state at its 4-chunk round starts");
+
+// Backward work slots of the segment mode: every tile (longest first, the
+// forward's LPT order) contributes ceil(L / (32 kSegChunks)) slots
+// (tile << 16) | segment.  One block; counters[2] = slot count.
+__global__ void __launch_bounds__(1024) k_seg_order(int ntiles, const int* __restrict__ tile_ptr,
+                                                    const int* __restrict__ order_fwd, int* __restrict__ slots,
+                                                    int* __restrict__ counters) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (ntiles + 1023) / 1024, r0 = min(tid * per, ntiles), r1 = min(r0 + per, ntiles);
+  constexpr int kSegEntries = 32 * kSegChunks;
+  int cnt = 0;
+  for (int r = r0; r < r1; ++r) {
+    const int t = order_fwd[r] >> 2;
+    cnt += (tile_ptr[t + 1] - tile_ptr[t] + kSegEntries - 1) / kSegEntries;
+  }
+  int inc = cnt;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  int base = inc - cnt;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  for (int r = r0; r < r1; ++r) {
+    const int t = order_fwd[r] >> 2;
+    const int ns = (tile_ptr[t + 1] - tile_ptr[t] + kSegEntries - 1) / kSegEntries;
+    for (int q = 0; q < ns; ++q) slots[base++] = (t << 16) | q;
+  }
+  if (tid == 1023) counters[2] = base;  // (the last thread's run ends at the total)
+}
+
+// pixel state before chunk `chunk` of the tile whose chunks start at `cbase` (chunk % kSegChunks == 0, > 0)
+__device__ __forceinline__ float* seg_state(float* segst, int cbase, int chunk) {
+  return segst + (size_t)((cbase + chunk) / kSegChunks) * (6 * 64);
+}
 
 template <int TS>
 struct TileShape {
@@ -389,6 +440,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 #pragma unroll
       for (int j = 0; j < PPL; ++j) any_live |= live[j];
       if (!__any_sync(0xffffffffu, any_live)) break;
+      if (TS == 8 && bp.segst && chunk > 0 && chunk % kSegChunks == 0) {
+        float* sg = seg_state(bp.segst, cbase, chunk);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          const int q = lane + 32 * j;
+          sg[q] = T[j];
+          sg[64 + q] = D[j];
+          sg[128 + q] = O[j];
+          sg[192 + q] = N[j][0];
+          sg[256 + q] = N[j][1];
+          sg[320 + q] = N[j][2];
+        }
+      }
       if (sid_next >= 0) prefetch_entry(&raw_all[warp][(chunk + 1) & 1][lane], sid_next, rec, rec64);
       __pipeline_commit();
       const int sid_after = base + 64 + lane < L ? pairs[lo + base + 64 + lane] : -1;
@@ -464,6 +528,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       out_N[3 * p + 2] = N[j][2];
       out_T[p] = T[j];
       out_last[p] = last[j];
+      if (bp.fin) {
+        const size_t P = (size_t)k.W * k.H;
+        bp.fin[p] = D[j];
+        bp.fin[P + p] = O[j];
+        bp.fin[2 * P + p] = N[j][0];
+        bp.fin[3 * P + p] = N[j][1];
+        bp.fin[4 * P + p] = N[j][2];
+      }
     }
   }
 }
@@ -476,6 +548,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 // compositing of a tile overlaps the float64 staging of its next entries
 // instead of alternating with it in one warp.
 constexpr int kLongRound = 128;
+// With fewer tiles than resident warps every tile of >= SS_LONG_MIN entries goes to
+// k_forward_long (config 2: 193 -> 148 us against the 148 longest only).
+#ifndef SS_LONG_TARGET
+#define SS_LONG_TARGET ntiles  // tiles handed to k_forward_long (at most)
+#endif
+#ifndef SS_LONG_BPS
+#define SS_LONG_BPS 6  // k_forward_long blocks per SM (persistent, tickets; 37 KB shared each)
+#endif
+
 
 __global__ void __launch_bounds__(128) k_forward_long(
     BlendParams bp, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
@@ -545,6 +626,15 @@ __global__ void __launch_bounds__(128) k_forward_long(
     for (int round = 0; round * kLongRound < L; ++round) {
       const int buf = round & 1;
       const float* stg = lsm + (size_t)buf * kLongRound * kStride;
+      if (bp.segst && comp && round > 0 && (round * 4) % kSegChunks == 0) {
+        float* sg = seg_state(bp.segst, cbase, round * 4);
+        sg[tid] = T;
+        sg[64 + tid] = D;
+        sg[128 + tid] = O;
+        sg[192 + tid] = N0;
+        sg[256 + tid] = N1;
+        sg[320 + tid] = N2;
+      }
       // cone test: warp w, chunk w of the round, all 64 pixels
       {
         const int cnt = min(32, L - round * kLongRound - 32 * warp);
@@ -612,6 +702,14 @@ __global__ void __launch_bounds__(128) k_forward_long(
       out_N[3 * p + 2] = N2;
       out_T[p] = T;
       out_last[p] = last;
+      if (bp.fin) {
+        const size_t P = (size_t)k.W * k.H;
+        bp.fin[p] = D;
+        bp.fin[P + p] = O;
+        bp.fin[2 * P + p] = N0;
+        bp.fin[3 * P + p] = N1;
+        bp.fin[4 * P + p] = N2;
+      }
     }
   }
 }
@@ -632,7 +730,11 @@ constexpr bool kBwdDF = false;
 constexpr bool kBwdDF = true;  // float-pair intersection in the backward (230 -> 209 us)
 #endif
 
-template <int TS, bool kSplit>
+// kSeg: work slots are (tile << 16) | segment; a slot walks chunks
+// [kSegChunks * segment, kSegChunks * (segment + 1)) back to front, starting
+// from the state the forward recorded before the segment's end (T) and the
+// suffix sums behind it (final - recorded D, O, N -> Q).
+template <int TS, bool kSplit, bool kSeg>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1)
     k_backward(BlendParams bp, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
                const int* __restrict__ pairs, const SplatRec* __restrict__ rec, const SplatRec64* __restrict__ rec64,
@@ -655,7 +757,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
   int roff[8];
   red_offsets(lane, roff);
   for (int code = next_tile(counter, order, nslots, lane); code >= 0; code = next_tile(counter, order, nslots, lane)) {
-    const int t = code >> 2, part = kSplit ? (code & 3) : 0;
+    const int t = kSeg ? (code >> 16) : (code >> 2), part = kSplit ? (code & 3) : 0;
+    const int seg = kSeg ? (code & 0xffff) : 0;
     const int tr = t / k.tx, tc = t % k.tx;
     TileFrame f;
     tile_frame<TS>(k, tr, tc, f);
@@ -686,15 +789,37 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     if (maxlast == 0) continue;
     const int lo = tile_ptr[t];
     const int cbase = chunk_ptr[t];
+    int c_lo = 0, top = (maxlast - 1) >> 5;
+    if (kSeg) {
+      c_lo = seg * kSegChunks;
+      if (c_lo > top) continue;  // no pixel reaches this segment (warp-uniform)
+      const int c_hi = c_lo + kSegChunks;
+      if (c_hi <= top) {  // later segments contribute: start from the recorded state
+        const float* sg = seg_state(bp.segst, cbase, c_hi);
+        const size_t P = (size_t)k.W * k.H;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          if (last[j] == 0) continue;  // (inside, contributing pixels only)
+          const int q = lane + 32 * j;
+          const size_t p = (size_t)px[j].row * k.W + px[j].col;
+          T[j] = sg[q];
+          Q[j] = gD[j] * (bp.fin[p] - sg[64 + q]) + gO[j] * (bp.fin[P + p] - sg[128 + q]) +
+                 gN[j][0] * (bp.fin[2 * P + p] - sg[192 + q]) + gN[j][1] * (bp.fin[3 * P + p] - sg[256 + q]) +
+                 gN[j][2] * (bp.fin[4 * P + p] - sg[320 + q]);
+        }
+        top = c_hi - 1;
+      }
+    }
     // Software pipeline over chunks (back to front): the contribution words
     // and splat ids of chunk c-2 are loaded and the active records of chunk
     // c-1 are copied (cp.async) while chunk c is processed.
     auto load_words = [&](int c, unsigned (&wd)[PPL], int& sid) {
 #pragma unroll
       for (int j = 0; j < PPL; ++j)
-        wd[j] = (c >= 0 && (part == 0 || part == j + 1)) ? bitmask[(size_t)(cbase + c) * (TS * TS) + lane + 32 * j]
-                                                         : 0u;
-      sid = (c >= 0 && c * 32 + lane < tile_ptr[t + 1] - lo) ? pairs[lo + c * 32 + lane] : -1;
+        wd[j] = (c >= c_lo && (part == 0 || part == j + 1))
+                    ? bitmask[(size_t)(cbase + c) * (TS * TS) + lane + 32 * j]
+                    : 0u;
+      sid = (c >= c_lo && c * 32 + lane < tile_ptr[t + 1] - lo) ? pairs[lo + c * 32 + lane] : -1;
     };
     auto or_words = [&](const unsigned (&wd)[PPL]) {
       unsigned m = 0u;
@@ -702,7 +827,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       for (int j = 0; j < PPL; ++j) m |= wd[j];
       return __reduce_or_sync(0xffffffffu, m);
     };
-    const int top = (maxlast - 1) >> 5;
     unsigned wcur[PPL], wnext[PPL], wnn[PPL];
     int scur, snext, snn;
     load_words(top, wcur, scur);
@@ -710,7 +834,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     if (((any_cur >> lane) & 1u) && scur >= 0) prefetch_entry(&raw_all[warp][top & 1][lane], scur, rec, rec64);
     __pipeline_commit();
     load_words(top - 1, wnext, snext);
-    for (int chunk = top; chunk >= 0; --chunk) {
+    for (int chunk = top; chunk >= c_lo; --chunk) {
       const int base = chunk * 32;
       const unsigned any_next = or_words(wnext);
       if (((any_next >> lane) & 1u) && snext >= 0)
@@ -1024,17 +1148,18 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   template __global__ void k_forward<TS, SPLIT>(BlendParams, int, const int*, const int*, const int*,               \
                                                 const SplatRec*, const SplatRec64*, float*, float*, float*, float*,  \
                                                 int*, unsigned*, const int*, const int*, int*, const int*);
-#define SS_INST_BWD(TS, SPLIT)                                                                                  \
-  template __global__ void k_backward<TS, SPLIT>(BlendParams, int, const int*, const int*, const int*,              \
+#define SS_INST_BWD(TS, SPLIT, SEG)                                                                             \
+  template __global__ void k_backward<TS, SPLIT, SEG>(BlendParams, int, const int*, const int*, const int*,         \
                                                  const SplatRec*, const SplatRec64*, const float*, const int*,       \
                                                  const unsigned*, const float*, const float*, const float*, float*,  \
                                                  const int*, const int*, int*, const int*, float*);
 SS_INST_FWD(8, false)
 
 SS_INST_FWD(16, false)
-SS_INST_BWD(8, false)
-SS_INST_BWD(8, true)
-SS_INST_BWD(16, false)
+SS_INST_BWD(8, false, false)
+SS_INST_BWD(8, true, false)
+SS_INST_BWD(8, false, true)
+SS_INST_BWD(16, false, false)
 
 // Deterministic mode: zero the per-position accumulators of the current pair count.
 __global__ void k_zero_pacc(float4* __restrict__ pacc, const long long* __restrict__ totals, long long cap) {

@@ -162,6 +162,14 @@ struct ss_records {
   int* pairs = nullptr;  // == pbucket: final per-tile lists
   unsigned* bitmask = nullptr;
   size_t cap_bitmask = 0;
+  // segment-parallel backward (few tiles): recorded pixel states, finals, work slots
+  bool seg = false;
+  float* segst = nullptr;
+  size_t cap_segst = 0;
+  float* fin = nullptr;
+  size_t cap_fin = 0;
+  int* segorder = nullptr;
+  size_t cap_segorder = 0;
   int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long
   size_t cap_misc = 0;
   long long* totals = nullptr;
@@ -236,11 +244,12 @@ void set_smem_attrs() {
   const int bytes = (int)(sizeof(uint32_t) * kMaxTiles);
   cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_backward<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
-  cudaFuncSetAttribute(k_backward<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sort_smem_bytes<kTileSortBig, 1024>());
-  cudaFuncSetAttribute(k_backward<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
+  cudaFuncSetAttribute(k_backward<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   done = true;
 }
 }  // namespace
@@ -274,7 +283,7 @@ void ss_records_destroy(ss_records* r, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   void* bufs[] = {r->rec,    r->rec64,   r->key64, r->key32,  r->rect, r->bsum, r->mat, r->tint,
                   r->tiles,  r->ptile,   r->psplat, r->pbucket, r->bitmask, r->misc, r->totals,
-                  r->Tf,     r->last,    r->acc,     r->pacc};
+                  r->Tf,     r->last,    r->acc,     r->pacc,  r->segst, r->fin, r->segorder};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, s);
   cudaStreamSynchronize(s);
@@ -346,10 +355,24 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets, [2] work slots
   // fewer tiles than resident blend warps (4 blocks x 4 warps per SM): split the longest in two
   // (not in deterministic mode: both halves of a split tile would write one list position)
-  const int split_target = (k.T == 8 && !rec->deterministic) ? std::max(0, num_sms() * 16 - ntiles) : 0;
+  // With few tiles the backward walks segments of kSegChunks chunks of each list in
+  // parallel (instead of splitting tiles into pixel halves): the forward records
+  // the per-pixel state at the segment boundaries.
+  const bool seg = SS_SEG_MODE && k.T == 8 && num_sms() * 16 > ntiles;
+  rec->seg = seg;
+  const int split_target = (k.T == 8 && !rec->deterministic && !seg) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
-  // ... and hand the longest lists (>= 768 entries) to the block-per-tile forward
-  const int long_target = (k.T == 8 && num_sms() * 16 > ntiles) ? num_sms() : 0;
+  if (seg) {
+    const size_t nchunk = (size_t)cap / 32 + ntiles + 1;
+    if (grow(rec->segst, rec->cap_segst, (nchunk / kSegChunks + 2) * 6 * 64, s) ||
+        grow(rec->fin, rec->cap_fin, (size_t)5 * P, s) ||
+        grow(rec->segorder, rec->cap_segorder, nchunk / kSegChunks + 2 * (size_t)ntiles + 2, s))
+      return SS_ERR_CUDA;
+  }
+  rec->bp.segst = seg ? rec->segst : nullptr;
+  rec->bp.fin = seg ? rec->fin : nullptr;
+  // ... and hand the long lists (>= SS_LONG_MIN entries) to the block-per-tile forward
+  const int long_target = (k.T == 8 && num_sms() * 16 > ntiles) ? SS_LONG_TARGET : 0;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -388,6 +411,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
     k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target,
                                     long_target);
+    if (seg) k_seg_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
   }
   rec->pairs = (int*)rec->pbucket;
   const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
@@ -396,7 +420,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     if (long_target) {  // the longest tiles, one block each, concurrently on the side stream
       SS_CUDA_TRY(cudaEventRecord(rec->long_fork, s));
       SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->long_fork, 0));
-      k_forward_long<<<long_target, 128, kLongSmem, rec->side>>>(
+      k_forward_long<<<std::min(long_target, num_sms() * SS_LONG_BPS), 128, kLongSmem, rec->side>>>(
           rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity,
           rec->Tf, rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1), counters + 4, counters + 5);
       SS_CUDA_TRY(cudaEventRecord(rec->long_join, rec->side));
@@ -551,13 +575,17 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
     int* order = rec->tiles + 5 * (ntiles + 1);
     int* counters = rec->misc + 4;
     StageTimer tm(rec, ST_BACKWARD, s);
-    if (rec->cam.T == 8)
-      (rec->split_target ? k_backward<8, true> : k_backward<8, false>)<<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+    if (rec->cam.T == 8 && rec->seg)  // segment slots: persistent warps, as many as are resident
+      k_backward<8, false, true><<<num_sms() * SS_BWD_MINB, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
+          rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
+          dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc);
+    else if (rec->cam.T == 8)
+      (rec->split_target ? k_backward<8, true, false> : k_backward<8, false, false>)<<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
                                                            rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
                                                            pacc);
     else
-      k_backward<16, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
+      k_backward<16, false, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
                                                             rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
                                                             dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
                                                            pacc);

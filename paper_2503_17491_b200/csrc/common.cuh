@@ -95,3 +95,13 @@ __device__ __forceinline__ void ray_at(const CamK& k, double u, double v, double
     cudaError_t _e = (expr);                       \
     if (_e != cudaSuccess) return SS_ERR_CUDA;     \
   } while (0)
+
+// entries for a tile to count as long (k_tile_order -> k_forward_long)
+#ifndef SS_LONG_MIN
+#define SS_LONG_MIN 256
+#endif
+
+// segment-parallel backward when tiles are few (blend.cu kSegChunks)
+#ifndef SS_SEG_MODE
+#define SS_SEG_MODE 1
+#endif
