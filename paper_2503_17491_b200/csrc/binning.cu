@@ -29,6 +29,10 @@ struct Incidence {
   double azc, elc, omega, dgam;
 };
 
+constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile (8 warps)
+constexpr int kTileSortBig = 8192;                // long-list variant (32 warps, dynamic shared memory)
+constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> merge-sort fallback
+
 // np.mod(x, 2*pi) for x = d + pi with d a difference of two angles in
 // [-pi, pi]: fmod is exact, so the subtraction below is bit-identical.
 __device__ __forceinline__ double mod_2pi(double x) {
@@ -220,7 +224,10 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
 }
 
 
-__global__ void __launch_bounds__(256)
+#ifndef SS_PRE_MINB
+#define SS_PRE_MINB 5  // 48 registers (A/B at config 1: 62 -> 53 us)
+#endif
+__global__ void __launch_bounds__(256, SS_PRE_MINB)
     k_preprocess(SplatsK sp, PoseK pose, CamK cam, RasterK rk, const double2* __restrict__ colt,
                  const double2* __restrict__ rowt, SplatRec* __restrict__ rec, SplatRec64* __restrict__ rec64,
                  unsigned long long* __restrict__ key64, uint32_t* __restrict__ key32, int4* __restrict__ rect,
@@ -381,7 +388,8 @@ __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restric
 }
 
 __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int* __restrict__ tile_ptr,
-                             int* __restrict__ chunk_ptr, long long* __restrict__ totals) {
+                             int* __restrict__ chunk_ptr, long long* __restrict__ totals, int* __restrict__ long_list,
+                             int* __restrict__ n_long) {
   __shared__ long long s_p[1024];
   __shared__ long long s_c[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -411,6 +419,7 @@ __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int
     chunk_ptr[t] = (int)rc;
     rp += c;
     rc += (c + 31) >> 5;
+    if (c > kTileSortMax) long_list[atomicAdd(n_long, 1)] = t;  // k_tile_sort_big, concurrently
   }
   if (tid == nt - 1) {
     tile_ptr[ntiles] = (int)s_p[nt - 1];
@@ -447,9 +456,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile (8 warps)
-constexpr int kTileSortBig = 8192;                // long-list variant (32 warps, dynamic shared memory)
-constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> merge-sort fallback
 
 struct SortSmem {
   uint16_t* sk[2];  // [MAX] 16-bit keys
@@ -651,7 +657,9 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
 }
 
 // Regular tiles (L <= kTileSortMax), one 256-thread block per tile; longer
-// lists go to long_list for k_tile_sort_big.
+// lists are sorted by k_tile_sort_big on a side stream at the same time, and a
+// tile whose shared-memory sort gives up (a long run of equal keys) goes to
+// a second list for a big-sort pass afterwards.
 #ifndef SS_SORT_NT
 #define SS_SORT_NT 256
 #endif
@@ -666,11 +674,7 @@ __global__ void __launch_bounds__(kTileSortNT) k_tile_sort(const int* __restrict
   if (*overflow) return;
   const int t = blockIdx.x;
   const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
-  if (L <= 1) return;
-  if (L > kTileSortMax) {
-    if (threadIdx.x == 0) long_list[atomicAdd(n_long, 1)] = t;
-    return;
-  }
+  if (L <= 1 || L > kTileSortMax) return;  // (longer lists: k_scan_tiles listed them for the big sort)
   const SortSmem m = carve_sort_smem<kTileSortMax, kTileSortNT>(smem);
   if (!sort_tile_smem<kTileSortMax, kTileSortNT>(m, pairs, lo, L, key32, key64) && threadIdx.x == 0)
     long_list[atomicAdd(n_long, 1)] = t;  // long run of equal keys: the big kernel's merge fallback

@@ -150,7 +150,7 @@ struct ss_records {
   // per camera / tile
   double2* tint = nullptr;  // tx column + ty row intervals
   size_t cap_tint = 0;
-  int* tiles = nullptr;  // tile_ptr | chunk_ptr | tile_count | cursor | long_list
+  int* tiles = nullptr;  // tile_ptr | chunk_ptr | tile_count | long_list2 | long_list | order (2) | order_fwd
   size_t cap_tiles = 0;
   // pairs: emitted (tile, splat) and the bucketed per-tile lists
   uint32_t* ptile = nullptr;
@@ -170,7 +170,7 @@ struct ss_records {
   size_t cap_fin = 0;
   int* segorder = nullptr;
   size_t cap_segorder = 0;
-  int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long
+  int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long, [3] n_long2, [4..9] blend counters
   size_t cap_misc = 0;
   long long* totals = nullptr;
   size_t cap_totals = 0;
@@ -186,6 +186,7 @@ struct ss_records {
   cudaEvent_t done = nullptr;
   cudaEvent_t fwd_end = nullptr;  // forward kernels finished (side-stream fork point)
   cudaEvent_t long_fork = nullptr, long_join = nullptr;  // block-per-tile forward on `side`
+  cudaEvent_t sort_fork = nullptr, sort_join = nullptr;  // big-list tile sort on `side`
   cudaStream_t side = nullptr;    // publishes the totals off the compute stream
   // optional per-stage CUDA-event timing (bench.py roofline), stream-ordered
   bool profiling = false;
@@ -274,6 +275,8 @@ ss_records* ss_records_create(void) {
   cudaEventCreateWithFlags(&r->fwd_end, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&r->long_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&r->long_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&r->sort_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&r->sort_join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
   return r;
 }
@@ -296,6 +299,8 @@ void ss_records_destroy(ss_records* r, void* stream) {
   if (r->fwd_end) cudaEventDestroy(r->fwd_end);
   if (r->long_fork) cudaEventDestroy(r->long_fork);
   if (r->long_join) cudaEventDestroy(r->long_join);
+  if (r->sort_fork) cudaEventDestroy(r->sort_fork);
+  if (r->sort_join) cudaEventDestroy(r->sort_join);
   if (r->side) cudaStreamDestroy(r->side);
   if (r->h_totals) cudaFreeHost(r->h_totals);
   delete r;
@@ -351,6 +356,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* chunk_ptr = rec->tiles + (ntiles + 1);
   int* tile_count = rec->tiles + 2 * (ntiles + 1);
   int* long_list = rec->tiles + 4 * (ntiles + 1);
+  int* long_list2 = rec->tiles + 3 * (ntiles + 1);  // shared-memory sort fallbacks
   int* order = rec->tiles + 5 * (ntiles + 1);  // up to 2 * ntiles work slots
   int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets, [2] work slots
   // fewer tiles than resident blend warps (4 blocks x 4 warps per SM): split the longest in two
@@ -358,7 +364,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   // With few tiles the backward walks segments of kSegChunks chunks of each list in
   // parallel (instead of splitting tiles into pixel halves): the forward records
   // the per-pixel state at the segment boundaries.
-  const bool seg = SS_SEG_MODE && k.T == 8 && num_sms() * 16 > ntiles;
+  const bool seg = SS_SEG_MODE && k.T == 8 && (SS_SEG_ALWAYS || num_sms() * 16 > ntiles);
   rec->seg = seg;
   const int split_target = (k.T == 8 && !rec->deterministic && !seg) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
@@ -372,10 +378,11 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   rec->bp.segst = seg ? rec->segst : nullptr;
   rec->bp.fin = seg ? rec->fin : nullptr;
   // ... and hand the long lists (>= SS_LONG_MIN entries) to the block-per-tile forward
-  const int long_target = (k.T == 8 && num_sms() * 16 > ntiles) ? SS_LONG_TARGET : 0;
+  const int long_target = (k.T == 8 && (SS_LONG_ALWAYS || num_sms() * 16 > ntiles)) ? SS_LONG_TARGET : 0;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
+  int* n_long2 = rec->misc + 3;
   double2* colt = rec->tint;
   double2* rowt = rec->tint + k.tx;
 
@@ -400,15 +407,24 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     set_smem_attrs();
     k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow);
     k_tile_prefix<<<(ntiles + 31) / 32, dim3(32, 32), 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count);
-    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals);
+    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long);
     k_tile_scatter<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
                                               rec->pbucket, overflow);
   }
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
-    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list, n_long, overflow);
-    k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
+    // lists over kTileSortMax (listed by k_scan_tiles) sort on the side stream while the
+    // regular ones sort here; tiles the shared-memory sort gave up on follow afterwards
+    SS_CUDA_TRY(cudaEventRecord(rec->sort_fork, s));
+    SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->sort_fork, 0));
+    k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
+    SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
+    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list2, n_long2,
+                                              overflow);
+    SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->sort_join, 0));
+    k_tile_sort_big<<<std::min(num_sms(), 16), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
+        tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list2, n_long2);
     k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target,
                                     long_target);
     if (seg) k_seg_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);

@@ -105,3 +105,9 @@ __device__ __forceinline__ void ray_at(const CamK& k, double u, double v, double
 #ifndef SS_SEG_MODE
 #define SS_SEG_MODE 1
 #endif
+#ifndef SS_SEG_ALWAYS
+#define SS_SEG_ALWAYS 0
+#endif
+#ifndef SS_LONG_ALWAYS
+#define SS_LONG_ALWAYS 0
+#endif
