@@ -25,3 +25,21 @@ for r in rows[2:]:
   python tools/sass_regions.py gpurun_out/prof_round.ncu-rep k_forward
 } > profiles/${tag}_ncu_full_summary.txt
 cat profiles/${tag}_ncu_full_summary.txt | head -12
+if [ -f gpurun_out/prof_map.ncu-rep ]; then
+  {
+    echo "# ncu --set full (clock-control none), config-2 mapping refine (tools/map_step.py), B200"
+    python tools/ncu_summary.py gpurun_out/prof_map.ncu-rep
+    echo
+    echo "# SASS regions of k_forward_long"
+    python tools/sass_regions.py gpurun_out/prof_map.ncu-rep k_forward_long
+  } > profiles/${tag}_ncu_map_summary.txt
+fi
+if [ -f gpurun_out/prof_reg.ncu-rep ]; then
+  {
+    echo "# ncu --set full (clock-control none), config-3 geometric registration (tools/geo_probe.py), B200"
+    python tools/ncu_summary.py gpurun_out/prof_reg.ncu-rep
+    echo
+    echo "# SASS regions of k_reg_solve"
+    python tools/sass_regions.py gpurun_out/prof_reg.ncu-rep k_reg_solve 0.01
+  } > profiles/${tag}_ncu_reg_summary.txt
+fi
