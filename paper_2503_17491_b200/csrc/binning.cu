@@ -657,18 +657,20 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
 }
 
 // Regular tiles (L <= kTileSortMax), one 256-thread block per tile; longer
-// lists are sorted by k_tile_sort_big on a side stream at the same time, and a
-// tile whose shared-memory sort gives up (a long run of equal keys) goes to
-// a second list for a big-sort pass afterwards.
+// lists are sorted by k_tile_sort_big on a side stream at the same time.  A
+// tile whose shared-memory sort gives up (a long run of equal keys) is merge
+// sorted in place by the same block (tmp: scratch of the list's size).
 #ifndef SS_SORT_NT
 #define SS_SORT_NT 256
 #endif
 constexpr int kTileSortNT = SS_SORT_NT;
 
+__device__ void merge_sort_tile(uint32_t* __restrict__ pairs, uint32_t* __restrict__ tmp, int lo, int L,
+                                const unsigned long long* __restrict__ key);
+
 __global__ void __launch_bounds__(kTileSortNT) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
-                                                   const uint32_t* __restrict__ key32,
+                                                   uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key32,
                                                    const unsigned long long* __restrict__ key64,
-                                                   int* __restrict__ long_list, int* __restrict__ n_long,
                                                    const int* __restrict__ overflow) {
   __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, kTileSortNT>()];
   if (*overflow) return;
@@ -676,8 +678,8 @@ __global__ void __launch_bounds__(kTileSortNT) k_tile_sort(const int* __restrict
   const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
   if (L <= 1 || L > kTileSortMax) return;  // (longer lists: k_scan_tiles listed them for the big sort)
   const SortSmem m = carve_sort_smem<kTileSortMax, kTileSortNT>(smem);
-  if (!sort_tile_smem<kTileSortMax, kTileSortNT>(m, pairs, lo, L, key32, key64) && threadIdx.x == 0)
-    long_list[atomicAdd(n_long, 1)] = t;  // long run of equal keys: the big kernel's merge fallback
+  if (!sort_tile_smem<kTileSortMax, kTileSortNT>(m, pairs, lo, L, key32, key64))
+    merge_sort_tile(pairs, tmp, lo, L, key64);  // long run of equal keys (block-uniform result)
 }
 
 __device__ int count_less(const uint32_t* run, int len, const unsigned long long* key, unsigned long long k,

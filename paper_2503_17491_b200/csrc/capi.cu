@@ -150,7 +150,7 @@ struct ss_records {
   // per camera / tile
   double2* tint = nullptr;  // tx column + ty row intervals
   size_t cap_tint = 0;
-  int* tiles = nullptr;  // tile_ptr | chunk_ptr | tile_count | long_list2 | long_list | order (2) | order_fwd
+  int* tiles = nullptr;  // tile_ptr | chunk_ptr | tile_count | (unused) | long_list | order (2) | order_fwd
   size_t cap_tiles = 0;
   // pairs: emitted (tile, splat) and the bucketed per-tile lists
   uint32_t* ptile = nullptr;
@@ -170,7 +170,7 @@ struct ss_records {
   size_t cap_fin = 0;
   int* segorder = nullptr;
   size_t cap_segorder = 0;
-  int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long, [3] n_long2, [4..9] blend counters
+  int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long, [4..9] blend counters
   size_t cap_misc = 0;
   long long* totals = nullptr;
   size_t cap_totals = 0;
@@ -356,7 +356,6 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* chunk_ptr = rec->tiles + (ntiles + 1);
   int* tile_count = rec->tiles + 2 * (ntiles + 1);
   int* long_list = rec->tiles + 4 * (ntiles + 1);
-  int* long_list2 = rec->tiles + 3 * (ntiles + 1);  // shared-memory sort fallbacks
   int* order = rec->tiles + 5 * (ntiles + 1);  // up to 2 * ntiles work slots
   int* counters = rec->misc + 4;  // [0] forward, [1] backward tile tickets, [2] work slots
   // fewer tiles than resident blend warps (4 blocks x 4 warps per SM): split the longest in two
@@ -382,7 +381,6 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
-  int* n_long2 = rec->misc + 3;
   double2* colt = rec->tint;
   double2* rowt = rec->tint + k.tx;
 
@@ -414,20 +412,21 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
     // lists over kTileSortMax (listed by k_scan_tiles) sort on the side stream while the
-    // regular ones sort here; tiles the shared-memory sort gave up on follow afterwards
+    // regular ones sort here (a regular tile whose equal-key runs defeat the shared-memory
+    // sort merge-sorts in place); the blend kernels' work order only needs the list
+    // lengths, so it is built on the side stream too
     SS_CUDA_TRY(cudaEventRecord(rec->sort_fork, s));
     SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->sort_fork, 0));
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
+    k_tile_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters,
+                                            split_target, long_target);
+    if (seg)
+      k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
-    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->key32, rec->key64, long_list2, n_long2,
+    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64,
                                               overflow);
     SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->sort_join, 0));
-    k_tile_sort_big<<<std::min(num_sms(), 16), 1024, sort_smem_bytes<kTileSortBig, 1024>(), s>>>(
-        tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list2, n_long2);
-    k_tile_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters, split_target,
-                                    long_target);
-    if (seg) k_seg_order<<<1, 1024, 0, s>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
   }
   rec->pairs = (int*)rec->pbucket;
   const int blocks = std::min((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);

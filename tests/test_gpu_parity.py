@@ -162,6 +162,21 @@ def test_long_lists_and_tie_runs_bit_exact(cuda, n, n_tie):
     assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
 
 
+def test_tie_runs_in_shared_memory_sized_lists_bit_exact(cuda):
+    """Lists short enough for the 8-warp shared-memory sort but holding a run of equal
+    ranges longer than its insertion limit: the block merge-sorts that tile in place."""
+    cam = W.synth_camera(512, 64)
+    params = _crowded_params(1600, 300, 5)
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), params)
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), SplatModel.from_params(params))
+    lens = np.diff(ref["tile_ptr"])
+    print("max list", lens.max())
+    assert 64 < lens.max() <= 2048
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"])
+    assert np.array_equal(rec.pair_splats, ref["pair_splats"])
+
+
 def test_deterministic_backward_bit_identical(cuda):
     """RasterConfig(deterministic=True): fixed-order reduction, bit-identical gradients run to run,
     within the 1e-3 gate of the oracle; the default (atomic) path agrees to float rounding."""
