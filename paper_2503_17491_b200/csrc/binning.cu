@@ -248,29 +248,65 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB)
 }
 
 
+// Block-wide (1024 threads) exclusive scan of one 64-bit value per thread by
+// warp shuffles (two barriers); *total gets the sum.
+__device__ __forceinline__ long long block_exscan_1024(long long v, long long* wsum, long long* total) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long inc = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const long long w = wsum[lane];
+    long long wi = w;
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += y;
+    }
+    wsum[lane] = wi - w;
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  return wsum[warp] + inc - v;
+}
+
 // Exclusive scan of the per-block pair counts (one block); totals[0] = pairs.
-__global__ void k_scan_blocks(int nb, uint32_t* __restrict__ block_sum, long long* __restrict__ totals) {
-  __shared__ unsigned long long part[1024];
+__global__ void __launch_bounds__(1024) k_scan_blocks(int nb, uint32_t* __restrict__ block_sum,
+                                                      long long* __restrict__ totals) {
+  __shared__ long long wsum[32], tot;
   const int tid = threadIdx.x;
   const int per = (nb + 1023) / 1024;
-  const int b = tid * per, e = min(b + per, nb);
-  unsigned long long s = 0;
-  for (int q = b; q < e; ++q) s += block_sum[q];
-  part[tid] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const unsigned long long x = tid >= off ? part[tid - off] : 0ull;
-    __syncthreads();
-    part[tid] += x;
-    __syncthreads();
+  const int b = min(tid * per, nb), e = min(b + per, nb);
+  uint32_t c[8];
+  long long s = 0;
+  if (per <= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      c[q] = b + q < e ? block_sum[b + q] : 0u;
+      s += c[q];
+    }
+  } else {
+    for (int q = b; q < e; ++q) s += block_sum[q];
   }
-  unsigned long long run = part[tid] - s;
-  for (int q = b; q < e; ++q) {
-    const uint32_t c = block_sum[q];
-    block_sum[q] = (uint32_t)run;
-    run += c;
+  long long run = block_exscan_1024(s, wsum, &tot);
+  if (per <= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (b + q < e) {
+        block_sum[b + q] = (uint32_t)run;
+        run += c[q];
+      }
+  } else {
+    for (int q = b; q < e; ++q) {
+      const uint32_t cq = block_sum[q];
+      block_sum[q] = (uint32_t)run;
+      run += cq;
+    }
   }
-  if (tid == 1023) totals[0] = (long long)part[1023];
+  if (tid == 0) totals[0] = tot;
 }
 
 // Emit the pairs of every splat at its offset (index order).  Each warp
@@ -387,32 +423,22 @@ __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restric
   }
 }
 
-__global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int* __restrict__ tile_ptr,
-                             int* __restrict__ chunk_ptr, long long* __restrict__ totals, int* __restrict__ long_list,
-                             int* __restrict__ n_long) {
-  __shared__ long long s_p[1024];
-  __shared__ long long s_c[1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (ntiles + nt - 1) / nt;
-  const int b = tid * per, e = min(b + per, ntiles);
-  long long sp = 0, sc = 0;
+__global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __restrict__ tile_count,
+                                                     int* __restrict__ tile_ptr, int* __restrict__ chunk_ptr,
+                                                     long long* __restrict__ totals, int* __restrict__ long_list,
+                                                     int* __restrict__ n_long) {
+  __shared__ long long wsum[32], tot;
+  const int tid = threadIdx.x;
+  const int per = (ntiles + 1023) / 1024;
+  const int b = min(tid * per, ntiles), e = min(b + per, ntiles);
+  // pair and chunk counts packed in one 64-bit scan (chunks <= pairs / 32 + tiles < 2^31)
+  long long s = 0;
   for (int t = b; t < e; ++t) {
     const int c = tile_count[t];
-    sp += c;
-    sc += (c + 31) >> 5;
+    s += ((long long)c << 32) + ((c + 31) >> 5);
   }
-  s_p[tid] = sp;
-  s_c[tid] = sc;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    const long long vp = tid >= off ? s_p[tid - off] : 0;
-    const long long vc = tid >= off ? s_c[tid - off] : 0;
-    __syncthreads();
-    s_p[tid] += vp;
-    s_c[tid] += vc;
-    __syncthreads();
-  }
-  long long rp = s_p[tid] - sp, rc = s_c[tid] - sc;
+  const long long ex = block_exscan_1024(s, wsum, &tot);
+  long long rp = ex >> 32, rc = ex & 0xffffffffll;
   for (int t = b; t < e; ++t) {
     const int c = tile_count[t];
     tile_ptr[t] = (int)rp;
@@ -421,10 +447,10 @@ __global__ void k_scan_tiles(int ntiles, const int* __restrict__ tile_count, int
     rc += (c + 31) >> 5;
     if (c > kTileSortMax) long_list[atomicAdd(n_long, 1)] = t;  // k_tile_sort_big, concurrently
   }
-  if (tid == nt - 1) {
-    tile_ptr[ntiles] = (int)s_p[nt - 1];
-    chunk_ptr[ntiles] = (int)s_c[nt - 1];
-    totals[1] = s_c[nt - 1];
+  if (tid == 0) {
+    tile_ptr[ntiles] = (int)(tot >> 32);
+    chunk_ptr[ntiles] = (int)(tot & 0xffffffffll);
+    totals[1] = tot & 0xffffffffll;
   }
 }
 
