@@ -847,17 +847,7 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   const int gmask = nbk - 1;
   const size_t gsmem = rs_grid_smem_bytes(nl, gmask);
   const bool staged = nl > 0 && gsmem <= (size_t)96 * 1024;
-  // then the |r| patterns of the larger family, for the per-block median select
-  int dev = 0, optin = 0;
-  SS_CUDA_TRY(cudaGetDevice(&dev));
-  SS_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  cudaFuncAttributes fa{};
-  SS_CUDA_TRY(cudaFuncGetAttributes(&fa, k_reg_solve));
-  const size_t budget = (size_t)std::max(0, optin - (int)fa.sharedSizeBytes - 1024);
-  const size_t sel_off = staged ? (gsmem + 15) / 16 * 16 : 0;
-  const int nfam = std::max(need_geo ? n_geo_scan : 0, need_photo ? M : 0);
-  const bool sel_fits = sel_off + (size_t)nfam * 8 <= budget;
-  const size_t dyn = sel_fits ? sel_off + (size_t)nfam * 8 : (staged ? gsmem : 0);
+  const size_t dyn = staged ? gsmem : 0;
   if (dyn > 0) SS_CUDA_TRY(cudaFuncSetAttribute(k_reg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int occ = 0;
   SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, dyn));
@@ -908,8 +898,6 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   k.min_residuals = cfg->min_residuals;
   k.assoc_k = cfg->assoc_k;
   k.mode = cfg->mode;
-  k.sel_off = (int)sel_off;
-  k.sel_cap = sel_fits ? nfam : -1;
   RsGeo geo{leaf_centroids, leaf_normals, nl, geo_scan, ng, bstart, ent, inv_cs, gmask, staged ? 1 : 0};
   RsPhoto ph{X_w, m, scan_range, scan_valid};
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,

@@ -36,7 +36,6 @@ struct RegSolveCfg {
   double huber_photo, huber_geo, trim_factor, spread_gate, assoc_gate, floor_photo, floor_geo, tol, damping_init,
       damping_max;
   int max_iters, min_residuals, assoc_k, mode;
-  int sel_off, sel_cap;  // families with n <= sel_cap select their median per block, |r| staged at dyn smem + sel_off
 };
 
 constexpr int kRsThreads = 256;
@@ -481,130 +480,6 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
   return (v1 + __longlong_as_double((long long)*((volatile unsigned long long*)vmin))) / 2.0;
 }
 
-// Exact median of the valid patterns in sv[0, n) (shared memory), one block, no
-// grid barrier.  A first sweep finds the count and the smallest / largest
-// pattern; the radix passes then start at the highest bit in which those two
-// differ (12-bit digits downwards), so the first histogram already splits the
-// occupied range instead of the mostly shared exponent bits.  *s_m gets the
-// number of valid entries (the median is 0 when there are none).
-__device__ double rs_median_block(const unsigned long long* sv, int n, unsigned* sh, unsigned* s_part, int* s_bin,
-                                  int* s_before, unsigned long long* s_min, int* s_m) {
-  __shared__ int s_ng;
-  __shared__ unsigned long long s_max[kRsThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  RS_SUB(-1);
-  int cnt = 0;
-  unsigned long long mn = ~0ull, mx = 0ull;
-  for (int i = tid; i < n; i += kRsThreads) {
-    const unsigned long long b = sv[i];
-    if (b != ~0ull) {
-      ++cnt;
-      mn = min(mn, b);
-      mx = max(mx, b);
-    }
-  }
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  for (int off = 16; off > 0; off >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-  }
-  if (lane == 0) {
-    s_part[warp] = (unsigned)cnt;
-    s_min[warp] = mn;
-    s_max[warp] = mx;
-  }
-  __syncthreads();
-  int m = 0;
-  for (int w = 0; w < kRsThreads / 32; ++w) {
-    m += (int)s_part[w];
-    mn = min(mn, s_min[w]);
-    mx = max(mx, s_max[w]);
-  }
-  *s_m = m;  // (every thread writes the same value)
-  __syncthreads();
-  RS_SUB(0);
-  if (m == 0) return 0.0;
-  if (mn == mx) return __longlong_as_double((long long)mn);  // all equal
-  const int k1 = (m % 2 == 0) ? m / 2 - 1 : m / 2;
-  int kk = k1, cnt_eq = 0, top = 63 - __clzll(mn ^ mx);  // <= 62: valid patterns are non-negative doubles
-  unsigned long long mask = ~((2ull << top) - 1ull), prefix = mn & mask;
-  bool exact = false;
-  unsigned long long v2c = ~0ull;
-  for (;;) {
-    const int lo = max(top - 11, 0);
-    const unsigned dmask = (1u << (top - lo + 1)) - 1u;
-    for (int j = tid; j <= (int)dmask; j += kRsThreads) sh[j] = 0u;
-    __syncthreads();
-    for (int i = tid; i < n; i += kRsThreads) {
-      const unsigned long long b = sv[i];
-      if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
-    }
-    __syncthreads();
-    RS_SUB(1);
-    rs_find_bin(sh, (int)dmask + 1, kk, s_bin, s_before, s_part);
-    RS_SUB(2);
-    const int bin = *s_bin;
-    kk -= *s_before;
-    const int cnt_bin = (int)sh[bin];
-    prefix |= (unsigned long long)bin << lo;
-    mask |= (unsigned long long)dmask << lo;
-    __syncthreads();
-    if (lo == 0) {
-      cnt_eq = cnt_bin;
-      exact = true;
-      break;
-    }
-    top = lo - 1;
-    if (cnt_bin <= kRsCand) {
-      // few values share the prefix: gather and rank them exactly
-      unsigned long long* sc = reinterpret_cast<unsigned long long*>(sh);  // kRsCand x 8 B fits
-      if (tid == 0) s_ng = 0;
-      __syncthreads();
-      for (int i = tid; i < n; i += kRsThreads) {
-        const unsigned long long b = sv[i];
-        if (b != ~0ull && (b & mask) == prefix) sc[atomicAdd(&s_ng, 1)] = b;
-      }
-      __syncthreads();
-      RS_SUB(3);
-      for (int j = tid; j < cnt_bin; j += kRsThreads) {
-        const unsigned long long c = sc[j];
-        int lt = 0, eqb = 0;
-        for (int q = 0; q < cnt_bin; ++q) {
-          lt += sc[q] < c;
-          eqb += (sc[q] == c) & (q < j);
-        }
-        const int rank = lt + eqb;  // distinct ranks 0..cnt_bin-1
-        if (rank == kk) sh[2 * kRsCand] = (unsigned)j;
-        if (rank == kk + 1) sh[2 * kRsCand + 1] = (unsigned)j;
-      }
-      if (tid == 0 && kk + 1 >= cnt_bin) sh[2 * kRsCand + 1] = 0xffffffffu;
-      __syncthreads();
-      prefix = sc[sh[2 * kRsCand]];
-      const unsigned j2 = sh[2 * kRsCand + 1];
-      v2c = j2 == 0xffffffffu ? ~0ull : sc[j2];
-      __syncthreads();
-      RS_SUB(4);
-      break;
-    }
-  }
-  const double v1 = __longlong_as_double((long long)prefix);
-  if (m % 2 != 0) return v1;
-  if (!exact && v2c != ~0ull) return (v1 + __longlong_as_double((long long)v2c)) / 2.0;
-  if (exact && k1 + 1 < (k1 - kk) + cnt_eq) return v1;
-  RS_SUB(5);
-  unsigned long long nx = ~0ull;
-  for (int i = tid; i < n; i += kRsThreads) {
-    const unsigned long long b = sv[i];
-    if (b != ~0ull && b > prefix) nx = min(nx, b);
-  }
-  for (int off = 16; off > 0; off >>= 1) nx = min(nx, __shfl_xor_sync(0xffffffffu, nx, off));
-  if (lane == 0) s_min[warp] = nx;
-  __syncthreads();
-  for (int w = 0; w < kRsThreads / 32; ++w) nx = min(nx, s_min[w]);
-  __syncthreads();
-  return (v1 + __longlong_as_double((long long)nx)) / 2.0;
-}
-
 // Block count of valid entries -> grid total (pcnt: per-block slots), and the
 // grid's smallest / largest valid pattern (pmm: per-block pairs) -> s_mm[0..1].
 __device__ int rs_count(cg::grid_group& grid, int okc, unsigned long long mn, unsigned long long mx,
@@ -841,6 +716,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
   __shared__ int s_bin, s_before, s_m;
   __shared__ unsigned long long s_min[kRsThreads / 32];
   __shared__ unsigned long long s_mm[2 * (kRsThreads / 32) + 2];
+  __shared__ unsigned long long s_pub[16];
+  static_assert(offsetof(RegSolveState, eval_photo) + sizeof(int) <= 16 * 8, "published fields in the first 16 words");
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = G * kRsThreads;
   const int kmax = min(min(cfg.assoc_k, geo.n_leaves), 8);
@@ -879,14 +756,20 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
   for (int e = 0;; ++e) {
     grid.sync();
     RS_MARK(0);
-    volatile RegSolveState* vs = st;
+    RS_SUB(-1);
+    // the published evaluation (P, floors, flags: the first 16 words of the state),
+    // loaded by one warp in parallel instead of ~18 dependent volatile loads per thread
+    if (tid < 16) s_pub[tid] = ((volatile unsigned long long*)st)[tid];
+    __syncthreads();
+    const RegSolveState* vs = reinterpret_cast<const RegSolveState*>(s_pub);
     if (vs->action == RS_DONE) {
 #ifdef SS_RS_PROF
       if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("RSPROF evals %d step+sync %llu resid %llu count %llu median %llu accum %llu part %llu sync %llu final %llu"
-               " | sub %llu %llu %llu %llu %llu %llu\n",
+               " | sub %llu %llu %llu %llu %llu %llu | state %llu zero %llu\n",
                e, rs_prof[0], rs_prof[1], rs_prof[2], rs_prof[3], rs_prof[4], rs_prof[5], rs_prof[6], rs_prof[7],
-               g_rs_sub[0], g_rs_sub[1], g_rs_sub[2], g_rs_sub[3], g_rs_sub[4], g_rs_sub[5]);
+               g_rs_sub[0], g_rs_sub[1], g_rs_sub[2], g_rs_sub[3], g_rs_sub[4], g_rs_sub[5], g_rs_sub[6],
+               g_rs_sub[7]);
       if (blockIdx.x == 0 && threadIdx.x == 0)
         for (int q = 0; q < 8; ++q) g_rs_sub[q] = 0;
 #endif
@@ -898,6 +781,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
     const double fgeo = vs->fg, fph = vs->fp;
     const int objective_only = vs->objective_only;
     const int fam_on[2] = {vs->eval_geo && geo.n_leaves > 0, vs->eval_photo};
+    RS_SUB(6);
     const int par = e & 1;
     // zero the next evaluation's scratch
     unsigned* Hnext = hist + (size_t)(par ^ 1) * 2 * kRsPasses * kRsBins;
@@ -915,6 +799,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
       unsigned* Hc = hist + ((size_t)par * 2 + f) * kRsPasses * kRsBins;
       unsigned long long* bits = f == 0 ? gbits : pbits;
       const int n = f == 0 ? geo.n_scan : ph.M;
+      RS_SUB(7);
       // --- residuals
       int okc = 0;
       unsigned long long vlo = ~0ull, vhi = 0ull;  // this thread's smallest / largest valid |r| pattern
@@ -987,40 +872,40 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         }
         okc = ok;
       } else {
-        for (int i = gtid; i < n; i += nthr) {
-          PhotoTmp t{};
-          const bool ok = photo_resid_one(ph.X, i, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t);
-          ptmp[i] = t;
-          const unsigned long long bv = ok ? (unsigned long long)__double_as_longlong(fabs(t.r)) : ~0ull;
-          bits[i] = bv;
-          if (ok) {
-            vlo = min(vlo, bv);
-            vhi = max(vhi, bv);
+        // two anchors per pass (branch-free residuals interleave; M ~ 1-2x the grid's threads)
+        for (int i = gtid; i < n; i += 2 * nthr) {
+          const int i2 = i + nthr < n ? i + nthr : i;
+          PhotoTmp t[2];
+          bool ok[2];
+          ok[0] = photo_resid_nb(ph.X, i, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[0]);
+          ok[1] = photo_resid_nb(ph.X, i2, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[1]);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            if (a == 1 && i2 == i) break;
+            const int ia = a ? i2 : i;
+            if (!ok[a]) t[a] = PhotoTmp{};
+            ptmp[ia] = t[a];
+            const unsigned long long bv = ok[a] ? (unsigned long long)__double_as_longlong(fabs(t[a].r)) : ~0ull;
+            bits[ia] = bv;
+            if (ok[a]) {
+              vlo = min(vlo, bv);
+              vhi = max(vhi, bv);
+            }
+            okc += ok[a];
           }
-          okc += ok;
         }
       }
       RS_MARK(1);
-      int m;
+      // (a per-block select from a shared-memory copy of all patterns, one grid barrier
+      // instead of one per pass, measured slower: 42 vs 37 us per geometric evaluation --
+      // shared-memory atomics on the clustered top digits and redundant passes)
+      const int m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
+      RS_MARK(2);
       double med = 0.0;
-      if (n <= cfg.sel_cap) {
-        // every block stages all |r| patterns in shared memory and selects the
-        // median itself: one grid barrier instead of one per radix pass
-        grid.sync();
-        RS_MARK(2);
-        unsigned long long* sv = reinterpret_cast<unsigned long long*>(rs_dyn + cfg.sel_off);
-        for (int q = tid; q < n; q += kRsThreads) sv[q] = bits[q];
-        __syncthreads();
-        med = rs_median_block(sv, n, sh, s_part, &s_bin, &s_before, s_min, &s_m);
-        m = s_m;
-      } else {
-        m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
-        RS_MARK(2);
-        if (m > 0)
-          med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
-                          st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
-                          s_min);
-      }
+      if (m > 0)
+        med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
+                        st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
+                        s_min);
       RS_MARK(3);
       if (m > 0) {  // else the family returns None (uniform); its partial sums stay zero
       // --- trim, Huber, normal equations

@@ -202,6 +202,39 @@ __device__ __forceinline__ bool photo_resid_one(const double* __restrict__ X, in
   return ok;
 }
 
+// photo_resid_one without branches (out-of-image anchors read pixel 0 and are
+// flagged): two calls on independent anchors interleave in the scheduler.
+__device__ __forceinline__ bool photo_resid_nb(const double* __restrict__ X, int i, const PoseK& T, const RegCam& cam,
+                                               const double* __restrict__ srange,
+                                               const uint8_t* __restrict__ svalid, double spread_gate,
+                                               PhotoTmp& t) {
+  double d[3], q[3];
+  for (int c = 0; c < 3; ++c) d[c] = X[3 * i + c] - T.t[c];
+  for (int c = 0; c < 3; ++c) q[c] = T.R[c] * d[0] + T.R[3 + c] * d[1] + T.R[6 + c] * d[2];
+  const double rho2 = q[0] * q[0] + q[1] * q[1];
+  const double r2 = rho2 + q[2] * q[2];
+  const double az = atan2(q[1], q[0]), el = atan2(q[2], hypot(q[0], q[1]));
+  const double u = cam.fx * az + cam.cx - cam.off_u, v = cam.fy * el + cam.cy - cam.off_v;
+  const double fi = floor(u), fj = floor(v);
+  const bool in = rho2 > 1e-12 && fi >= 0.0 && fi + 1.0 < cam.W && fj >= 0.0 && fj + 1.0 < cam.H;
+  const int i0 = in ? (int)fi : 0, j0 = in ? (int)fj : 0;
+  const double fu = u - fi, fv = v - fj;
+  const size_t p00 = (size_t)j0 * cam.W + i0;
+  const bool val4 = svalid[p00] && svalid[p00 + 1] && svalid[p00 + cam.W] && svalid[p00 + cam.W + 1];
+  const double d00 = srange[p00], d10 = srange[p00 + 1], d01 = srange[p00 + cam.W], d11 = srange[p00 + cam.W + 1];
+  const double hi = fmax(fmax(d00, d10), fmax(d01, d11)), lo = fmin(fmin(d00, d10), fmin(d01, d11));
+  const double top = d00 * (1 - fu) + d10 * fu;
+  const double bot = d01 * (1 - fu) + d11 * fu;
+  const double val = top * (1 - fv) + bot * fv;
+  t.r = sqrt(r2) - val;
+  t.du = (d10 - d00) * (1 - fv) + (d11 - d01) * fv;
+  t.dv = bot - top;
+  t.q[0] = q[0];
+  t.q[1] = q[1];
+  t.q[2] = q[2];
+  return in && val4 && hi - lo <= spread_gate;
+}
+
 // Residual of every anchor at pose T; |r| bits for the median of ok anchors.
 __global__ void k_photo_resid(const double* __restrict__ X, int M, PoseK T, RegCam cam,
                               const double* __restrict__ srange, const uint8_t* __restrict__ svalid,
