@@ -73,7 +73,6 @@ struct BlendParams {
 // chunks of 32 entries per backward segment (A/B at config 2, backward us:
 // halves-split tiles 240, segments of 16 chunks 189, 8 -> 135, 4 -> 121)
 constexpr int kSegChunks = SS_SEG_CHUNKS;
-static_assert(kSegChunks % 4 == 0, "k_forward_long records state at its 4-chunk round starts");
 
 // Backward work slots of the segment mode: every tile (longest first, the
 // forward's LPT order) contributes ceil(L / (32 kSegChunks)) slots
@@ -626,15 +625,7 @@ __global__ void __launch_bounds__(128) k_forward_long(
     for (int round = 0; round * kLongRound < L; ++round) {
       const int buf = round & 1;
       const float* stg = lsm + (size_t)buf * kLongRound * kStride;
-      if (bp.segst && comp && round > 0 && (round * 4) % kSegChunks == 0) {
-        float* sg = seg_state(bp.segst, cbase, round * 4);
-        sg[tid] = T;
-        sg[64 + tid] = D;
-        sg[128 + tid] = O;
-        sg[192 + tid] = N0;
-        sg[256 + tid] = N1;
-        sg[320 + tid] = N2;
-      }
+
       // cone test: warp w, chunk w of the round, all 64 pixels
       {
         const int cnt = min(32, L - round * kLongRound - 32 * warp);
@@ -662,6 +653,16 @@ __global__ void __launch_bounds__(128) k_forward_long(
         for (int w = 0; w < 4; ++w) {
           const int base = round * kLongRound + 32 * w;
           if (base >= L) break;
+          const int gch = round * 4 + w;
+          if (bp.segst && gch > 0 && gch % kSegChunks == 0) {  // state before this segment boundary
+            float* sg = seg_state(bp.segst, cbase, gch);
+            sg[tid] = T;
+            sg[64 + tid] = D;
+            sg[128 + tid] = O;
+            sg[192 + tid] = N0;
+            sg[256 + tid] = N1;
+            sg[320 + tid] = N2;
+          }
           unsigned m = live ? cwbuf[w][tid] : 0u;
           unsigned word = 0u;
           while (m) {
