@@ -29,7 +29,10 @@ struct Incidence {
   double azc, elc, omega, dgam;
 };
 
-constexpr int kTileSortMax = 2048;                // entries sorted in shared memory per tile (8 warps)
+#ifndef SS_SORT_MAX
+#define SS_SORT_MAX 2048
+#endif
+constexpr int kTileSortMax = SS_SORT_MAX;         // entries sorted in shared memory per tile (8 warps)
 constexpr int kTileSortBig = 8192;                // long-list variant (32 warps, dynamic shared memory)
 constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> merge-sort fallback
 
@@ -686,25 +689,25 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
 // lists are sorted by k_tile_sort_big on a side stream at the same time.  A
 // tile whose shared-memory sort gives up (a long run of equal keys) is merge
 // sorted in place by the same block (tmp: scratch of the list's size).
-#ifndef SS_SORT_NT
-#define SS_SORT_NT 256
-#endif
-constexpr int kTileSortNT = SS_SORT_NT;
+// Block size: 128 threads when tiles are many (short lists: more blocks per SM hide the
+// sort's barriers; config 1 63 -> 59 us), 256 when they are few and long (config 2:
+// 60 us against 67 with 128).
 
 __device__ void merge_sort_tile(uint32_t* __restrict__ pairs, uint32_t* __restrict__ tmp, int lo, int L,
                                 const unsigned long long* __restrict__ key);
 
-__global__ void __launch_bounds__(kTileSortNT) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tile_sort(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
                                                    uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key32,
                                                    const unsigned long long* __restrict__ key64,
                                                    const int* __restrict__ overflow) {
-  __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, kTileSortNT>()];
+  __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, NT>()];
   if (*overflow) return;
   const int t = blockIdx.x;
   const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
   if (L <= 1 || L > kTileSortMax) return;  // (longer lists: k_scan_tiles listed them for the big sort)
-  const SortSmem m = carve_sort_smem<kTileSortMax, kTileSortNT>(smem);
-  if (!sort_tile_smem<kTileSortMax, kTileSortNT>(m, pairs, lo, L, key32, key64))
+  const SortSmem m = carve_sort_smem<kTileSortMax, NT>(smem);
+  if (!sort_tile_smem<kTileSortMax, NT>(m, pairs, lo, L, key32, key64))
     merge_sort_tile(pairs, tmp, lo, L, key64);  // long run of equal keys (block-uniform result)
 }
 

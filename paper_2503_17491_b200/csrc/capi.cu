@@ -424,8 +424,10 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     if (seg)
       k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
-    k_tile_sort<<<ntiles, kTileSortNT, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64,
-                                              overflow);
+    if (num_sms() * 16 <= ntiles)
+      k_tile_sort<128><<<ntiles, 128, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow);
+    else
+      k_tile_sort<256><<<ntiles, 256, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow);
     SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->sort_join, 0));
   }
   rec->pairs = (int*)rec->pbucket;
