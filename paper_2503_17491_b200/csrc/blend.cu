@@ -300,6 +300,36 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return y;
 }
 
+// Packed float32 pairs (FMUL2 / FFMA2, sm_100): the cone test of a lane's two
+// pixels against one entry in 6 instructions instead of 12; a scalar operand
+// packed as {c, c} folds into the instruction's broadcast operand.
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(float a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pack2(a, a)), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fma2(float a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pack2(a, a)), "l"(b), "l"(c));
+  return d;
+}
+// q = c . p for pixels (lo, hi) of the pair P[6] = {(p_k lo, p_k hi)}, in the order
+// of the scalar expression c0 p0 + c1 p1 + ... (one rounding chain per pixel)
+__device__ __forceinline__ unsigned long long cone2(const float4& c0, const float4& c1,
+                                                   const unsigned long long (&P)[6]) {
+  unsigned long long q = mul2(c0.x, P[0]);
+  q = fma2(c0.y, P[1], q);
+  q = fma2(c0.z, P[2], q);
+  q = fma2(c0.w, P[3], q);
+  q = fma2(c1.x, P[4], q);
+  return fma2(c1.y, P[5], q);
+}
+
 struct Hit {
   float sa, sb, lam, r, G, alpha;
   bool use, clamped;
@@ -427,6 +457,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
     }
     xm *= 1.0001f;
     ym *= 1.0001f;
+    static_assert(PPL % 2 == 0 && !kSplit, "pixel pairs; the forward is never split");
+    unsigned long long PP[PPL / 2][6];
+#pragma unroll
+    for (int h = 0; h < PPL / 2; ++h)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) PP[h][q] = pack2(px[2 * h].p[q], px[2 * h + 1].p[q]);
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     const int cbase = chunk_ptr[t];
     // records of chunk c+1 are copied (cp.async) while chunk c is processed
@@ -464,19 +500,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       unsigned word[PPL], cw[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) word[j] = cw[j] = 0u;
-      // phase A: branch-free cone test of every (pixel, entry) -> candidate bits
+      // phase A: branch-free cone test of every (pixel, entry) -> candidate bits,
+      // two pixels per packed FFMA2 chain
       for (int i = 0; i < cnt; ++i) {
         const float* e = st + i * kStride;
         const float4 c0 = *reinterpret_cast<const float4*>(e);
         const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-          if (kSplit && !use[j]) continue;
-          const float* p = px[j].p;
-          const float q = c0.x * p[0] + c0.y * p[1] + c0.z * p[2] + c0.w * p[3] + c1.x * p[4] + c1.y * p[5];
+        for (int h = 0; h < PPL / 2; ++h) {
+          const unsigned long long q = cone2(c0, c1, PP[h]);
           // sign bit of q (q < 0 or -0; q = +0 only on the cone's safety margin):
           // entry i lands at bit cnt-1-i, reversed below
-          cw[j] = (cw[j] << 1) | (__float_as_uint(q) >> 31);
+          cw[2 * h] = (cw[2 * h] << 1) | ((unsigned)q >> 31);
+          cw[2 * h + 1] = (cw[2 * h + 1] << 1) | ((unsigned)(q >> 32) >> 31);
         }
       }
 #pragma unroll
@@ -599,6 +635,9 @@ __global__ void __launch_bounds__(128) k_forward_long(
     }
     xm *= 1.0001f;
     ym *= 1.0001f;
+    unsigned long long PP[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) PP[q] = pack2(px[0].p[q], px[1].p[q]);
     // compositing threads (warps 0-1): pixel tid
     const bool comp = warp < 2;
     const Pix pc = warp == 0 ? px[0] : px[1];  // (warps 0-1: pixel lane + 32 * warp == tid)
@@ -634,12 +673,9 @@ __global__ void __launch_bounds__(128) k_forward_long(
           const float* e = stg + (32 * warp + i) * kStride;
           const float4 c0 = *reinterpret_cast<const float4*>(e);
           const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
-          const float* p0 = px[0].p;
-          const float* p1 = px[1].p;
-          const float q0 = c0.x * p0[0] + c0.y * p0[1] + c0.z * p0[2] + c0.w * p0[3] + c1.x * p0[4] + c1.y * p0[5];
-          const float q1 = c0.x * p1[0] + c0.y * p1[1] + c0.z * p1[2] + c0.w * p1[3] + c1.x * p1[4] + c1.y * p1[5];
-          cw0 = (cw0 << 1) | (__float_as_uint(q0) >> 31);
-          cw1 = (cw1 << 1) | (__float_as_uint(q1) >> 31);
+          const unsigned long long q = cone2(c0, c1, PP);
+          cw0 = (cw0 << 1) | ((unsigned)q >> 31);
+          cw1 = (cw1 << 1) | ((unsigned)(q >> 32) >> 31);
         }
         if (cnt > 0) {
           cw0 = __brev(cw0) >> (32 - cnt);
