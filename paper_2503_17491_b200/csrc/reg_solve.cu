@@ -75,6 +75,14 @@ struct RegSolveState {
   double P[12];
   double fg, fp;
   int objective_only, action, eval_geo, eval_photo;
+  // a family already evaluated at exactly this pose (the accepted trial before a full
+  // evaluation) reuses its residuals, count and median: only the trim floor changed
+  int reuse[2], pub_m[2];
+  double pub_med[2];
+  // the evaluation just finished (block 0, thread 0)
+  double lastP[12];
+  int last_fam[2], cur_m[2];
+  double cur_med[2];
   // LM state (block 0, thread 0)
   double T[12], Ttry[12], H[36], b[6], delta[6];
   double lam, obj0, term_hub[2], term_s[2];
@@ -220,6 +228,19 @@ __device__ void rs_begin_phase(RegSolveState* st, const RegSolveCfg& cfg, int ph
   rs_begin_iteration(st, cfg);
 }
 
+// Publish-time reuse decision (see RegSolveState::reuse).
+__device__ void rs_set_reuse(RegSolveState* st) {
+  bool same = true;
+  for (int q = 0; q < 12; ++q)
+    same = same && __double_as_longlong(st->P[q]) == __double_as_longlong(st->lastP[q]);
+  const int ev[2] = {st->eval_geo, st->eval_photo};
+  for (int f = 0; f < 2; ++f) {
+    st->reuse[f] = same && ev[f] && st->last_fam[f];
+    st->pub_m[f] = st->cur_m[f];
+    st->pub_med[f] = st->cur_med[f];
+  }
+}
+
 // Next outer iteration of the phase (or the next phase): a full evaluation at T.
 __device__ void rs_begin_iteration(RegSolveState* st, const RegSolveCfg& cfg) {
   if (st->it_total >= rs_phase_budget(cfg, st->phase)) {
@@ -236,6 +257,7 @@ __device__ void rs_begin_iteration(RegSolveState* st, const RegSolveCfg& cfg) {
   st->eval_photo = st->use_photo;
   st->stage = 0;
   st->action = RS_EVAL;
+  rs_set_reuse(st);
 }
 
 // Inner LM loop: next trial pose, or the end of the phase when damping is exhausted.
@@ -256,6 +278,7 @@ __device__ void rs_try(RegSolveState* st, const RegSolveCfg& cfg) {
     st->objective_only = 1;
     st->stage = 1;
     st->action = RS_EVAL;
+    rs_set_reuse(st);
     return;
   }
   rs_begin_phase(st, cfg, st->phase + 1);  // damping exhausted: keep the estimate, end the phase
@@ -264,6 +287,9 @@ __device__ void rs_try(RegSolveState* st, const RegSolveCfg& cfg) {
 // red: per family (geo, photo) kRsAcc sums of the evaluation just finished.
 __device__ void rs_step(RegSolveState* st, const RegSolveCfg& cfg, const double* red) {
   st->n_eval += 1;
+  for (int q = 0; q < 12; ++q) st->lastP[q] = st->P[q];  // (cur_m / cur_med: written during the evaluation)
+  st->last_fam[0] = st->eval_geo;
+  st->last_fam[1] = st->eval_photo;
   const double* fam[2] = {red, red + kRsAcc};
   const int on[2] = {st->eval_geo, st->eval_photo};
   const double hub_par[2] = {cfg.huber_geo, cfg.huber_photo};
@@ -716,8 +742,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
   __shared__ int s_bin, s_before, s_m;
   __shared__ unsigned long long s_min[kRsThreads / 32];
   __shared__ unsigned long long s_mm[2 * (kRsThreads / 32) + 2];
-  __shared__ unsigned long long s_pub[16];
-  static_assert(offsetof(RegSolveState, eval_photo) + sizeof(int) <= 16 * 8, "published fields in the first 16 words");
+  __shared__ unsigned long long s_pub[20];
+  static_assert(offsetof(RegSolveState, pub_med) + 2 * sizeof(double) <= 20 * 8, "published fields in the first 20 words");
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = G * kRsThreads;
   const int kmax = min(min(cfg.assoc_k, geo.n_leaves), 8);
@@ -757,9 +783,9 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
     grid.sync();
     RS_MARK(0);
     RS_SUB(-1);
-    // the published evaluation (P, floors, flags: the first 16 words of the state),
+    // the published evaluation (P, floors, flags, reuse: the first 20 words of the state),
     // loaded by one warp in parallel instead of ~18 dependent volatile loads per thread
-    if (tid < 16) s_pub[tid] = ((volatile unsigned long long*)st)[tid];
+    if (tid < 20) s_pub[tid] = ((volatile unsigned long long*)st)[tid];
     __syncthreads();
     const RegSolveState* vs = reinterpret_cast<const RegSolveState*>(s_pub);
     if (vs->action == RS_DONE) {
@@ -800,112 +826,124 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
       unsigned long long* bits = f == 0 ? gbits : pbits;
       const int n = f == 0 ? geo.n_scan : ph.M;
       RS_SUB(7);
-      // --- residuals
-      int okc = 0;
-      unsigned long long vlo = ~0ull, vhi = 0ull;  // this thread's smallest / largest valid |r| pattern
-      if (f == 0) {
-        // k nearest usable leaf centroids within the gate, then the leaf whose plane
-        // is closest (registration.py:249-265); leaves staged through shared memory
-        // S consecutive lanes share one scan point (n_scan <= grid threads, checked by
-        // the host), each visiting every S-th cell of the point's 27-cell
-        // neighbourhood in the leaf grid; their sorted k-best lists merge by
-        // butterfly shuffles.  The lists live in registers (static indexing) and
-        // order by (d2, leaf index), so the result does not depend on visit order.
-        int S = 1;
-        while (S < 32 && 2 * S * n <= nthr) S *= 2;
-        const int i = gtid / S, sub = gtid & (S - 1);
-        double p[3] = {0, 0, 0}, q3[3] = {0, 0, 0};
-        if (i < n) {
-          for (int c = 0; c < 3; ++c) q3[c] = geo.scan[3 * i + c];
-          for (int c = 0; c < 3; ++c)
-            p[c] = P.R[3 * c] * q3[0] + P.R[3 * c + 1] * q3[1] + P.R[3 * c + 2] * q3[2] + P.t[c];
-        }
-        double kd[8];
-        int ki[8];
-        switch (kmax) {  // (uniform)
-#define RS_KNN_CASE(K) \
-  case K:              \
-    rs_knn<K>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki); \
-    break;
-          RS_KNN_CASE(1)
-          RS_KNN_CASE(2)
-          RS_KNN_CASE(3)
-          RS_KNN_CASE(4)
-          RS_KNN_CASE(5)
-          RS_KNN_CASE(6)
-          RS_KNN_CASE(7)
-          default:
-            rs_knn<8>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki);
-#undef RS_KNN_CASE
-        }
-        bool ok = false;
-        GeoTmp g{};
-        if (i < n && sub == 0) {
-          const double gate2 = cfg.assoc_gate * cfg.assoc_gate;
-          double best = __longlong_as_double(0x7ff0000000000000LL);
-          int bl = -1;
-#pragma unroll
-          for (int a = 0; a < 8; ++a) {
-            if (a >= kmax || !(kd[a] < gate2)) continue;  // beyond distance_upper_bound
-            const double* nn = geo.nrm + 3 * ki[a];
-            const double* cc = geo.cent + 3 * ki[a];
-            const double pd = fabs(nn[0] * (p[0] - cc[0]) + nn[1] * (p[1] - cc[1]) + nn[2] * (p[2] - cc[2]));
-            if (pd < best) {
-              best = pd;
-              bl = ki[a];
-            }
-          }
-          ok = kd[0] < gate2;
-          if (ok) {
-            const double* nn = geo.nrm + 3 * bl;
-            const double* cc = geo.cent + 3 * bl;
-            g.r = (nn[0] * (p[0] - cc[0]) + nn[1] * (p[1] - cc[1])) + nn[2] * (p[2] - cc[2]);
-            for (int c = 0; c < 3; ++c) {
-              g.n[c] = nn[c];
-              g.q[c] = q3[c];
-            }
-          }
-          gtmp[i] = g;
-          const unsigned long long bv = ok ? (unsigned long long)__double_as_longlong(fabs(g.r)) : ~0ull;
-          bits[i] = bv;
-          if (ok) vlo = vhi = bv;
-        }
-        okc = ok;
+      // a family evaluated at exactly this pose by the previous (trial) evaluation keeps
+      // its residuals (gtmp / ptmp, bits), count and median: only the trim floor differs
+      int m = 0;
+      double med = 0.0;
+      if (vs->reuse[f]) {
+        m = vs->pub_m[f];
+        med = vs->pub_med[f];
       } else {
-        // two anchors per pass (branch-free residuals interleave; M ~ 1-2x the grid's threads)
-        for (int i = gtid; i < n; i += 2 * nthr) {
-          const int i2 = i + nthr < n ? i + nthr : i;
-          PhotoTmp t[2];
-          bool ok[2];
-          ok[0] = photo_resid_nb(ph.X, i, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[0]);
-          ok[1] = photo_resid_nb(ph.X, i2, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[1]);
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-            if (a == 1 && i2 == i) break;
-            const int ia = a ? i2 : i;
-            if (!ok[a]) t[a] = PhotoTmp{};
-            ptmp[ia] = t[a];
-            const unsigned long long bv = ok[a] ? (unsigned long long)__double_as_longlong(fabs(t[a].r)) : ~0ull;
-            bits[ia] = bv;
-            if (ok[a]) {
-              vlo = min(vlo, bv);
-              vhi = max(vhi, bv);
-            }
-            okc += ok[a];
+        // --- residuals
+        int okc = 0;
+        unsigned long long vlo = ~0ull, vhi = 0ull;  // this thread's smallest / largest valid |r| pattern
+        if (f == 0) {
+          // k nearest usable leaf centroids within the gate, then the leaf whose plane
+          // is closest (registration.py:249-265); leaves staged through shared memory
+          // S consecutive lanes share one scan point (n_scan <= grid threads, checked by
+          // the host), each visiting every S-th cell of the point's 27-cell
+          // neighbourhood in the leaf grid; their sorted k-best lists merge by
+          // butterfly shuffles.  The lists live in registers (static indexing) and
+          // order by (d2, leaf index), so the result does not depend on visit order.
+          int S = 1;
+          while (S < 32 && 2 * S * n <= nthr) S *= 2;
+          const int i = gtid / S, sub = gtid & (S - 1);
+          double p[3] = {0, 0, 0}, q3[3] = {0, 0, 0};
+          if (i < n) {
+            for (int c = 0; c < 3; ++c) q3[c] = geo.scan[3 * i + c];
+            for (int c = 0; c < 3; ++c)
+              p[c] = P.R[3 * c] * q3[0] + P.R[3 * c + 1] * q3[1] + P.R[3 * c + 2] * q3[2] + P.t[c];
           }
+          double kd[8];
+          int ki[8];
+          switch (kmax) {  // (uniform)
+  #define RS_KNN_CASE(K) \
+    case K:              \
+      rs_knn<K>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki); \
+      break;
+            RS_KNN_CASE(1)
+            RS_KNN_CASE(2)
+            RS_KNN_CASE(3)
+            RS_KNN_CASE(4)
+            RS_KNN_CASE(5)
+            RS_KNN_CASE(6)
+            RS_KNN_CASE(7)
+            default:
+              rs_knn<8>(p, i < n, sub, S, s_bst, s_ent, geo.mask, geo.inv_cs, kd, ki);
+  #undef RS_KNN_CASE
+          }
+          bool ok = false;
+          GeoTmp g{};
+          if (i < n && sub == 0) {
+            const double gate2 = cfg.assoc_gate * cfg.assoc_gate;
+            double best = __longlong_as_double(0x7ff0000000000000LL);
+            int bl = -1;
+  #pragma unroll
+            for (int a = 0; a < 8; ++a) {
+              if (a >= kmax || !(kd[a] < gate2)) continue;  // beyond distance_upper_bound
+              const double* nn = geo.nrm + 3 * ki[a];
+              const double* cc = geo.cent + 3 * ki[a];
+              const double pd = fabs(nn[0] * (p[0] - cc[0]) + nn[1] * (p[1] - cc[1]) + nn[2] * (p[2] - cc[2]));
+              if (pd < best) {
+                best = pd;
+                bl = ki[a];
+              }
+            }
+            ok = kd[0] < gate2;
+            if (ok) {
+              const double* nn = geo.nrm + 3 * bl;
+              const double* cc = geo.cent + 3 * bl;
+              g.r = (nn[0] * (p[0] - cc[0]) + nn[1] * (p[1] - cc[1])) + nn[2] * (p[2] - cc[2]);
+              for (int c = 0; c < 3; ++c) {
+                g.n[c] = nn[c];
+                g.q[c] = q3[c];
+              }
+            }
+            gtmp[i] = g;
+            const unsigned long long bv = ok ? (unsigned long long)__double_as_longlong(fabs(g.r)) : ~0ull;
+            bits[i] = bv;
+            if (ok) vlo = vhi = bv;
+          }
+          okc = ok;
+        } else {
+          // two anchors per pass (branch-free residuals interleave; M ~ 1-2x the grid's threads)
+          for (int i = gtid; i < n; i += 2 * nthr) {
+            const int i2 = i + nthr < n ? i + nthr : i;
+            PhotoTmp t[2];
+            bool ok[2];
+            ok[0] = photo_resid_nb(ph.X, i, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[0]);
+            ok[1] = photo_resid_nb(ph.X, i2, P, cam, ph.srange, ph.svalid, cfg.spread_gate, t[1]);
+  #pragma unroll
+            for (int a = 0; a < 2; ++a) {
+              if (a == 1 && i2 == i) break;
+              const int ia = a ? i2 : i;
+              if (!ok[a]) t[a] = PhotoTmp{};
+              ptmp[ia] = t[a];
+              const unsigned long long bv = ok[a] ? (unsigned long long)__double_as_longlong(fabs(t[a].r)) : ~0ull;
+              bits[ia] = bv;
+              if (ok[a]) {
+                vlo = min(vlo, bv);
+                vhi = max(vhi, bv);
+              }
+              okc += ok[a];
+            }
+          }
+        }
+        RS_MARK(1);
+        // (a per-block select from a shared-memory copy of all patterns, one grid barrier
+        // instead of one per pass, measured slower: 42 vs 37 us per geometric evaluation --
+        // shared-memory atomics on the clustered top digits and redundant passes)
+        m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
+        RS_MARK(2);
+        if (m > 0)
+          med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
+                          st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
+                          s_min);
+        if (blockIdx.x == 0 && tid == 0) {
+          st->cur_m[f] = m;
+          st->cur_med[f] = med;
         }
       }
-      RS_MARK(1);
-      // (a per-block select from a shared-memory copy of all patterns, one grid barrier
-      // instead of one per pass, measured slower: 42 vs 37 us per geometric evaluation --
-      // shared-memory atomics on the clustered top digits and redundant passes)
-      const int m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
-      RS_MARK(2);
-      double med = 0.0;
-      if (m > 0)
-        med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
-                        st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
-                        s_min);
       RS_MARK(3);
       if (m > 0) {  // else the family returns None (uniform); its partial sums stay zero
       // --- trim, Huber, normal equations
