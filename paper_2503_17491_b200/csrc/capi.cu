@@ -1066,7 +1066,7 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   LeafRec* recs = (LeafRec*)take((size_t)cap_nodes * sizeof(LeafRec));
   int2* leaf_seg = (int2*)take((size_t)cap_leaves * 8);
   LeafRec* leaf_rec = (LeafRec*)take((size_t)cap_leaves * sizeof(LeafRec));
-  int* counts = (int*)take(16);  // [0] nodes of level parity 0, [1] parity 1, [2] leaves, [3] overflow
+  int* counts = (int*)take(32);  // [0] nodes of level parity 0, [1] parity 1, [2] leaves, [3] overflow, [4] level
   // top levels (node bound 2^level below the grid): one cooperative kernel, all SMs per level
   const int G = num_sms();
   int top_levels = 0;
@@ -1092,6 +1092,7 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
   // bound on its node count (blocks past the actual count exit), the next
   // level is laid out on the device; the host checks for leftovers at the end.
   int level = 0;
+  bool tree_done = false;
   if (top_levels > 0) {
     int occ = 0;
     SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_leaf_top, kLtTopThreads, 0));
@@ -1109,8 +1110,24 @@ int ss_leaf_tree_build(const double* pts, int32_t n, const double* viewpoint3, i
                     (void*)&a_ls, (void*)&a_tau, (void*)&a_lv, (void*)&tws};
     SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_leaf_top, dim3(G), dim3(kLtTopThreads), args, 0, s));
     level = top_levels;
+    // every further level in one more cooperative launch (one block per node, grid-stride)
+    int occ2 = 0;
+    SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_leaf_rest, kLtTopThreads, 0));
+    if (occ2 >= 1) {
+      int a_l0 = level, a_max = 64;
+      void* args2[] = {(void*)&a_pts, (void*)&a_idx, (void*)&a_tmp, (void*)&a_proj, (void*)&a_n0, (void*)&a_n1,
+                       (void*)&a_counts, (void*)&a_recs, (void*)&a_seg, (void*)&a_lrec, (void*)&a_cap, (void*)&a_vp,
+                       (void*)&a_ls, (void*)&a_tau, (void*)&a_l0, (void*)&a_max};
+      SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_leaf_rest, dim3(G), dim3(kLtTopThreads), args2, 0, s));
+      int h5[5];
+      SS_CUDA_TRY(cudaMemcpyAsync(h5, counts, sizeof(h5), cudaMemcpyDeviceToHost, s));
+      SS_CUDA_TRY(cudaStreamSynchronize(s));
+      if (h5[3]) return SS_ERR_CAPACITY;
+      level = h5[4];
+      tree_done = h5[level & 1] == 0;  // else nodes remain past max_levels: the level loop below
+    }
   }
-  for (int batch = 0;; ++batch) {
+  for (int batch = 0; !tree_done; ++batch) {
     const int depth = batch == 0 ? std::max(1, 2 + (int)std::ceil(std::log2((double)n + 1.0)) - level) : 8;
     for (int q = 0; q < depth; ++q, ++level) {
       const int par = level & 1;

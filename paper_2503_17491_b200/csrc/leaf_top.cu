@@ -543,4 +543,35 @@ __global__ void __launch_bounds__(kLtTopThreads, 1)
 #endif
 }
 
+// The remaining levels (many nodes) in one cooperative kernel: each block takes
+// nodes grid-stride, one node at a time (leaf_node, as k_leaf_level does),
+// block 0 lays out the next level between grid barriers.  Runs until a level
+// has no node (or max_levels); counts[4] = the first level not processed.
+__global__ void __launch_bounds__(kLtTopThreads, 1)
+    k_leaf_rest(const double* __restrict__ pts, int* __restrict__ idx, int* __restrict__ tmp, double* __restrict__ proj,
+                int2* __restrict__ nodes0, int2* __restrict__ nodes1, int* __restrict__ counts,
+                LeafRec* __restrict__ recs, int2* __restrict__ leaf_seg, LeafRec* __restrict__ leaf_rec,
+                int cap_leaves, double3 vp, int leaf_size, double tau, int level0, int max_levels) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  int level = level0;
+  for (; level < level0 + max_levels; ++level) {
+    const int par = level & 1;
+    const int2* cur = par ? nodes1 : nodes0;
+    int2* nxt = par ? nodes0 : nodes1;
+    const int K = ((volatile int*)counts)[par];
+    if (K == 0) break;  // (uniform)
+    for (int node = blockIdx.x; node < K; node += gridDim.x) {
+      leaf_node<kLtTopThreads>(node, pts, idx, tmp, proj, cur, vp, leaf_size, tau, recs);
+      __syncthreads();  // (leaf_node's shared memory is reused by the next node)
+    }
+    grid.sync();
+    if (blockIdx.x == 0)
+      next_level_block<kLtTopThreads>(cur, K, recs, nxt, counts + (par ^ 1), leaf_seg, leaf_rec, counts + 2,
+                                      cap_leaves, counts + 3);
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[4] = level;
+}
+
 }  // namespace ss

@@ -177,19 +177,17 @@ __device__ unsigned long long block_select(const double* __restrict__ proj, int 
   return prefix;
 }
 
+// One node of a level by one block of NT threads (record -> out[node]).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pts, int* __restrict__ idx,
-                                                           int* __restrict__ tmp, double* __restrict__ proj,
-                                                           const int2* __restrict__ nodes,
-                                                           const int* __restrict__ n_nodes, double3 viewpoint,
-                                                           int leaf_size, double tau, LeafRec* __restrict__ out) {
-  if ((int)blockIdx.x >= *n_nodes) return;  // grid sized by a bound on the level's node count
+__device__ void leaf_node(int node, const double* __restrict__ pts, int* __restrict__ idx, int* __restrict__ tmp,
+                          double* __restrict__ proj, const int2* __restrict__ nodes, double3 viewpoint,
+                          int leaf_size, double tau, LeafRec* __restrict__ out) {
   __shared__ double sred[NT / 32];
   __shared__ double s_axis[3], s_n[3], s_w[3];
   __shared__ unsigned hist[kLtBins];
   __shared__ unsigned long long cand[kLtCand];
   __shared__ int sint[2 * (NT / 32) + 8];
-  const int2 nd = nodes[blockIdx.x];
+  const int2 nd = nodes[node];
   const int b = nd.x, n = nd.y - nd.x;
   const int tid = threadIdx.x;
   // mean (registration.py:121)
@@ -209,7 +207,7 @@ __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pt
   rec.c[1] = c[1];
   rec.c[2] = c[2];
   if (n < 3) {  // (:122-124)
-    if (tid == 0) out[blockIdx.x] = rec;
+    if (tid == 0) out[node] = rec;
     return;
   }
   // biased covariance (:125)
@@ -251,7 +249,7 @@ __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pt
       for (int k = 0; k < 3; ++k) rec.n[k] = nn[k];
       rec.usable = 1;
     }
-    out[blockIdx.x] = rec;
+    out[node] = rec;
   };
   if (flat || n <= leaf_size) {  // (:128-131)
     emit_leaf(w1 > 1e-12);
@@ -342,20 +340,31 @@ __global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pt
   if (tid == 0) {
     rec.split = 1;
     rec.nl = nl;
-    out[blockIdx.x] = rec;
+    out[node] = rec;
   }
 }
 
+template <int NT>
+__global__ void __launch_bounds__(NT) k_leaf_level(const double* __restrict__ pts, int* __restrict__ idx,
+                                                   int* __restrict__ tmp, double* __restrict__ proj,
+                                                   const int2* __restrict__ nodes, const int* __restrict__ n_nodes,
+                                                   double3 viewpoint, int leaf_size, double tau,
+                                                   LeafRec* __restrict__ out) {
+  if ((int)blockIdx.x >= *n_nodes) return;  // grid sized by a bound on the level's node count
+  leaf_node<NT>(blockIdx.x, pts, idx, tmp, proj, nodes, viewpoint, leaf_size, tau, out);
+}
+
 // Lay out the next level (children of split nodes, in node order) and append
-// this level's leaves (in node order): one block, counts scanned per thread run.
-__global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cur, const int* __restrict__ n_cur_p,
-                                                     const LeafRec* __restrict__ recs, int2* __restrict__ next,
-                                                     int* __restrict__ n_next_p, int2* __restrict__ leaf_seg,
-                                                     LeafRec* __restrict__ leaf_rec, int* __restrict__ n_leaves_p,
-                                                     int max_leaves, int* __restrict__ overflow) {
-  __shared__ int s_c[1024], s_l[1024];
-  const int n_cur = *n_cur_p, tid = threadIdx.x;
-  const int per = (n_cur + 1023) / 1024;
+// this level's leaves (in node order): one block of NT threads, counts scanned
+// per thread run.
+template <int NT>
+__device__ void next_level_block(const int2* __restrict__ cur, int n_cur, const LeafRec* __restrict__ recs,
+                                 int2* __restrict__ next, int* __restrict__ n_next_p, int2* __restrict__ leaf_seg,
+                                 LeafRec* __restrict__ leaf_rec, int* __restrict__ n_leaves_p, int max_leaves,
+                                 int* __restrict__ overflow) {
+  __shared__ int s_c[NT], s_l[NT];
+  const int tid = threadIdx.x;
+  const int per = (n_cur + NT - 1) / NT;
   const int b = min(tid * per, n_cur), e = min(b + per, n_cur);
   int nc = 0, nl = 0;
   for (int i = b; i < e; ++i) {
@@ -367,7 +376,7 @@ __global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cu
   s_c[tid] = nc;
   s_l[tid] = nl;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
+  for (int off = 1; off < NT; off <<= 1) {
     const int vc = tid >= off ? s_c[tid - off] : 0, vl = tid >= off ? s_l[tid - off] : 0;
     __syncthreads();
     s_c[tid] += vc;
@@ -391,10 +400,19 @@ __global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cu
     }
   }
   __syncthreads();
-  if (tid == 1023) {
-    *n_next_p = s_c[1023];
-    *n_leaves_p = leaf0 + s_l[1023];
+  if (tid == NT - 1) {
+    *n_next_p = s_c[NT - 1];
+    *n_leaves_p = leaf0 + s_l[NT - 1];
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_next_level(const int2* __restrict__ cur, const int* __restrict__ n_cur_p,
+                                                     const LeafRec* __restrict__ recs, int2* __restrict__ next,
+                                                     int* __restrict__ n_next_p, int2* __restrict__ leaf_seg,
+                                                     LeafRec* __restrict__ leaf_rec, int* __restrict__ n_leaves_p,
+                                                     int max_leaves, int* __restrict__ overflow) {
+  next_level_block<1024>(cur, *n_cur_p, recs, next, n_next_p, leaf_seg, leaf_rec, n_leaves_p, max_leaves, overflow);
 }
 
 // point -> leaf: blockIdx.x = leaf, blockIdx.y = 1024-point chunk of its segment
