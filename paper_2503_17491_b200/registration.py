@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import engine
-from ._lib import SsRegCfg, SsRegSolveCfg, check, lib
+from ._lib import SS_ERR_CAPACITY, SsRegCfg, SsRegSolveCfg, check, lib
 from .errors import RegistrationError
 from .geometry import SE3Pose, SphericalCamera, pose_rt
 from .rasterizer import RasterConfig
@@ -74,9 +74,23 @@ class RegistrationResult:
 class DeviceScan:
     """Scan range image on the device (build_range_image, geometry.py:252-268)."""
 
+    _stage = None  # reused pinned staging buffer and the event of its last upload
+
     def __init__(self, cam, scan: np.ndarray):
         dev = engine.require_cuda()
-        pts = torch.as_tensor(np.ascontiguousarray(np.asarray(scan, dtype=np.float64).reshape(-1, 3)), device=dev)
+        arr = np.ascontiguousarray(np.asarray(scan, dtype=np.float64).reshape(-1, 3))
+        # pinned staging: the upload is stream-ordered without blocking the host (so it
+        # can be prepared while a render is in flight, see register())
+        st = DeviceScan._stage
+        if st is None or st[0].shape[0] < arr.shape[0]:
+            st = (torch.empty((max(arr.shape[0], 1), 3), dtype=torch.float64).pin_memory(), torch.cuda.Event())
+            DeviceScan._stage = st
+        else:
+            st[1].synchronize()  # the previous upload from this buffer has finished
+        host = st[0][: arr.shape[0]]
+        host.numpy()[...] = arr
+        pts = host.to(dev, non_blocking=True)
+        st[1].record()
         self.cam = cam
         self.range = torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev)
         self.valid = torch.empty((cam.height, cam.width), dtype=torch.uint8, device=dev)
@@ -146,17 +160,34 @@ def build_leaf_tree(points, viewpoint, leaf_size: int = 64, flatness_tau: float 
 
 
 def sample_anchors(model_or_params, geo_cam, pose, cfg: RegistrationConfig, raster: RasterConfig | None = None,
-                   thin: int = 1):
+                   thin: int = 1, overlap=None):
     """Device sample_model (registration.py:190-213): world anchors, thinned by ``thin``.
 
-    Returns (X float64 [n,3] device tensor, number of confident pixels)."""
+    Returns (X float64 [n,3] device tensor, number of confident pixels).  ``overlap``: an
+    optional host callable run while the render executes (its result is returned third)."""
     raster = raster or RasterConfig()
     params = engine.as_device_params(model_or_params)
     rec = engine.Records.acquire()
     try:
-        D, N, O = engine.forward(geo_cam, pose_rt(pose), params, raster, rec)
+        # no host wait after the render: the anchor extraction below synchronises anyway,
+        # and the capacity check is read afterwards (re-run on the rare overflow)
+        D, N, O = engine.forward(geo_cam, pose_rt(pose), params, raster, rec, sync=False)
+        extra = overlap() if overlap is not None else None
+        X, counts = _anchors(D, O, geo_cam, pose, cfg, thin)
+        if rec.check(True) == SS_ERR_CAPACITY:
+            D, N, O = engine.forward(geo_cam, pose_rt(pose), params, raster, rec)
+            X, counts = _anchors(D, O, geo_cam, pose, cfg, thin)
+        else:
+            check(rec.check(True), "rasterize_forward")
     finally:
         rec.release()
+    if overlap is not None:
+        return X[: counts[1]], int(counts[0]), extra
+    return X[: counts[1]], int(counts[0])
+
+
+def _anchors(D, O, geo_cam, pose, cfg, thin):
+    """ss_reg_anchors on a rendered (D, O): (X buffer, counts [confident, kept]); synchronises."""
     dev = D.device
     P = geo_cam.width * geo_cam.height
     cap = (P + thin - 1) // thin
@@ -171,7 +202,7 @@ def sample_anchors(model_or_params, geo_cam, pose, cfg: RegistrationConfig, rast
                                float(cfg.spread_gate), int(thin), ctypes.c_void_p(X.data_ptr()), int(cap), counts,
                                ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(engine.stream_ptr())),
           "sample_model")
-    return X[: counts[1]], int(counts[0])
+    return X, counts
 
 
 class PhotoProblem:
@@ -232,11 +263,12 @@ def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, r
     if s > 1:
         geo_cam = SphericalCamera(cam.width * s, cam.height * s, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
     # model surface points (sample_model, :190-213) and the photometric anchors X_w = model_pts[::s*s] (:430)
-    model_pts, n_model = sample_anchors(model, geo_cam, initial, cfg, raster, thin=1)
+    # the scan's upload and range image are prepared while the model renders
+    model_pts, n_model, dscan = sample_anchors(model, geo_cam, initial, cfg, raster, thin=1,
+                                               overlap=lambda: DeviceScan(cam, scan))
     if n_model < cfg.min_residuals:
         raise RegistrationError("model renders to too few confident pixels")
     X_w = model_pts[:: s * s].contiguous() if s > 1 else model_pts
-    dscan = DeviceScan(cam, scan)
     if not device_loop:
         if cfg.mode != "photometric":
             raise RegistrationError("the host loop covers the photometric mode only; use device_loop=True")
