@@ -70,7 +70,11 @@ __device__ unsigned long long g_rs_sub[8], g_rs_sub_last;
 
 enum { RS_EVAL = 0, RS_DONE = 1 };
 
-struct RegSolveState {
+// The LM state machine's fields: the published evaluation (the first 20 words,
+// read by every block) and the state of block 0 / thread 0, which keeps it in
+// shared memory during the launch (the copy in global memory is written back at
+// the end; the published words are copied out after every step).
+struct RegSolveLM {
   // published evaluation
   double P[12];
   double fg, fp;
@@ -89,6 +93,9 @@ struct RegSolveState {
   double last_r2[2];
   int last_m[2], nterms;
   int it_total, converged, status, stage, n_eval, phase, use_geo, use_photo;
+};
+
+struct RegSolveState : RegSolveLM {  // + the grid-wide median scratch
   unsigned long long vmin[2][2];
   int ncand[2][2];
   unsigned long long cand[2][2][kRsCand];
@@ -211,10 +218,10 @@ __device__ int rs_phase_budget(const RegSolveCfg& cfg, int phase) {
 }
 __device__ int rs_nphases(const RegSolveCfg& cfg) { return cfg.mode == RM_SEQ ? 2 : 1; }
 
-__device__ void rs_begin_iteration(RegSolveState* st, const RegSolveCfg& cfg);
+__device__ void rs_begin_iteration(RegSolveLM* st, const RegSolveCfg& cfg);
 
 // Start phase `ph` (registration.py:441-450): damping and convergence reset.
-__device__ void rs_begin_phase(RegSolveState* st, const RegSolveCfg& cfg, int ph) {
+__device__ void rs_begin_phase(RegSolveLM* st, const RegSolveCfg& cfg, int ph) {
   if (ph >= rs_nphases(cfg)) {
     st->action = RS_DONE;
     return;
@@ -229,7 +236,7 @@ __device__ void rs_begin_phase(RegSolveState* st, const RegSolveCfg& cfg, int ph
 }
 
 // Publish-time reuse decision (see RegSolveState::reuse).
-__device__ void rs_set_reuse(RegSolveState* st) {
+__device__ void rs_set_reuse(RegSolveLM* st) {
   bool same = true;
   for (int q = 0; q < 12; ++q)
     same = same && __double_as_longlong(st->P[q]) == __double_as_longlong(st->lastP[q]);
@@ -242,7 +249,7 @@ __device__ void rs_set_reuse(RegSolveState* st) {
 }
 
 // Next outer iteration of the phase (or the next phase): a full evaluation at T.
-__device__ void rs_begin_iteration(RegSolveState* st, const RegSolveCfg& cfg) {
+__device__ void rs_begin_iteration(RegSolveLM* st, const RegSolveCfg& cfg) {
   if (st->it_total >= rs_phase_budget(cfg, st->phase)) {
     rs_begin_phase(st, cfg, st->phase + 1);
     return;
@@ -261,7 +268,7 @@ __device__ void rs_begin_iteration(RegSolveState* st, const RegSolveCfg& cfg) {
 }
 
 // Inner LM loop: next trial pose, or the end of the phase when damping is exhausted.
-__device__ void rs_try(RegSolveState* st, const RegSolveCfg& cfg) {
+__device__ void rs_try(RegSolveLM* st, const RegSolveCfg& cfg) {
   while (st->lam <= cfg.damping_max) {
     double A[36], y[6];
     for (int q = 0; q < 36; ++q) A[q] = st->H[q] + (q % 7 == 0 ? st->lam : 0.0);
@@ -285,7 +292,7 @@ __device__ void rs_try(RegSolveState* st, const RegSolveCfg& cfg) {
 }
 
 // red: per family (geo, photo) kRsAcc sums of the evaluation just finished.
-__device__ void rs_step(RegSolveState* st, const RegSolveCfg& cfg, const double* red) {
+__device__ void rs_step(RegSolveLM* st, const RegSolveCfg& cfg, const double* red) {
   st->n_eval += 1;
   for (int q = 0; q < 12; ++q) st->lastP[q] = st->P[q];  // (cur_m / cur_med: written during the evaluation)
   st->last_fam[0] = st->eval_geo;
@@ -743,7 +750,12 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
   __shared__ unsigned long long s_min[kRsThreads / 32];
   __shared__ unsigned long long s_mm[2 * (kRsThreads / 32) + 2];
   __shared__ unsigned long long s_pub[20];
-  static_assert(offsetof(RegSolveState, pub_med) + 2 * sizeof(double) <= 20 * 8, "published fields in the first 20 words");
+  static_assert(offsetof(RegSolveLM, pub_med) + 2 * sizeof(double) <= 20 * 8, "published fields in the first 20 words");
+  __shared__ RegSolveLM s_lm;  // block 0: the LM state during the launch
+  auto publish = [&]() {  // block 0, thread 0: the next evaluation's words to every block
+    for (int q = 0; q < 20; ++q)
+      reinterpret_cast<unsigned long long*>(st)[q] = reinterpret_cast<const unsigned long long*>(&s_lm)[q];
+  };
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = G * kRsThreads;
   const int kmax = min(min(cfg.assoc_k, geo.n_leaves), 8);
@@ -763,17 +775,19 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
     __syncthreads();
   }
   if (blockIdx.x == 0 && tid == 0) {
-    st->it_total = 0;
-    st->status = 0;
-    st->n_eval = 0;
-    st->last_m[0] = st->last_m[1] = 0;
-    st->last_r2[0] = st->last_r2[1] = 0.0;
+    s_lm = *static_cast<const RegSolveLM*>(st);  // (initial pose from the host)
+    s_lm.it_total = 0;
+    s_lm.status = 0;
+    s_lm.n_eval = 0;
+    s_lm.last_m[0] = s_lm.last_m[1] = 0;
+    s_lm.last_r2[0] = s_lm.last_r2[1] = 0.0;
     for (int a = 0; a < 2; ++a)
       for (int f = 0; f < 2; ++f) {
         st->vmin[a][f] = ~0ull;
         st->ncand[a][f] = 0;
       }
-    rs_begin_phase(st, cfg, 0);
+    rs_begin_phase(&s_lm, cfg, 0);
+    publish();
   }
 #ifdef SS_RS_PROF
   unsigned long long rs_prof[10] = {}, rs_last = 0;
@@ -789,6 +803,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
     __syncthreads();
     const RegSolveState* vs = reinterpret_cast<const RegSolveState*>(s_pub);
     if (vs->action == RS_DONE) {
+      if (blockIdx.x == 0 && tid == 0) *static_cast<RegSolveLM*>(st) = s_lm;  // results for the host
 #ifdef SS_RS_PROF
       if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("RSPROF evals %d step+sync %llu resid %llu count %llu median %llu accum %llu part %llu sync %llu final %llu"
@@ -940,8 +955,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
                           st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
                           s_min);
         if (blockIdx.x == 0 && tid == 0) {
-          st->cur_m[f] = m;
-          st->cur_med[f] = med;
+          s_lm.cur_m[f] = m;
+          s_lm.cur_med[f] = med;
         }
       }
       RS_MARK(3);
@@ -1018,7 +1033,10 @@ __global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph,
         __syncthreads();
       }
       RS_MARK(7);
-      if (tid == 0) rs_step(st, cfg, sfin);
+      if (tid == 0) {
+        rs_step(&s_lm, cfg, sfin);
+        publish();
+      }
     }
   }
 }
