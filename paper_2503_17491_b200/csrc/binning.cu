@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(256)
 //   k_tile_scatter      each block re-reads its pairs and places them with
 //                       shared-memory cursors (order inside a tile is
 //                       irrelevant: k_tile_sort establishes it).
-constexpr int kPairChunk = 16384;
+#ifndef SS_PAIR_CHUNK
+#define SS_PAIR_CHUNK 16384
+#endif
+constexpr int kPairChunk = SS_PAIR_CHUNK;
 constexpr int kMaxTiles = 16384;  // shared-memory histogram capacity
 
 __global__ void __launch_bounds__(1024)

@@ -1010,7 +1010,8 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   // with coalesced 16-byte loads, its outputs leave the same way.
   __shared__ double2 s_rec[kFinBlock * 5];
   __shared__ float4 s_acc[kFinBlock * 4];
-  __shared__ __align__(16) float s_out[kFinBlock * 15];
+  float* s_out = reinterpret_cast<float*>(s_rec);  // (15 floats per splat reuse the 80-byte records once read)
+  static_assert(sizeof(float) * kFinBlock * 15 <= sizeof(double2) * kFinBlock * 5, "s_out fits s_rec");
   __shared__ __align__(16) float s_ta[kFinBlock * 3];
   __shared__ __align__(16) float s_tb[kFinBlock * 3];
   __shared__ __align__(16) float s_ls[kFinBlock * 2];
@@ -1072,16 +1073,23 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   }
   __syncthreads();
   const int nout = raw_space ? 12 : 15;
-  if (tid < cnt) {
   double B[10];
+  float4 ga, gb, gc, gd;
+  if (tid < cnt) {
 #pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    const double2 x = s_rec[tid * 5 + q];
-    B[2 * q] = x.x;
-    B[2 * q + 1] = x.y;
+    for (int q = 0; q < 5; ++q) {
+      const double2 x = s_rec[tid * 5 + q];
+      B[2 * q] = x.x;
+      B[2 * q + 1] = x.y;
+    }
+    ga = s_acc[tid * 4];
+    gb = s_acc[tid * 4 + 1];
+    gc = s_acc[tid * 4 + 2];
+    gd = s_acc[tid * 4 + 3];
   }
+  __syncthreads();  // every record read before s_out (aliasing s_rec) is written
+  if (tid < cnt) {
   const double *Ba = B, *Bb = B + 3, *Bc = B + 6;
-  const float4 ga = s_acc[tid * 4], gb = s_acc[tid * 4 + 1], gc = s_acc[tid * 4 + 2], gd = s_acc[tid * 4 + 3];
   const double V0[3] = {ga.x, ga.y, ga.z}, V1[3] = {ga.w, gb.x, gb.y}, V2[3] = {gb.z, gb.w, gc.x};
   const double Gd = gc.y;
   const float Nc[3] = {gc.z, gc.w, gd.x};
