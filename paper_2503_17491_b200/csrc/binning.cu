@@ -363,30 +363,29 @@ __global__ void __launch_bounds__(256)
 }
 
 // Counting sort of the pairs by tile without global atomics:
-//   k_tile_hist_blocks  per block of kPairChunk pairs, a shared-memory tile
+//   k_tile_hist_blocks  per block of `chunk` pairs, a shared-memory tile
 //                       histogram written as row b of a blocks x tiles matrix;
 //   k_tile_prefix       per tile, exclusive prefix over blocks + tile totals;
 //   k_scan_tiles        tile_ptr and chunk_ptr (32-entry chunks);
 //   k_tile_scatter      each block re-reads its pairs and places them with
 //                       shared-memory cursors (order inside a tile is
 //                       irrelevant: k_tile_sort establishes it).
-#ifndef SS_PAIR_CHUNK
-#define SS_PAIR_CHUNK 16384
-#endif
-constexpr int kPairChunk = SS_PAIR_CHUNK;
+// pairs per counting-sort block: 16 k when tiles are many (config 1: 37 us, 8 k 40),
+// 8 k when they are few (config 2: 29 us, 16 k 34) -- a launch argument `chunk`
+constexpr int kPairChunkMany = 16384, kPairChunkFew = 8192;
 constexpr int kMaxTiles = 16384;  // shared-memory histogram capacity
 
 __global__ void __launch_bounds__(1024)
     k_tile_hist_blocks(const uint32_t* __restrict__ pair_tile, const long long* __restrict__ totals, long long cap,
-                       int ntiles, uint32_t* __restrict__ mat, const int* __restrict__ overflow) {
+                       int ntiles, uint32_t* __restrict__ mat, const int* __restrict__ overflow, int chunk) {
   extern __shared__ uint32_t h[];
   const long long n = min(totals[0], cap);
-  const long long b0 = (long long)blockIdx.x * kPairChunk;
+  const long long b0 = (long long)blockIdx.x * chunk;
   if (b0 >= n && blockIdx.x > 0) return;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) h[t] = 0;
   __syncthreads();
   if (!*overflow) {
-    const long long e = min(b0 + kPairChunk, n);
+    const long long e = min(b0 + chunk, n);
     for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[pair_tile[i]], 1u);
   }
   __syncthreads();
@@ -396,12 +395,13 @@ __global__ void __launch_bounds__(1024)
 // Per tile, exclusive prefix of the block histograms over the pair blocks
 // (in place) and the tile totals.  Block = 32 tiles x 32 block-segments.
 __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
-                                                      uint32_t* __restrict__ mat, int* __restrict__ tile_count) {
+                                                      uint32_t* __restrict__ mat, int* __restrict__ tile_count,
+                                                      int chunk) {
   __shared__ uint32_t part[32][33];
   const int tx = threadIdx.x, seg = threadIdx.y;
   const int t = blockIdx.x * 32 + tx;
   const long long n = min(totals[0], cap);
-  const int nb = (int)max(1LL, (n + kPairChunk - 1) / kPairChunk);
+  const int nb = (int)max(1LL, (n + chunk - 1) / chunk);
   const int per = (nb + 31) / 32;
   const int b0 = min(seg * per, nb), b1 = min(b0 + per, nb);
   uint32_t s = 0;
@@ -463,15 +463,16 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __re
 __global__ void __launch_bounds__(1024)
     k_tile_scatter(const uint32_t* __restrict__ pair_tile, const uint32_t* __restrict__ pair_splat,
                    const long long* __restrict__ totals, long long cap, int ntiles, const uint32_t* __restrict__ mat,
-                   const int* __restrict__ tile_ptr, uint32_t* __restrict__ bucketed, const int* __restrict__ overflow) {
+                   const int* __restrict__ tile_ptr, uint32_t* __restrict__ bucketed, const int* __restrict__ overflow,
+                   int chunk) {
   extern __shared__ uint32_t cur[];
   if (*overflow) return;
   const long long n = min(totals[0], cap);
-  const long long b0 = (long long)blockIdx.x * kPairChunk;
+  const long long b0 = (long long)blockIdx.x * chunk;
   if (b0 >= n) return;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) cur[t] = (uint32_t)tile_ptr[t] + mat[(size_t)blockIdx.x * ntiles + t];
   __syncthreads();
-  const long long e = min(b0 + kPairChunk, n);
+  const long long e = min(b0 + chunk, n);
   for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) {
     const uint32_t pos = atomicAdd(&cur[pair_tile[i]], 1u);
     bucketed[pos] = pair_splat[i];

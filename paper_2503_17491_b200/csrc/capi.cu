@@ -339,7 +339,8 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   rec->cap_pairs = cap;
   const int nb = (n + 255) / 256;
   if (ntiles > kMaxTiles) return SS_ERR_UNSUPPORTED;
-  const int pblocks = (int)((cap + kPairChunk - 1) / kPairChunk);
+  const int pchunk = num_sms() * 16 > ntiles ? kPairChunkFew : kPairChunkMany;
+  const int pblocks = (int)((cap + pchunk - 1) / pchunk);
   if (grow(rec->rec, rec->cap_rec, (size_t)n + 1, s) || grow(rec->rec64, rec->cap_rec64, (size_t)n + 1, s) ||
       grow(rec->key64, rec->cap_key64, (size_t)n + 1, s) || grow(rec->key32, rec->cap_key32, (size_t)n + 1, s) ||
       grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) || grow(rec->bsum, rec->cap_bsum, (size_t)nb + 1, s) ||
@@ -403,11 +404,11 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     StageTimer tm(rec, ST_BUCKET, s);
     const size_t hsm = sizeof(uint32_t) * ntiles;
     set_smem_attrs();
-    k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow);
-    k_tile_prefix<<<(ntiles + 31) / 32, dim3(32, 32), 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count);
+    k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow, pchunk);
+    k_tile_prefix<<<(ntiles + 31) / 32, dim3(32, 32), 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count, pchunk);
     k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long);
     k_tile_scatter<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
-                                              rec->pbucket, overflow);
+                                              rec->pbucket, overflow, pchunk);
   }
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
