@@ -789,13 +789,13 @@ __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ 
 // tiles with at least 96 entries become two slots, one per pixel half
 // (counters[2] = slot count).  (Splitting the forward measured slower: both
 // halves re-stage every entry of the list.)
-// long_target > 0: up to long_target of the longest tiles with >= SS_LONG_MIN entries go
+// long_target > 0: up to long_target of the longest tiles with >= long_min entries go
 // to the block-per-tile forward (k_forward_long, tickets counters[4] < counters[5]);
 // the warp-per-tile forward starts its tickets after them (counters[0] = nlong).
 __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_ptr,
                                                      int* __restrict__ order_fwd, int* __restrict__ order,
                                                      int* __restrict__ counters, int split_target,
-                                                     int long_target) {
+                                                     int long_target, int long_min) {
   __shared__ int hist[1024];
   const int tid = threadIdx.x;
   hist[tid] = 0;
@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   if (tid == 0) {
     const int n96 = hist[1023 - 23];  // exclusive prefix: tiles in buckets < 1000, i.e. L >= 96
     s_nsplit = min(split_target, n96);
-    const int n768 = SS_LONG_MIN <= 0 ? ntiles : hist[1023 - (SS_LONG_MIN / 4 - 1)];  // L >= SS_LONG_MIN
+    const int n768 = long_min <= 0 ? ntiles : hist[1023 - (min(long_min, 4092) / 4 - 1)];  // L >= long_min
     const int nlong = min(long_target, n768);
     counters[0] = nlong;
     counters[4] = 0;

@@ -377,8 +377,11 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   }
   rec->bp.segst = seg ? rec->segst : nullptr;
   rec->bp.fin = seg ? rec->fin : nullptr;
-  // ... and hand the long lists (>= SS_LONG_MIN entries) to the block-per-tile forward
-  const int long_target = (k.T == 8 && (SS_LONG_ALWAYS || num_sms() * 16 > ntiles)) ? SS_LONG_TARGET : 0;
+  // ... and hand the long lists to the block-per-tile forward: every list of >= SS_LONG_MIN
+  // entries when tiles are few, only the tail (>= SS_LONG_MIN_MANY) when they are many
+  const bool few_tiles = num_sms() * 16 > ntiles;
+  const int long_min = few_tiles ? SS_LONG_MIN : SS_LONG_MIN_MANY;
+  const int long_target = (k.T == 8 && (few_tiles || SS_LONG_MIN_MANY > 0)) ? SS_LONG_TARGET : 0;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -421,7 +424,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
     k_tile_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters,
-                                            split_target, long_target);
+                                            split_target, long_target, long_min);
     if (seg)
       k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
