@@ -192,6 +192,14 @@ def config0_graph(dev, replays: int = 300):
             "note": "forward + mapping loss + backward to raw parameters captured once, replayed back to back"}
 
 
+# Our kernels per config-1 step (launch list profiles/r01_v11_bench_launches.csv):
+# forward k_tile_intervals, k_preprocess, k_scan_blocks, k_emit, k_tile_hist_blocks,
+# k_tile_prefix, k_scan_tiles, k_tile_scatter, k_tile_sort_big + k_tile_order (side stream),
+# k_tile_sort, k_forward_long (side; tail lists only), k_forward, k_publish_totals (side);
+# k_mapping_loss; backward k_backward, k_finalize.  (Plus torch fills that are not ours.)
+KERNELS_PER_STEP = 17
+
+
 def secondary_metrics(dev):
     """BASELINE's secondary metrics on one GPU: mapping frames/s (config 2: refine
     iterations on a 10-keyframe, 200k-surfel map, 64x1024) and photometric
@@ -511,7 +519,7 @@ def run_b200(args, ws, rank, local):
                 "config": {"workload": WORKLOAD, "renders_per_step": ws, "camera": "128x2048",
                            "splats_per_rank": 500_000, "parallelism": f"independent maps x{ws}",
                            "l2": "flushed between timed steps (256 MiB write outside the events)"},
-                "clocks": clocks, "gpu_launches": int(sum(stage_n)) + args.steps, "stage_ms": stage,
+                "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "stage_ms": stage,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "secondary": secondary}
         print(json.dumps(line), flush=True)
     if ws > 1:
