@@ -192,7 +192,7 @@ def config0_graph(dev, replays: int = 300):
             "note": "forward + mapping loss + backward to raw parameters captured once, replayed back to back"}
 
 
-# Our kernels per config-1 step (launch list profiles/r01_v11_bench_launches.csv):
+# Our kernels per config-1 step (launch list profiles/r01_v12_step_launches.csv):
 # forward k_tile_intervals, k_preprocess, k_scan_blocks, k_emit, k_tile_hist_blocks,
 # k_tile_prefix, k_scan_tiles, k_tile_scatter, k_tile_sort_big + k_tile_order (side stream),
 # k_tile_sort, k_forward_long (side; tail lists only), k_forward, k_publish_totals (side);
