@@ -162,6 +162,25 @@ def test_long_lists_and_tie_runs_bit_exact(cuda, n, n_tie):
     assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
 
 
+def test_many_tiles_with_tail_lists(cuda):
+    """4,096 tiles (more than resident warps) with a crowded cone: lists of >= 1,536
+    entries go to the block-per-tile forward alongside the warp kernel; tile lists
+    bit-exact and images within the 1e-4 protocol."""
+    cam = W.synth_camera(2048, 128)
+    params = _crowded_params(40000, 0, 7)
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), params)
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), SplatModel.from_params(params))
+    lens = np.diff(ref["tile_ptr"])
+    print("tiles", lens.shape[0], "max list", lens.max(), "lists >= 1536:", int((lens >= 1536).sum()))
+    assert lens.shape[0] == 4096 and int((lens >= 1536).sum()) > 0
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"])
+    assert np.array_equal(rec.pair_splats, ref["pair_splats"])
+    rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
+                       np.full(out.range.shape, 1.0))
+    assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
+
+
 def test_tie_runs_in_shared_memory_sized_lists_bit_exact(cuda):
     """Lists short enough for the 8-warp shared-memory sort but holding a run of equal
     ranges longer than its insertion limit: the block merge-sorts that tile in place."""
