@@ -179,6 +179,20 @@ def test_many_tiles_with_tail_lists(cuda):
     rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref,
                        np.full(out.range.shape, 1.0))
     assert rep["range_norm"] < 1e-4 and rep["opacity_norm"] < 1e-4, rep
+    # backward over the same records (warp-per-tile slots; the block kernel's contribution words)
+    rng = np.random.default_rng(11)
+    gD = rng.normal(size=(cam.height, cam.width))
+    gN = 0.1 * rng.normal(size=(cam.height, cam.width, 3))
+    gO = 0.05 * rng.normal(size=(cam.height, cam.width))
+    model = SplatModel.from_params(params)
+    sg = rasterize_backward(model, rec, out, PixelGradients(gD, gN, gO))
+    got = np.concatenate([sg.d_centers, sg.d_t_alpha, sg.d_t_beta, sg.d_normal, sg.d_scales, sg.d_opacity[:, None]],
+                         axis=1)
+    plain = O.backward_lists(ct, ref["arr"], np.eye(3), ref["tile_ptr"], ref["pair_splats"], ref["range"],
+                             ref["normal"], ref["opacity"], gD, gN, gO)
+    rep = grad_report(got, plain)
+    print("tail-list grad parity", rep)
+    assert_grads(rep)
 
 
 def test_tie_runs_in_shared_memory_sized_lists_bit_exact(cuda):
