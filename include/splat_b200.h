@@ -12,6 +12,8 @@
  *   ss_render_forward        rasterizer.py:455-499  rasterize_forward
  *   ss_records_*             rasterizer.py:136-148  BlendRecords
  *   ss_render_backward       rasterizer.py:534-701  rasterize_backward
+ *   ss_render_backward_blend rasterizer.py:556-684  (its per-tile accumulation loop)
+ *   ss_render_finalize       rasterizer.py:686-701  (its per-splat gradient mapping)
  *                            (+ splats.py:133-163 tangent_raw_gradients and the
  *                             raw-space chain rule of mapping.py:479-494 when
  *                             raw_space = 1)
@@ -107,6 +109,11 @@ int ss_records_check(ss_records* rec, int wait);
  * sums use float atomics (order-dependent rounding, ~1e-7 relative). */
 int ss_records_set_deterministic(ss_records* rec, int32_t deterministic);
 
+/* Buffer generation of `rec`: incremented whenever a forward or backward had
+ * to reallocate any of the records' device buffers.  A CUDA graph captured
+ * over `rec` is only valid while the generation it was captured at holds. */
+int ss_records_generation(const ss_records* rec, uint64_t* generation);
+
 /* Reserve pair capacity for the next forwards on `rec` (at least n_pairs). */
 int ss_records_reserve(ss_records* rec, int64_t n_pairs);
 
@@ -143,6 +150,18 @@ int ss_records_stage_times(ss_records* rec, double* ms, int32_t* launches, int32
 int ss_render_backward(const ss_records* rec, const ss_splats* splats, const float* dD,
                        const float* dN, const float* dO, const float* d_scales_extra,
                        float* grads, int raw_space, void* stream);
+
+/* ss_render_backward in two halves, so that a caller can overlap the per-splat
+ * finalize with a collective over the finished rows (shared-map multi-GPU
+ * training): ss_render_backward_blend runs the blend backward
+ * into the records' per-splat accumulators; ss_render_finalize turns the
+ * accumulators of splats [begin, end) into rows begin..end-1 of `grads`
+ * (same layout as above; begin a multiple of 128) and clears them.  Calling
+ * blend once and finalize over a partition of [0, n) equals ss_render_backward. */
+int ss_render_backward_blend(const ss_records* rec, const ss_splats* splats, const float* dD,
+                             const float* dN, const float* dO, void* stream);
+int ss_render_finalize(const ss_records* rec, const ss_splats* splats, const float* d_scales_extra,
+                       float* grads, int raw_space, int32_t begin, int32_t end, void* stream);
 
 /* Mapping loss of one keyframe (mapping.py:128-196) on device images.
  * kf_range/kf_valid: target range image; kf_normal/kf_nvalid: target normals.

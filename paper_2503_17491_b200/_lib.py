@@ -86,10 +86,16 @@ def lib() -> ctypes.CDLL:
     L.ss_records_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.ss_records_export.argtypes = [vp, vp, vp, vp]
     L.ss_render_backward.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, ctypes.c_int, vp]
+    L.ss_render_backward_blend.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp]
+    L.ss_render_backward_blend.restype = ctypes.c_int
+    L.ss_render_finalize.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, ctypes.c_int, i32, i32, vp]
+    L.ss_render_finalize.restype = ctypes.c_int
     L.ss_fp32_peak_tflops.argtypes = [ctypes.POINTER(d), vp]
     L.ss_fp32_peak_tflops.restype = ctypes.c_int
     L.ss_records_set_deterministic.argtypes = [vp, i32]
     L.ss_records_set_deterministic.restype = ctypes.c_int
+    L.ss_records_generation.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.ss_records_generation.restype = ctypes.c_int
     L.ss_records_reserve.argtypes = [vp, i64]
     L.ss_records_reserve.restype = ctypes.c_int
     L.ss_records_sticky_overflow.argtypes = [vp, vp, vp]
@@ -155,7 +161,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build",
             "ss_records_set_deterministic", "ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats",
             "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact", "ss_adam_step_dev",
-            "ss_store_loss_parts", "ss_records_sticky_overflow", "ss_records_reserve"]
+            "ss_store_loss_parts", "ss_records_sticky_overflow", "ss_records_reserve", "ss_records_generation",
+            "ss_render_backward_blend", "ss_render_finalize"]
 
 
 def check(status: int, what: str = "") -> None:

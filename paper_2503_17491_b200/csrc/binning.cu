@@ -826,7 +826,9 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   if (tid == 0) {
     const int n96 = hist[1023 - 23];  // exclusive prefix: tiles in buckets < 1000, i.e. L >= 96
     s_nsplit = min(split_target, n96);
-    const int n768 = long_min <= 0 ? ntiles : hist[1023 - (min(long_min, 4092) / 4 - 1)];  // L >= long_min
+    // L >= 4 k4 with k4 = ceil(long_min / 4) clamped to [1, 1023]: exclusive prefix hist[1024 - k4]
+    const int k4 = min(max((long_min + 3) >> 2, 1), 1023);
+    const int n768 = long_min <= 0 ? ntiles : hist[1024 - k4];
     const int nlong = min(long_target, n768);
     counters[0] = nlong;
     counters[4] = 0;

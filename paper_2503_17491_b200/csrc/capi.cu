@@ -181,6 +181,21 @@ struct ss_records {
   size_t cap_last = 0;
   float* acc = nullptr;
   size_t cap_acc = 0;
+  // Buffer generation: bumped whenever any device buffer above moved (a grow() freed
+  // and reallocated it).  CUDA graphs captured over these records hold the old
+  // pointers, so their owners key the graphs on this counter.
+  unsigned long long generation = 0;
+  uintptr_t buf_sig = 0;
+  void note_buffers() {
+    const void* bufs[] = {rec, rec64, key64, key32, rect, bsum, mat, tint, tiles, ptile, psplat, pbucket, bitmask,
+                          misc, totals, Tf, last, acc, pacc, segst, fin, segorder};
+    uintptr_t h = 1469598103934665603ull;
+    for (const void* b : bufs) h = (h ^ (uintptr_t)b) * 1099511628211ull;
+    if (h != buf_sig) {
+      buf_sig = h;
+      ++generation;
+    }
+  }
   long long* h_totals = nullptr;  // mapped pinned: totals[2], status, overflow
   long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
@@ -284,6 +299,9 @@ ss_records* ss_records_create(void) {
 void ss_records_destroy(ss_records* r, void* stream) {
   if (!r) return;
   cudaStream_t s = (cudaStream_t)stream;
+  // work queued on the side stream (totals publication, big-list sort, long-list
+  // forward) may still read these buffers and the mapped host words
+  if (r->side) cudaStreamSynchronize(r->side);
   void* bufs[] = {r->rec,    r->rec64,   r->key64, r->key32,  r->rect, r->bsum, r->mat, r->tint,
                   r->tiles,  r->ptile,   r->psplat, r->pbucket, r->bitmask, r->misc, r->totals,
                   r->Tf,     r->last,    r->acc,     r->pacc,  r->segst, r->fin, r->segorder};
@@ -353,6 +371,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       grow(rec->misc, rec->cap_misc, 16, s) || grow(rec->totals, rec->cap_totals, 2, s) ||
       grow(rec->Tf, rec->cap_Tf, P, s) || grow(rec->last, rec->cap_last, P, s))
     return SS_ERR_CUDA;
+  rec->note_buffers();
   int* tile_ptr = rec->tiles;
   int* chunk_ptr = rec->tiles + (ntiles + 1);
   int* tile_count = rec->tiles + 2 * (ntiles + 1);
@@ -375,6 +394,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
         grow(rec->segorder, rec->cap_segorder, nchunk / kSegChunks + 2 * (size_t)ntiles + 2, s))
       return SS_ERR_CUDA;
   }
+  rec->note_buffers();
   rec->bp.segst = seg ? rec->segst : nullptr;
   rec->bp.fin = seg ? rec->fin : nullptr;
   // ... and hand the long lists to the block-per-tile forward: every list of >= SS_LONG_MIN
@@ -500,6 +520,12 @@ int ss_records_reserve(ss_records* rec, int64_t n_pairs) {
   return SS_OK;
 }
 
+int ss_records_generation(const ss_records* rec, uint64_t* generation) {
+  if (!rec || !generation) return SS_ERR_INVALID_ARGUMENT;
+  *generation = rec->generation;
+  return SS_OK;
+}
+
 int ss_records_set_deterministic(ss_records* rec, int32_t deterministic) {
   if (!rec) return SS_ERR_INVALID_ARGUMENT;
   rec->deterministic = deterministic ? 1 : 0;
@@ -560,25 +586,17 @@ int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_sp
   return SS_OK;
 }
 
-int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const float* dD, const float* dN,
-                       const float* dO, const float* d_scales_extra, float* grads, int raw_space, void* stream) {
-  ss_records* rec = const_cast<ss_records*>(rec_c);
-  if (!rec) return SS_ERR_STALE_RECORDS;
-  // A forward still in flight (or being captured into a CUDA graph) is fine:
-  // stream order covers it and the kernels skip work if its capacity
-  // overflowed; completed forwards must have been valid.
-  if (!rec->pending && !rec->valid) return SS_ERR_STALE_RECORDS;
-  if (!splats || splats->n != rec->n) return SS_ERR_STALE_RECORDS;
-  if (!dD || !dN || !dO || !grads) return SS_ERR_INVALID_ARGUMENT;
-  cudaStream_t s = (cudaStream_t)stream;
+// The blend half of the backward: per-splat accumulators from the pixel gradients.
+static int backward_blend(ss_records* rec, const ss_splats* splats, const float* dD, const float* dN,
+                          const float* dO, cudaStream_t s) {
   const int n = rec->n;
-  if (n == 0) return SS_OK;
   // acc is all-zero between backward passes: zeroed once when (re)allocated, and
   // k_finalize clears every row it consumes (no per-call 32 MB memset)
   {
     float* before = rec->acc;
     if (grow(rec->acc, rec->cap_acc, (size_t)n * kAcc, s)) return SS_ERR_CUDA;
     if (rec->acc != before) SS_CUDA_TRY(cudaMemsetAsync(rec->acc, 0, sizeof(float) * rec->cap_acc, s));
+    rec->note_buffers();
   }
   const int ntiles = rec->ntiles;
   const int* tile_ptr = rec->tiles;
@@ -588,41 +606,100 @@ int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const f
   if (rec->deterministic) {
     if (grow(rec->pacc, rec->cap_pacc, (size_t)rec->cap_pairs * kAcc, s)) return SS_ERR_CUDA;
     pacc = rec->pacc;
+    rec->note_buffers();
     k_zero_pacc<<<num_sms() * 4, 256, 0, s>>>((float4*)pacc, rec->totals, rec->cap_pairs);
   }
-  {
-    const int blocks =
-        std::min((ntiles + rec->split_target + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
-    int* order = rec->tiles + 5 * (ntiles + 1);
-    int* counters = rec->misc + 4;
-    StageTimer tm(rec, ST_BACKWARD, s);
-    if (rec->cam.T == 8 && rec->seg)  // segment slots: persistent warps, as many as are resident
-      k_backward<8, false, true><<<num_sms() * SS_BWD_MINB, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
-          rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-          dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc);
-    else if (rec->cam.T == 8)
-      (rec->split_target ? k_backward<8, true, false> : k_backward<8, false, false>)<<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
-                                                           rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                           rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
-                                                           pacc);
-    else
-      k_backward<16, false, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs,
-                                                            rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-                                                            dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
-                                                           pacc);
-    SS_CUDA_TRY(cudaGetLastError());
-    if (pacc)
-      k_det_gather<<<(n + 255) / 256, 256, 0, s>>>(n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
-                                                   rec->acc, rec->misc + 1);
-  }
-  {
-    StageTimer tm(rec, ST_FINALIZE, s);
-    k_finalize<<<(n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(to_k(splats), rec->pose, rec->rec64, rec->acc,
-                                                                    d_scales_extra, grads, raw_space,
-                                                                    rec->misc + 5);
-  }
+  const int blocks = std::min((ntiles + rec->split_target + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
+  int* order = rec->tiles + 5 * (ntiles + 1);
+  int* counters = rec->misc + 4;
+  StageTimer tm(rec, ST_BACKWARD, s);
+  if (rec->cam.T == 8 && rec->seg)  // segment slots: persistent warps, as many as are resident
+    k_backward<8, false, true><<<num_sms() * SS_BWD_MINB, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
+        rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
+        dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc);
+  else if (rec->cam.T == 8)
+    (rec->split_target ? k_backward<8, true, false> : k_backward<8, false, false>)
+        <<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+                                                          rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
+                                                          rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
+                                                          pacc);
+  else
+    k_backward<16, false, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
+        rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
+        dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2, pacc);
+  SS_CUDA_TRY(cudaGetLastError());
+  if (pacc)
+    k_det_gather<<<(n + 255) / 256, 256, 0, s>>>(n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
+                                                 rec->acc, rec->misc + 1);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
+}
+
+// The finalize half on splats [begin, end): camera-frame -> world / raw gradients
+// into rows begin..end-1 of `grads`, clearing the consumed accumulators.
+static int backward_finalize(ss_records* rec, const ss_splats* splats, const float* d_scales_extra, float* grads,
+                             int raw_space, int begin, int end, cudaStream_t s) {
+  if (end <= begin) return SS_OK;
+  const int w = raw_space ? 12 : 15;
+  SplatsK sk = to_k(splats);
+  sk.n = end - begin;
+  sk.centers += 3 * (size_t)begin;
+  sk.raw_ta += 3 * (size_t)begin;
+  sk.raw_tb += 3 * (size_t)begin;
+  sk.log_scales += 2 * (size_t)begin;
+  sk.logit_opacity += begin;
+  StageTimer tm(rec, ST_FINALIZE, s);
+  k_finalize<<<(sk.n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(
+      sk, rec->pose, rec->rec64 + begin, rec->acc + (size_t)begin * kAcc,
+      d_scales_extra ? d_scales_extra + 2 * (size_t)begin : nullptr, grads + (size_t)begin * w, raw_space,
+      rec->misc + 5);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+static int backward_args(const ss_records* rec, const ss_splats* splats) {
+  if (!rec) return SS_ERR_STALE_RECORDS;
+  // A forward still in flight (or being captured into a CUDA graph) is fine:
+  // stream order covers it and the kernels skip work if its capacity
+  // overflowed; completed forwards must have been valid.
+  if (!rec->pending && !rec->valid) return SS_ERR_STALE_RECORDS;
+  if (!splats || splats->n != rec->n) return SS_ERR_STALE_RECORDS;
+  return SS_OK;
+}
+
+int ss_render_backward(const ss_records* rec_c, const ss_splats* splats, const float* dD, const float* dN,
+                       const float* dO, const float* d_scales_extra, float* grads, int raw_space, void* stream) {
+  ss_records* rec = const_cast<ss_records*>(rec_c);
+  int st = backward_args(rec, splats);
+  if (st) return st;
+  if (!dD || !dN || !dO || !grads) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rec->n == 0) return SS_OK;
+  st = backward_blend(rec, splats, dD, dN, dO, s);
+  if (st) return st;
+  return backward_finalize(rec, splats, d_scales_extra, grads, raw_space, 0, rec->n, s);
+}
+
+int ss_render_backward_blend(const ss_records* rec_c, const ss_splats* splats, const float* dD, const float* dN,
+                             const float* dO, void* stream) {
+  ss_records* rec = const_cast<ss_records*>(rec_c);
+  int st = backward_args(rec, splats);
+  if (st) return st;
+  if (!dD || !dN || !dO) return SS_ERR_INVALID_ARGUMENT;
+  if (rec->n == 0) return SS_OK;
+  return backward_blend(rec, splats, dD, dN, dO, (cudaStream_t)stream);
+}
+
+int ss_render_finalize(const ss_records* rec_c, const ss_splats* splats, const float* d_scales_extra, float* grads,
+                       int raw_space, int32_t begin, int32_t end, void* stream) {
+  ss_records* rec = const_cast<ss_records*>(rec_c);
+  int st = backward_args(rec, splats);
+  if (st) return st;
+  if (!grads || begin < 0 || end > rec->n || begin > end) return SS_ERR_INVALID_ARGUMENT;
+  // row chunks start on kFinBlock boundaries: the kernel's vector loads stay 16-byte aligned
+  if (begin % kFinBlock != 0) return SS_ERR_INVALID_ARGUMENT;
+  if (!rec->acc || rec->cap_acc < (size_t)rec->n * kAcc) return SS_ERR_STALE_RECORDS;  // no blend pass yet
+  return backward_finalize(rec, splats, d_scales_extra, grads, raw_space, begin, end, (cudaStream_t)stream);
 }
 
 int ss_fp32_peak_tflops(double* tflops, void* stream) {
@@ -836,6 +913,8 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
                  double* T_out_Rt, int32_t* info6, double* r2_out2, void* workspace, void* stream) {
   if (!cam || !T0_Rt || !cfg || !T_out_Rt || !info6 || !r2_out2 || !workspace) return SS_ERR_INVALID_ARGUMENT;
   if (cfg->mode < 0 || cfg->mode > 3 || cfg->max_iters < 0 || cfg->assoc_k < 1) return SS_ERR_INVALID_ARGUMENT;
+  // the association keeps register-resident k-best lists of at most 8 leaves
+  if (cfg->mode != 0 && cfg->assoc_k > 8) return SS_ERR_UNSUPPORTED;
   const bool need_geo = cfg->mode != 0, need_photo = cfg->mode != 1;
   if (need_geo && (n_leaves < 0 || n_geo_scan < 0 || (n_leaves > 0 && (!leaf_centroids || !leaf_normals)) ||
                    (n_geo_scan > 0 && !geo_scan)))

@@ -7,6 +7,35 @@
 // child gets the median point of an odd-sized split.  Plain float64
 // arithmetic, no scaling branches (the leaf-tree covariances are far from the
 // over/underflow thresholds that trigger them).
+//
+// The routines restated here (dlartg, dlaev2, dlapy2, dsteqr, dsytd2, dorm2r)
+// follow reference LAPACK, which is distributed under the modified BSD licence:
+//   Copyright (c) 1992-2013 The University of Tennessee and The University of
+//   Tennessee Research Foundation.  All rights reserved.
+//   Copyright (c) 2000-2013 The University of California Berkeley.  All rights reserved.
+//   Copyright (c) 2006-2013 The University of Colorado Denver.  All rights reserved.
+//   Redistribution and use in source and binary forms, with or without
+//   modification, are permitted provided that the following conditions are met:
+//   - Redistributions of source code must retain the above copyright notice,
+//     this list of conditions and the following disclaimer.
+//   - Redistributions in binary form must reproduce the above copyright notice,
+//     this list of conditions and the following disclaimer listed in this
+//     license in the documentation and/or other materials provided with the
+//     distribution.
+//   - Neither the name of the copyright holders nor the names of its
+//     contributors may be used to endorse or promote products derived from
+//     this software without specific prior written permission.
+//   THIS SOFTWARE IS PROVIDED BY THE COPYRIGHT HOLDERS AND CONTRIBUTORS "AS IS"
+//   AND ANY EXPRESS OR IMPLIED WARRANTIES, INCLUDING, BUT NOT LIMITED TO, THE
+//   IMPLIED WARRANTIES OF MERCHANTABILITY AND FITNESS FOR A PARTICULAR PURPOSE
+//   ARE DISCLAIMED.  IN NO EVENT SHALL THE COPYRIGHT OWNER OR CONTRIBUTORS BE
+//   LIABLE FOR ANY DIRECT, INDIRECT, INCIDENTAL, SPECIAL, EXEMPLARY, OR
+//   CONSEQUENTIAL DAMAGES (INCLUDING, BUT NOT LIMITED TO, PROCUREMENT OF
+//   SUBSTITUTE GOODS OR SERVICES; LOSS OF USE, DATA, OR PROFITS; OR BUSINESS
+//   INTERRUPTION) HOWEVER CAUSED AND ON ANY THEORY OF LIABILITY, WHETHER IN
+//   CONTRACT, STRICT LIABILITY, OR TORT (INCLUDING NEGLIGENCE OR OTHERWISE)
+//   ARISING IN ANY WAY OUT OF THE USE OF THIS SOFTWARE, EVEN IF ADVISED OF THE
+//   POSSIBILITY OF SUCH DAMAGE.
 #pragma once
 #include <math.h>
 

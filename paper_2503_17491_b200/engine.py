@@ -99,6 +99,12 @@ class Records:
         """Status of the last forward (SS_ERR_CAPACITY means: re-run it)."""
         return int(lib().ss_records_check(self.ptr, int(bool(wait))))
 
+    def generation(self) -> int:
+        """Buffer generation (bumped when a forward / backward reallocated a device buffer)."""
+        g = ctypes.c_uint64(0)
+        check(lib().ss_records_generation(self.ptr, ctypes.byref(g)), "records")
+        return int(g.value)
+
     def counts(self):
         n = ctypes.c_int64(0)
         tx = ctypes.c_int32(0)
@@ -184,6 +190,32 @@ def backward(records: Records, splats: dict, dD, dN, dO, raw_space: bool, d_scal
                                   ctypes.c_void_p(stream_ptr()))
     check(st, "rasterize_backward")
     return out
+
+
+FINALIZE_ALIGN = 128  # ss_render_finalize row chunks start on multiples of this
+
+
+def backward_blend(records: Records, splats: dict, dD, dN, dO) -> None:
+    """First half of ``backward``: the blend backward into the records' accumulators."""
+    require_cuda()
+    sp = ss_splats(splats)
+    dD, dN, dO = (x.contiguous().float() for x in (dD, dN, dO))
+    st = lib().ss_render_backward_blend(records.ptr, ctypes.byref(sp), ctypes.c_void_p(dD.data_ptr()),
+                                        ctypes.c_void_p(dN.data_ptr()), ctypes.c_void_p(dO.data_ptr()),
+                                        ctypes.c_void_p(stream_ptr()))
+    check(st, "rasterize_backward")
+    records._pix_grads = (dD, dN, dO)  # alive until the stream consumed them
+
+
+def finalize(records: Records, splats: dict, out, begin: int, end: int, raw_space: bool = True,
+             d_scales_extra=None) -> None:
+    """Second half of ``backward`` for splats [begin, end) into rows begin..end-1 of ``out``."""
+    sp = ss_splats(splats)
+    ex = 0 if d_scales_extra is None else d_scales_extra.data_ptr()
+    st = lib().ss_render_finalize(records.ptr, ctypes.byref(sp), ctypes.c_void_p(ex),
+                                  ctypes.c_void_p(out.data_ptr()), int(bool(raw_space)), int(begin), int(end),
+                                  ctypes.c_void_p(stream_ptr()))
+    check(st, "rasterize_backward")
 
 
 def mapping_loss(D, N, O, kf_range, kf_valid, kf_normal, kf_nvalid, w_opacity=0.05, w_normal=0.1,

@@ -239,10 +239,9 @@ class DeviceMap:
         return np.array([cfg.lr_centers * self.scene_scale, cfg.lr_tangents, cfg.lr_tangents, cfg.lr_log_scales,
                          cfg.lr_logit_opacity], dtype=np.float64)
 
-    def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None,
-                     sync: bool = True):
-        """Render keyframe ``kf_index``, mapping loss, backward: (n x 12 raw gradient, loss parts
-        [range, opacity, normal, scale] float64) on the device."""
+    def _render_loss(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None, sync: bool):
+        """Render keyframe ``kf_index`` and its mapping loss: (dD, dN, dO, parts); the scale-loss
+        gradient lands in ``self.d_scales``."""
         raster = raster or RasterConfig()
         kf = self.keyframes[kf_index]
         sp = self.params
@@ -254,8 +253,27 @@ class DeviceMap:
                                   float(cfg.w_scale), ctypes.c_void_p(self.d_scales.data_ptr()),
                                   ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(engine.stream_ptr())),
               "scale_loss")
-        g = engine.backward(self.rec, sp, dD, dN, dO, raw_space=True, d_scales_extra=self.d_scales)
+        return dD, dN, dO, parts
+
+    def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None,
+                     sync: bool = True):
+        """Render keyframe ``kf_index``, mapping loss, backward: (n x 12 raw gradient, loss parts
+        [range, opacity, normal, scale] float64) on the device."""
+        dD, dN, dO, parts = self._render_loss(kf_index, cfg, raster, sync)
+        g = engine.backward(self.rec, self.params, dD, dN, dO, raw_space=True, d_scales_extra=self.d_scales)
         return g, parts
+
+    def blend_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None,
+                       sync: bool = True):
+        """``raw_gradient`` up to the per-splat accumulators (render, loss, blend backward);
+        ``finalize_rows`` then produces the raw gradient rows.  Returns the loss parts."""
+        dD, dN, dO, parts = self._render_loss(kf_index, cfg, raster, sync)
+        engine.backward_blend(self.rec, self.params, dD, dN, dO)
+        return parts
+
+    def finalize_rows(self, begin: int, end: int, out: torch.Tensor) -> None:
+        """Raw gradient rows [begin, end) of the last ``blend_gradient`` into ``out``."""
+        engine.finalize(self.rec, self.params, out, begin, end, raw_space=True, d_scales_extra=self.d_scales)
 
     def apply_adam(self, g: torch.Tensor, cfg: MappingConfig) -> None:
         """Fused Adam step + log-scale clamp (mapping.py:367-379, 495-496)."""
@@ -300,9 +318,12 @@ class DeviceMap:
     _HIST = 4096
 
     def _graph_key(self, cfg, raster):
+        # the graphs hold raw device pointers: the parameter / moment tensors and every
+        # buffer of the shared records (whose generation moves when an eager forward or
+        # backward reallocated one of them)
         return (self.n, len(self.keyframes), tuple(self.params[k].data_ptr() for k in engine.PARAM_NAMES),
-                self.m.data_ptr(), self.v.data_ptr(), tuple(sorted(vars(cfg).items())),
-                tuple(sorted(vars(raster).items())), self.scene_scale)
+                self.m.data_ptr(), self.v.data_ptr(), self.d_scales.data_ptr(), self.rec.generation(),
+                tuple(sorted(vars(cfg).items())), tuple(sorted(vars(raster).items())), self.scene_scale)
 
     def _graph_step(self, kf_index, cfg, raster):
         g, parts = self.raw_gradient(kf_index, cfg, raster, sync=False)
@@ -354,12 +375,36 @@ class DeviceMap:
             # allocate at that size, backward buffers included (nothing may be allocated under capture)
             self.raw_gradient(len(self.keyframes) - 1, cfg, raster)
             self._graphs = {}
-            self._gkey = key
+            self._gkey = self._graph_key(cfg, raster)  # after the allocations above
             self._t_dev = torch.zeros(1, dtype=torch.int32, device=dev)
             self._bias = torch.ones(2, dtype=torch.float32, device=dev)
             self._it = torch.zeros(1, dtype=torch.int32, device=dev)
             self._sticky = torch.zeros(1, dtype=torch.int32, device=dev)
             self._hist = torch.zeros((self._HIST, 4), dtype=torch.float64, device=dev)
+
+    # Step-by-step replay for callers that interleave several maps (parallel.LocalMapShard):
+    # begin_replay(), then replay_step(k) per iteration, then end_replay().
+    def begin_replay(self, cfg: MappingConfig, raster: RasterConfig | None = None) -> None:
+        """Capture (or reuse) the per-keyframe step graphs and reset the on-device step state."""
+        raster = raster or RasterConfig()
+        self._prepare_graphs(cfg, raster)
+        self._t_dev.fill_(self.t)
+        self._it.zero_()
+        self._sticky.zero_()
+        self._replay = (cfg, raster)
+
+    def replay_step(self, kf_index: int) -> None:
+        """One refine iteration on keyframe ``kf_index`` (graph replay, no host synchronisation)."""
+        cfg, raster = self._replay
+        self._graph_for(kf_index, cfg, raster).replay()
+
+    def end_replay(self) -> bool:
+        """Synchronise; False if a replay overflowed its pair capacity (its results are invalid)."""
+        ok = not int(self._sticky.item())
+        self.t = int(self._t_dev.item())
+        if not ok:
+            self._gkey = None
+        return ok
 
     def _refine_graphs(self, cfg, iters, rng, raster):
         """Graph-replayed refine; None when it cannot be used (the eager loop runs instead)."""

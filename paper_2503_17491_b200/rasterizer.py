@@ -140,12 +140,39 @@ class BlendRecords:
         return self._pair_splats
 
 
-# float32 device copies of models, keyed by object identity and version
+# float32 device copies of models, keyed by object identity, version, the parameter
+# arrays' identities and buffers, and a content fingerprint of each array
 _dev_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_FP_W: dict = {}
+
+
+def _fingerprint(a) -> int:
+    """Position-sensitive content fingerprint of a parameter array: the wrapping sum of
+    its 64-bit words times fixed odd pseudo-random weights (~1 ms per 1.5 M values).
+    Any in-place edit the reference's version counter would not see
+    (``model.centers[i] = ...`` without ``touch()``) changes it; the reference itself
+    re-reads the arrays on every call."""
+    x = np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(-1).view(np.int64)
+    w = _FP_W.get(x.size)
+    if w is None:
+        w = np.random.default_rng(x.size).integers(0, 2 ** 62, x.size, dtype=np.int64) | 1
+        if len(_FP_W) > 8:
+            _FP_W.clear()
+        _FP_W[x.size] = w
+    return int(np.add.reduce(x * w, dtype=np.int64)) if x.size else 0
+
+
+def _cache_key(model) -> tuple:
+    key = [int(getattr(model, "version", 0)), len(model)]
+    for k in engine.PARAM_NAMES:
+        a = getattr(model, k)
+        ptr = a.ctypes.data if isinstance(a, np.ndarray) else 0
+        key.append((id(a), ptr, _fingerprint(a)))
+    return tuple(key)
 
 
 def _device_params(model) -> dict:
-    key = (int(getattr(model, "version", 0)), len(model))
+    key = _cache_key(model)
     try:
         hit = _dev_cache.get(model)
     except TypeError:

@@ -11,9 +11,9 @@ Around it: the model render of ``sample_model`` is the B200 rasterizer, the
 PCA leaf tree (:98-164) is built level-parallel on the device
 (``ss_leaf_tree_build``), the scan range image by ``ss_range_image``.  The
 host only draws the reference's geometric scan subsample (same numpy RNG
-call) and re-orthonormalises the final rotation (SVD).
-``register(..., device_loop=False)`` (photometric mode) runs the loop on the
-host over ``ss_photo_system`` evaluations instead (parity check of the kernel).
+call) and re-orthonormalises the final rotation (SVD).  ``PhotoProblem``
+exposes single ``_photo_system`` evaluations (``ss_photo_system``) for
+callers that drive their own loop.
 """
 from __future__ import annotations
 
@@ -250,7 +250,7 @@ _MODE = {"photometric": 0, "geometric": 1, "joint": 2, "sequential": 3}
 
 
 def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, raster: RasterConfig | None = None,
-             rng=None, device_loop: bool = True) -> RegistrationResult:
+             rng=None) -> RegistrationResult:
     """Align a sensor-frame scan to the model (registration.py:387-524)."""
     cfg = cfg or RegistrationConfig()
     scan = np.asarray(scan, dtype=float).reshape(-1, 3)
@@ -269,10 +269,6 @@ def register(model, scan, cam, initial, cfg: RegistrationConfig | None = None, r
     if n_model < cfg.min_residuals:
         raise RegistrationError("model renders to too few confident pixels")
     X_w = model_pts[:: s * s].contiguous() if s > 1 else model_pts
-    if not device_loop:
-        if cfg.mode != "photometric":
-            raise RegistrationError("the host loop covers the photometric mode only; use device_loop=True")
-        return _solve(PhotoProblem(X_w, dscan, cfg), initial, cfg)
     tree, geo_scan = None, None
     if cfg.mode != "photometric":
         geo_scan = scan
@@ -323,57 +319,3 @@ def _solve_device(X_w: torch.Tensor, scan: DeviceScan, initial, cfg: Registratio
     if int(X_w.shape[0]) == 0:
         raise RegistrationError("too few residuals survive association")
     return solve_device(cfg, initial, scan, X_w.contiguous())
-
-
-def _solve(prob: PhotoProblem, initial, cfg: RegistrationConfig) -> RegistrationResult:
-    """The reference's GN/LM loop (registration.py:437-524), photometric phase only."""
-    T = initial.copy()
-    it_total = 0
-    converged = False
-    last = (0.0, 0)
-    lam = cfg.damping_init
-    budget = cfg.max_iters
-    while it_total < budget:
-        it_total += 1
-        anneal = cfg.assoc_gate * 0.5 ** it_total
-        fp = max(cfg.trim_floor_photo, anneal)
-        photo = prob.evaluate(T, fp)
-        n_photo = 0
-        if photo is not None:
-            Hs, bs, hub, m, r2 = photo
-            s = 1.0 / m
-            H = s * Hs
-            b = s * bs
-            n_photo = m
-            last = (r2, m)
-        if n_photo < cfg.min_residuals:
-            raise RegistrationError("too few residuals survive association")
-        obj0 = s * hub
-        accepted = False
-        delta = np.zeros(6)
-        while lam <= cfg.damping_max:
-            try:
-                delta = np.linalg.solve(H + lam * np.eye(6), -b)
-            except np.linalg.LinAlgError:
-                lam = max(lam, 1e-8) * 10.0
-                continue
-            if not np.all(np.isfinite(delta)):
-                lam = max(lam, 1e-8) * 10.0
-                continue
-            T_try = T.retract(delta)
-            p2 = prob.evaluate(T_try, fp, objective_only=True)
-            if p2 is not None and s * p2[2] <= obj0 + 1e-12:
-                T = T_try
-                lam = max(lam * 0.25, cfg.damping_init)
-                accepted = True
-                break
-            lam = max(lam, 1e-8) * 10.0
-        if not accepted:
-            break
-        if np.linalg.norm(delta) < cfg.tol:
-            converged = True
-            break
-    T = T.orthonormalized()
-    r2, m = last
-    rms = float(np.sqrt(r2 / m)) if m else 0.0
-    return RegistrationResult(T, converged, it_total, 0.0, rms, 0, int(m), cfg.mode)

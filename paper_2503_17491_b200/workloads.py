@@ -281,3 +281,50 @@ def config3_problem(n_surfels: int = 300_000, seed: int = 0, width: int = 1024, 
     scan = (tg["range"][tg["valid"]][:, None].astype(np.float64) * cam.pixel_directions[tg["valid"]])
     initial = truth.compose(SE3Pose(so3_exp(np.deg2rad(2.0) * rng.normal(size=3)), 0.2 * rng.normal(size=3)))
     return params, cam, scan, truth, initial
+
+
+# --- device-built local maps (configs 2 and 4) ---------------------------------------
+
+_KF_CACHE: dict = {}
+
+
+def keyframe_targets(n: int = 10, seed: int = 0, width: int = 1024, height: int = 64):
+    """[(camera, pose, target images)] along the config-2 trajectory (keyframe_poses) over
+    the procedural scene; cached per process (the numpy ray cast is the slow part)."""
+    key = (n, seed, width, height)
+    if key not in _KF_CACHE:
+        scene = Scene(0)
+        cam = synth_camera(width, height)
+        _KF_CACHE[key] = [(cam, pose, target_images(scene, cam, pose)) for pose in keyframe_poses(n, seed)]
+    return _KF_CACHE[key]
+
+
+def device_keyframes(targets) -> list:
+    """DeviceKeyframe per (camera, pose, targets) entry, indexed in order."""
+    from .mapping import DeviceKeyframe
+    return [DeviceKeyframe(cam, pose, tg["range"], tg["valid"], tg["normal"], tg["nvalid"], i)
+            for i, (cam, pose, tg) in enumerate(targets)]
+
+
+def build_local_map(dkfs: list, n_spawn: int, seed: int, raster=None):
+    """A local map grown the reference's way: LocalMap.start on the first keyframe, then
+    add_keyframe with each further one (mapping.py:392-438: render, densify mask, prune,
+    weighted spawn of up to n_spawn surfels), on the device.  SURVEY 8(d) config 2:
+    10 keyframes x 20k at 64x1024 gives 200,000 surfels."""
+    from .mapping import DeviceMap, MappingConfig
+    cfg = MappingConfig(n_spawn=n_spawn)
+    rng = np.random.default_rng(seed)
+    dm = DeviceMap.start(dkfs[0], cfg, rng, raster)
+    for kf in dkfs[1:]:
+        dm.add_keyframe(kf, cfg, rng, raster)
+    return dm
+
+
+def merge_maps(maps: list, keyframes: list):
+    """One DeviceMap holding the union of the given maps' surfels (config 4b's shared map)."""
+    import torch
+
+    from .engine import PARAM_NAMES
+    from .mapping import DeviceMap
+    params = {k: torch.cat([m.params[k] for m in maps]) for k in PARAM_NAMES}
+    return DeviceMap(params, keyframes, maps[0].scene_scale)

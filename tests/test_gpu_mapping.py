@@ -100,3 +100,71 @@ def test_graph_refine_matches_eager(cuda):
     for k in NAMES:
         x, y = a.params[k].cpu().numpy(), b.params[k].cpu().numpy()
         assert np.linalg.norm(x - y) <= 2e-3 * np.linalg.norm(y), k
+
+
+def test_split_backward_equals_full(cuda):
+    """ss_render_backward_blend + ss_render_finalize over row chunks == ss_render_backward."""
+    from paper_2503_17491_b200.parallel import row_chunks
+    cfg = MP.MappingConfig(n_spawn=1200)
+    dm = _golden_map()
+    g_full, p_full = dm.raw_gradient(1, cfg)
+    dm.blend_gradient(1, cfg)
+    out = torch.full_like(g_full, float("nan"))
+    for b, e in row_chunks(dm.n, 5):
+        dm.finalize_rows(b, e, out)
+    torch.cuda.synchronize()
+    diff = (out - g_full).abs().max().item()
+    scale = g_full.abs().max().item()
+    assert diff <= 1e-6 * scale, (diff, scale)  # same kernels; float-atomic order only
+
+
+def test_shared_map_device_ops_world1(cuda):
+    """parallel.device_ops + SharedMapTrainer at world size 1 (an NCCL communicator of one
+    rank): one trainer step equals DeviceMap.step on the keyframe the sampler draws."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2503_17491_b200.parallel import SharedMapTrainer, device_ops
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        cfg = MP.MappingConfig(n_spawn=1200)
+        a, b = _golden_map(), _golden_map()
+        tr = SharedMapTrainer(device_ops(a, cfg), len(a.keyframes), cfg, seed=7, chunks=4)
+        picks = [tr.step() for _ in range(3)]
+        rng = np.random.default_rng(7)
+        ref_picks = [MP.sample_keyframe_index(len(b.keyframes), cfg.kf_sample_p, rng) for _ in range(3)]
+        assert picks == ref_picks
+        for k in ref_picks:
+            b.step(k, cfg)
+        assert a.t == b.t == 3
+        for k in NAMES:
+            x, y = a.params[k].cpu().numpy(), b.params[k].cpu().numpy()
+            assert np.linalg.norm(x - y) <= 2e-3 * np.linalg.norm(y), k
+    finally:
+        dist.destroy_process_group()
+
+
+def test_local_map_shard_replay_matches_refine(cuda):
+    """parallel.LocalMapShard (graph replay, maps interleaved round robin) equals each map's
+    own refine() with the same sampler seeds."""
+    from paper_2503_17491_b200.parallel import LocalMapShard
+    cfg = MP.MappingConfig(n_spawn=1200)
+    maps = [_golden_map(), _golden_map()]
+    sh = LocalMapShard(maps, cfg, seed=11)
+    sh.begin()
+    for _ in range(6):
+        sh.step()
+    assert sh.end()
+    for i, dm in enumerate(maps):
+        ref = _golden_map()
+        ref.refine(cfg, 3, np.random.default_rng(11 + i), graphs=False)
+        assert dm.t == ref.t == 3
+        for k in NAMES:
+            x, y = dm.params[k].cpu().numpy(), ref.params[k].cpu().numpy()
+            assert np.linalg.norm(x - y) <= 2e-3 * np.linalg.norm(y), k

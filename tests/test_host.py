@@ -59,3 +59,26 @@ def test_se3_exp_round_trip():
     T = se3_exp(d)
     assert np.allclose(T.rotation.T @ T.rotation, np.eye(3), atol=1e-12)
     assert np.allclose(SE3Pose.identity().retract(d).translation, T.translation)
+
+
+def test_device_cache_key_sees_inplace_edits():
+    """The float32 device copy of a model is reused only while the parameter arrays are
+    unchanged: in-place edits without touch() (which the reference's version counter
+    would not see) and array reassignment both change the key."""
+    import numpy as np
+    from paper_2503_17491_b200 import SplatModel
+    from paper_2503_17491_b200 import workloads as W
+    from paper_2503_17491_b200.rasterizer import _cache_key
+    m = SplatModel.from_params(W.random_splats(1000, 3))
+    k0 = _cache_key(m)
+    assert _cache_key(m) == k0
+    m.centers[5, 1] += 1e-3
+    k1 = _cache_key(m)
+    assert k1 != k0
+    m.log_scales[[0, 1]] = m.log_scales[[1, 0]]  # a row swap keeps sums: position-sensitive key
+    assert _cache_key(m) != k1
+    k2 = _cache_key(m)
+    m.logit_opacity = m.logit_opacity.copy()  # same values, new array
+    assert _cache_key(m) != k2
+    m.touch()
+    assert _cache_key(m)[0] == m.version
