@@ -483,6 +483,21 @@ __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t va, uns
   return ka < kb || (ka == kb && va < vb);
 }
 
+// Lanes holding the same BITS-bit digit as this lane (0 for an invalid lane): one ballot per
+// bit.  (__match_any_sync iterates over the distinct values of the warp; with the ~32
+// distinct digits of a sort pass it measured 57.8 -> 44.8 us for k_tile_sort at config 1.)
+template <int BITS>
+__device__ __forceinline__ uint32_t warp_match(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bb : ~bb;
+  }
+  return valid ? m : 0u;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -594,7 +609,7 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
       const int idx = warp * seg + j * 32 + lane;
       const bool ok = idx < L;
       dg[j] = ok ? (int)(((cur ? sk1 : sk0)[idx] >> sh) & 0xffu) : 256;
-      const uint32_t peers = __match_any_sync(0xffffffffu, dg[j]);
+      const uint32_t peers = warp_match<8>((uint32_t)dg[j], ok);
       const int leader = 31 - __clz(peers);
       uint16_t before = 0;
       if (dg[j] < 256) before = wc[dg[j]];
@@ -802,7 +817,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   if (tid < 4) counters[tid] = 0;
   __syncthreads();  // (counters[0] is set to the long-tile count below, after the scan)
   for (int t = tid; t < ntiles; t += 1024) {
-    const int L = tile_ptr[t + 1] - tile_ptr[t];
+    const int L = max(0, tile_ptr[t + 1] - tile_ptr[t]);
     atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1);
   }
   __syncthreads();
@@ -837,7 +852,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   __syncthreads();
   const int nsplit = s_nsplit;
   for (int t = tid; t < ntiles; t += 1024) {
-    const int L = tile_ptr[t + 1] - tile_ptr[t];
+    const int L = max(0, tile_ptr[t + 1] - tile_ptr[t]);
     const int r = atomicAdd(&hist[1023 - (min(L, 4095) >> 2)], 1);  // LPT rank
     order_fwd[r] = t << 2;
     if (r < nsplit) {

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(1024) k_seg_order(int ntiles, const int* __res
   int cnt = 0;
   for (int r = r0; r < r1; ++r) {
     const int t = order_fwd[r] >> 2;
-    cnt += (tile_ptr[t + 1] - tile_ptr[t] + kSegEntries - 1) / kSegEntries;
+    cnt += (max(0, tile_ptr[t + 1] - tile_ptr[t]) + kSegEntries - 1) / kSegEntries;
   }
   int inc = cnt;
   for (int off = 1; off < 32; off <<= 1) {
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(1024) k_seg_order(int ntiles, const int* __res
   for (int w = 0; w < warp; ++w) base += wsum[w];
   for (int r = r0; r < r1; ++r) {
     const int t = order_fwd[r] >> 2;
-    const int ns = (tile_ptr[t + 1] - tile_ptr[t] + kSegEntries - 1) / kSegEntries;
+    const int ns = (max(0, tile_ptr[t + 1] - tile_ptr[t]) + kSegEntries - 1) / kSegEntries;
     for (int q = 0; q < ns; ++q) slots[base++] = (t << 16) | q;
   }
   if (tid == 1023) counters[2] = base;  // (the last thread's run ends at the total)

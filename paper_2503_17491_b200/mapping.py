@@ -387,7 +387,7 @@ class DeviceMap:
     def begin_replay(self, cfg: MappingConfig, raster: RasterConfig | None = None) -> None:
         """Capture (or reuse) the per-keyframe step graphs and reset the on-device step state."""
         raster = raster or RasterConfig()
-        self._prepare_graphs(cfg, raster)
+        self.capture_graphs(cfg, raster)  # every keyframe's graph now: no capture inside a timed loop
         self._t_dev.fill_(self.t)
         self._it.zero_()
         self._sticky.zero_()
