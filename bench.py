@@ -807,6 +807,34 @@ def registration_config3(dev):
                            "note": "config 3: 300k surfels on visible surfaces (device-resident map); per "
                                    "registration: 2x render + anchors, scan range image, GN/LM loop in one "
                                    "cooperative kernel; latency-bound (see DESIGN 5b)"}
+    # frame batches: B independent photometric registrations at once (register_batch: one
+    # C-ABI call, B streams, B concurrent cooperative loops with num_SMs / B blocks each)
+    bparams, bcam, bscans, btruths, binit = W.config3_frames(8)
+    bdp = engine.as_device_params(bparams)
+    bscans_dev = [torch.as_tensor(sc, device=dev) for sc in bscans]
+    for _ in range(2):
+        REG.register_batch(bdp, bscans_dev, bcam, binit, rcfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        bres = REG.register_batch(bdp, bscans_dev, bcam, binit, rcfg)
+    torch.cuda.synchronize()
+    dtb = (time.perf_counter() - t0) / reps
+    for _ in range(2):
+        REG.register(bdp, bscans[0], bcam, binit[0], rcfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for f in range(8):
+        REG.register(bdp, bscans[f], bcam, binit[f], rcfg)
+    torch.cuda.synchronize()
+    dt1 = (time.perf_counter() - t0) / 8
+    out["registration_batch8"] = {
+        "metric": "photometric registrations/s, 8 frames per register_batch call (config-3 map, 20 GN iterations)",
+        "value": 8 / dtb, "unit": "registrations/s", "ms_per_batch": dtb * 1e3, "single_frame_value": 1.0 / dt1,
+        "speedup_vs_single": dt1 * 8 / dtb,
+        "max_final_err_m": max(float(np.abs(r.pose.translation - t.translation).max()) for r, t in zip(bres, btruths)),
+        "note": "frames ray-cast at 8 true poses 0.25 m apart, initial poses perturbed by 0.2 m / 2 deg; scans "
+                "device-resident; per-frame results equal register() (tests/test_gpu_registration.py)"}
     scfg = REG.RegistrationConfig()  # the reference's default mode: sequential
     res = REG.register(dparams, scan, cam, initial, scfg)
     torch.cuda.synchronize()

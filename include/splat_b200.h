@@ -31,6 +31,7 @@
  *   ss_spawn_weights, ss_densify_mask, ss_spawn_splats, ss_prune_*
  *                            mapping.py:202-311, 412-438 map growth
  *   ss_reg_solve             registration.py:437-524 the GN/LM loop of register
+ *   ss_reg_solve_async       the same, enqueued only (batches of frames, one stream each)
  *                            (every mode) + _geo_system :231-274, se3.py:121-150
  */
 #ifndef SPLAT_B200_H
@@ -313,6 +314,47 @@ typedef struct {
  * SS_ERR_REGISTRATION when fewer than min_residuals residuals survive.
  * workspace: ss_reg_solve_workspace_bytes(n_leaves, n_geo_scan, M).  Synchronises. */
 size_t ss_reg_solve_workspace_bytes(int32_t n_leaves, int32_t n_geo_scan, int32_t M);
+
+/* Result record of one loop: final pose (row-major R | t, before the host's SVD
+ * re-orthonormalisation), sum r^2 of the last geometric / photometric systems,
+ * info = {iterations, converged, n_geo, n_photo, evaluations, status (!= 0: too few
+ * residuals, the reference's RegistrationError)}. */
+typedef struct {
+  double T[12];
+  double r2[2];
+  int32_t info[6];
+} ss_reg_out;
+
+/* ss_reg_solve without the host synchronisation, for running several independent
+ * registrations at once (frame batches, one stream each): the loop runs on `stream`
+ * with at most max_blocks cooperative blocks (0: one per SM; with B concurrent loops,
+ * num_SMs / B each, the grid barriers then span fewer blocks) and its ss_reg_out is
+ * copied to out_host (pinned host memory; valid once the stream is synchronised).
+ * Each concurrent call needs its own workspace. */
+int ss_reg_solve_async(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves,
+                       const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
+                       const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam,
+                       const double* T0_Rt, const ss_reg_solve_cfg* cfg, int32_t max_blocks,
+                       ss_reg_out* out_host, void* workspace, void* stream);
+
+/* B photometric registrations against one model, each register(mode="photometric")
+ * (registration.py:387-524, sample_model :190-213 with the [::thin] anchor subsample of
+ * :430), enqueued from C with no host work between the frames: on streams[b], the model
+ * render at geo_cam from poses0_Rt[12 b ...] (records recs[b]) and the range image of
+ * scan b (scan_pts rows scan_offsets[b] .. scan_offsets[b+1], device, ready); then every
+ * frame's anchors (waiting for its own render); then the B loops back to back, max_blocks
+ * cooperative blocks each (they run concurrently), results to out_host[b] (pinned; info[5] = 2: too few confident
+ * pixels).  Per-frame device buffers: render_buf (5 geo pixels floats), scan_range /
+ * scan_valid (cam pixels), anchors (anchor_cap x 3), anchor_ws / solve_ws (the strides:
+ * ss_anchor_workspace_bytes(geo), ss_reg_solve_workspace_bytes(0, 0, anchor_cap)).
+ * Synchronises every stream before returning. */
+int ss_register_photo_batch(int32_t B, const ss_camera* geo_cam, const ss_camera* cam, const ss_splats* splats,
+                            const ss_raster_cfg* rcfg, ss_records* const* recs, void* const* streams,
+                            const double* poses0_Rt, const double* scan_pts, const int32_t* scan_offsets,
+                            int32_t thin, double vis_opacity, double spread_gate, const ss_reg_solve_cfg* cfg,
+                            int32_t max_blocks, float* render_buf, double* scan_range, uint8_t* scan_valid,
+                            double* anchors, int32_t anchor_cap, void* anchor_ws, size_t anchor_ws_stride,
+                            void* solve_ws, size_t solve_ws_stride, ss_reg_out* out_host);
 int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
                  int32_t n_geo_scan, const double* X_w, int32_t M, const double* scan_range,
                  const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,

@@ -57,6 +57,10 @@ class SsRegCfg(ctypes.Structure):
     _fields_ = [("huber_photo", ctypes.c_double), ("trim_factor", ctypes.c_double), ("spread_gate", ctypes.c_double)]
 
 
+class SsRegOut(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_double * 12), ("r2", ctypes.c_double * 2), ("info", ctypes.c_int32 * 6)]
+
+
 SS_OK = 0
 SS_ERR_INVALID_ARGUMENT = 1
 SS_ERR_STALE_RECORDS = 2
@@ -146,6 +150,14 @@ def lib() -> ctypes.CDLL:
     L.ss_reg_solve.argtypes = [vp, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp,
                                ctypes.POINTER(SsRegSolveCfg), vp, vp, vp, vp, vp]
     L.ss_reg_solve.restype = ctypes.c_int
+    L.ss_reg_solve_async.argtypes = [vp, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.POINTER(SsCamera), vp,
+                                     ctypes.POINTER(SsRegSolveCfg), i32, vp, vp, vp]
+    L.ss_reg_solve_async.restype = ctypes.c_int
+    L.ss_register_photo_batch.argtypes = [i32, ctypes.POINTER(SsCamera), ctypes.POINTER(SsCamera),
+                                          ctypes.POINTER(SsSplats), ctypes.POINTER(SsRasterCfg), vp, vp, vp, vp, vp,
+                                          i32, d, d, ctypes.POINTER(SsRegSolveCfg), i32, vp, vp, vp, vp, i32, vp,
+                                          ctypes.c_size_t, vp, ctypes.c_size_t, vp]
+    L.ss_register_photo_batch.restype = ctypes.c_int
     for name in ("ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_render_forward", "ss_records_counts", "ss_records_export", "ss_render_backward",
                  "ss_mapping_loss", "ss_photo_system"):
         getattr(L, name).restype = ctypes.c_int
@@ -162,7 +174,8 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_records_set_deterministic", "ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats",
             "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact", "ss_adam_step_dev",
             "ss_store_loss_parts", "ss_records_sticky_overflow", "ss_records_reserve", "ss_records_generation",
-            "ss_render_backward_blend", "ss_render_finalize"]
+            "ss_render_backward_blend", "ss_render_finalize", "ss_reg_solve_async",
+            "ss_register_photo_batch"]
 
 
 def check(status: int, what: str = "") -> None:

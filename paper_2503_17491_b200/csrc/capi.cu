@@ -1,6 +1,7 @@
 // C ABI of the B200 hot path (declared in include/splat_b200.h).
 // Unity build: the kernel sources are included here so the library is one
 // translation unit without relocatable device code.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -904,14 +905,152 @@ size_t ss_reg_solve_workspace_bytes(int32_t n_leaves, int32_t n_geo_scan, int32_
   const size_t l = (size_t)(n_leaves > 0 ? n_leaves : 1);
   return g * (sizeof(GeoTmp) + 8) + m * (sizeof(PhotoTmp) + 8) + (size_t)4 * kRsPasses * kRsBins * 4 +
          (size_t)1024 * 2 * kRsAcc * 8 + 1024 * 4 + 1024 * 16 + sizeof(RegSolveState) + (kRsGridBuckets + 1) * 4 +
-         l * (sizeof(RsLeafEntry) + 4) + 1024;
+         l * (sizeof(RsLeafEntry) + 4) + 1024 + sizeof(ss_reg_out) + 32;
 }
+
+namespace {
+// Packs the final loop state into the public result record (one thread).
+__global__ void k_reg_out(const RegSolveState* __restrict__ st, ss_reg_out* __restrict__ out) {
+  for (int q = 0; q < 12; ++q) out->T[q] = st->T[q];
+  out->r2[0] = st->last_r2[0];
+  out->r2[1] = st->last_r2[1];
+  out->info[0] = st->it_total;
+  out->info[1] = st->converged;
+  out->info[2] = st->last_m[0];
+  out->info[3] = st->last_m[1];
+  out->info[4] = st->n_eval;
+  out->info[5] = st->status;
+}
+
+// Enqueues the loop on `s` with at most max_blocks blocks (0: one per SM) and the packing
+// of its result into out_dev (device memory; may be the workspace's tail).
+int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves,
+                     const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
+                     const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt,
+                     const ss_reg_solve_cfg* cfg, int32_t max_blocks, ss_reg_out* out_dev, void* workspace,
+                     cudaStream_t s);
+}  // namespace
 
 int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
                  int32_t n_geo_scan, const double* X_w, int32_t M, const double* scan_range,
                  const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,
                  double* T_out_Rt, int32_t* info6, double* r2_out2, void* workspace, void* stream) {
-  if (!cam || !T0_Rt || !cfg || !T_out_Rt || !info6 || !r2_out2 || !workspace) return SS_ERR_INVALID_ARGUMENT;
+  if (!T_out_Rt || !info6 || !r2_out2 || !workspace) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  ss_reg_out* od = (ss_reg_out*)((unsigned char*)workspace +
+                                 ss_reg_solve_workspace_bytes(n_leaves, n_geo_scan, M) - sizeof(ss_reg_out) - 16);
+  od = (ss_reg_out*)(((uintptr_t)od) & ~(uintptr_t)15);
+  int st = reg_solve_launch(leaf_centroids, leaf_normals, n_leaves, geo_scan, n_geo_scan, X_w, M, scan_range,
+                            scan_valid, cam, T0_Rt, cfg, 0, od, workspace, s);
+  if (st) return st;
+  ss_reg_out out{};
+  SS_CUDA_TRY(cudaMemcpyAsync(&out, od, sizeof(out), cudaMemcpyDeviceToHost, s));
+  SS_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int q = 0; q < 12; ++q) T_out_Rt[q] = out.T[q];
+  for (int q = 0; q < 6; ++q) info6[q] = out.info[q];
+  r2_out2[0] = out.r2[0];
+  r2_out2[1] = out.r2[1];
+  return out.info[5] ? SS_ERR_REGISTRATION : SS_OK;
+}
+
+int ss_reg_solve_async(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves,
+                       const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
+                       const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt,
+                       const ss_reg_solve_cfg* cfg, int32_t max_blocks, ss_reg_out* out_host, void* workspace,
+                       void* stream) {
+  if (!out_host || !workspace || max_blocks < 0) return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  ss_reg_out* od = (ss_reg_out*)((unsigned char*)workspace +
+                                 ss_reg_solve_workspace_bytes(n_leaves, n_geo_scan, M) - sizeof(ss_reg_out) - 16);
+  od = (ss_reg_out*)(((uintptr_t)od) & ~(uintptr_t)15);
+  int st = reg_solve_launch(leaf_centroids, leaf_normals, n_leaves, geo_scan, n_geo_scan, X_w, M, scan_range,
+                            scan_valid, cam, T0_Rt, cfg, max_blocks, od, workspace, s);
+  if (st) return st;
+  SS_CUDA_TRY(cudaMemcpyAsync(out_host, od, sizeof(ss_reg_out), cudaMemcpyDeviceToHost, s));
+  return SS_OK;
+}
+
+int ss_register_photo_batch(int32_t B, const ss_camera* geo_cam, const ss_camera* cam, const ss_splats* splats,
+                            const ss_raster_cfg* rcfg, ss_records* const* recs, void* const* streams,
+                            const double* poses0_Rt, const double* scan_pts, const int32_t* scan_offsets,
+                            int32_t thin, double vis_opacity, double spread_gate, const ss_reg_solve_cfg* cfg,
+                            int32_t max_blocks, float* render_buf, double* scan_range, uint8_t* scan_valid,
+                            double* anchors, int32_t anchor_cap, void* anchor_ws, size_t anchor_ws_stride,
+                            void* solve_ws, size_t solve_ws_stride, ss_reg_out* out_host) {
+  if (B < 0 || !geo_cam || !cam || !splats || !rcfg || !recs || !streams || !poses0_Rt || !scan_offsets || !cfg ||
+      !render_buf || !scan_range || !scan_valid || !anchors || !anchor_ws || !solve_ws || !out_host || thin < 1 ||
+      anchor_cap < 1)
+    return SS_ERR_INVALID_ARGUMENT;
+  if (cfg->mode != 0) return SS_ERR_UNSUPPORTED;  // photometric only (the other modes: the Python batch path)
+  const size_t Pg = (size_t)geo_cam->width * geo_cam->height, P = (size_t)cam->width * cam->height;
+  static const bool timing = std::getenv("SS_BATCH_TIMING") != nullptr;  // phase host timestamps (diagnostics)
+  auto now = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t0 = timing ? now() : 0.0;
+  // 1. every frame's render and scan range image, each on its own stream
+  for (int b = 0; b < B; ++b) {
+    cudaStream_t s = (cudaStream_t)streams[b];
+    float* D = render_buf + (size_t)b * 5 * Pg;
+    int st = ss_render_forward(geo_cam, poses0_Rt + 12 * b, splats, rcfg, D, D + Pg, D + 4 * Pg, recs[b], s);
+    if (st) return st;
+    const int32_t n = scan_offsets[b + 1] - scan_offsets[b];
+    st = ss_range_image(cam, scan_pts + 3 * (size_t)scan_offsets[b], n, scan_range + (size_t)b * P,
+                        scan_valid + (size_t)b * P, s);
+    if (st) return st;
+  }
+  const double t1 = timing ? now() : 0.0;
+  // 2. every frame's anchors (each waits for its own render only), all before any loop: a
+  // loop started earlier competes with the remaining renders (measured: B = 8 7.4 vs 6.0 ms)
+  std::vector<int32_t> M(B), n_model(B);
+  for (int b = 0; b < B; ++b) {
+    cudaStream_t s = (cudaStream_t)streams[b];
+    float* D = render_buf + (size_t)b * 5 * Pg;
+    int st = ss_records_check(recs[b], 1);
+    for (int attempt = 0; st == SS_ERR_CAPACITY && attempt < 3; ++attempt) {  // rare: re-render at the exact size
+      st = ss_render_forward(geo_cam, poses0_Rt + 12 * b, splats, rcfg, D, D + Pg, D + 4 * Pg, recs[b], s);
+      if (!st) st = ss_records_check(recs[b], 1);
+    }
+    if (st) return st;
+    int32_t counts[2] = {0, 0};
+    st = ss_reg_anchors(geo_cam, D, D + 4 * Pg, poses0_Rt + 12 * b, vis_opacity, spread_gate, thin,
+                        anchors + (size_t)b * anchor_cap * 3, anchor_cap, counts,
+                        (unsigned char*)anchor_ws + b * anchor_ws_stride, s);
+    if (st) return st;
+    n_model[b] = counts[0];
+    M[b] = counts[1];
+  }
+  // 3. the loops, concurrent (max_blocks each), results to the host
+  for (int b = 0; b < B; ++b) {
+    cudaStream_t s = (cudaStream_t)streams[b];
+    if (n_model[b] < cfg->min_residuals) {  // the reference's "too few confident pixels"
+      ss_reg_out bad{};
+      for (int q = 0; q < 12; ++q) bad.T[q] = poses0_Rt[12 * b + q];
+      bad.info[5] = 2;
+      out_host[b] = bad;
+      continue;
+    }
+    unsigned char* ws = (unsigned char*)solve_ws + b * solve_ws_stride;
+    ss_reg_out* od = (ss_reg_out*)(((uintptr_t)(ws + solve_ws_stride - sizeof(ss_reg_out) - 16)) & ~(uintptr_t)15);
+    int st = reg_solve_launch(nullptr, nullptr, 0, nullptr, 0, anchors + (size_t)b * anchor_cap * 3, M[b],
+                              scan_range + (size_t)b * P, scan_valid + (size_t)b * P, cam, poses0_Rt + 12 * b, cfg,
+                              max_blocks, od, ws, s);
+    if (st) return st;
+    SS_CUDA_TRY(cudaMemcpyAsync(out_host + b, od, sizeof(ss_reg_out), cudaMemcpyDeviceToHost, s));
+  }
+  const double t2 = timing ? now() : 0.0;
+  for (int b = 0; b < B; ++b) SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+  if (timing)
+    std::fprintf(stderr, "photo_batch B=%d: renders enqueued %.3f ms, anchors and loops enqueued %.3f, done %.3f\n", B,
+                 t1 - t0, t2 - t1, now() - t2);
+  return SS_OK;
+}
+
+namespace {
+int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves,
+                     const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
+                     const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt,
+                     const ss_reg_solve_cfg* cfg, int32_t max_blocks, ss_reg_out* out_dev, void* workspace,
+                     cudaStream_t s) {
+  if (!cam || !T0_Rt || !cfg || !workspace) return SS_ERR_INVALID_ARGUMENT;
   if (cfg->mode < 0 || cfg->mode > 3 || cfg->max_iters < 0 || cfg->assoc_k < 1) return SS_ERR_INVALID_ARGUMENT;
   // the association keeps register-resident k-best lists of at most 8 leaves
   if (cfg->mode != 0 && cfg->assoc_k > 8) return SS_ERR_UNSUPPORTED;
@@ -923,7 +1062,6 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   RegCam rc;
   int st = make_regcam(cam, rc);
   if (st) return st;
-  cudaStream_t s = (cudaStream_t)stream;
   // leaf grid buckets: a power of two >= 2 n_leaves in [64, kRsGridBuckets]; staged in
   // shared memory when it fits beside the kernel's static shared memory
   const int nl = need_geo ? n_leaves : 0;
@@ -937,7 +1075,7 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   int occ = 0;
   SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, dyn));
   if (occ < 1) return SS_ERR_CUDA;
-  const int G = std::min(num_sms(), 1024);
+  const int G = std::min(max_blocks > 0 ? std::min(max_blocks, num_sms()) : num_sms(), 1024);
   const int ng = need_geo ? n_geo_scan : 0, m = need_photo ? M : 0;
   if (ng > G * kRsThreads) return SS_ERR_UNSUPPORTED;  // one scan point per thread
   unsigned char* w = (unsigned char*)workspace;
@@ -988,20 +1126,11 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
                   (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&pmm, (void*)&state};
   SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, dyn, s));
-  RegSolveState out{};
-  SS_CUDA_TRY(cudaMemcpyAsync(&out, state, sizeof(out), cudaMemcpyDeviceToHost, s));
-  SS_CUDA_TRY(cudaStreamSynchronize(s));
-  for (int q = 0; q < 12; ++q) T_out_Rt[q] = out.T[q];
-  info6[0] = out.it_total;
-  info6[1] = out.converged;
-  info6[2] = out.last_m[0];
-  info6[3] = out.last_m[1];
-  info6[4] = out.n_eval;
-  info6[5] = out.status;
-  r2_out2[0] = out.last_r2[0];
-  r2_out2[1] = out.last_r2[1];
-  return out.status ? SS_ERR_REGISTRATION : SS_OK;
+  k_reg_out<<<1, 1, 0, s>>>(state, out_dev);
+  SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
 }
+}  // namespace
 
 int ss_spawn_weights(int32_t width, int32_t height, int32_t wrap, const double* range, const uint8_t* valid,
                      double* w_out, void* stream) {

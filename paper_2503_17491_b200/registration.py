@@ -24,12 +24,12 @@ import numpy as np
 import torch
 
 from . import engine
-from ._lib import SS_ERR_CAPACITY, SsRegCfg, SsRegSolveCfg, check, lib
+from ._lib import SS_ERR_CAPACITY, SsRegCfg, SsRegOut, SsRegSolveCfg, check, lib
 from .errors import RegistrationError
 from .geometry import SE3Pose, SphericalCamera, pose_rt
 from .rasterizer import RasterConfig
 
-__all__ = ["RegistrationConfig", "RegistrationResult", "register", "DeviceScan", "PhotoProblem"]
+__all__ = ["RegistrationConfig", "RegistrationResult", "register", "register_batch", "DeviceScan", "PhotoProblem"]
 
 
 @dataclass
@@ -319,3 +319,250 @@ def _solve_device(X_w: torch.Tensor, scan: DeviceScan, initial, cfg: Registratio
     if int(X_w.shape[0]) == 0:
         raise RegistrationError("too few residuals survive association")
     return solve_device(cfg, initial, scan, X_w.contiguous())
+
+
+# --- frame batches ------------------------------------------------------------------------
+
+class _BatchSlot:
+    """Per-frame resources of register_batch, reused across calls: a stream, blend
+    records, pinned scan staging, the pinned result record and the loop's workspace."""
+
+    def __init__(self):
+        self.stream = torch.cuda.Stream()
+        self.rec = engine.Records()
+        self.stage = torch.empty((1, 3), dtype=torch.float64).pin_memory()
+        self.out_pinned = torch.empty(ctypes.sizeof(SsRegOut), dtype=torch.uint8).pin_memory()
+        self.ws = torch.empty(0, dtype=torch.uint8, device=engine.require_cuda())
+
+    def scan_to_device(self, scan: np.ndarray):
+        n = scan.shape[0]
+        if self.stage.shape[0] < n:
+            self.stage = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        self.stage[:n].numpy()[...] = scan
+        return self.stage[:n].to(engine.require_cuda(), non_blocking=True)
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        if self.ws.numel() < nbytes:
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.ws.device)
+        return self.ws
+
+
+_SLOTS: list = []
+TIMELINE = None  # a list to collect per-frame (render start, loop launch, loop end) ms (diagnostics)
+
+
+def register_batch(model, scans, cam, initials, cfg: RegistrationConfig | None = None,
+                   raster: RasterConfig | None = None, rng=None) -> list:
+    """B independent registrations at once, each exactly ``register`` (registration.py:
+    387-524) on its own scan and initial pose against the same model.
+
+    Every frame gets its own CUDA stream: the B model renders and anchor extractions
+    (sample_model, :190-213) are enqueued together, then the B GN/LM loops run as
+    concurrent cooperative kernels with num_SMs / B blocks each (``ss_reg_solve_async``)
+    -- a single loop is bound by its grid barriers, not by the GPU's width (DESIGN 5b).
+    The results equal B calls of ``register`` (the geometric subsample draws take ``rng``
+    frame by frame, or a fresh default_rng(0) per frame as ``register`` does)."""
+    cfg = cfg or RegistrationConfig()
+    B = len(scans)
+    if len(initials) != B:
+        raise ValueError("one initial pose per scan")
+    if B == 0:
+        return []
+    if cfg.mode not in _MODE:
+        raise RegistrationError(f"unknown registration mode {cfg.mode!r}")
+    on_dev = all(torch.is_tensor(sc) and sc.is_cuda for sc in scans)  # device-resident scans: no upload
+    if on_dev:
+        scans = [sc.to(torch.float64).reshape(-1, 3) for sc in scans]
+    else:
+        scans = [np.asarray(sc.cpu().numpy() if torch.is_tensor(sc) else sc, dtype=float).reshape(-1, 3)
+                 for sc in scans]
+    if any(sc.shape[0] == 0 for sc in scans):
+        raise RegistrationError("empty scan")
+    if on_dev and (cfg.mode != "photometric" or TIMELINE is not None):
+        scans = [sc.cpu().numpy() for sc in scans]
+    dev = engine.require_cuda()
+    raster = raster or RasterConfig()
+    s = max(int(cfg.geo_supersample), 1)
+    geo_cam = cam if s == 1 else SphericalCamera(cam.width * s, cam.height * s, cam.az_min, cam.az_max,
+                                                 cam.el_min, cam.el_max)
+    params = engine.as_device_params(model)
+    while len(_SLOTS) < B:
+        _SLOTS.append(_BatchSlot())
+    slots = _SLOTS[:B]
+    main = torch.cuda.current_stream()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks = max(1, nsm // B)
+    if cfg.mode == "photometric" and TIMELINE is None:
+        return _photo_batch_native(params, scans, cam, geo_cam, initials, cfg, raster, s, slots, blocks)
+    # 1. every frame's model render and scan range image, each on its own stream
+    renders, dscans = [], []
+    ev = [] if TIMELINE is not None else None
+    for b, slot in enumerate(slots):
+        slot.stream.wait_stream(main)
+        with torch.cuda.stream(slot.stream):
+            if ev is not None:
+                ev.append([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+                ev[b][0].record()
+            D, _, O = engine.forward(geo_cam, pose_rt(initials[b]), params, raster, slot.rec, sync=False)
+            renders.append((D, O))
+            pts = slot.scan_to_device(scans[b])
+            ds = DeviceScan.__new__(DeviceScan)
+            ds.cam = cam
+            ds.range = torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev)
+            ds.valid = torch.empty((cam.height, cam.width), dtype=torch.uint8, device=dev)
+            c = engine.ss_camera(cam)
+            check(lib().ss_range_image(ctypes.byref(c), ctypes.c_void_p(pts.data_ptr()), int(pts.shape[0]),
+                                       ctypes.c_void_p(ds.range.data_ptr()), ctypes.c_void_p(ds.valid.data_ptr()),
+                                       ctypes.c_void_p(engine.stream_ptr())), "build_range_image")
+            dscans.append(ds)
+    # 2. per frame: anchors (waits for its own stream only), leaf tree, the loop (enqueued)
+    keep = []
+    for b, slot in enumerate(slots):
+        with torch.cuda.stream(slot.stream):
+            D, O = renders[b]
+            X, counts = _anchors(D, O, geo_cam, initials[b], cfg, 1)
+            if slot.rec.check(True) == SS_ERR_CAPACITY:  # rare: re-render with the exact capacity
+                D, _, O = engine.forward(geo_cam, pose_rt(initials[b]), params, raster, slot.rec)
+                X, counts = _anchors(D, O, geo_cam, initials[b], cfg, 1)
+            model_pts, n_model = X[: counts[1]], int(counts[0])
+            if n_model < cfg.min_residuals:
+                raise RegistrationError(f"frame {b}: model renders to too few confident pixels")
+            X_w = model_pts[:: s * s].contiguous() if s > 1 else model_pts
+            tree, geo_scan = None, None
+            if cfg.mode != "photometric":
+                geo = scans[b]
+                if geo.shape[0] > cfg.max_geo_points:
+                    r = rng or np.random.default_rng(0)
+                    geo = geo[r.choice(geo.shape[0], cfg.max_geo_points, replace=False)]
+                tree = build_leaf_tree(model_pts, initials[b].translation, cfg.leaf_size, cfg.flatness_tau)
+                geo_scan = torch.as_tensor(np.ascontiguousarray(geo), device=dev)
+            Xp = X_w if cfg.mode != "geometric" else None
+            M = int(Xp.shape[0]) if Xp is not None else 0
+            nl = int(tree.dev_centroids.shape[0]) if tree is not None else 0
+            ng = int(geo_scan.shape[0]) if geo_scan is not None else 0
+            ws = slot.workspace(int(lib().ss_reg_solve_workspace_bytes(nl, ng, M)))
+            # one scan point per thread in the geometric family: at least ng / 256 blocks
+            nblk = max(blocks, -(-ng // 256)) if ng else blocks
+            c = engine.ss_camera(cam)
+            k = _solve_cfg(cfg)
+            t0 = pose_rt(initials[b])
+            ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else 0)  # noqa: E731
+            if ev is not None:
+                ev[b][1].record()
+            check(lib().ss_reg_solve_async(ptr(tree.dev_centroids if tree is not None else None),
+                                           ptr(tree.dev_normals if tree is not None else None), nl, ptr(geo_scan), ng,
+                                           ptr(Xp), M, ctypes.c_void_p(dscans[b].range.data_ptr()),
+                                           ctypes.c_void_p(dscans[b].valid.data_ptr()), ctypes.byref(c),
+                                           t0.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k), nblk,
+                                           ctypes.c_void_p(slot.out_pinned.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                           ctypes.c_void_p(engine.stream_ptr())), "register")
+            keep.append((X, tree, geo_scan, t0))  # alive until the loops finished
+            if ev is not None:
+                ev[b][2].record()
+    # 3. collect
+    results = []
+    failed = None
+    for b, slot in enumerate(slots):
+        slot.stream.synchronize()
+        if ev is not None:
+            TIMELINE.append([ev[0][0].elapsed_time(e) for e in ev[b][:3]])
+        main.wait_stream(slot.stream)
+        out = SsRegOut.from_buffer_copy(slot.out_pinned.numpy().tobytes())
+        info = list(out.info)
+        if info[5] and failed is None:
+            failed = b
+        T = SE3Pose(np.array(out.T[:9]).reshape(3, 3), np.array(out.T[9:])).orthonormalized()
+        rms = lambda s2, m: float(np.sqrt(s2 / m)) if m else 0.0  # noqa: E731
+        res = RegistrationResult(T, bool(info[1]), int(info[0]), rms(out.r2[0], info[2]), rms(out.r2[1], info[3]),
+                                 int(info[2]), int(info[3]), cfg.mode)
+        res.n_evaluations = int(info[4])
+        results.append(res)
+    if failed is not None:
+        raise RegistrationError(f"frame {failed}: too few residuals survive association")
+    return results
+
+
+def _solve_cfg(cfg: RegistrationConfig) -> SsRegSolveCfg:
+    return SsRegSolveCfg(float(cfg.huber_photo), float(cfg.huber_geo), float(cfg.trim_factor), float(cfg.spread_gate),
+                         float(cfg.assoc_gate), float(cfg.trim_floor_photo), float(cfg.trim_floor_geo), float(cfg.tol),
+                         float(cfg.damping_init), float(cfg.damping_max), int(cfg.max_iters), int(cfg.min_residuals),
+                         int(cfg.assoc_k), _MODE[cfg.mode])
+
+
+_NATIVE: dict = {}
+
+
+def _photo_batch_native(params, scans, cam, geo_cam, initials, cfg, raster, s, slots, blocks):
+    """register_batch's photometric path: one C-ABI call enqueues every frame's render,
+    range image, anchors and loop (ss_register_photo_batch)."""
+    dev = engine.require_cuda()
+    B = len(scans)
+    Pg, P = geo_cam.width * geo_cam.height, cam.width * cam.height
+    thin = s * s
+    cap = (Pg + thin - 1) // thin
+    a_stride = (int(lib().ss_anchor_workspace_bytes(geo_cam.width, geo_cam.height)) + 255) // 256 * 256
+    s_stride = (int(lib().ss_reg_solve_workspace_bytes(0, 0, cap)) + 255) // 256 * 256
+    offs = np.zeros(B + 1, dtype=np.int32)
+    offs[1:] = np.cumsum([sc.shape[0] for sc in scans])
+    key = (B, Pg, P, cap)
+    bufs = _NATIVE.get(key)
+    if bufs is None:
+        _NATIVE.clear()
+        bufs = {"render": torch.empty(B * 5 * Pg, dtype=torch.float32, device=dev),
+                "range": torch.empty(B * P, dtype=torch.float64, device=dev),
+                "valid": torch.empty(B * P, dtype=torch.uint8, device=dev),
+                "anchors": torch.empty(B * cap * 3, dtype=torch.float64, device=dev),
+                "aws": torch.empty(B * a_stride, dtype=torch.uint8, device=dev),
+                "sws": torch.empty(B * s_stride, dtype=torch.uint8, device=dev),
+                "out": torch.empty(B * ctypes.sizeof(SsRegOut), dtype=torch.uint8).pin_memory(),
+                "pts_host": torch.empty((1, 3), dtype=torch.float64).pin_memory()}
+        _NATIVE[key] = bufs
+    n = int(offs[-1])
+    main = torch.cuda.current_stream()
+    if torch.is_tensor(scans[0]):
+        pts = torch.cat(scans).contiguous()
+    else:
+        if bufs["pts_host"].shape[0] < n:
+            bufs["pts_host"] = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        host = bufs["pts_host"][:n]
+        np.concatenate(scans, out=host.numpy())
+        pts = host.to(dev, non_blocking=True)  # on the caller's stream; the frame streams wait for it
+    for slot in slots:
+        slot.stream.wait_stream(main)
+    recs = (ctypes.c_void_p * B)(*[slot.rec.ptr.value for slot in slots])
+    streams = (ctypes.c_void_p * B)(*[slot.stream.cuda_stream for slot in slots])
+    poses = np.ascontiguousarray(np.stack([pose_rt(p) for p in initials]))
+    gc, c = engine.ss_camera(geo_cam), engine.ss_camera(cam)
+    sp, rk, k = engine.ss_splats(params), engine.ss_cfg(raster), _solve_cfg(cfg)
+    st = lib().ss_register_photo_batch(B, ctypes.byref(gc), ctypes.byref(c), ctypes.byref(sp), ctypes.byref(rk),
+                                       recs, streams, poses.ctypes.data_as(ctypes.c_void_p),
+                                       ctypes.c_void_p(pts.data_ptr()), offs.ctypes.data_as(ctypes.c_void_p), thin,
+                                       float(cfg.visibility_opacity), float(cfg.spread_gate), ctypes.byref(k), blocks,
+                                       ctypes.c_void_p(bufs["render"].data_ptr()),
+                                       ctypes.c_void_p(bufs["range"].data_ptr()),
+                                       ctypes.c_void_p(bufs["valid"].data_ptr()),
+                                       ctypes.c_void_p(bufs["anchors"].data_ptr()), cap,
+                                       ctypes.c_void_p(bufs["aws"].data_ptr()), a_stride,
+                                       ctypes.c_void_p(bufs["sws"].data_ptr()), s_stride,
+                                       ctypes.c_void_p(bufs["out"].data_ptr()))
+    check(st, "register")
+    for slot in slots:
+        main.wait_stream(slot.stream)
+    raw = bufs["out"].numpy().tobytes()
+    results, failed = [], None
+    for b in range(B):
+        out = SsRegOut.from_buffer_copy(raw[b * ctypes.sizeof(SsRegOut):(b + 1) * ctypes.sizeof(SsRegOut)])
+        info = list(out.info)
+        if info[5] and failed is None:
+            failed = (b, info[5])
+        T = SE3Pose(np.array(out.T[:9]).reshape(3, 3), np.array(out.T[9:])).orthonormalized()
+        rms = lambda s2, m: float(np.sqrt(s2 / m)) if m else 0.0  # noqa: E731
+        res = RegistrationResult(T, bool(info[1]), int(info[0]), rms(out.r2[0], info[2]), rms(out.r2[1], info[3]),
+                                 int(info[2]), int(info[3]), cfg.mode)
+        res.n_evaluations = int(info[4])
+        results.append(res)
+    if failed is not None:
+        b, code = failed
+        raise RegistrationError(f"frame {b}: " + ("model renders to too few confident pixels" if code == 2 else
+                                                  "too few residuals survive association"))
+    return results

@@ -328,3 +328,20 @@ def merge_maps(maps: list, keyframes: list):
     from .mapping import DeviceMap
     params = {k: torch.cat([m.params[k] for m in maps]) for k in PARAM_NAMES}
     return DeviceMap(params, keyframes, maps[0].scene_scale)
+
+
+def config3_frames(n_frames: int = 8, seed: int = 0, width: int = 1024, height: int = 64, step: float = 0.25):
+    """Frames for batched registration against the config-3 map: true poses along x (``step``
+    m apart), a scan ray-cast at each, initial poses perturbed by N(0, 0.2 m) / N(0, 2 deg) per
+    axis.  Returns (map params, camera, scans, truths, initials)."""
+    params, cam, _, _, _ = config3_problem(seed=seed, width=width, height=height)
+    rng = np.random.default_rng(1000 + seed)
+    scene = Scene(0)
+    scans, truths, initials = [], [], []
+    for f in range(n_frames):
+        truth = SE3Pose(so3_exp([0.0, 0.0, np.deg2rad(1.0) * rng.normal()]), np.array([step * f, 0.0, 0.0]))
+        tg = target_images(scene, cam, truth)
+        scans.append(tg["range"][tg["valid"]][:, None].astype(np.float64) * cam.pixel_directions[tg["valid"]])
+        truths.append(truth)
+        initials.append(truth.compose(SE3Pose(so3_exp(np.deg2rad(2.0) * rng.normal(size=3)), 0.2 * rng.normal(size=3))))
+    return params, cam, scans, truths, initials

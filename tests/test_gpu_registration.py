@@ -160,3 +160,23 @@ def test_device_loop_too_few_residuals(cuda):
     with pytest.raises(RegistrationError):
         REG._solve_device(X, scan, SE3Pose(G["initial_R"], G["initial_t"]),
                           REG.RegistrationConfig(mode="photometric"))
+
+
+@pytest.mark.parametrize("mode", ["photometric", "sequential"])
+def test_register_batch_equals_single_frames(cuda, mode):
+    """register_batch (B = 6 concurrent loops with num_SMs / 6 blocks each) gives every frame
+    exactly what register gives it alone: same iterations, residual counts and pose (the
+    block count changes only the order of the per-block partial sums)."""
+    from paper_2503_17491_b200 import workloads as W
+    params, cam, scans, truths, initials = W.config3_frames(6)
+    cfg = REG.RegistrationConfig(mode=mode, max_iters=20)
+    batch = REG.register_batch(params, scans, cam, initials, cfg)
+    for b in range(6):
+        one = REG.register(params, scans[b], cam, initials[b], cfg)
+        print(mode, b, "iters", batch[b].iterations, one.iterations, "err",
+              np.abs(batch[b].pose.translation - truths[b].translation).max())
+        assert batch[b].iterations == one.iterations and batch[b].converged == one.converged
+        assert batch[b].n_photo == one.n_photo and batch[b].n_geo == one.n_geo
+        assert np.abs(batch[b].pose.translation - one.pose.translation).max() <= 1e-9
+        assert np.abs(batch[b].pose.rotation - one.pose.rotation).max() <= 1e-9
+        assert np.abs(batch[b].pose.translation - truths[b].translation).max() < 0.02
