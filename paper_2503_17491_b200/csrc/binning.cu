@@ -137,14 +137,13 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
   const float Kp = kq > 1.0 ? (float)(2.0 * log(kq) * (1.0 + 1e-4) + 1e-4) : -1.0f;
   SplatRec r;
   r.r0 = make_float4((float)o, Kp, (float)nc[0], (float)nc[1]);
-  r.r1 = make_float4((float)nc[2], 0.f, 0.f, 0.f);
   rec[i] = r;
   SplatRec64 r64;
   r64.v[0] = make_double2(Ba[0], Ba[1]);
   r64.v[1] = make_double2(Ba[2], Bb[0]);
   r64.v[2] = make_double2(Bb[1], Bb[2]);
   r64.v[3] = make_double2(Bc[0], Bc[1]);
-  r64.v[4] = make_double2(Bc[2], range);
+  r64.v[4] = make_double2(Bc[2], nc[2]);
   rec64[i] = r64;
   key64[i] = (unsigned long long)__double_as_longlong(range);
 

@@ -46,7 +46,7 @@ namespace ss {
 
 constexpr int kWarpsPerBlock = 4;
 #ifndef SS_FWD_MINB
-#define SS_FWD_MINB 5
+#define SS_FWD_MINB 4  // 128 registers, 4 blocks per SM (A/B at config 1: 5 blocks 154 us, 4 blocks 134 us)
 #endif
 #ifndef SS_BWD_MINB
 #define SS_BWD_MINB 4
@@ -181,14 +181,13 @@ __device__ __forceinline__ void pixel_geo(const CamK& k, int tr, int tc, int p, 
 // Raw per-entry record copy (7 x 16 B) brought into shared memory with
 // cp.async one chunk ahead of its use.
 struct RawEntry {
-  float4 r0, r1;
+  float4 r0;
   double2 v[5];
 };
 
 __device__ __forceinline__ void prefetch_entry(RawEntry* dst, int sid, const SplatRec* __restrict__ rec,
                                                const SplatRec64* __restrict__ rec64) {
   __pipeline_memcpy_async(&dst->r0, &rec[sid].r0, 16);
-  __pipeline_memcpy_async(&dst->r1, &rec[sid].r1, 16);
 #pragma unroll
   for (int q = 0; q < 5; ++q) __pipeline_memcpy_async(&dst->v[q], &rec64[sid].v[q], 16);
 }
@@ -197,7 +196,6 @@ template <bool kCone, bool kDF = false>
 __device__ __forceinline__ void stage_entry(float* dst, int sid, const RawEntry& raw, const TileFrame& f, float xm,
                                             float ym) {
   const float4 p0 = raw.r0;
-  const float4 p1 = raw.r1;
   double B[10];
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
@@ -233,7 +231,7 @@ __device__ __forceinline__ void stage_entry(float* dst, int sid, const RawEntry&
   } else {
     d4[1] = make_float4(0.f, 0.f, p0.x, (float)det);
   }
-  d4[2] = make_float4(p0.z, p0.w, p1.x, __int_as_float(sid));
+  d4[2] = make_float4(p0.z, p0.w, (float)B[9], __int_as_float(sid));  // (B[9]: ncam.z)
   if (kDF) {
   // kt as a float pair (hi + lo); k1, k2 only ever multiply tile-small x, y
   float th[3], tl[3];
@@ -511,8 +509,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
           const unsigned long long q = cone2(c0, c1, PP[h]);
           // sign bit of q (q < 0 or -0; q = +0 only on the cone's safety margin):
           // entry i lands at bit cnt-1-i, reversed below
+#ifdef SS_NO_FUNNEL
           cw[2 * h] = (cw[2 * h] << 1) | ((unsigned)q >> 31);
           cw[2 * h + 1] = (cw[2 * h + 1] << 1) | ((unsigned)(q >> 32) >> 31);
+#else
+          // (cw << 1) | sign bit: one SHF.L.W per pixel
+          cw[2 * h] = __funnelshift_l((unsigned)q, cw[2 * h], 1);
+          cw[2 * h + 1] = __funnelshift_l((unsigned)(q >> 32), cw[2 * h + 1], 1);
+#endif
         }
       }
 #pragma unroll
@@ -653,7 +657,6 @@ __global__ void __launch_bounds__(128) k_forward_long(
         const int sid = pairs[lo + idx];
         RawEntry raw;
         raw.r0 = rec[sid].r0;
-        raw.r1 = rec[sid].r1;
 #pragma unroll
         for (int q = 0; q < 5; ++q) raw.v[q] = rec64[sid].v[q];
         stage_entry<true>(lsm + ((size_t)buf * kLongRound + e) * kStride, sid, raw, f, xm, ym);
@@ -674,8 +677,8 @@ __global__ void __launch_bounds__(128) k_forward_long(
           const float4 c0 = *reinterpret_cast<const float4*>(e);
           const float4 c1 = *reinterpret_cast<const float4*>(e + 4);
           const unsigned long long q = cone2(c0, c1, PP);
-          cw0 = (cw0 << 1) | ((unsigned)q >> 31);
-          cw1 = (cw1 << 1) | ((unsigned)(q >> 32) >> 31);
+          cw0 = __funnelshift_l((unsigned)q, cw0, 1);
+          cw1 = __funnelshift_l((unsigned)(q >> 32), cw1, 1);
         }
         if (cnt > 0) {
           cw0 = __brev(cw0) >> (32 - cnt);

@@ -467,8 +467,9 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
           rec->Tf, rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1), counters + 4, counters + 5);
       SS_CUDA_TRY(cudaEventRecord(rec->long_join, rec->side));
     }
+    static const int fwd_pad = std::getenv("SS_FWD_PADSMEM") ? std::atoi(std::getenv("SS_FWD_PADSMEM")) : 0;  // (A/B)
     if (k.T == 8)
-      k_forward<8, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      k_forward<8, false><<<blocks, kWarpsPerBlock * 32, fwd_pad, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                           rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
                                                           counters, counters + 3);

@@ -35,15 +35,15 @@ struct SplatsK {
 };
 
 // Per-splat records written by the preprocess kernel and staged per
-// (tile, splat) pair by the blend kernels:
-//   SplatRec   (float32, 32 B): r0 = (opacity, Kp, ncam.x, ncam.y), r1 = (ncam.z, 0, 0, 0)
+// (tile, splat) pair by the blend kernels (96 B per staged entry):
+//   SplatRec   (float32, 16 B): r0 = (opacity, Kp, ncam.x, ncam.y)
 //              Kp = 2 ln(opacity/alpha_cutoff) (+ tiny margin): alpha >= cutoff <=> sa^2+sb^2 <= K
-//   SplatRec64 (float64, 80 B): Ba, Bb, Bc (camera frame) and |Bc|
+//   SplatRec64 (float64, 80 B): Ba, Bb, Bc (camera frame) and ncam.z
 struct SplatRec {
-  float4 r0, r1;
+  float4 r0;
 };
 struct SplatRec64 {
-  double2 v[5];  // Ba.xy | Ba.z Bb.x | Bb.yz | Bc.xy | Bc.z range
+  double2 v[5];  // Ba.xy | Ba.z Bb.x | Bb.yz | Bc.xy | Bc.z ncam.z
 };
 
 // --- IEEE float64 helpers with contraction disabled (bit-exact binning) ---
