@@ -162,26 +162,35 @@ def _fingerprint(a) -> int:
     return int(np.add.reduce(x * w, dtype=np.int64)) if x.size else 0
 
 
-def _cache_key(model) -> tuple:
+def _identity_key(model) -> tuple:
     key = [int(getattr(model, "version", 0)), len(model)]
     for k in engine.PARAM_NAMES:
         a = getattr(model, k)
-        ptr = a.ctypes.data if isinstance(a, np.ndarray) else 0
-        key.append((id(a), ptr, _fingerprint(a)))
+        key.append((id(a), a.ctypes.data if isinstance(a, np.ndarray) else 0))
     return tuple(key)
 
 
+def _cache_key(model) -> tuple:
+    """(identity key: version, length, the arrays' identities and buffers; content fingerprints)."""
+    return _identity_key(model), tuple(_fingerprint(getattr(model, k)) for k in engine.PARAM_NAMES)
+
+
 def _device_params(model) -> dict:
-    key = _cache_key(model)
+    """float32 device copy of ``model``'s parameters, reused while the model is unchanged.
+    The content fingerprints are only computed when everything else matches (a changed
+    version or array already forces the upload)."""
+    ident = _identity_key(model)
     try:
         hit = _dev_cache.get(model)
     except TypeError:
         hit = None
-    if hit is not None and hit[0] == key:
-        return hit[1]
+    if hit is not None and hit[0][0] == ident:
+        fp = tuple(_fingerprint(getattr(model, k)) for k in engine.PARAM_NAMES)
+        if hit[0][1] == fp:
+            return hit[1]
     t = engine.splats_to_device(model)
     try:
-        _dev_cache[model] = (key, t)
+        _dev_cache[model] = (_cache_key(model), t)
     except TypeError:
         pass
     return t

@@ -81,4 +81,4 @@ def test_device_cache_key_sees_inplace_edits():
     m.logit_opacity = m.logit_opacity.copy()  # same values, new array
     assert _cache_key(m) != k2
     m.touch()
-    assert _cache_key(m)[0] == m.version
+    assert _cache_key(m)[0][0] == m.version
