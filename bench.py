@@ -745,6 +745,20 @@ def mapping_config2(dev):
     F = 92 * E + 204 * U + 300 * dm.n
     peak = fp32_peak()
     t_it = cpu_refine_iterations(dm, targets, cfg, 2)
+    fx = np.load(os.path.join(ROOT, "tests", "golden", "golden_quality.npz"))
+    q = W.quality_run(fx)
+    reduced = {"config": "reference's reduced config-2 run (tests/golden/golden_quality.npz): 512x32, "
+                         f"{int(fx['n_keyframes'])} keyframes, n_spawn {int(fx['n_spawn'])}, {int(fx['iters'])} "
+                         "refine iterations, same images and seeds on both sides",
+               "reference": {"splats": int(fx["n_built"]), "rmse_m_before": float(fx["rmse_before"][0]),
+                             "rmse_m_after": float(fx["rmse_after"][0]),
+                             "confident_rmse_m_before": float(fx["rmse_before"][1]),
+                             "confident_rmse_m_after": float(fx["rmse_after"][1]),
+                             "loss_first": float(fx["losses"][0]), "loss_last": float(fx["losses"][-1]),
+                             "refine_s_per_iteration_numpy_1core": float(fx["ref_refine_s_per_iter"])},
+               "ours": {"splats": q["splats"], "rmse_m_before": q["rmse_before"][0], "rmse_m_after": q["rmse_after"][0],
+                        "confident_rmse_m_before": q["rmse_before"][1], "confident_rmse_m_after": q["rmse_after"][1],
+                        "loss_first": q["loss_first"], "loss_last": q["loss_last"]}}
     return {"metric": "mapping frames/s (refine iterations: render+loss+backward+Adam)",
             "value": iters * 1000.0 / ms, "unit": "frames/s", "iterations": iters, "splats": dm.n,
             "timed_runs_ms": times, "map_build_ms": build_ms,
@@ -752,6 +766,7 @@ def mapping_config2(dev):
             "depth_rmse_m_before": rmse0[0], "depth_rmse_m_after": rmse1[0],
             "confident_depth_rmse_m_before": rmse0[1], "confident_depth_rmse_m_after": rmse1[1],
             "confident_fraction_after": rmse1[2],
+            "quality_vs_reference": reduced,
             "roofline": {"bound": "fp32", "units_mean_per_keyframe": {"E": E, "U": U, "TP": TP, "N": dm.n},
                          "algorithmic_flops_per_iteration": F,
                          "achieved_tflops": F / (ms / iters * 1e-3) / 1e12,

@@ -345,3 +345,48 @@ def config3_frames(n_frames: int = 8, seed: int = 0, width: int = 1024, height: 
         truths.append(truth)
         initials.append(truth.compose(SE3Pose(so3_exp(np.deg2rad(2.0) * rng.normal(size=3)), 0.2 * rng.normal(size=3))))
     return params, cam, scans, truths, initials
+
+
+def map_depth_rmse(dm, dkfs, raster=None) -> tuple:
+    """Depth RMSE of a device map over keyframes: rendered range D vs the keyframe range on
+    valid pixels, and D / O vs it where O > 0.5 (sample_model's depth); plus the fraction
+    of valid pixels that are confident."""
+    from . import engine
+    from .geometry import pose_rt
+    from .mapping import RasterConfig
+    se = cnt = se2 = cnt2 = 0.0
+    for kf in dkfs:
+        D, _, O = engine.forward(kf.camera, pose_rt(kf.pose), dm.params, raster or RasterConfig(), dm.rec)
+        v = kf.valid.bool()
+        se += float(((D.double() - kf.range64)[v] ** 2).sum())
+        cnt += int(v.sum())
+        c = v & (O > 0.5)
+        se2 += float(((D.double() / O.double().clamp_min(1e-12) - kf.range64)[c] ** 2).sum())
+        cnt2 += int(c.sum())
+    return float(np.sqrt(se / max(cnt, 1))), float(np.sqrt(se2 / max(cnt2, 1))), cnt2 / max(cnt, 1)
+
+
+def quality_run(fx) -> dict:
+    """The reduced config-2 run of tests/golden/golden_quality.npz (made by the reference:
+    LocalMap.start + add_keyframe, then refine) repeated on the device with the same
+    keyframe images, configuration and seeds: the depth RMSE the reference reached beside
+    ours.  ``fx`` is the loaded npz."""
+    from .geometry import SE3Pose, SphericalCamera
+    from .mapping import DeviceKeyframe, DeviceMap, MappingConfig
+    dkfs = []
+    for i in range(int(fx["n_keyframes"])):
+        w, h, a0, a1, e0, e1 = fx[f"kf{i}_cam"]
+        cam = SphericalCamera(int(w), int(h), float(a0), float(a1), float(e0), float(e1))
+        dkfs.append(DeviceKeyframe(cam, SE3Pose(fx[f"kf{i}_R"], fx[f"kf{i}_t"]), fx[f"kf{i}_range"],
+                                   fx[f"kf{i}_valid"], fx[f"kf{i}_normal"], fx[f"kf{i}_nvalid"], i))
+    cfg = MappingConfig(n_spawn=int(fx["n_spawn"]))
+    rng = np.random.default_rng(int(fx["build_seed"]))
+    dm = DeviceMap.start(dkfs[0], cfg, rng)
+    for kf in dkfs[1:]:
+        dm.add_keyframe(kf, cfg, rng)
+    n_built = dm.n
+    before = map_depth_rmse(dm, dkfs)
+    losses = dm.refine(cfg, int(fx["iters"]), np.random.default_rng(int(fx["refine_seed"])))
+    after = map_depth_rmse(dm, dkfs)
+    return {"splats": n_built, "rmse_before": before, "rmse_after": after,
+            "loss_first": float(losses[0]), "loss_last": float(losses[-1])}

@@ -357,3 +357,72 @@ def make_densify_case():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "densify":
     make_densify_case()
+
+
+def depth_rmse_ref(lmap, kfs):
+    """Depth RMSE of a local map over its keyframes: rendered range D against the keyframe
+    range on valid pixels, and D / O against it on pixels with O > 0.5 (sample_model's
+    depth, registration.py:190-213)."""
+    se = cnt = se2 = cnt2 = 0.0
+    for kf in kfs:
+        r, _ = rasterize_forward(kf.camera, kf.pose, lmap.model)
+        v = kf.range_image.valid
+        se += float(((r.range - kf.range_image.range)[v] ** 2).sum())
+        cnt += int(v.sum())
+        c = v & (r.opacity > 0.5)
+        se2 += float(((r.range / np.maximum(r.opacity, 1e-12) - kf.range_image.range)[c] ** 2).sum())
+        cnt2 += int(c.sum())
+    return float(np.sqrt(se / max(cnt, 1))), float(np.sqrt(se2 / max(cnt2, 1))), cnt2 / max(cnt, 1)
+
+
+def make_quality_case(iters=30):
+    """A reduced config-2 run of the reference (SURVEY 8(d) config 2 at 512x32, 4 keyframes
+    1 m apart, n_spawn 3000): LocalMap.start + add_keyframe (mapping.py:392-438), then
+    `iters` refine iterations (mapping.py:455-498); depth RMSE and losses before/after, the
+    reference-side quality number bench.py's config-2 line is reported beside."""
+    import time
+
+    from splatscan.mapping import LocalMap, MappingConfig, add_keyframe, make_keyframe, refine
+    from splatscan.synth import ScanSpec, raycast_scan, room_with_boxes
+
+    scene = room_with_boxes(n_boxes=4, seed=5)
+    spec = ScanSpec(width=512, height=32)
+    cfg = MappingConfig(n_spawn=3000)
+    rng0 = np.random.default_rng(3)
+    poses = [SE3Pose(so3_exp([0.0, 0.0, np.deg2rad(2.0) * rng0.normal()]), np.array([0.5 * i, 0.0, 0.0]))
+             for i in range(4)]
+    kfs = [make_keyframe(i, raycast_scan(scene, p, spec).cloud, p, spec.width, spec.height) for i, p in enumerate(poses)]
+    for kf in kfs:  # the device consumes float32 images
+        kf.range_image.range[...] = f32(kf.range_image.range)
+        kf.normal_image.normals[...] = f32(kf.normal_image.normals)
+    rng = np.random.default_rng(17)
+    t0 = time.perf_counter()
+    lmap = LocalMap.start(kfs[0], cfg, rng)
+    for kf in kfs[1:]:
+        add_keyframe(lmap, kf, cfg, rng)
+    t_build = time.perf_counter() - t0
+    n_built = len(lmap.model)
+    before = depth_rmse_ref(lmap, kfs)
+    t0 = time.perf_counter()
+    losses = refine(lmap, cfg, iters, np.random.default_rng(23))
+    t_refine = time.perf_counter() - t0
+    after = depth_rmse_ref(lmap, kfs)
+    out = {}
+    for i, kf in enumerate(kfs):
+        c = kf.camera
+        out[f"kf{i}_cam"] = np.array([c.width, c.height, c.az_min, c.az_max, c.el_min, c.el_max])
+        out[f"kf{i}_R"], out[f"kf{i}_t"] = kf.pose.rotation, kf.pose.translation
+        out[f"kf{i}_range"] = kf.range_image.range.astype(np.float32)
+        out[f"kf{i}_valid"] = kf.range_image.valid
+        out[f"kf{i}_normal"] = kf.normal_image.normals.astype(np.float32)
+        out[f"kf{i}_nvalid"] = kf.normal_image.valid
+    np.savez_compressed(os.path.join(OUT, "golden_quality.npz"), n_keyframes=len(kfs), n_spawn=cfg.n_spawn,
+                        build_seed=17, refine_seed=23, iters=iters, n_built=n_built, n_final=len(lmap.model),
+                        losses=np.array(losses), rmse_before=np.array(before), rmse_after=np.array(after),
+                        ref_build_s=t_build, ref_refine_s_per_iter=t_refine / iters, **out)
+    print("quality: splats", n_built, "rmse before", before, "after", after, "loss", losses[0], losses[-1],
+          "refine s/iter", t_refine / iters)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "quality":
+    make_quality_case()

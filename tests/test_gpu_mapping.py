@@ -168,3 +168,21 @@ def test_local_map_shard_replay_matches_refine(cuda):
         for k in NAMES:
             x, y = dm.params[k].cpu().numpy(), ref.params[k].cpu().numpy()
             assert np.linalg.norm(x - y) <= 2e-3 * np.linalg.norm(y), k
+
+
+@pytest.mark.gpu
+def test_reduced_run_quality_vs_reference(cuda):
+    """The reference's reduced config-2 run (tests/golden/golden_quality.npz: LocalMap.start +
+    3 add_keyframe at 512x32, then 30 refine iterations) repeated on the device with the same
+    images and seeds: same map size, and the depth RMSE before and after refinement within
+    5 % of the reference's (the runs differ by float32 rounding only, so the weighted spawn
+    draws and the refine trajectory stay close)."""
+    from paper_2503_17491_b200 import workloads as W
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_quality.npz"))
+    r = W.quality_run(fx)
+    assert abs(r["splats"] - int(fx["n_built"])) <= 0.01 * int(fx["n_built"])
+    for k in ("rmse_before", "rmse_after"):
+        ours, ref = np.array(r[k][:2]), fx[k][:2]
+        assert np.all(np.abs(ours - ref) <= 0.05 * ref), (k, ours, ref)
+    assert r["rmse_after"][0] < r["rmse_before"][0]
+    assert abs(r["loss_first"] - float(fx["losses"][0])) <= 1e-3 * float(fx["losses"][0])

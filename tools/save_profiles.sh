@@ -43,3 +43,16 @@ if [ -f gpurun_out/prof_reg.ncu-rep ]; then
     python tools/sass_regions.py gpurun_out/prof_reg.ncu-rep k_reg_solve 0.01
   } > profiles/${tag}_ncu_reg_summary.txt
 fi
+# per-launch DRAM bytes of the config-1 kernels, read by bench.py's roofline.traffic
+ncu -i gpurun_out/prof_round.ncu-rep --page raw --csv 2>/dev/null | python -c "
+import csv,json,sys
+rows=list(csv.reader(sys.stdin)); h=rows[0]; out={'source': 'ncu --set full --clock-control none, tools/prof_step.py config 1, profiles/${tag}_ncu_full_summary.txt (bytes per launch)'}
+for r in rows[2:]:
+  d=dict(zip(h,r)); sc={'Mbyte':1e6,'Kbyte':1e3,'Gbyte':1e9,'byte':1}
+  f=lambda k: float(d[k].replace(',',''))*sc[rows[1][h.index(k)]]
+  name=d['Kernel Name'].split('(')[0].replace('void ','')
+  key=name.split('<')[0]+('<8>' if name.startswith(('k_forward<','k_backward<')) else '')
+  out.setdefault(key, int(round(f('dram__bytes_read.sum')+f('dram__bytes_write.sum'))))
+json.dump(out, open('profiles/r02_traffic.json','w')); print(out)
+"
+python tools/ncu_pipes.py gpurun_out/prof_round.ncu-rep >> profiles/${tag}_ncu_full_summary.txt
