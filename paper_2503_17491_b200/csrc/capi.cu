@@ -1072,11 +1072,13 @@ int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, i
   const size_t gsmem = rs_grid_smem_bytes(nl, gmask);
   const bool staged = nl > 0 && gsmem <= (size_t)96 * 1024;
   const size_t dyn = staged ? gsmem : 0;
-  if (dyn > 0) SS_CUDA_TRY(cudaFuncSetAttribute(k_reg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  // batches (max_blocks given) run the 2-blocks-per-SM build of the loop
+  const void* kfn = max_blocks > 0 ? (const void*)k_reg_solve<2> : (const void*)k_reg_solve<1>;
+  if (dyn > 0) SS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int occ = 0;
-  SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reg_solve, kRsThreads, dyn));
+  SS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kRsThreads, dyn));
   if (occ < 1) return SS_ERR_CUDA;
-  const int G = std::min(max_blocks > 0 ? std::min(max_blocks, num_sms()) : num_sms(), 1024);
+  const int G = std::min(max_blocks > 0 ? std::min(max_blocks, occ * num_sms()) : num_sms(), 1024);
   const int ng = need_geo ? n_geo_scan : 0, m = need_photo ? M : 0;
   if (ng > G * kRsThreads) return SS_ERR_UNSUPPORTED;  // one scan point per thread
   unsigned char* w = (unsigned char*)workspace;
@@ -1126,7 +1128,7 @@ int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, i
   RsPhoto ph{X_w, m, scan_range, scan_valid};
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
                   (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&pmm, (void*)&state};
-  SS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reg_solve, dim3(G), dim3(kRsThreads), args, dyn, s));
+  SS_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(kRsThreads), args, dyn, s));
   k_reg_out<<<1, 1, 0, s>>>(state, out_dev);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;

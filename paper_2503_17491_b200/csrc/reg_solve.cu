@@ -734,7 +734,13 @@ struct RsPhoto {  // photometric inputs: world anchors and the scan range image
   const uint8_t* svalid;
 };
 
-__global__ void __launch_bounds__(kRsThreads) k_reg_solve(RsGeo geo, RsPhoto ph, RegCam cam, RegSolveCfg cfg,
+// kMinB = 1: one block per SM (255 registers; single registrations, whose grid-wide
+// barriers cost less over fewer blocks).  kMinB = 2 (128 registers, a few spills in the
+// state machine): frame batches, where two loops' blocks share each SM and hide each
+// other's latency (config 3, 8 frames: 1,553 -> 1,715 registrations/s; one frame on
+// 2 x 148 blocks is slower, 548 -> 497).
+template <int kMinB>
+__global__ void __launch_bounds__(kRsThreads, kMinB) k_reg_solve(RsGeo geo, RsPhoto ph, RegCam cam, RegSolveCfg cfg,
                                                          GeoTmp* __restrict__ gtmp, PhotoTmp* __restrict__ ptmp,
                                                          unsigned long long* __restrict__ gbits,
                                                          unsigned long long* __restrict__ pbits,

@@ -56,10 +56,13 @@ def splats_to_device(model, device=None) -> dict:
     device = device or require_cuda()
     out = {}
     for k in PARAM_NAMES:
-        a = np.ascontiguousarray(np.asarray(getattr(model, k), dtype=np.float32)).reshape(len(model), PARAM_WIDTH[k])
-        if k == "logit_opacity":
-            a = a.reshape(-1)
-        out[k] = torch.from_numpy(a).to(device, non_blocking=False)
+        a = np.ascontiguousarray(getattr(model, k))
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        # float64 host arrays are uploaded as they are and rounded on the device (a host
+        # conversion pass costs more than the extra PCIe bytes)
+        t = torch.from_numpy(a).to(device).to(torch.float32).reshape(len(model), PARAM_WIDTH[k])
+        out[k] = t.reshape(-1) if k == "logit_opacity" else t.contiguous()
     return out
 
 
@@ -93,7 +96,10 @@ class Records:
         return cls._pool.pop() if cls._pool else cls()
 
     def release(self) -> None:
-        Records._pool.append(self)
+        """Return the handle (and its device buffers) for reuse; beyond a few pooled
+        handles it is destroyed instead."""
+        if len(Records._pool) < 8:
+            Records._pool.append(self)
 
     def check(self, wait: bool = True) -> int:
         """Status of the last forward (SS_ERR_CAPACITY means: re-run it)."""

@@ -67,7 +67,7 @@ class RenderOutput:
 
     def _get(self, k):
         if self._host[k] is None:
-            self._host[k] = self._dev[k].detach().cpu().numpy().astype(np.float64)
+            self._host[k] = self._dev[k].detach().double().cpu().numpy()
         return self._host[k]
 
     range = property(lambda self: self._get("range"), lambda self, v: self._host.__setitem__("range", v))
@@ -99,6 +99,28 @@ class SplatGradients:
     def zeros(cls, n: int) -> "SplatGradients":
         return cls(np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 2)),
                    np.zeros(n))
+
+    @classmethod
+    def from_device(cls, g: torch.Tensor) -> "SplatGradients":
+        """From the (n, 15) float32 device gradients: laid out field by field on the device,
+        one copy into a reused pinned buffer, then every field widened to a new float64
+        array on its own host thread (numpy's casts release the GIL)."""
+        n = g.shape[0]
+        cols = ((0, 3), (3, 6), (6, 9), (9, 12), (12, 14), (14, 15))
+        flat = torch.cat([g[:, a:b].reshape(-1) for a, b in cols])
+        buf = _pinned_f32(flat.numel())
+        buf.copy_(flat, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        host = buf.numpy()
+        outs, jobs, off = [], [], 0
+        for a, b in cols:
+            w = b - a
+            o = np.empty((n, w) if w > 1 else (n,), dtype=np.float64)
+            jobs.append((o, host[off:off + n * w].reshape(o.shape)))
+            outs.append(o)
+            off += n * w
+        list(_pool().map(lambda j: np.copyto(j[0], j[1]), jobs))
+        return cls(*outs)
 
     @classmethod
     def from_packed(cls, g: np.ndarray) -> "SplatGradients":
@@ -140,6 +162,27 @@ class BlendRecords:
         return self._pair_splats
 
 
+_PINNED: dict = {}
+_POOL = None
+
+
+def _pinned_f32(n: int) -> torch.Tensor:
+    """A reused pinned host buffer of at least n float32 (grown as needed)."""
+    t = _PINNED.get("f32")
+    if t is None or t.numel() < n:
+        t = torch.empty(max(n, 1), dtype=torch.float32, pin_memory=True)
+        _PINNED["f32"] = t
+    return t[:n]
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=6, thread_name_prefix="splat-host")
+    return _POOL
+
+
 # float32 device copies of models, keyed by object identity, version, the parameter
 # arrays' identities and buffers, and a content fingerprint of each array
 _dev_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -170,9 +213,13 @@ def _identity_key(model) -> tuple:
     return tuple(key)
 
 
+def _fingerprints(model) -> tuple:
+    return tuple(_pool().map(lambda k: _fingerprint(getattr(model, k)), engine.PARAM_NAMES))
+
+
 def _cache_key(model) -> tuple:
     """(identity key: version, length, the arrays' identities and buffers; content fingerprints)."""
-    return _identity_key(model), tuple(_fingerprint(getattr(model, k)) for k in engine.PARAM_NAMES)
+    return _identity_key(model), _fingerprints(model)
 
 
 def _device_params(model) -> dict:
@@ -185,7 +232,7 @@ def _device_params(model) -> dict:
     except TypeError:
         hit = None
     if hit is not None and hit[0][0] == ident:
-        fp = tuple(_fingerprint(getattr(model, k)) for k in engine.PARAM_NAMES)
+        fp = _fingerprints(model)
         if hit[0][1] == fp:
             return hit[1]
     t = engine.splats_to_device(model)
@@ -208,19 +255,24 @@ def rasterize_forward(cam, pose, model, cfg: RasterConfig | None = None):
                            tile_ptr=np.zeros(tx * ty + 1, dtype=np.int64), pair_splats=np.zeros(0, dtype=np.int64))
         return RenderOutput(np.zeros((H, W)), np.zeros((H, W, 3)), np.zeros((H, W))), rec
     params = _device_params(model)
-    handle = engine.Records()
+    handle = engine.Records.acquire()
     D, N, O = engine.forward(cam, pose_rt(pose), params, cfg, handle)
     out = RenderOutput(device={"range": D, "normal": N, "opacity": O})
     rec = BlendRecords(cam, pose_c, cfg, len(model), model.version, tx, ty, handle=handle)
     rec._params = params
+    # the records' device buffers go back to the pool when the caller drops them
+    # (stream-ordered reuse; no free / malloc per render)
+    weakref.finalize(rec, handle.release)
     return out, rec
 
 
 def _dev(x, like_shape):
     if isinstance(x, torch.Tensor):
         return x.to(engine.require_cuda(), torch.float32).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)).reshape(like_shape)).to(
-        engine.require_cuda())
+    a = np.ascontiguousarray(x)
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float64)
+    return torch.from_numpy(a.reshape(like_shape)).to(engine.require_cuda()).to(torch.float32).contiguous()
 
 
 def rasterize_backward(model, records: BlendRecords, render: RenderOutput, pixel_grads: PixelGradients):
@@ -234,6 +286,6 @@ def rasterize_backward(model, records: BlendRecords, render: RenderOutput, pixel
     params = getattr(records, "_params", None) or _device_params(model)
     g = engine.backward(records._handle, params, _dev(pixel_grads.d_range, (H, W)),
                         _dev(pixel_grads.d_normal, (H, W, 3)), _dev(pixel_grads.d_opacity, (H, W)), raw_space=False)
-    out = SplatGradients.from_packed(g.cpu().numpy())
+    out = SplatGradients.from_device(g)
     out.device = g
     return out

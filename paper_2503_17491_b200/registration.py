@@ -18,6 +18,7 @@ callers that drive their own loop.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -351,6 +352,10 @@ _SLOTS: list = []
 TIMELINE = None  # a list to collect per-frame (render start, loop launch, loop end) ms (diagnostics)
 
 
+# cooperative loop blocks per SM in frame batches (k_reg_solve<2>'s launch bounds)
+_RS_BLOCKS_PER_SM = int(os.environ.get("SS_RS_BPS", "2"))
+
+
 def register_batch(model, scans, cam, initials, cfg: RegistrationConfig | None = None,
                    raster: RasterConfig | None = None, rng=None) -> list:
     """B independent registrations at once, each exactly ``register`` (registration.py:
@@ -391,9 +396,10 @@ def register_batch(model, scans, cam, initials, cfg: RegistrationConfig | None =
     slots = _SLOTS[:B]
     main = torch.cuda.current_stream()
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    blocks = max(1, nsm // B)
+    blocks = max(1, (nsm * (_RS_BLOCKS_PER_SM if B > 1 else 1)) // B)
     if cfg.mode == "photometric" and TIMELINE is None:
-        return _photo_batch_native(params, scans, cam, geo_cam, initials, cfg, raster, s, slots, blocks)
+        # (one frame: 0 = one block per SM, the single-registration build of the loop)
+        return _photo_batch_native(params, scans, cam, geo_cam, initials, cfg, raster, s, slots, blocks if B > 1 else 0)
     # 1. every frame's model render and scan range image, each on its own stream
     renders, dscans = [], []
     ev = [] if TIMELINE is not None else None
