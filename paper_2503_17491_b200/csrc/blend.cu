@@ -522,7 +522,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 #pragma unroll
       for (int j = 0; j < PPL; ++j) cw[j] = __brev(cw[j]) >> (32 - cnt);
       // phase B: every lane walks its own candidates front to back (packed: no
-      // lane idles on another pixel's candidate entry)
+      // lane idles on another pixel's candidate entry).  (Walking both pixels'
+      // candidates in one loop, two independent chains per iteration, measured
+      // 147 us against 135: the predicated second chain costs more than the ILP gains.)
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         unsigned m = live[j] ? cw[j] : 0u;

@@ -818,15 +818,14 @@ size_t ss_anchor_workspace_bytes(int32_t width, int32_t height) {
   return P * 10 + ((P + 255) / 256 + 1) * 4 + 64;
 }
 
-int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, const double* pose_Rt,
-                   double vis_opacity, double spread_gate, int32_t thin, double* X_out, int32_t cap,
-                   int32_t* counts_out, void* workspace, void* stream) {
-  if (!geo_cam || !D || !O || !pose_Rt || !X_out || !counts_out || !workspace || thin < 1)
-    return SS_ERR_INVALID_ARGUMENT;
+namespace {
+// sample_model's anchors enqueued on s; *counts_dev = the device counts {confident pixels, anchors}
+int reg_anchors_enqueue(const ss_camera* geo_cam, const float* D, const float* O, const double* pose_Rt,
+                        double vis_opacity, double spread_gate, int32_t thin, double* X_out, int32_t cap,
+                        int** counts_dev, void* workspace, cudaStream_t s) {
   RegCam rc;
   int st = make_regcam(geo_cam, rc);
   if (st) return st;
-  cudaStream_t s = (cudaStream_t)stream;
   const int P = rc.W * rc.H;
   const int nb = (P + 255) / 256;
   unsigned char* w = (unsigned char*)workspace;
@@ -843,6 +842,21 @@ int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, con
   k_excl_scan_small<<<1, 1024, 0, s>>>(nb, bsum);
   k_anchor_emit<<<nb, 256, 0, s>>>(rc.W, rc.H, rc, pk, thin, depth, keep, bsum, X_out, cap, counts);
   SS_CUDA_TRY(cudaGetLastError());
+  *counts_dev = counts;
+  return SS_OK;
+}
+}  // namespace
+
+int ss_reg_anchors(const ss_camera* geo_cam, const float* D, const float* O, const double* pose_Rt,
+                   double vis_opacity, double spread_gate, int32_t thin, double* X_out, int32_t cap,
+                   int32_t* counts_out, void* workspace, void* stream) {
+  if (!geo_cam || !D || !O || !pose_Rt || !X_out || !counts_out || !workspace || thin < 1)
+    return SS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int* counts = nullptr;
+  int st = reg_anchors_enqueue(geo_cam, D, O, pose_Rt, vis_opacity, spread_gate, thin, X_out, cap, &counts,
+                               workspace, s);
+  if (st) return st;
   SS_CUDA_TRY(cudaMemcpyAsync(counts_out, counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaStreamSynchronize(s));
   return SS_OK;
@@ -929,7 +943,7 @@ int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, i
                      const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
                      const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt,
                      const ss_reg_solve_cfg* cfg, int32_t max_blocks, ss_reg_out* out_dev, void* workspace,
-                     cudaStream_t s);
+                     cudaStream_t s, const int* dev_counts = nullptr);
 }  // namespace
 
 int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32_t n_leaves, const double* geo_scan,
@@ -985,62 +999,138 @@ int ss_register_photo_batch(int32_t B, const ss_camera* geo_cam, const ss_camera
   if (cfg->mode != 0) return SS_ERR_UNSUPPORTED;  // photometric only (the other modes: the Python batch path)
   const size_t Pg = (size_t)geo_cam->width * geo_cam->height, P = (size_t)cam->width * cam->height;
   static const bool timing = std::getenv("SS_BATCH_TIMING") != nullptr;  // phase host timestamps (diagnostics)
+  // SS_BATCH_PHASED: anchors counted on the host between the phases (A/B)
+  static const bool phased = std::getenv("SS_BATCH_PHASED") != nullptr;
   auto now = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t0 = timing ? now() : 0.0;
-  // 1. every frame's render and scan range image, each on its own stream
-  for (int b = 0; b < B; ++b) {
+  auto frame_render = [&](int b) -> int {
     cudaStream_t s = (cudaStream_t)streams[b];
     float* D = render_buf + (size_t)b * 5 * Pg;
-    int st = ss_render_forward(geo_cam, poses0_Rt + 12 * b, splats, rcfg, D, D + Pg, D + 4 * Pg, recs[b], s);
+    return ss_render_forward(geo_cam, poses0_Rt + 12 * b, splats, rcfg, D, D + Pg, D + 4 * Pg, recs[b], s);
+  };
+  auto frame_out_dev = [&](int b) {
+    unsigned char* ws = (unsigned char*)solve_ws + b * solve_ws_stride;
+    return (ss_reg_out*)(((uintptr_t)(ws + solve_ws_stride - sizeof(ss_reg_out) - 16)) & ~(uintptr_t)15);
+  };
+  // anchors and loop of frame b on its stream; with dev_counts the loop reads the anchor
+  // counts on the device (M = anchor_cap sizes its workspace only)
+  auto frame_loop = [&](int b, int32_t M, const int* dev_counts) -> int {
+    cudaStream_t s = (cudaStream_t)streams[b];
+    ss_reg_out* od = frame_out_dev(b);
+    int st = reg_solve_launch(nullptr, nullptr, 0, nullptr, 0, anchors + (size_t)b * anchor_cap * 3, M,
+                              scan_range + (size_t)b * P, scan_valid + (size_t)b * P, cam, poses0_Rt + 12 * b, cfg,
+                              max_blocks, od, (unsigned char*)solve_ws + b * solve_ws_stride, s, dev_counts);
     if (st) return st;
+    SS_CUDA_TRY(cudaMemcpyAsync(out_host + b, od, sizeof(ss_reg_out), cudaMemcpyDeviceToHost, s));
+    return (int)SS_OK;
+  };
+  auto frame_anchors = [&](int b, int** counts_dev) -> int {
+    float* D = render_buf + (size_t)b * 5 * Pg;
+    return reg_anchors_enqueue(geo_cam, D, D + 4 * Pg, poses0_Rt + 12 * b, vis_opacity, spread_gate, thin,
+                               anchors + (size_t)b * anchor_cap * 3, anchor_cap, counts_dev,
+                               (unsigned char*)anchor_ws + b * anchor_ws_stride, (cudaStream_t)streams[b]);
+  };
+  auto frame_scan = [&](int b) -> int {
     const int32_t n = scan_offsets[b + 1] - scan_offsets[b];
-    st = ss_range_image(cam, scan_pts + 3 * (size_t)scan_offsets[b], n, scan_range + (size_t)b * P,
-                        scan_valid + (size_t)b * P, s);
-    if (st) return st;
-  }
-  const double t1 = timing ? now() : 0.0;
-  // 2. every frame's anchors (each waits for its own render only), all before any loop: a
-  // loop started earlier competes with the remaining renders (measured: B = 8 7.4 vs 6.0 ms)
-  std::vector<int32_t> M(B), n_model(B);
-  for (int b = 0; b < B; ++b) {
-    cudaStream_t s = (cudaStream_t)streams[b];
-    float* D = render_buf + (size_t)b * 5 * Pg;
+    return ss_range_image(cam, scan_pts + 3 * (size_t)scan_offsets[b], n, scan_range + (size_t)b * P,
+                          scan_valid + (size_t)b * P, streams[b]);
+  };
+  // one frame start to finish with host reads (the phased schedule, and the re-run of a
+  // frame whose render outgrew its records' speculative capacity)
+  auto frame_sync = [&](int b) -> int {
     int st = ss_records_check(recs[b], 1);
     for (int attempt = 0; st == SS_ERR_CAPACITY && attempt < 3; ++attempt) {  // rare: re-render at the exact size
-      st = ss_render_forward(geo_cam, poses0_Rt + 12 * b, splats, rcfg, D, D + Pg, D + 4 * Pg, recs[b], s);
+      st = frame_render(b);
       if (!st) st = ss_records_check(recs[b], 1);
     }
     if (st) return st;
-    int32_t counts[2] = {0, 0};
-    st = ss_reg_anchors(geo_cam, D, D + 4 * Pg, poses0_Rt + 12 * b, vis_opacity, spread_gate, thin,
-                        anchors + (size_t)b * anchor_cap * 3, anchor_cap, counts,
-                        (unsigned char*)anchor_ws + b * anchor_ws_stride, s);
+    int* cd = nullptr;
+    st = frame_anchors(b, &cd);
     if (st) return st;
-    n_model[b] = counts[0];
-    M[b] = counts[1];
-  }
-  // 3. the loops, concurrent (max_blocks each), results to the host
-  for (int b = 0; b < B; ++b) {
-    cudaStream_t s = (cudaStream_t)streams[b];
-    if (n_model[b] < cfg->min_residuals) {  // the reference's "too few confident pixels"
+    int32_t counts[2] = {0, 0};
+    SS_CUDA_TRY(cudaMemcpyAsync(counts, cd, sizeof(counts), cudaMemcpyDeviceToHost, (cudaStream_t)streams[b]));
+    SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+    if (counts[0] < cfg->min_residuals) {  // the reference's "too few confident pixels"
       ss_reg_out bad{};
       for (int q = 0; q < 12; ++q) bad.T[q] = poses0_Rt[12 * b + q];
       bad.info[5] = 2;
       out_host[b] = bad;
-      continue;
+      return (int)SS_OK;
     }
-    unsigned char* ws = (unsigned char*)solve_ws + b * solve_ws_stride;
-    ss_reg_out* od = (ss_reg_out*)(((uintptr_t)(ws + solve_ws_stride - sizeof(ss_reg_out) - 16)) & ~(uintptr_t)15);
-    int st = reg_solve_launch(nullptr, nullptr, 0, nullptr, 0, anchors + (size_t)b * anchor_cap * 3, M[b],
-                              scan_range + (size_t)b * P, scan_valid + (size_t)b * P, cam, poses0_Rt + 12 * b, cfg,
-                              max_blocks, od, ws, s);
+    return frame_loop(b, counts[1], nullptr);
+  };
+  double t1 = 0.0, t2 = 0.0;
+  // 1. every frame's render and scan range image, each on its own stream
+  for (int b = 0; b < B; ++b) {
+    int st = frame_render(b);
+    if (!st) st = frame_scan(b);
     if (st) return st;
-    SS_CUDA_TRY(cudaMemcpyAsync(out_host + b, od, sizeof(ss_reg_out), cudaMemcpyDeviceToHost, s));
   }
-  const double t2 = timing ? now() : 0.0;
-  for (int b = 0; b < B; ++b) SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+  t1 = timing ? now() : 0.0;
+  if (!phased) {
+    // 2. every frame's anchors, then 3. every frame's loop, all enqueued with no host
+    // round trip: the loops read the anchor counts on the device.  (Loops are enqueued
+    // after all anchors: a loop started beside the remaining renders slows them more
+    // than it gains -- per-frame render/anchors/loop chains measured 1,201 against
+    // 1,399 registrations/s at 8 frames.)
+    std::vector<int*> cd(B, nullptr);
+    for (int b = 0; b < B; ++b) {
+      const int st = frame_anchors(b, &cd[b]);
+      if (st) return st;
+    }
+    for (int b = 0; b < B; ++b) {
+      const int st = frame_loop(b, anchor_cap, cd[b]);
+      if (st) return st;
+    }
+    t2 = timing ? now() : 0.0;
+    for (int b = 0; b < B; ++b) SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+    // a render that overflowed its speculative pair capacity skipped its blend: redo that frame
+    for (int b = 0; b < B; ++b) {
+      int st = ss_records_check(recs[b], 1);
+      if (st == SS_ERR_CAPACITY) {
+        st = frame_render(b);
+        if (!st) st = frame_sync(b);
+        if (st) return st;
+        SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+      } else if (st) {
+        return st;
+      }
+    }
+  } else {
+    // 2. every frame's anchors with a host read of its counts, then 3. the loops
+    std::vector<int32_t> M(B, -1);
+    for (int b = 0; b < B; ++b) {
+      int st = ss_records_check(recs[b], 1);
+      for (int attempt = 0; st == SS_ERR_CAPACITY && attempt < 3; ++attempt) {
+        st = frame_render(b);
+        if (!st) st = ss_records_check(recs[b], 1);
+      }
+      if (st) return st;
+      int* c = nullptr;
+      st = frame_anchors(b, &c);
+      if (st) return st;
+      int32_t counts[2] = {0, 0};
+      SS_CUDA_TRY(cudaMemcpyAsync(counts, c, sizeof(counts), cudaMemcpyDeviceToHost, (cudaStream_t)streams[b]));
+      SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+      if (counts[0] < cfg->min_residuals) {  // the reference's "too few confident pixels"
+        ss_reg_out bad{};
+        for (int q = 0; q < 12; ++q) bad.T[q] = poses0_Rt[12 * b + q];
+        bad.info[5] = 2;
+        out_host[b] = bad;
+      } else {
+        M[b] = counts[1];
+      }
+    }
+    for (int b = 0; b < B; ++b) {
+      if (M[b] < 0) continue;
+      const int st = frame_loop(b, M[b], nullptr);
+      if (st) return st;
+    }
+    t2 = timing ? now() : 0.0;
+    for (int b = 0; b < B; ++b) SS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)streams[b]));
+  }
   if (timing)
-    std::fprintf(stderr, "photo_batch B=%d: renders enqueued %.3f ms, anchors and loops enqueued %.3f, done %.3f\n", B,
+    std::fprintf(stderr, "photo_batch B=%d (%s): enqueued %.3f ms, +%.3f, done +%.3f\n", B, phased ? "phased" : "async",
                  t1 - t0, t2 - t1, now() - t2);
   return SS_OK;
 }
@@ -1050,7 +1140,7 @@ int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, i
                      const double* geo_scan, int32_t n_geo_scan, const double* X_w, int32_t M,
                      const double* scan_range, const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt,
                      const ss_reg_solve_cfg* cfg, int32_t max_blocks, ss_reg_out* out_dev, void* workspace,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int* dev_counts) {
   if (!cam || !T0_Rt || !cfg || !workspace) return SS_ERR_INVALID_ARGUMENT;
   if (cfg->mode < 0 || cfg->mode > 3 || cfg->max_iters < 0 || cfg->assoc_k < 1) return SS_ERR_INVALID_ARGUMENT;
   // the association keeps register-resident k-best lists of at most 8 leaves
@@ -1125,7 +1215,7 @@ int reg_solve_launch(const double* leaf_centroids, const double* leaf_normals, i
   k.assoc_k = cfg->assoc_k;
   k.mode = cfg->mode;
   RsGeo geo{leaf_centroids, leaf_normals, nl, geo_scan, ng, bstart, ent, inv_cs, gmask, staged ? 1 : 0};
-  RsPhoto ph{X_w, m, scan_range, scan_valid};
+  RsPhoto ph{X_w, m, scan_range, scan_valid, need_photo ? dev_counts : nullptr};
   void* args[] = {(void*)&geo, (void*)&ph, (void*)&rc, (void*)&k, (void*)&gtmp, (void*)&ptmp,
                   (void*)&gbits, (void*)&pbits, (void*)&hist, (void*)&part, (void*)&pcnt, (void*)&pmm, (void*)&state};
   SS_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(kRsThreads), args, dyn, s));

@@ -732,6 +732,11 @@ struct RsPhoto {  // photometric inputs: world anchors and the scan range image
   int M;
   const double* srange;
   const uint8_t* svalid;
+  // device counts {confident model pixels, anchors} of an anchor pass enqueued just
+  // before (frame batches, no host round trip): M is then min(counts[1], M) and a
+  // model with fewer than min_residuals confident pixels ends the loop at once with
+  // status 2, the host path's "too few confident pixels"
+  const int* counts;
 };
 
 // kMinB = 1: one block per SM (255 registers; single registrations, whose grid-wide
@@ -748,6 +753,13 @@ __global__ void __launch_bounds__(kRsThreads, kMinB) k_reg_solve(RsGeo geo, RsPh
                                                          int* __restrict__ pcnt, unsigned long long* __restrict__ pmm,
                                                          RegSolveState* st) {
   cg::grid_group grid = cg::this_grid();
+  if (ph.counts) {
+    if (ph.counts[0] < cfg.min_residuals) {  // (uniform over the grid: no block reaches a grid barrier)
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->status = 2;
+      return;
+    }
+    ph.M = min(ph.counts[1], ph.M);
+  }
   __shared__ __align__(16) unsigned sh[kRsBins];
   __shared__ double sred[kRsThreads / 32][kRsAcc];
   __shared__ double sfin[2 * kRsAcc];
