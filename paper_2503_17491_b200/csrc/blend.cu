@@ -903,7 +903,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
       // one group: each lane evaluates its own member (every pixel still sees
       // its contributions back to front) and adds it with vector atomics.
       // An entry with more lanes is evaluated alone and reduced through the
-      // shared-memory transpose.
+      // shared-memory transpose.  (Measured and dropped at config 1: a level
+      // schedule -- entry level = 1 + the highest level of earlier entries
+      // sharing a lane, non-consecutive entries may share a level -- 186 us
+      // against 175; lanes owning two horizontally adjacent pixels instead of
+      // rows r and r + 4, 207 us.)
       unsigned wl = 0u;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) wl |= word[j];
@@ -930,8 +934,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
             any &= ~(1u << i2);
             if ((l2 >> lane) & 1u) mi = i2;
           }
-#endif
         }
+#endif
         Entry x;
         load_entry<kBwdDF>(st + max(mi, 0) * kStride, x);
         float a[14];
