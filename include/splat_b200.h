@@ -128,6 +128,12 @@ int ss_records_counts(const ss_records* rec, int64_t* n_pairs, int32_t* tiles_x,
  * buffers as int64, matching BlendRecords (rasterizer.py:145-146). */
 int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_splats, void* stream);
 
+/* Per-pixel blend state of a finished forward into caller device buffers (W x H
+ * each, either may be NULL): the transmittance left after the tile list
+ * (_chunk_transmittance's carried-out value, rasterizer.py:402-414) and the
+ * 1-based list position of the last contributing entry (0: none). */
+int ss_records_pixel_state(const ss_records* rec, float* final_T, int32_t* last, void* stream);
+
 /* Work counts of a finished forward for the roofline: evaluations E =
  * sum over tiles of pixels x list length, contributions U = (pixel, splat)
  * pairs with nonzero blend weight.  Synchronises the stream. */

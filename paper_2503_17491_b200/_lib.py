@@ -89,6 +89,8 @@ def lib() -> ctypes.CDLL:
                                     ctypes.POINTER(SsRasterCfg), vp, vp, vp, vp, vp]
     L.ss_records_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.ss_records_export.argtypes = [vp, vp, vp, vp]
+    L.ss_records_pixel_state.argtypes = [vp, vp, vp, vp]
+    L.ss_records_pixel_state.restype = ctypes.c_int
     L.ss_render_backward.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, ctypes.c_int, vp]
     L.ss_render_backward_blend.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp]
     L.ss_render_backward_blend.restype = ctypes.c_int
@@ -166,7 +168,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_forward", "ss_records_counts",
-            "ss_records_export", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
+            "ss_records_export", "ss_records_pixel_state", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",

@@ -10,6 +10,7 @@
 
 #include "binning.cu"
 #include "blend.cu"
+#include "blend_seg.cu"
 #include "keyframe.cu"
 #include "densify.cu"
 #include "leaf_tree.cu"
@@ -171,6 +172,14 @@ struct ss_records {
   size_t cap_fin = 0;
   int* segorder = nullptr;
   size_t cap_segorder = 0;
+  // segment-parallel forward (few tiles): per-segment partial blends, the terminating
+  // segment of every pixel, and the slots of the recompute pass
+  float* segpart = nullptr;
+  size_t cap_segpart = 0;
+  int* term_seg = nullptr;
+  size_t cap_term_seg = 0;
+  int* seg3 = nullptr;
+  size_t cap_seg3 = 0;
   int* misc = nullptr;  // [0] status, [1] overflow, [2] n_long, [4..9] blend counters
   size_t cap_misc = 0;
   long long* totals = nullptr;
@@ -189,7 +198,7 @@ struct ss_records {
   uintptr_t buf_sig = 0;
   void note_buffers() {
     const void* bufs[] = {rec, rec64, key64, key32, rect, bsum, mat, tint, tiles, ptile, psplat, pbucket, bitmask,
-                          misc, totals, Tf, last, acc, pacc, segst, fin, segorder};
+                          misc, totals, Tf, last, acc, pacc, segst, fin, segorder, segpart, term_seg, seg3};
     uintptr_t h = 1469598103934665603ull;
     for (const void* b : bufs) h = (h ^ (uintptr_t)b) * 1099511628211ull;
     if (h != buf_sig) {
@@ -305,7 +314,8 @@ void ss_records_destroy(ss_records* r, void* stream) {
   if (r->side) cudaStreamSynchronize(r->side);
   void* bufs[] = {r->rec,    r->rec64,   r->key64, r->key32,  r->rect, r->bsum, r->mat, r->tint,
                   r->tiles,  r->ptile,   r->psplat, r->pbucket, r->bitmask, r->misc, r->totals,
-                  r->Tf,     r->last,    r->acc,     r->pacc,  r->segst, r->fin, r->segorder};
+                  r->Tf,     r->last,    r->acc,     r->pacc,  r->segst, r->fin, r->segorder,
+                  r->segpart, r->term_seg, r->seg3};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, s);
   cudaStreamSynchronize(s);
@@ -388,11 +398,19 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   rec->seg = seg;
   const int split_target = (k.T == 8 && !rec->deterministic && !seg) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
+  // segment-parallel forward (blend_seg.cu) wherever the backward walks segments
+  // (SS_SEG_FWD=0: the block-per-tile forward instead, for A/B)
+  static const bool seg_fwd_on = !std::getenv("SS_SEG_FWD") || std::atoi(std::getenv("SS_SEG_FWD")) != 0;
+  const bool seg_fwd = seg && seg_fwd_on;
   if (seg) {
     const size_t nchunk = (size_t)cap / 32 + ntiles + 1;
+    const size_t nsegs = nchunk / kSegChunks + (size_t)ntiles + 2;
     if (grow(rec->segst, rec->cap_segst, (nchunk / kSegChunks + 2) * 6 * 64, s) ||
         grow(rec->fin, rec->cap_fin, (size_t)5 * P, s) ||
         grow(rec->segorder, rec->cap_segorder, nchunk / kSegChunks + 2 * (size_t)ntiles + 2, s))
+      return SS_ERR_CUDA;
+    if (seg_fwd && (grow(rec->segpart, rec->cap_segpart, nsegs * kSegFields * 64, s) ||
+                    grow(rec->term_seg, rec->cap_term_seg, P, s) || grow(rec->seg3, rec->cap_seg3, nsegs, s)))
       return SS_ERR_CUDA;
   }
   rec->note_buffers();
@@ -402,7 +420,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   // entries when tiles are few, only the tail (>= SS_LONG_MIN_MANY) when they are many
   const bool few_tiles = num_sms() * 16 > ntiles;
   const int long_min = few_tiles ? SS_LONG_MIN : SS_LONG_MIN_MANY;
-  const int long_target = (k.T == 8 && (few_tiles || SS_LONG_MIN_MANY > 0)) ? SS_LONG_TARGET : 0;
+  const int long_target = (k.T == 8 && !seg_fwd && (few_tiles || SS_LONG_MIN_MANY > 0)) ? SS_LONG_TARGET : 0;
   int* status = rec->misc;
   int* overflow = rec->misc + 1;
   int* n_long = rec->misc + 2;
@@ -468,7 +486,20 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       SS_CUDA_TRY(cudaEventRecord(rec->long_join, rec->side));
     }
     static const int fwd_pad = std::getenv("SS_FWD_PADSMEM") ? std::atoi(std::getenv("SS_FWD_PADSMEM")) : 0;  // (A/B)
-    if (k.T == 8)
+    if (seg_fwd) {
+      // pass 1 over the (tile, segment) slots k_seg_order listed, pass 2 per tile, pass 3
+      // over the slots pass 2 listed (counters [6] / [8] tickets, [7] pass-3 slot count)
+      const int pblk = num_sms() * SS_FWD_MINB;
+      k_fwd_seg<1><<<pblk, kWarpsPerBlock * 32, 0, s>>>(
+          rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->segorder, counters + 6, counters + 2);
+      k_fwd_seg_combine<<<(ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, s>>>(
+          rec->bp, ntiles, tile_ptr, chunk_ptr, rec->segpart, out_range, out_normal, out_opacity, rec->Tf, rec->last,
+          rec->term_seg, rec->seg3, counters + 7, overflow);
+      k_fwd_seg<3><<<pblk, kWarpsPerBlock * 32, 0, s>>>(
+          rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
+          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->seg3, counters + 8, counters + 7);
+    } else if (k.T == 8)
       k_forward<8, false><<<blocks, kWarpsPerBlock * 32, fwd_pad, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                           rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
@@ -585,6 +616,19 @@ int ss_records_export(const ss_records* rec, int64_t* tile_ptr, int64_t* pair_sp
     k_widen_i32<<<(int)((rec->n_pairs + 255) / 256), 256, 0, s>>>((int)rec->n_pairs, rec->pairs,
                                                                    (long long*)pair_splats);
   SS_CUDA_TRY(cudaGetLastError());
+  return SS_OK;
+}
+
+int ss_records_pixel_state(const ss_records* rec, float* final_T, int32_t* last, void* stream) {
+  if (rec && rec->pending) {
+    int cs = ss_records_check(const_cast<ss_records*>(rec), 1);
+    if (cs) return cs;
+  }
+  if (!rec || !rec->valid) return SS_ERR_STALE_RECORDS;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t P = (size_t)rec->cam.W * rec->cam.H;
+  if (final_T) SS_CUDA_TRY(cudaMemcpyAsync(final_T, rec->Tf, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  if (last) SS_CUDA_TRY(cudaMemcpyAsync(last, rec->last, P * sizeof(int), cudaMemcpyDeviceToDevice, s));
   return SS_OK;
 }
 
