@@ -1554,8 +1554,7 @@ int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, floa
   a.lo = (float)log_scale_lo;
   a.hi = (float)log_scale_hi;
   k_adam_tick<<<1, 1, 0, s>>>(t_dev, beta1, beta2, bias_ws);
-  const long long tot = 12LL * n;
-  k_adam_dev<<<(int)((tot + 255) / 256), 256, 0, s>>>(n, a, bias_ws, grads, m, v);
+  k_adam_dev<<<(n + 255) / 256, 256, 0, s>>>(n, a, bias_ws, grads, m, v);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
@@ -1587,8 +1586,7 @@ int ss_adam_step(float* centers, float* raw_t_alpha, float* raw_t_beta, float* l
   a.b2c = (float)(1.0 - std::pow(beta2, t));
   a.lo = (float)log_scale_lo;
   a.hi = (float)log_scale_hi;
-  const long long tot = 12LL * n;
-  k_adam<<<(int)((tot + 255) / 256), 256, 0, s>>>(n, a, grads, m, v);
+  k_adam<<<(n + 255) / 256, 256, 0, s>>>(n, a, grads, m, v);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }

@@ -101,32 +101,48 @@ struct AdamK {
   float b1, b2, eps, b1c, b2c, lo, hi;
 };
 
-__global__ void k_adam(int n, AdamK a, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= 12 * n) return;
-  const int i = k / 12, c = k % 12;
-  int grp, off, w;
-  if (c < 3) {
-    grp = 0; off = c; w = 3;
-  } else if (c < 6) {
-    grp = 1; off = c - 3; w = 3;
-  } else if (c < 9) {
-    grp = 2; off = c - 6; w = 3;
-  } else if (c < 11) {
-    grp = 3; off = c - 9; w = 2;
-  } else {
-    grp = 4; off = 0; w = 1;
+// One thread per splat: its 12 gradient / moment values as three float4 rows, the
+// five parameter groups element-wise (one thread per (splat, component) measured
+// 40 us for 200 k splats: five scattered parameter arrays per warp instruction).
+__device__ __forceinline__ void adam_splat(int i, const AdamK& a, float ib1c, float ib2c,
+                                           const float* __restrict__ g, float* __restrict__ m,
+                                           float* __restrict__ v) {
+  const float4* g4 = reinterpret_cast<const float4*>(g) + 3 * (size_t)i;
+  float4* m4 = reinterpret_cast<float4*>(m) + 3 * (size_t)i;
+  float4* v4 = reinterpret_cast<float4*>(v) + 3 * (size_t)i;
+  float gg[12], mm[12], vv[12];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const float4 a4 = g4[q], b4 = m4[q], c4 = v4[q];
+    gg[4 * q] = a4.x; gg[4 * q + 1] = a4.y; gg[4 * q + 2] = a4.z; gg[4 * q + 3] = a4.w;
+    mm[4 * q] = b4.x; mm[4 * q + 1] = b4.y; mm[4 * q + 2] = b4.z; mm[4 * q + 3] = b4.w;
+    vv[4 * q] = c4.x; vv[4 * q + 1] = c4.y; vv[4 * q + 2] = c4.z; vv[4 * q + 3] = c4.w;
   }
-  const float gk = g[k];
-  const float mk = a.b1 * m[k] + (1.f - a.b1) * gk;
-  const float vk = a.b2 * v[k] + (1.f - a.b2) * gk * gk;
-  m[k] = mk;
-  v[k] = vk;
-  const float upd = a.lr[grp] * (mk / a.b1c) / (sqrtf(vk / a.b2c) + a.eps);
-  float* pp = a.p[grp] + (size_t)i * w + off;
-  float x = *pp - upd;
-  if (grp == 3) x = fminf(fmaxf(x, a.lo), a.hi);
-  *pp = x;
+  constexpr int grp_of[12] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 3, 3, 4};
+  constexpr int off_of[12] = {0, 1, 2, 0, 1, 2, 0, 1, 2, 0, 1, 0};
+  constexpr int width[5] = {3, 3, 3, 2, 1};
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const int grp = grp_of[c];
+    mm[c] = a.b1 * mm[c] + (1.f - a.b1) * gg[c];
+    vv[c] = a.b2 * vv[c] + (1.f - a.b2) * gg[c] * gg[c];
+    const float upd = a.lr[grp] * (mm[c] * ib1c) / (sqrtf(vv[c] * ib2c) + a.eps);
+    float* pp = a.p[grp] + (size_t)i * width[grp] + off_of[c];
+    float x = *pp - upd;
+    if (grp == 3) x = fminf(fmaxf(x, a.lo), a.hi);
+    *pp = x;
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    m4[q] = make_float4(mm[4 * q], mm[4 * q + 1], mm[4 * q + 2], mm[4 * q + 3]);
+    v4[q] = make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_adam(int n, AdamK a, const float* __restrict__ g, float* __restrict__ m,
+                                              float* __restrict__ v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) adam_splat(i, a, 1.f / a.b1c, 1.f / a.b2c, g, m, v);
 }
 
 // Device-resident step counter for CUDA-graph replays of the refine step:
@@ -138,35 +154,11 @@ __global__ void k_adam_tick(int* __restrict__ t_dev, double b1, double b2, float
   bias[1] = (float)(1.0 - pow(b2, (double)t));
 }
 
-__global__ void k_adam_dev(int n, AdamK a, const float* __restrict__ bias, const float* __restrict__ g,
-                           float* __restrict__ m, float* __restrict__ v) {
-  a.b1c = bias[0];
-  a.b2c = bias[1];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= 12 * n) return;
-  const int i = k / 12, c = k % 12;
-  int grp, off, w;
-  if (c < 3) {
-    grp = 0; off = c; w = 3;
-  } else if (c < 6) {
-    grp = 1; off = c - 3; w = 3;
-  } else if (c < 9) {
-    grp = 2; off = c - 6; w = 3;
-  } else if (c < 11) {
-    grp = 3; off = c - 9; w = 2;
-  } else {
-    grp = 4; off = 0; w = 1;
-  }
-  const float gk = g[k];
-  const float mk = a.b1 * m[k] + (1.f - a.b1) * gk;
-  const float vk = a.b2 * v[k] + (1.f - a.b2) * gk * gk;
-  m[k] = mk;
-  v[k] = vk;
-  const float upd = a.lr[grp] * (mk / a.b1c) / (sqrtf(vk / a.b2c) + a.eps);
-  float* pp = a.p[grp] + (size_t)i * w + off;
-  float x = *pp - upd;
-  if (grp == 3) x = fminf(fmaxf(x, a.lo), a.hi);
-  *pp = x;
+__global__ void __launch_bounds__(256) k_adam_dev(int n, AdamK a, const float* __restrict__ bias,
+                                                  const float* __restrict__ g, float* __restrict__ m,
+                                                  float* __restrict__ v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) adam_splat(i, a, 1.f / bias[0], 1.f / bias[1], g, m, v);
 }
 
 // history[it] = the 4 loss parts of this step; it += 1 (graph-replayed refine).
