@@ -522,9 +522,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 #pragma unroll
       for (int j = 0; j < PPL; ++j) cw[j] = __brev(cw[j]) >> (32 - cnt);
       // phase B: every lane walks its own candidates front to back (packed: no
-      // lane idles on another pixel's candidate entry).  (Walking both pixels'
-      // candidates in one loop, two independent chains per iteration, measured
-      // 147 us against 135: the predicated second chain costs more than the ILP gains.)
+      // lane idles on another pixel's candidate entry).  Measured and dropped:
+      // walking both pixels' candidates in one loop (two independent chains per
+      // iteration) 147 us against 135; listing the chunk's candidates of all lanes
+      // and running the exact intersections 32 at a time whoever owns them, then
+      // compositing per lane from shared memory, 218 us (the divergent list
+      // building and compositing loops cost more than the idle lanes did).
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         unsigned m = live[j] ? cw[j] : 0u;
