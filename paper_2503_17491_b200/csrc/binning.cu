@@ -165,6 +165,9 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
   g.omega = omega;
   g.dgam = dgam;
   if (!(range > 1e-9)) return 0u;  // not alive (rasterizer.py:303-305)
+  // (every row: starting at the splat's own row and extending both ways until a miss,
+  // as for the columns below, measured 56 us against 52 at config 1 -- the divergent
+  // extension loops cost more than 16 uniform row tests)
   int r_lo = -1, r_hi = -2;
   for (int rr = 0; rr < cam.ty; ++rr) {
     if (row_hit(cam, rowt, g, rr)) {
