@@ -343,3 +343,58 @@ def test_config2_long_lists_parity(cuda):
     rep = grad_report(got, plain)
     print("config2 grad parity", rep)
     assert_grads(rep)
+
+
+def test_segment_forward_with_early_cutoffs(cuda):
+    """Few tiles (512x64: 512 tiles < resident warps, so the segment-parallel forward runs)
+    with long lists of nearly opaque splats: most pixels reach the transmittance cut-off in
+    some middle segment, so every pass of the segment forward is exercised (partial blends,
+    the combine that finds the cut-off segment, the sequential re-blend of that segment).
+    Images under the 1e-4 protocol with the oracle's threshold margins, gradients under the
+    1e-3 gates, and the cut-off pixels' final transmittance below min_T as in the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_17491_b200 import engine
+    from paper_2503_17491_b200._lib import lib
+
+    cam = W.synth_camera(512, 64)
+    params = _crowded_params(20000, 0, 5)
+    params["logit_opacity"] = np.full_like(params["logit_opacity"], 3.0)  # opacity ~0.95
+    p64 = {k: np.asarray(v, np.float64) for k, v in params.items()}
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), p64, margins=True)
+    lens = np.diff(ref["tile_ptr"])
+    assert lens.max() > 4 * 128  # several 128-entry segments per list
+    model = SplatModel.from_params(params)
+    out, rec = rasterize_forward(cam, SE3Pose.identity(), model)
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"])
+    assert np.array_equal(rec.pair_splats, ref["pair_splats"])
+    rep = image_report({"range": out.range, "normal": out.normal, "opacity": out.opacity}, ref, ref["margin"])
+    print("segment-forward image parity", rep)
+    assert_images(rep)
+    P = cam.width * cam.height
+    T = torch.empty(P, dtype=torch.float32, device="cuda")
+    last = torch.empty(P, dtype=torch.int32, device="cuda")
+    assert lib().ss_records_pixel_state(rec._handle.ptr, ctypes.c_void_p(T.data_ptr()), ctypes.c_void_p(last.data_ptr()),
+                                        ctypes.c_void_p(engine.stream_ptr())) == 0
+    torch.cuda.synchronize()
+    T = T.cpu().numpy().reshape(cam.height, cam.width)
+    last = last.cpu().numpy().reshape(cam.height, cam.width)
+    cut = T < 1e-4
+    deep = (last[cut] > 128).mean() if cut.any() else 0.0
+    print("pixels past the cut-off", cut.mean(), "of which beyond the first segment", deep)
+    assert cut.mean() > 0.3 and deep > 0.05
+    rng = np.random.default_rng(4)
+    gD = rng.normal(size=(cam.height, cam.width))
+    gN = 0.1 * rng.normal(size=(cam.height, cam.width, 3))
+    gO = 0.05 * rng.normal(size=(cam.height, cam.width))
+    sg = rasterize_backward(model, rec, out, PixelGradients(gD, gN, gO))
+    got = np.concatenate([sg.d_centers, sg.d_t_alpha, sg.d_t_beta, sg.d_normal, sg.d_scales, sg.d_opacity[:, None]],
+                         axis=1)
+    plain = O.backward_lists(ct, ref["arr"], np.eye(3), ref["tile_ptr"], ref["pair_splats"], ref["range"],
+                             ref["normal"], ref["opacity"], gD, gN, gO)
+    grep = grad_report(got, plain)
+    print("segment-forward grad parity", grep)
+    assert_grads(grep)
