@@ -63,6 +63,7 @@ __device__ __forceinline__ bool row_hit(const CamK& k, const double2* __restrict
 __global__ void k_tile_intervals(CamK k, double2* __restrict__ colt, double2* __restrict__ rowt,
                                  int* __restrict__ misc16, long long* __restrict__ totals2,
                                  int* __restrict__ tile_count, int ntiles) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 16) misc16[i] = 0;
   if (i < 2) totals2[i] = 0;
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB)
                  const double2* __restrict__ rowt, SplatRec* __restrict__ rec, SplatRec64* __restrict__ rec64,
                  unsigned long long* __restrict__ key64, uint32_t* __restrict__ key32, int4* __restrict__ rect,
                  uint32_t* __restrict__ block_sum, int* __restrict__ status) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t cnt = 0;
   if (i < sp.n) cnt = preprocess_one(sp, pose, cam, rk, colt, rowt, rec, rec64, key64, key32, rect, status, i);
@@ -281,6 +283,7 @@ __device__ __forceinline__ long long block_exscan_1024(long long v, long long* w
 // Exclusive scan of the per-block pair counts (one block); totals[0] = pairs.
 __global__ void __launch_bounds__(1024) k_scan_blocks(int nb, uint32_t* __restrict__ block_sum,
                                                       long long* __restrict__ totals) {
+  pdl_wait();
   __shared__ long long wsum[32], tot;
   const int tid = threadIdx.x;
   const int per = (nb + 1023) / 1024;
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(int nb, uint32_t* __restri
 __global__ void __launch_bounds__(256)
     k_emit(int n, const int4* __restrict__ rect, const uint32_t* __restrict__ block_off, int tx, long long cap,
            uint32_t* __restrict__ pair_tile, uint32_t* __restrict__ pair_splat, int* __restrict__ overflow) {
+  pdl_wait();
   __shared__ uint32_t ws[8];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -380,6 +384,7 @@ constexpr int kMaxTiles = 16384;  // shared-memory histogram capacity
 __global__ void __launch_bounds__(1024)
     k_tile_hist_blocks(const uint32_t* __restrict__ pair_tile, const long long* __restrict__ totals, long long cap,
                        int ntiles, uint32_t* __restrict__ mat, const int* __restrict__ overflow, int chunk) {
+  pdl_wait();
   extern __shared__ uint32_t h[];
   const long long n = min(totals[0], cap);
   const long long b0 = (long long)blockIdx.x * chunk;
@@ -399,6 +404,7 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
                                                       uint32_t* __restrict__ mat, int* __restrict__ tile_count,
                                                       int chunk) {
+  pdl_wait();
   __shared__ uint32_t part[32][33];
   const int tx = threadIdx.x, seg = threadIdx.y;
   const int t = blockIdx.x * 32 + tx;
@@ -435,6 +441,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __re
                                                      int* __restrict__ tile_ptr, int* __restrict__ chunk_ptr,
                                                      long long* __restrict__ totals, int* __restrict__ long_list,
                                                      int* __restrict__ n_long) {
+  pdl_wait();
   __shared__ long long wsum[32], tot;
   const int tid = threadIdx.x;
   const int per = (ntiles + 1023) / 1024;
@@ -467,6 +474,7 @@ __global__ void __launch_bounds__(1024)
                    const long long* __restrict__ totals, long long cap, int ntiles, const uint32_t* __restrict__ mat,
                    const int* __restrict__ tile_ptr, uint32_t* __restrict__ bucketed, const int* __restrict__ overflow,
                    int chunk) {
+  pdl_wait();
   extern __shared__ uint32_t cur[];
   if (*overflow) return;
   const long long n = min(totals[0], cap);
@@ -722,6 +730,7 @@ __global__ void __launch_bounds__(NT) k_tile_sort(const int* __restrict__ tile_p
                                                    uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key32,
                                                    const unsigned long long* __restrict__ key64,
                                                    const int* __restrict__ overflow) {
+  pdl_wait();
   __shared__ __align__(16) unsigned char smem[sort_smem_bytes<kTileSortMax, NT>()];
   if (*overflow) return;
   const int t = blockIdx.x;

@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
               float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask,
               const int* __restrict__ overflow, const int* __restrict__ order, int* __restrict__ counter,
               const int* __restrict__ nslots) {
+  pdl_wait();
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;  // pair capacity exceeded: the host re-runs the render
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
@@ -787,6 +788,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
                const float* __restrict__ gD_img, const float* __restrict__ gN_img, const float* __restrict__ gO_img,
                float* __restrict__ acc, const int* __restrict__ overflow, const int* __restrict__ order,
                int* __restrict__ counter, const int* __restrict__ nslots, float* __restrict__ pacc) {
+  pdl_wait();
   constexpr int PPL = TileShape<TS>::PPL;
   if (*overflow) return;
   // deterministic mode (pacc != null): every entry is reduced by the fixed-order
@@ -1016,6 +1018,7 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
                                                         const float* __restrict__ d_scales_extra,
                                                         float* __restrict__ out, int raw_space,
                                                         int* __restrict__ bwd_ticket) {
+  pdl_wait();
   // the backward's persistent tile ticket restarts for the next backward pass
   if (blockIdx.x == 0 && threadIdx.x == 0) *bwd_ticket = 0;
   // The block's records and accumulators are staged through shared memory
@@ -1220,6 +1223,7 @@ SS_INST_BWD(16, false, false)
 
 // Deterministic mode: zero the per-position accumulators of the current pair count.
 __global__ void k_zero_pacc(float4* __restrict__ pacc, const long long* __restrict__ totals, long long cap) {
+  pdl_wait();
   const long long n = min(totals[0], cap) * (kAcc / 4);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     pacc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1233,6 +1237,7 @@ __global__ void __launch_bounds__(256) k_det_gather(int n, int tx, const int4* _
                                                     const int* __restrict__ tile_ptr, const int* __restrict__ pairs,
                                                     const float* __restrict__ pacc, float* __restrict__ acc,
                                                     const int* __restrict__ overflow) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n || *overflow) return;
   float a[14];

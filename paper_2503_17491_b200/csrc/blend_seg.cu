@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, SS_FWD_MINB)
               float* __restrict__ out_T, int* __restrict__ out_last, unsigned* __restrict__ bitmask,
               float* __restrict__ segpart, const int* __restrict__ term_seg, const int* __restrict__ overflow,
               const int* __restrict__ slots, int* __restrict__ counter, const int* __restrict__ nslots) {
+  pdl_wait();
   constexpr int TS = 8, PPL = 2;
   if (*overflow) return;
   __shared__ __align__(16) float stage[kWarpsPerBlock][32 * kStride];
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(128) k_fwd_seg_combine(BlendParams bp, int nti
                                                          float* __restrict__ out_T, int* __restrict__ out_last,
                                                          int* __restrict__ term_seg, int* __restrict__ slots3,
                                                          int* __restrict__ nslots3, const int* __restrict__ overflow) {
+  pdl_wait();
   constexpr int TS = 8, PPL = 2;
   if (*overflow) return;
   const int lane = threadIdx.x & 31;

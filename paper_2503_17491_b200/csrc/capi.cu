@@ -256,6 +256,30 @@ struct StageTimer {
 };
 enum { ST_PREPROCESS, ST_EMIT, ST_BUCKET, ST_TILE_SORT, ST_UNUSED, ST_FORWARD, ST_BACKWARD, ST_FINALIZE, ST_COUNT };
 
+// Launch with programmatic stream serialization (PDL): the kernel's blocks may be
+// scheduled while the previous kernel on the stream drains; every kernel launched
+// this way starts with pdl_wait().  `allow` = false where the kernel follows a
+// cross-stream event wait or sits between profiling events.  SS_PDL=0 disables.
+bool pdl_enabled() {
+  static const bool on = !std::getenv("SS_PDL") || std::atoi(std::getenv("SS_PDL")) != 0;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(bool allow, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (allow && pdl_enabled()) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 __global__ void k_count_contrib(long long nwords, const unsigned* __restrict__ bm, unsigned long long* out) {
   unsigned long long c = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x)
@@ -429,28 +453,29 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
 
   PoseK pk = rec->pose;
   SplatsK sk = to_k(splats);
+  const bool pa = !rec->profiling;  // (PDL launches: not between profiling events)
   {
     StageTimer tm(rec, ST_PREPROCESS, s);
     const int nti = std::max(std::max(k.tx + k.ty, ntiles), 16);
-    k_tile_intervals<<<(nti + 127) / 128, 128, 0, s>>>(k, colt, rowt, rec->misc, rec->totals, tile_count, ntiles);
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_intervals, dim3((nti + 127) / 128), dim3(128), 0, s, k, colt, rowt, rec->misc, rec->totals, tile_count, ntiles));
     if (n > 0)
-      k_preprocess<<<nb, 256, 0, s>>>(sk, pk, k, rk, colt, rowt, rec->rec, rec->rec64, rec->key64, rec->key32,
-                                      rec->rect, rec->bsum, status);
+      SS_CUDA_TRY(pdl_launch(pa, k_preprocess, dim3(nb), dim3(256), 0, s, sk, pk, k, rk, colt, rowt, rec->rec, rec->rec64, rec->key64, rec->key32,
+                                      rec->rect, rec->bsum, status));
   }
   if (n > 0) {
     StageTimer tm(rec, ST_EMIT, s);
-    k_scan_blocks<<<1, 1024, 0, s>>>(nb, rec->bsum, rec->totals);
-    k_emit<<<nb, 256, 0, s>>>(n, rec->rect, rec->bsum, k.tx, cap, rec->ptile, rec->psplat, overflow);
+    SS_CUDA_TRY(pdl_launch(pa, k_scan_blocks, dim3(1), dim3(1024), 0, s, nb, rec->bsum, rec->totals));
+    SS_CUDA_TRY(pdl_launch(pa, k_emit, dim3(nb), dim3(256), 0, s, n, rec->rect, rec->bsum, k.tx, cap, rec->ptile, rec->psplat, overflow));
   }
   {
     StageTimer tm(rec, ST_BUCKET, s);
     const size_t hsm = sizeof(uint32_t) * ntiles;
     set_smem_attrs();
-    k_tile_hist_blocks<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow, pchunk);
-    k_tile_prefix<<<(ntiles + 31) / 32, dim3(32, 32), 0, s>>>(rec->totals, cap, ntiles, rec->mat, tile_count, pchunk);
-    k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long);
-    k_tile_scatter<<<pblocks, 1024, hsm, s>>>(rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
-                                              rec->pbucket, overflow, pchunk);
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_hist_blocks, dim3(pblocks), dim3(1024), hsm, s, rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow, pchunk));
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_prefix, dim3((ntiles + 31) / 32), dim3(dim3(32, 32)), 0, s, rec->totals, cap, ntiles, rec->mat, tile_count, pchunk));
+    SS_CUDA_TRY(pdl_launch(pa, k_scan_tiles, dim3(1), dim3(1024), 0, s, ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long));
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_scatter, dim3(pblocks), dim3(1024), hsm, s, rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
+                                              rec->pbucket, overflow, pchunk));
   }
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
@@ -468,9 +493,9 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
     if (num_sms() * 16 <= ntiles)
-      k_tile_sort<128><<<ntiles, 128, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow);
+      SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<128>, dim3(ntiles), dim3(128), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
     else
-      k_tile_sort<256><<<ntiles, 256, 0, s>>>(tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow);
+      SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<256>, dim3(ntiles), dim3(256), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
     SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->sort_join, 0));
   }
   rec->pairs = (int*)rec->pbucket;
@@ -490,25 +515,25 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       // pass 1 over the (tile, segment) slots k_seg_order listed, pass 2 per tile, pass 3
       // over the slots pass 2 listed (counters [6] / [8] tickets, [7] pass-3 slot count)
       const int pblk = num_sms() * SS_FWD_MINB;
-      k_fwd_seg<1><<<pblk, kWarpsPerBlock * 32, 0, s>>>(
+      SS_CUDA_TRY(pdl_launch(false, k_fwd_seg<1>, dim3(pblk), dim3(kWarpsPerBlock * 32), 0, s, 
           rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->segorder, counters + 6, counters + 2);
-      k_fwd_seg_combine<<<(ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, s>>>(
+          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->segorder, counters + 6, counters + 2));
+      SS_CUDA_TRY(pdl_launch(pa, k_fwd_seg_combine, dim3((ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock), dim3(kWarpsPerBlock * 32), 0, s, 
           rec->bp, ntiles, tile_ptr, chunk_ptr, rec->segpart, out_range, out_normal, out_opacity, rec->Tf, rec->last,
-          rec->term_seg, rec->seg3, counters + 7, overflow);
-      k_fwd_seg<3><<<pblk, kWarpsPerBlock * 32, 0, s>>>(
+          rec->term_seg, rec->seg3, counters + 7, overflow));
+      SS_CUDA_TRY(pdl_launch(pa, k_fwd_seg<3>, dim3(pblk), dim3(kWarpsPerBlock * 32), 0, s, 
           rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
-          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->seg3, counters + 8, counters + 7);
+          rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->seg3, counters + 8, counters + 7));
     } else if (k.T == 8)
-      k_forward<8, false><<<blocks, kWarpsPerBlock * 32, fwd_pad, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      SS_CUDA_TRY(pdl_launch(false, k_forward<8, false>, dim3(blocks), dim3(kWarpsPerBlock * 32), fwd_pad, s, rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                           rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
-                                                          counters, counters + 3);
+                                                          counters, counters + 3));
     else
-      k_forward<16, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      SS_CUDA_TRY(pdl_launch(false, k_forward<16, false>, dim3(blocks), dim3(kWarpsPerBlock * 32), 0, s, rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                            rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                            rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
-                                                          counters, counters + 3);
+                                                          counters, counters + 3));
     if (long_target) SS_CUDA_TRY(cudaStreamWaitEvent(s, rec->long_join, 0));
   }
   SS_CUDA_TRY(cudaGetLastError());
@@ -653,30 +678,30 @@ static int backward_blend(ss_records* rec, const ss_splats* splats, const float*
     if (grow(rec->pacc, rec->cap_pacc, (size_t)rec->cap_pairs * kAcc, s)) return SS_ERR_CUDA;
     pacc = rec->pacc;
     rec->note_buffers();
-    k_zero_pacc<<<num_sms() * 4, 256, 0, s>>>((float4*)pacc, rec->totals, rec->cap_pairs);
+    SS_CUDA_TRY(pdl_launch(!rec->profiling, k_zero_pacc, dim3(num_sms() * 4), dim3(256), 0, s, (float4*)pacc, rec->totals, rec->cap_pairs));
   }
   const int blocks = std::min((ntiles + rec->split_target + kWarpsPerBlock - 1) / kWarpsPerBlock, num_sms() * 8);
   int* order = rec->tiles + 5 * (ntiles + 1);
   int* counters = rec->misc + 4;
+  const bool pa = !rec->profiling;
   StageTimer tm(rec, ST_BACKWARD, s);
   if (rec->cam.T == 8 && rec->seg)  // segment slots: persistent warps, as many as are resident
-    k_backward<8, false, true><<<num_sms() * SS_BWD_MINB, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
+    SS_CUDA_TRY(pdl_launch(pa, k_backward<8, false, true>, dim3(num_sms() * SS_BWD_MINB), dim3(kWarpsPerBlock * 32), kBwdDynSmem, s, 
         rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-        dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc);
+        dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc));
   else if (rec->cam.T == 8)
-    (rec->split_target ? k_backward<8, true, false> : k_backward<8, false, false>)
-        <<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
-                                                          rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
-                                                          rec->acc, rec->misc + 1, order, counters + 1, counters + 2,
-                                                          pacc);
+    SS_CUDA_TRY(pdl_launch(pa, rec->split_target ? k_backward<8, true, false> : k_backward<8, false, false>,
+                           dim3(blocks), dim3(kWarpsPerBlock * 32), kBwdDynSmem, s, rec->bp, ntiles, tile_ptr,
+                           chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD, dN, dO,
+                           rec->acc, rec->misc + 1, order, counters + 1, counters + 2, pacc));
   else
-    k_backward<16, false, false><<<blocks, kWarpsPerBlock * 32, kBwdDynSmem, s>>>(
+    SS_CUDA_TRY(pdl_launch(pa, k_backward<16, false, false>, dim3(blocks), dim3(kWarpsPerBlock * 32), kBwdDynSmem, s, 
         rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
-        dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2, pacc);
+        dN, dO, rec->acc, rec->misc + 1, order, counters + 1, counters + 2, pacc));
   SS_CUDA_TRY(cudaGetLastError());
   if (pacc)
-    k_det_gather<<<(n + 255) / 256, 256, 0, s>>>(n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
-                                                 rec->acc, rec->misc + 1);
+    SS_CUDA_TRY(pdl_launch(pa, k_det_gather, dim3((n + 255) / 256), dim3(256), 0, s, n, rec->cam.tx, rec->rect, rec->key64, tile_ptr, rec->pairs, pacc,
+                                                 rec->acc, rec->misc + 1));
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
@@ -695,10 +720,10 @@ static int backward_finalize(ss_records* rec, const ss_splats* splats, const flo
   sk.log_scales += 2 * (size_t)begin;
   sk.logit_opacity += begin;
   StageTimer tm(rec, ST_FINALIZE, s);
-  k_finalize<<<(sk.n + kFinBlock - 1) / kFinBlock, kFinBlock, 0, s>>>(
+  SS_CUDA_TRY(pdl_launch(!rec->profiling, k_finalize, dim3((sk.n + kFinBlock - 1) / kFinBlock), dim3(kFinBlock), 0, s,
       sk, rec->pose, rec->rec64 + begin, rec->acc + (size_t)begin * kAcc,
       d_scales_extra ? d_scales_extra + 2 * (size_t)begin : nullptr, grads + (size_t)begin * w, raw_space,
-      rec->misc + 5);
+      rec->misc + 5));
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
@@ -1600,8 +1625,8 @@ int ss_mapping_loss(int32_t width, int32_t height, const float* range, const flo
   int P = width * height;
   int blocks = (P + 511) / 512;  // two pixels per thread
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-  k_mapping_loss<<<blocks, 256, 0, s>>>(P, range, normal, opacity, kf_range, kf_valid, kf_normal, kf_nvalid,
-                                        w_opacity, w_normal, range_floor, dD, dN, dO, parts4);
+  SS_CUDA_TRY(pdl_launch(true, k_mapping_loss, dim3(blocks), dim3(256), 0, s, P, range, normal, opacity, kf_range,
+                         kf_valid, kf_normal, kf_nvalid, w_opacity, w_normal, range_floor, dD, dN, dO, parts4));
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }

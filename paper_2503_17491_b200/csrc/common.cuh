@@ -7,6 +7,13 @@
 
 #define SS_PI 3.14159265358979323846
 
+// Programmatic dependent launch: kernels of the render / backward / mapping step are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization, so the next
+// kernel's blocks are scheduled while the previous one drains; each of them waits
+// here, first thing, until its predecessor has completed and its writes are visible
+// (a no-op for an ordinary launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Camera constants in float64, computed on the host with the reference's
 // operation order (geometry.py:95-109, 160-174; rasterizer.py:273-276).
 struct CamK {

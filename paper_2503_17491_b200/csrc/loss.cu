@@ -11,6 +11,7 @@ __global__ void k_mapping_loss(int P, const float* __restrict__ D, const float* 
                                const uint8_t* __restrict__ kf_nvalid, double w_opacity, double w_normal,
                                double range_floor, float* __restrict__ dD, float* __restrict__ dN,
                                float* __restrict__ dO, double* __restrict__ parts) {
+  pdl_wait();
   double ld = 0.0, lo = 0.0, ln = 0.0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
     bool M = kf_valid[p] != 0;
@@ -70,6 +71,7 @@ namespace ss {
 // and the loss sum into loss[0].
 __global__ void k_scale_loss(int n, const float* __restrict__ log_scales, double cap, double w_scale,
                              float* __restrict__ d_scales, double* __restrict__ loss) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double l = 0.0;
   if (i < n) {
@@ -141,6 +143,7 @@ __device__ __forceinline__ void adam_splat(int i, const AdamK& a, float ib1c, fl
 
 __global__ void __launch_bounds__(256) k_adam(int n, AdamK a, const float* __restrict__ g, float* __restrict__ m,
                                               float* __restrict__ v) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) adam_splat(i, a, 1.f / a.b1c, 1.f / a.b2c, g, m, v);
 }
@@ -148,6 +151,7 @@ __global__ void __launch_bounds__(256) k_adam(int n, AdamK a, const float* __res
 // Device-resident step counter for CUDA-graph replays of the refine step:
 // t += 1 and the bias corrections 1 - beta^t (what the host computes for ss_adam_step).
 __global__ void k_adam_tick(int* __restrict__ t_dev, double b1, double b2, float* __restrict__ bias) {
+  pdl_wait();
   const int t = *t_dev + 1;
   *t_dev = t;
   bias[0] = (float)(1.0 - pow(b1, (double)t));
@@ -157,6 +161,7 @@ __global__ void k_adam_tick(int* __restrict__ t_dev, double b1, double b2, float
 __global__ void __launch_bounds__(256) k_adam_dev(int n, AdamK a, const float* __restrict__ bias,
                                                   const float* __restrict__ g, float* __restrict__ m,
                                                   float* __restrict__ v) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) adam_splat(i, a, 1.f / bias[0], 1.f / bias[1], g, m, v);
 }
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(256) k_adam_dev(int n, AdamK a, const float* _
 // history[it] = the 4 loss parts of this step; it += 1 (graph-replayed refine).
 __global__ void k_store_parts(const double* __restrict__ parts, double* __restrict__ hist, int* __restrict__ it,
                               int cap) {
+  pdl_wait();
   const int i = *it;
   if (i < cap)
     for (int q = 0; q < 4; ++q) hist[4 * i + q] = parts[q];
