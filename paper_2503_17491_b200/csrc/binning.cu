@@ -486,6 +486,9 @@ __global__ void __launch_bounds__(1024)
   for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) {
     const uint32_t pos = atomicAdd(&cur[pair_tile[i]], 1u);
     bucketed[pos] = pair_splat[i];
+    // (placing each pair's float32 sort key beside it here, so that k_tile_sort reads keys
+    // contiguously instead of gathering key32[id], measured 38 -> 52 us here against
+    // 53 -> 46 us in the sort: a net loss)
   }
 }
 
