@@ -66,7 +66,7 @@ __global__ void k_tile_intervals(CamK k, double2* __restrict__ colt, double2* __
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 16) misc16[i] = 0;
-  if (i < 2) totals2[i] = 0;
+  if (i < 3) totals2[i] = 0;  // pairs, chunks, longest list
   if (i < ntiles) tile_count[i] = 0;
   double c, h;
   if (i < k.tx) {
@@ -454,14 +454,19 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __re
   }
   const long long ex = block_exscan_1024(s, wsum, &tot);
   long long rp = ex >> 32, rc = ex & 0xffffffffll;
+  int cmax = 0;
   for (int t = b; t < e; ++t) {
     const int c = tile_count[t];
     tile_ptr[t] = (int)rp;
     chunk_ptr[t] = (int)rc;
     rp += c;
     rc += (c + 31) >> 5;
+    cmax = max(cmax, c);
     if (c > kTileSortMax) long_list[atomicAdd(n_long, 1)] = t;  // k_tile_sort_big, concurrently
   }
+  // the longest list (published with the totals: the next render's work layout, see capi.cu)
+  cmax = __reduce_max_sync(0xffffffffu, cmax);
+  if ((tid & 31) == 0 && cmax > 0) atomicMax(reinterpret_cast<unsigned long long*>(totals + 2), (unsigned long long)cmax);
   if (tid == 0) {
     tile_ptr[ntiles] = (int)(tot >> 32);
     chunk_ptr[ntiles] = (int)(tot & 0xffffffffll);

@@ -112,6 +112,7 @@ __global__ void k_publish_totals(const long long* __restrict__ totals, const int
   if (threadIdx.x == 0) {
     host[0] = totals[0];
     host[1] = totals[1];
+    host[3] = totals[2];  // longest tile list
     const long long sm = (long long)(unsigned)misc[0] | ((long long)(unsigned)misc[1] << 32);
     host[2] = sm;
     __threadfence_system();
@@ -206,7 +207,10 @@ struct ss_records {
       ++generation;
     }
   }
-  long long* h_totals = nullptr;  // mapped pinned: totals[2], status, overflow
+  long long* h_totals = nullptr;  // mapped pinned: pairs, chunks, status | overflow, longest list
+  // longest tile list of the last checked forward: many-tile renders with lists this long
+  // (tail lists) use the segment-parallel forward and backward
+  long long last_max_list = 0;
   long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
   cudaEvent_t fwd_end = nullptr;  // forward kernels finished (side-stream fork point)
@@ -403,7 +407,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       grow(rec->ptile, rec->cap_ptile, (size_t)cap, s) || grow(rec->psplat, rec->cap_psplat, (size_t)cap, s) ||
       grow(rec->pbucket, rec->cap_pbucket, (size_t)cap, s) ||
       grow(rec->bitmask, rec->cap_bitmask, ((size_t)cap / 32 + ntiles + 1) * TT, s) ||
-      grow(rec->misc, rec->cap_misc, 16, s) || grow(rec->totals, rec->cap_totals, 2, s) ||
+      grow(rec->misc, rec->cap_misc, 16, s) || grow(rec->totals, rec->cap_totals, 3, s) ||
       grow(rec->Tf, rec->cap_Tf, P, s) || grow(rec->last, rec->cap_last, P, s))
     return SS_ERR_CUDA;
   rec->note_buffers();
@@ -418,7 +422,13 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   // With few tiles the backward walks segments of kSegChunks chunks of each list in
   // parallel (instead of splitting tiles into pixel halves): the forward records
   // the per-pixel state at the segment boundaries.
-  const bool seg = SS_SEG_MODE && k.T == 8 && (SS_SEG_ALWAYS || num_sms() * 16 > ntiles);
+  // Segment mode: fewer tiles than resident blend warps, or (many tiles) lists long enough
+  // that the longest tiles would set the blend kernels' duration on their own (the last
+  // checked forward on these records had a list of >= SS_SEG_LIST entries; config 4a maps:
+  // lists up to ~3,700 entries, backward 311 us as whole-tile walks)
+  static const long long seg_list = std::getenv("SS_SEG_LIST") ? std::atoll(std::getenv("SS_SEG_LIST")) : SS_SEG_LIST;
+  const bool seg = SS_SEG_MODE && k.T == 8 &&
+                   (SS_SEG_ALWAYS || num_sms() * 16 > ntiles || (seg_list > 0 && rec->last_max_list >= seg_list));
   rec->seg = seg;
   const int split_target = (k.T == 8 && !rec->deterministic && !seg) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
@@ -492,7 +502,9 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     if (seg)
       k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
-    if (num_sms() * 16 <= ntiles)
+    // (segment mode with many tiles means long lists: 256-thread sorts, 117 -> 112 us on a
+    // config-4a map)
+    if (num_sms() * 16 <= ntiles && !seg)
       SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<128>, dim3(ntiles), dim3(128), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
     else
       SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<256>, dim3(ntiles), dim3(256), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
@@ -606,6 +618,7 @@ int ss_records_check(ss_records* rec, int wait) {
   const int overflow = ((int*)(rec->h_totals + 2))[1];
   rec->n_pairs = rec->h_totals[0];
   rec->n_chunks = rec->h_totals[1];
+  rec->last_max_list = rec->h_totals[3];
   if (dev_status) return dev_status;
   if (overflow || rec->n_pairs > rec->cap_pairs) {
     rec->want_pairs = rec->n_pairs + rec->n_pairs / 4 + 1024;

@@ -115,6 +115,9 @@ __device__ __forceinline__ void ray_at(const CamK& k, double u, double v, double
 #ifndef SS_SEG_ALWAYS
 #define SS_SEG_ALWAYS 0
 #endif
+#ifndef SS_SEG_LIST
+#define SS_SEG_LIST 1536  // segment mode for many tiles once the longest list reaches this (0: never)
+#endif
 // with many tiles only lists of >= SS_LONG_MIN_MANY entries take the block kernel (0: none)
 #ifndef SS_LONG_MIN_MANY
 #define SS_LONG_MIN_MANY 1536  // (config-3 registration render: forward 224 -> 181 us; config 1 unchanged)
