@@ -826,10 +826,19 @@ __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ 
 // long_target > 0: up to long_target of the longest tiles with >= long_min entries go
 // to the block-per-tile forward (k_forward_long, tickets counters[4] < counters[5]);
 // the warp-per-tile forward starts its tickets after them (counters[0] = nlong).
+__device__ void build_seg_slots(int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ order_fwd,
+                                int* __restrict__ slots, int* __restrict__ counters, int min_list);
+
+// (seg_slots != null: also the segment-mode backward slots, with lists of >= seg_min entries
+// segmented -- seg_min < 0: automatic, every list when the longest one (totals[2]) exceeds
+// twice the pairs per resident blend warp (total pairs / seg_warps), else none -- and the
+// threshold to counters[9])
 __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_ptr,
                                                      int* __restrict__ order_fwd, int* __restrict__ order,
                                                      int* __restrict__ counters, int split_target,
-                                                     int long_target, int long_min) {
+                                                     int long_target, int long_min, int* __restrict__ seg_slots,
+                                                     int seg_min, int seg_warps,
+                                                     const long long* __restrict__ totals) {
   __shared__ int hist[1024];
   const int tid = threadIdx.x;
   hist[tid] = 0;
@@ -884,6 +893,21 @@ __global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __re
   if (tid == 0) {
     counters[2] = ntiles + nsplit;
     counters[3] = ntiles;
+  }
+  if (seg_slots) {
+    int mn = seg_min;
+    if (mn < 0) {  // automatic: segments everywhere when the longest list exceeds twice a warp's fair share
+      const long long fair = totals[0] / max(seg_warps, 1);
+      mn = totals[2] > 2 * fair ? 0 : 0x7fffffff;
+    }
+    if (tid == 0) counters[9] = mn;
+    __syncthreads();  // (order_fwd complete)
+    if (mn == 0x7fffffff) {  // whole-tile slots in LPT order
+      for (int r = tid; r < ntiles; r += 1024) seg_slots[r] = ((order_fwd[r] >> 2) << 16) | 0xffff;
+      if (tid == 0) counters[2] = ntiles;
+    } else {
+      build_seg_slots(ntiles, tile_ptr, order_fwd, seg_slots, counters, mn);
+    }
   }
 }
 

@@ -65,6 +65,9 @@ struct BlendParams {
   // segment of a list independently (segst == nullptr: off).
   float* segst;  // [global chunk / kSegChunks][6][64]
   float* fin;    // [5][W * H]: final D, O, N0, N1, N2
+  // lists of >= *seg_min entries are recorded and walked in segments (the rest are
+  // whole-tile backward slots); k_tile_order sets it on the device (0: every list)
+  const int* seg_min;
 };
 
 #ifndef SS_SEG_CHUNKS
@@ -74,21 +77,22 @@ struct BlendParams {
 // halves-split tiles 240, segments of 16 chunks 189, 8 -> 135, 4 -> 121)
 constexpr int kSegChunks = SS_SEG_CHUNKS;
 
-// Backward work slots of the segment mode: every tile (longest first, the
-// forward's LPT order) contributes ceil(L / (32 kSegChunks)) slots
-// (tile << 16) | segment.  One block; counters[2] = slot count.
-__global__ void __launch_bounds__(1024) k_seg_order(int ntiles, const int* __restrict__ tile_ptr,
-                                                    const int* __restrict__ order_fwd, int* __restrict__ slots,
-                                                    int* __restrict__ counters) {
+// Backward work slots of the segment modes, built by one 1024-thread block (the end of
+// k_tile_order): tiles in the forward's LPT order; a tile whose list has >= min_list
+// entries contributes ceil(L / (32 kSegChunks)) slots (tile << 16) | segment, any other
+// tile one whole-tile slot (tile << 16) | 0xffff.  counters[2] = slot count.
+__device__ void build_seg_slots(int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ order_fwd,
+                                int* __restrict__ slots, int* __restrict__ counters, int min_list) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int per = (ntiles + 1023) / 1024, r0 = min(tid * per, ntiles), r1 = min(r0 + per, ntiles);
   constexpr int kSegEntries = 32 * kSegChunks;
+  auto nslot = [&](int t) {
+    const int L = max(0, tile_ptr[t + 1] - tile_ptr[t]);
+    return L < min_list ? (L > 0 ? 1 : 0) : (L + kSegEntries - 1) / kSegEntries;
+  };
   int cnt = 0;
-  for (int r = r0; r < r1; ++r) {
-    const int t = order_fwd[r] >> 2;
-    cnt += (max(0, tile_ptr[t + 1] - tile_ptr[t]) + kSegEntries - 1) / kSegEntries;
-  }
+  for (int r = r0; r < r1; ++r) cnt += nslot(order_fwd[r] >> 2);
   int inc = cnt;
   for (int off = 1; off < 32; off <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, inc, off);
@@ -100,7 +104,12 @@ __global__ void __launch_bounds__(1024) k_seg_order(int ntiles, const int* __res
   for (int w = 0; w < warp; ++w) base += wsum[w];
   for (int r = r0; r < r1; ++r) {
     const int t = order_fwd[r] >> 2;
-    const int ns = (max(0, tile_ptr[t + 1] - tile_ptr[t]) + kSegEntries - 1) / kSegEntries;
+    const int L = max(0, tile_ptr[t + 1] - tile_ptr[t]);
+    if (L > 0 && L < min_list) {
+      slots[base++] = (t << 16) | 0xffff;
+      continue;
+    }
+    const int ns = nslot(t);
     for (int q = 0; q < ns; ++q) slots[base++] = (t << 16) | q;
   }
   if (tid == 1023) counters[2] = base;  // (the last thread's run ends at the total)
@@ -464,6 +473,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       for (int q = 0; q < 6; ++q) PP[h][q] = pack2(px[2 * h].p[q], px[2 * h + 1].p[q]);
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     const int cbase = chunk_ptr[t];
+    const bool rec_seg = bp.segst && L >= *bp.seg_min;  // (segment backward for this tile)
     // records of chunk c+1 are copied (cp.async) while chunk c is processed
     int sid_cur = lane < L ? pairs[lo + lane] : -1;
     if (sid_cur >= 0) prefetch_entry(&raw_all[warp][0][lane], sid_cur, rec, rec64);
@@ -474,7 +484,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
 #pragma unroll
       for (int j = 0; j < PPL; ++j) any_live |= live[j];
       if (!__any_sync(0xffffffffu, any_live)) break;
-      if (TS == 8 && bp.segst && chunk > 0 && chunk % kSegChunks == 0) {
+      if (TS == 8 && rec_seg && chunk > 0 && chunk % kSegChunks == 0) {
         float* sg = seg_state(bp.segst, cbase, chunk);
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
@@ -573,7 +583,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_FWD_MINB : 1
       out_N[3 * p + 2] = N[j][2];
       out_T[p] = T[j];
       out_last[p] = last[j];
-      if (bp.fin) {
+      if (rec_seg) {
         const size_t P = (size_t)k.W * k.H;
         bp.fin[p] = D[j];
         bp.fin[P + p] = O[j];
@@ -656,6 +666,7 @@ __global__ void __launch_bounds__(128) k_forward_long(
     bool live = comp && pc.ray_ok;
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     const int cbase = chunk_ptr[t];
+    const bool rec_seg = bp.segst && L >= *bp.seg_min;
     auto stage_range = [&](int round, int buf, int e0, int stride) {
       for (int e = e0; e < kLongRound; e += stride) {
         const int idx = round * kLongRound + e;
@@ -699,7 +710,7 @@ __global__ void __launch_bounds__(128) k_forward_long(
           const int base = round * kLongRound + 32 * w;
           if (base >= L) break;
           const int gch = round * 4 + w;
-          if (bp.segst && gch > 0 && gch % kSegChunks == 0) {  // state before this segment boundary
+          if (rec_seg && gch > 0 && gch % kSegChunks == 0) {  // state before this segment boundary
             float* sg = seg_state(bp.segst, cbase, gch);
             sg[tid] = T;
             sg[64 + tid] = D;
@@ -748,7 +759,7 @@ __global__ void __launch_bounds__(128) k_forward_long(
       out_N[3 * p + 2] = N2;
       out_T[p] = T;
       out_last[p] = last;
-      if (bp.fin) {
+      if (rec_seg) {
         const size_t P = (size_t)k.W * k.H;
         bp.fin[p] = D;
         bp.fin[P + p] = O;
@@ -837,7 +848,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, TS == 8 ? SS_BWD_MINB : 1
     const int lo = tile_ptr[t];
     const int cbase = chunk_ptr[t];
     int c_lo = 0, top = (maxlast - 1) >> 5;
-    if (kSeg) {
+    if (kSeg && seg != 0xffff) {  // (0xffff: a whole-tile slot, walked from the end like kSeg = false)
       c_lo = seg * kSegChunks;
       if (c_lo > top) continue;  // no pixel reaches this segment (warp-uniform)
       const int c_hi = c_lo + kSegChunks;

@@ -167,6 +167,7 @@ struct ss_records {
   size_t cap_bitmask = 0;
   // segment-parallel backward (few tiles): recorded pixel states, finals, work slots
   bool seg = false;
+  bool hyb = false;  // many tiles: segment slots for the long lists, whole-tile slots for the rest
   float* segst = nullptr;
   size_t cap_segst = 0;
   float* fin = nullptr;
@@ -208,9 +209,7 @@ struct ss_records {
     }
   }
   long long* h_totals = nullptr;  // mapped pinned: pairs, chunks, status | overflow, longest list
-  // longest tile list of the last checked forward: many-tile renders with lists this long
-  // (tail lists) use the segment-parallel forward and backward
-  long long last_max_list = 0;
+  long long last_max_list = 0;  // longest tile list of the last checked forward (diagnostics)
   long long* d_h_totals = nullptr;  // its device alias
   cudaEvent_t done = nullptr;
   cudaEvent_t fwd_end = nullptr;  // forward kernels finished (side-stream fork point)
@@ -422,21 +421,24 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   // With few tiles the backward walks segments of kSegChunks chunks of each list in
   // parallel (instead of splitting tiles into pixel halves): the forward records
   // the per-pixel state at the segment boundaries.
-  // Segment mode: fewer tiles than resident blend warps, or (many tiles) lists long enough
-  // that the longest tiles would set the blend kernels' duration on their own (the last
-  // checked forward on these records had a list of >= SS_SEG_LIST entries; config 4a maps:
-  // lists up to ~3,700 entries, backward 311 us as whole-tile walks)
-  static const long long seg_list = std::getenv("SS_SEG_LIST") ? std::atoll(std::getenv("SS_SEG_LIST")) : SS_SEG_LIST;
-  const bool seg = SS_SEG_MODE && k.T == 8 &&
-                   (SS_SEG_ALWAYS || num_sms() * 16 > ntiles || (seg_list > 0 && rec->last_max_list >= seg_list));
+  const bool seg = SS_SEG_MODE && k.T == 8 && (SS_SEG_ALWAYS || num_sms() * 16 > ntiles);
   rec->seg = seg;
+  // Many tiles: the backward walks the tiles as whole-tile slots, or -- when the longest
+  // list exceeds twice the pairs per resident warp, so that the longest tile's walk would
+  // set the kernel's duration -- every list in segments from states the forward recorded
+  // (config-4a maps, lists up to ~3,700 entries: backward 320 -> 212 us).  Decided on the
+  // device from this render's lists (k_tile_order), so the same inputs always take the
+  // same path.  SS_HYBRID=0: the plain whole-tile backward (A/B).
+  static const bool hyb_on = !std::getenv("SS_HYBRID") || std::atoi(std::getenv("SS_HYBRID")) != 0;
+  const bool hyb = SS_SEG_MODE && k.T == 8 && !seg && hyb_on;
+  rec->hyb = hyb;
   const int split_target = (k.T == 8 && !rec->deterministic && !seg) ? std::max(0, num_sms() * 16 - ntiles) : 0;
   rec->split_target = split_target;
   // segment-parallel forward (blend_seg.cu) wherever the backward walks segments
   // (SS_SEG_FWD=0: the block-per-tile forward instead, for A/B)
   static const bool seg_fwd_on = !std::getenv("SS_SEG_FWD") || std::atoi(std::getenv("SS_SEG_FWD")) != 0;
   const bool seg_fwd = seg && seg_fwd_on;
-  if (seg) {
+  if (seg || hyb) {
     const size_t nchunk = (size_t)cap / 32 + ntiles + 1;
     const size_t nsegs = nchunk / kSegChunks + (size_t)ntiles + 2;
     if (grow(rec->segst, rec->cap_segst, (nchunk / kSegChunks + 2) * 6 * 64, s) ||
@@ -448,8 +450,9 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       return SS_ERR_CUDA;
   }
   rec->note_buffers();
-  rec->bp.segst = seg ? rec->segst : nullptr;
-  rec->bp.fin = seg ? rec->fin : nullptr;
+  rec->bp.segst = (seg || hyb) ? rec->segst : nullptr;
+  rec->bp.fin = (seg || hyb) ? rec->fin : nullptr;
+  rec->bp.seg_min = rec->misc + 4 + 9;  // (k_tile_order's threshold, counters[9])
   // ... and hand the long lists to the block-per-tile forward: every list of >= SS_LONG_MIN
   // entries when tiles are few, only the tail (>= SS_LONG_MIN_MANY) when they are many
   const bool few_tiles = num_sms() * 16 > ntiles;
@@ -498,13 +501,11 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
         tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
     k_tile_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters,
-                                            split_target, long_target, long_min);
-    if (seg)
-      k_seg_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), rec->segorder, counters);
+                                            split_target, long_target, long_min,
+                                            (seg || hyb) ? rec->segorder : nullptr, seg ? 0 : SS_SEG_MIN_LIST,
+                                            num_sms() * SS_BWD_MINB * kWarpsPerBlock, rec->totals);
     SS_CUDA_TRY(cudaEventRecord(rec->sort_join, rec->side));
-    // (segment mode with many tiles means long lists: 256-thread sorts, 117 -> 112 us on a
-    // config-4a map)
-    if (num_sms() * 16 <= ntiles && !seg)
+    if (num_sms() * 16 <= ntiles)
       SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<128>, dim3(ntiles), dim3(128), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
     else
       SS_CUDA_TRY(pdl_launch(pa, k_tile_sort<256>, dim3(ntiles), dim3(256), 0, s, tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, overflow));
@@ -698,7 +699,7 @@ static int backward_blend(ss_records* rec, const ss_splats* splats, const float*
   int* counters = rec->misc + 4;
   const bool pa = !rec->profiling;
   StageTimer tm(rec, ST_BACKWARD, s);
-  if (rec->cam.T == 8 && rec->seg)  // segment slots: persistent warps, as many as are resident
+  if (rec->cam.T == 8 && (rec->seg || rec->hyb))  // segment / whole-tile slots: persistent warps
     SS_CUDA_TRY(pdl_launch(pa, k_backward<8, false, true>, dim3(num_sms() * SS_BWD_MINB), dim3(kWarpsPerBlock * 32), kBwdDynSmem, s, 
         rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, rec->Tf, rec->last, rec->bitmask, dD,
         dN, dO, rec->acc, rec->misc + 1, rec->segorder, counters + 1, counters + 2, pacc));

@@ -115,8 +115,8 @@ __device__ __forceinline__ void ray_at(const CamK& k, double u, double v, double
 #ifndef SS_SEG_ALWAYS
 #define SS_SEG_ALWAYS 0
 #endif
-#ifndef SS_SEG_LIST
-#define SS_SEG_LIST 1536  // segment mode for many tiles once the longest list reaches this (0: never)
+#ifndef SS_SEG_MIN_LIST
+#define SS_SEG_MIN_LIST -1  // many tiles: lists this long are walked in segments (-1: a fair share, see k_tile_order)
 #endif
 // with many tiles only lists of >= SS_LONG_MIN_MANY entries take the block kernel (0: none)
 #ifndef SS_LONG_MIN_MANY
