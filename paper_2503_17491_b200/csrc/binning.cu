@@ -33,8 +33,12 @@ struct Incidence {
 #define SS_SORT_MAX 2048
 #endif
 constexpr int kTileSortMax = SS_SORT_MAX;         // entries sorted in shared memory per tile (8 warps)
-constexpr int kTileSortBig = 8192;                // long-list variant (32 warps, dynamic shared memory)
-constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys -> merge-sort fallback
+// long-list variant (32 warps, 214 KB of dynamic shared memory: one block per SM, the big
+// sort's grid anyway); 8,192 before a config-4b map's lists of up to ~12,800 entries sent
+// 252 lists per render to the global merge sort
+constexpr int kTileSortBig = 16384;
+constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys: the block's bitonic sort
+constexpr int kMaxLongRuns = 128;                 // (more of them per list: merge-sort fallback)
 
 // np.mod(x, 2*pi) for x = d + pi with d a difference of two angles in
 // [-pi, pi]: fmod is exact, so the subtraction below is bit-identical.
@@ -593,7 +597,10 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
     m.red[warp] = kmin;
     m.red[NW + warp] = kmax;
   }
-  if (tid == 0) *m.bad = 0;
+  if (tid == 0) {
+    m.bad[0] = 0;
+    m.bad[1] = 0;  // long equal-key runs listed
+  }
   __syncthreads();
   for (int w = 0; w < NW; ++w) {
     kmin = min(kmin, m.red[w]);
@@ -688,9 +695,12 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
     __syncthreads();
     cur ^= 1;
   }
-  // exact (float64, index) order inside runs of equal sort keys
+  // exact (float64, index) order inside runs of equal sort keys: short runs by one
+  // thread's insertion sort, longer ones (duplicated splats: maps merged from the same
+  // keyframes) listed and then bitonic-sorted by the whole block below
   const uint16_t* K = cur ? sk1 : sk0;
   uint32_t* V = cur ? sv1 : sv0;
+  int* runs = reinterpret_cast<int*>(m.dtot);  // (free after the digit passes) [2 * kMaxLongRuns]
   for (int i = tid; i < L; i += NT) {
     const uint16_t k = K[i];
     if (i > 0 && K[i - 1] == k) continue;
@@ -698,7 +708,13 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
     int j = i + 1;
     while (j < L && K[j] == k) ++j;
     if (j - i > kMaxTieRun) {
-      *m.bad = 1;
+      const int r = atomicAdd(m.bad + 1, 1);
+      if (r < kMaxLongRuns) {
+        runs[2 * r] = i;
+        runs[2 * r + 1] = j;
+      } else {
+        *m.bad = 1;
+      }
       continue;
     }
     for (int x = i + 1; x < j; ++x) {
@@ -715,6 +731,54 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
     }
   }
   __syncthreads();
+  // long runs: a block bitonic sort by (float64 range bits, id), the bits as two 32-bit
+  // halves in buffers the digit passes no longer use, the ids in place; the "flip" form
+  // of the network keeps every minimum at the lower index, so the power-of-two padding
+  // can stay virtual (+inf, never compared)
+  const int nruns = min(m.bad[1], kMaxLongRuns);
+  if (nruns > 0 && !*m.bad) {
+    uint32_t* khi = cur ? sv0 : sv1;
+    uint32_t* klo = reinterpret_cast<uint32_t*>(m.sk[0]);  // sk[0] | sk[1]: MAX x 4 bytes
+    for (int r = 0; r < nruns; ++r) {
+      const int i0 = runs[2 * r], n = runs[2 * r + 1] - i0;
+      uint32_t* Vr = V + i0;
+      int P = 1;
+      while (P < n) P <<= 1;
+      for (int x = tid; x < n; x += NT) {
+        const unsigned long long k = key64[Vr[x]];
+        khi[x] = (uint32_t)(k >> 32);
+        klo[x] = (uint32_t)k;
+      }
+      __syncthreads();
+      auto ce = [&](int x, int y) {  // x < y < n: the smaller (bits, id) to x
+        const unsigned long long a = ((unsigned long long)khi[x] << 32) | klo[x];
+        const unsigned long long b2 = ((unsigned long long)khi[y] << 32) | klo[y];
+        const uint32_t va = Vr[x], vb = Vr[y];
+        if (a > b2 || (a == b2 && va > vb)) {
+          khi[x] = (uint32_t)(b2 >> 32);
+          klo[x] = (uint32_t)b2;
+          Vr[x] = vb;
+          khi[y] = (uint32_t)(a >> 32);
+          klo[y] = (uint32_t)a;
+          Vr[y] = va;
+        }
+      };
+      for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int x = tid; x < P; x += NT) {  // flip: x against its mirror in the kk-block
+          const int y = x ^ (kk - 1);
+          if (y > x && y < n) ce(x, y);
+        }
+        __syncthreads();
+        for (int jj = kk >> 2; jj > 0; jj >>= 1) {
+          for (int x = tid; x < P; x += NT) {
+            const int y = x ^ jj;
+            if (y > x && y < n) ce(x, y);
+          }
+          __syncthreads();
+        }
+      }
+    }
+  }
   const bool ok = !*m.bad;
   if (ok)
     for (int i = tid; i < L; i += NT) pairs[lo + i] = V[i];
@@ -745,8 +809,12 @@ __global__ void __launch_bounds__(NT) k_tile_sort(const int* __restrict__ tile_p
   const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
   if (L <= 1 || L > kTileSortMax) return;  // (longer lists: k_scan_tiles listed them for the big sort)
   const SortSmem m = carve_sort_smem<kTileSortMax, NT>(smem);
-  if (!sort_tile_smem<kTileSortMax, NT>(m, pairs, lo, L, key32, key64))
+  if (!sort_tile_smem<kTileSortMax, NT>(m, pairs, lo, L, key32, key64)) {
+#ifdef SS_DBG_FALLBACK
+    if (threadIdx.x == 0) printf("merge-sort fallback: tile %d, list %d\n", t, L);
+#endif
     merge_sort_tile(pairs, tmp, lo, L, key64);  // long run of equal keys (block-uniform result)
+  }
 }
 
 __device__ int count_less(const uint32_t* run, int len, const unsigned long long* key, unsigned long long k,
@@ -809,6 +877,9 @@ __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ 
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     bool ok = false;
     if (L <= kTileSortBig) ok = sort_tile_smem<kTileSortBig, 1024>(m, pairs, lo, L, key32, key64);
+#ifdef SS_DBG_FALLBACK
+    if (!ok && threadIdx.x == 0) printf("merge-sort fallback: tile %d, list %d\n", t, L);
+#endif
     if (!ok) merge_sort_tile(pairs, tmp, lo, L, key64);
   }
 }
