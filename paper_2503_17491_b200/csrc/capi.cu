@@ -523,7 +523,6 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
           rec->Tf, rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1), counters + 4, counters + 5);
       SS_CUDA_TRY(cudaEventRecord(rec->long_join, rec->side));
     }
-    static const int fwd_pad = std::getenv("SS_FWD_PADSMEM") ? std::atoi(std::getenv("SS_FWD_PADSMEM")) : 0;  // (A/B)
     if (seg_fwd) {
       // pass 1 over the (tile, segment) slots k_seg_order listed, pass 2 per tile, pass 3
       // over the slots pass 2 listed (counters [6] / [8] tickets, [7] pass-3 slot count)
@@ -538,7 +537,7 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
           rec->bp, tile_ptr, chunk_ptr, rec->pairs, rec->rec, rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
           rec->last, rec->bitmask, rec->segpart, rec->term_seg, overflow, rec->seg3, counters + 8, counters + 7));
     } else if (k.T == 8)
-      SS_CUDA_TRY(pdl_launch(false, k_forward<8, false>, dim3(blocks), dim3(kWarpsPerBlock * 32), fwd_pad, s, rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
+      SS_CUDA_TRY(pdl_launch(false, k_forward<8, false>, dim3(blocks), dim3(kWarpsPerBlock * 32), 0, s, rec->bp, ntiles, tile_ptr, chunk_ptr, rec->pairs, rec->rec,
                                                           rec->rec64, out_range, out_normal, out_opacity, rec->Tf,
                                                           rec->last, rec->bitmask, overflow, order + 2 * (ntiles + 1),
                                                           counters, counters + 3));
