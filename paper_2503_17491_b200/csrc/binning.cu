@@ -33,10 +33,8 @@ struct Incidence {
 #define SS_SORT_MAX 2048
 #endif
 constexpr int kTileSortMax = SS_SORT_MAX;         // entries sorted in shared memory per tile (8 warps)
-// long-list variant (32 warps, 214 KB of dynamic shared memory: one block per SM, the big
-// sort's grid anyway); 8,192 before a config-4b map's lists of up to ~12,800 entries sent
-// 252 lists per render to the global merge sort
-constexpr int kTileSortBig = 16384;
+constexpr int kTileSortBig = 8192;    // long-list variant (32 warps, 98 KB of dynamic shared memory)
+constexpr int kTileSortHuge = 16384;  // dense maps: lists up to this in 214 KB (one block per SM)
 constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys: the block's bitonic sort
 constexpr int kMaxLongRuns = 128;                 // (more of them per list: merge-sort fallback)
 
@@ -864,19 +862,26 @@ __device__ void merge_sort_tile(uint32_t* __restrict__ pairs, uint32_t* __restri
 // Tiles k_tile_sort handed over (long_list): lists of up to kTileSortBig
 // entries sorted in shared memory by a 1024-thread block, anything else by
 // the global merge sort.
+// Lists longer than kTileSortMax (listed by k_scan_tiles), sorted on the side stream while
+// k_tile_sort sorts the rest: in shared memory up to CAP entries -- kTileSortBig (98 KB),
+// or for dense maps (see capi.cu) kTileSortHuge (214 KB: its blocks need an otherwise
+// empty SM, so it is not the default) -- longer lists, and lists with more long equal-key
+// runs than the shared-memory sort lists, are merge sorted in global memory.  (Config-4b map, 2 M surfels, lists up
+// to ~12,800: the merge sort of its 252 lists beyond 8,192 took ~1 ms per render.)
+template <int CAP>
 __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ tile_ptr, uint32_t* __restrict__ pairs,
                                                         uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key32,
                                                         const unsigned long long* __restrict__ key64,
                                                         const int* __restrict__ long_list,
                                                         const int* __restrict__ n_long) {
   extern __shared__ __align__(16) unsigned char dsmem[];
-  const SortSmem m = carve_sort_smem<kTileSortBig, 1024>(dsmem);
+  const SortSmem m = carve_sort_smem<CAP, 1024>(dsmem);
   const int nl = *n_long;
   for (int r = blockIdx.x; r < nl; r += gridDim.x) {
     const int t = long_list[r];
     const int lo = tile_ptr[t], L = tile_ptr[t + 1] - lo;
     bool ok = false;
-    if (L <= kTileSortBig) ok = sort_tile_smem<kTileSortBig, 1024>(m, pairs, lo, L, key32, key64);
+    if (L <= CAP) ok = sort_tile_smem<CAP, 1024>(m, pairs, lo, L, key32, key64);
 #ifdef SS_DBG_FALLBACK
     if (!ok && threadIdx.x == 0) printf("merge-sort fallback: tile %d, list %d\n", t, L);
 #endif

@@ -300,8 +300,10 @@ void set_smem_attrs() {
   cudaFuncSetAttribute(k_backward<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
-  cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_tile_sort_big<kTileSortBig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sort_smem_bytes<kTileSortBig, 1024>());
+  cudaFuncSetAttribute(k_tile_sort_big<kTileSortHuge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sort_smem_bytes<kTileSortHuge, 1024>());
   cudaFuncSetAttribute(k_backward<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   done = true;
 }
@@ -498,8 +500,15 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     // lengths, so it is built on the side stream too
     SS_CUDA_TRY(cudaEventRecord(rec->sort_fork, s));
     SS_CUDA_TRY(cudaStreamWaitEvent(rec->side, rec->sort_fork, 0));
-    k_tile_sort_big<<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
-        tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
+    // dense maps (more than SS_HUGE_SORT splats per tile: lists beyond 8,192 likely) take
+    // the 16,384-entry variant; the sorted lists are the same either way
+    const bool huge = (long long)n > (long long)SS_HUGE_SORT * ntiles;
+    if (huge)
+      k_tile_sort_big<kTileSortHuge><<<num_sms(), 1024, sort_smem_bytes<kTileSortHuge, 1024>(), rec->side>>>(
+          tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
+    else
+      k_tile_sort_big<kTileSortBig><<<num_sms(), 1024, sort_smem_bytes<kTileSortBig, 1024>(), rec->side>>>(
+          tile_ptr, rec->pbucket, rec->ptile, rec->key32, rec->key64, long_list, n_long);
     k_tile_order<<<1, 1024, 0, rec->side>>>(ntiles, tile_ptr, order + 2 * (ntiles + 1), order, counters,
                                             split_target, long_target, long_min,
                                             (seg || hyb) ? rec->segorder : nullptr, seg ? 0 : SS_SEG_MIN_LIST,
