@@ -150,7 +150,11 @@ __device__ __forceinline__ uint32_t preprocess_one(SplatsK sp, PoseK pose, CamK 
   rec64[i] = r64;
   key64[i] = (unsigned long long)__double_as_longlong(range);
 
-  // --- cone-bound incidence (rasterizer.py:256-305), float64 without contraction
+  // --- cone-bound incidence (rasterizer.py:256-305), float64 without contraction.
+  // (Measured and dropped: deciding every row / column test in float32 first and falling
+  // back to float64 only when a margin is under 1e-5 rad -- 0.2 % of the splats at config
+  // 1, tile lists still bit-exact -- took 61 us against 52: the float64 transcendentals
+  // here are not what bounds this kernel.)
   Incidence g;
   const double reach = x_mul(rk.cutoff_sigma, fmax(s0, s1));
   const bool near_ = range <= x_add(reach, 1e-12);
