@@ -260,9 +260,10 @@ def map_work(dm, raster):
     return tot / max(len(dm.keyframes), 1)
 
 
-# Our kernels per config-1 step (launch list profiles/r02_step_launches.csv): forward
+# Our kernels per config-1 step (launch list profiles/r02_v3_step_launches.csv): forward
 # k_tile_intervals, k_preprocess, k_scan_blocks, k_emit, k_tile_hist_blocks, k_tile_prefix,
-# k_scan_tiles, k_tile_scatter, k_tile_sort_big + k_tile_order (side stream), k_tile_sort,
+# k_scan_tiles, k_tile_scatter, k_tile_sort_big + k_tile_order (side stream; the order kernel
+# also lists the backward's slots), k_tile_sort,
 # k_forward_long (side; tail lists only), k_forward, k_publish_totals (side); k_mapping_loss;
 # backward k_backward, k_finalize.  (Plus torch fills that are not ours.)
 KERNELS_PER_STEP = 17
