@@ -484,23 +484,47 @@ __global__ void __launch_bounds__(1024)
     k_tile_scatter(const uint32_t* __restrict__ pair_tile, const uint32_t* __restrict__ pair_splat,
                    const long long* __restrict__ totals, long long cap, int ntiles, const uint32_t* __restrict__ mat,
                    const int* __restrict__ tile_ptr, uint32_t* __restrict__ bucketed, const int* __restrict__ overflow,
-                   int chunk) {
+                   int chunk, const int* __restrict__ tile_count) {
   pdl_wait();
-  extern __shared__ uint32_t cur[];
+  // The block's pairs are first grouped by tile in shared memory, then written out in that
+  // order: every tile's pairs of this block land as one contiguous run (scattered 4-byte
+  // stores cost a partial sector each).  Shared memory: per tile the running slot and the
+  // global-minus-local offset, the staged ids and tiles.
+  extern __shared__ uint32_t sm[];
+  uint32_t* lcur = sm;
+  uint32_t* gdel = sm + ntiles;
+  uint32_t* sspl = sm + 2 * ntiles;
+  uint16_t* stile = reinterpret_cast<uint16_t*>(sspl + chunk);
+  __shared__ long long wsum[32], tot;
   if (*overflow) return;
   const long long n = min(totals[0], cap);
   const long long b0 = (long long)blockIdx.x * chunk;
   if (b0 >= n) return;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) cur[t] = (uint32_t)tile_ptr[t] + mat[(size_t)blockIdx.x * ntiles + t];
-  __syncthreads();
-  const long long e = min(b0 + chunk, n);
-  for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) {
-    const uint32_t pos = atomicAdd(&cur[pair_tile[i]], 1u);
-    bucketed[pos] = pair_splat[i];
-    // (placing each pair's float32 sort key beside it here, so that k_tile_sort reads keys
-    // contiguously instead of gathering key32[id], measured 38 -> 52 us here against
-    // 53 -> 46 us in the sort: a net loss)
+  const int nb = (int)((n + chunk - 1) / chunk);
+  const int cnt = (int)(min(b0 + chunk, n) - b0);
+  const int tid = threadIdx.x;
+  const int per = (ntiles + 1023) / 1024;
+  const int t0 = min(tid * per, ntiles), t1 = min(t0 + per, ntiles);
+  const size_t row = (size_t)blockIdx.x * ntiles, next = row + ntiles;
+  long long sum = 0;
+  for (int t = t0; t < t1; ++t)
+    sum += (blockIdx.x + 1 < nb ? mat[next + t] : (uint32_t)tile_count[t]) - mat[row + t];
+  long long run = block_exscan_1024(sum, wsum, &tot);
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t c = (blockIdx.x + 1 < nb ? mat[next + t] : (uint32_t)tile_count[t]) - mat[row + t];
+    lcur[t] = (uint32_t)run;
+    gdel[t] = (uint32_t)tile_ptr[t] + mat[row + t] - (uint32_t)run;
+    run += c;
   }
+  __syncthreads();
+  for (int q = tid; q < cnt; q += 1024) {
+    const uint32_t t = pair_tile[b0 + q];
+    const uint32_t slot = atomicAdd(&lcur[t], 1u);
+    sspl[slot] = pair_splat[b0 + q];
+    stile[slot] = (uint16_t)t;
+  }
+  __syncthreads();
+  for (int q = tid; q < cnt; q += 1024) bucketed[gdel[stile[q]] + q] = sspl[q];
 }
 
 __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t va, unsigned long long kb, uint32_t vb) {

@@ -296,7 +296,8 @@ void set_smem_attrs() {
   if (done) return;
   const int bytes = (int)(sizeof(uint32_t) * kMaxTiles);
   cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * bytes + (size_t)kPairChunkMany * 6));
   cudaFuncSetAttribute(k_backward<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
@@ -489,8 +490,9 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     SS_CUDA_TRY(pdl_launch(pa, k_tile_hist_blocks, dim3(pblocks), dim3(1024), hsm, s, rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow, pchunk));
     SS_CUDA_TRY(pdl_launch(pa, k_tile_prefix, dim3((ntiles + 31) / 32), dim3(dim3(32, 32)), 0, s, rec->totals, cap, ntiles, rec->mat, tile_count, pchunk));
     SS_CUDA_TRY(pdl_launch(pa, k_scan_tiles, dim3(1), dim3(1024), 0, s, ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long));
-    SS_CUDA_TRY(pdl_launch(pa, k_tile_scatter, dim3(pblocks), dim3(1024), hsm, s, rec->ptile, rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr,
-                                              rec->pbucket, overflow, pchunk));
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_scatter, dim3(pblocks), dim3(1024), 2 * hsm + (size_t)pchunk * 6, s, rec->ptile,
+                           rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr, rec->pbucket, overflow, pchunk,
+                           tile_count));
   }
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
