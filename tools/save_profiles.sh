@@ -22,7 +22,7 @@ for r in rows[2:]:
   python tools/sass_regions.py gpurun_out/prof_round.ncu-rep k_backward
   echo
   echo "# SASS regions of k_forward"
-  python tools/sass_regions.py gpurun_out/prof_round.ncu-rep k_forward
+  python tools/sass_regions.py gpurun_out/prof_round.ncu-rep "^k_forward$"
 } > profiles/${tag}_ncu_full_summary.txt
 cat profiles/${tag}_ncu_full_summary.txt | head -12
 if [ -f gpurun_out/prof_map.ncu-rep ]; then
