@@ -411,18 +411,34 @@ __device__ __forceinline__ double hub_value(double r, double d) {
 // Grid-wide exact median of the valid |r| patterns in bits[0, n) (np.median).
 // m: number of valid entries (> 0).  Hc: this evaluation's kRsPasses x kRsBins
 // histograms (zeroed); cand / ncand / vmin: this evaluation's scratch.
-__device__ double rs_median(cg::grid_group& grid, const unsigned long long* __restrict__ bits, int n, int m,
-                            unsigned long long vlo, unsigned long long vhi, unsigned* __restrict__ Hc,
+// lanes per scan point in the geometric residual loop (the largest power of two <= 32 with
+// S n <= grid threads); the point's residual is written by lane 0 of its group
+__device__ __forceinline__ int rs_geo_stride(int n, int nthr) {
+  int S = 1;
+  while (S < 32 && 2 * S * n <= nthr) S *= 2;
+  return S;
+}
+
+// (*m_io < 0: the count is not known yet -- the first pass then histograms every valid
+// pattern on the fixed top digit, bits 62-51, and the count is that histogram's total,
+// written back to *m_io: one grid barrier fewer than counting first (rs_count).  With no
+// barrier between the residuals and that pass, each pattern is read by the thread that
+// wrote it: entry i by thread i * owner_stride + k * nthr (the residual loops' owners).
+// A zero count returns 0.)
+__device__ double rs_median(cg::grid_group& grid, const unsigned long long* __restrict__ bits, int n, int* m_io,
+                            int owner_stride, unsigned long long vlo, unsigned long long vhi, unsigned* __restrict__ Hc,
                             unsigned long long* cand, int* ncand, unsigned long long* vmin, unsigned* sh,
                             unsigned* s_part, int* s_bin, int* s_before, unsigned long long* s_min) {
   // vlo / vhi: smallest / largest valid pattern (rs_count).  The radix passes start at
   // the highest bit in which they differ (12-bit digits downwards).
-  if (vlo == vhi) return __longlong_as_double((long long)vlo);  // all equal
+  int m = *m_io;
+  const bool counted = m < 0;
+  if (!counted && vlo == vhi) return __longlong_as_double((long long)vlo);  // all equal
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gtid = blockIdx.x * kRsThreads + tid, nthr = gridDim.x * kRsThreads;
-  const int k1 = (m % 2 == 0) ? m / 2 - 1 : m / 2;
-  int top = 63 - __clzll(vlo ^ vhi);  // <= 62: valid patterns are non-negative doubles
-  unsigned long long mask = ~((2ull << top) - 1ull), prefix = vlo & mask;
+  int k1 = counted ? 0 : ((m % 2 == 0) ? m / 2 - 1 : m / 2);
+  int top = counted ? 62 : 63 - __clzll(vlo ^ vhi);  // <= 62: valid patterns are non-negative doubles
+  unsigned long long mask = ~((2ull << top) - 1ull), prefix = (counted ? 0ull : vlo) & mask;
   int kk = k1, cnt_eq = 0;
   bool exact = false;
   unsigned long long v2c = ~0ull;
@@ -432,9 +448,17 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
     const unsigned dmask = (1u << (top - lo + 1)) - 1u;
     for (int j = tid; j <= (int)dmask; j += kRsThreads) sh[j] = 0u;
     __syncthreads();
-    for (int i = gtid; i < n; i += nthr) {
-      const unsigned long long b = bits[i];
-      if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
+    if (p == 0 && counted) {
+      const int st = nthr / owner_stride;
+      for (int i = gtid % owner_stride == 0 ? gtid / owner_stride : n; i < n; i += st) {
+        const unsigned long long b = bits[i];
+        if (b != ~0ull) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
+      }
+    } else {
+      for (int i = gtid; i < n; i += nthr) {
+        const unsigned long long b = bits[i];
+        if (b != ~0ull && (b & mask) == prefix) atomicAdd(&sh[(unsigned)(b >> lo) & dmask], 1u);
+      }
     }
     __syncthreads();
     unsigned* Hp = Hc + p * kRsBins;  // p < kRsPasses: at most ceil(63 / 12) passes
@@ -443,6 +467,20 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
     RS_SUB(0);
     grid.sync();
     RS_SUB(1);
+    if (p == 0 && counted) {  // the count: the first histogram's total (every valid pattern)
+      unsigned c = 0;
+      for (int j = tid; j <= (int)dmask; j += kRsThreads) c += ((volatile unsigned*)Hp)[j];
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0) s_part[warp] = c;
+      __syncthreads();
+      m = 0;
+      for (int w = 0; w < kRsThreads / 32; ++w) m += (int)s_part[w];
+      __syncthreads();
+      *m_io = m;
+      if (m == 0) return 0.0;
+      k1 = (m % 2 == 0) ? m / 2 - 1 : m / 2;
+      kk = k1;
+    }
     rs_find_bin(Hp, (int)dmask + 1, kk, s_bin, s_before, s_part);
     RS_SUB(2);
     const int bin = *s_bin;
@@ -878,8 +916,7 @@ __global__ void __launch_bounds__(kRsThreads, kMinB) k_reg_solve(RsGeo geo, RsPh
           // neighbourhood in the leaf grid; their sorted k-best lists merge by
           // butterfly shuffles.  The lists live in registers (static indexing) and
           // order by (d2, leaf index), so the result does not depend on visit order.
-          int S = 1;
-          while (S < 32 && 2 * S * n <= nthr) S *= 2;
+          const int S = rs_geo_stride(n, nthr);
           const int i = gtid / S, sub = gtid & (S - 1);
           double p[3] = {0, 0, 0}, q3[3] = {0, 0, 0};
           if (i < n) {
@@ -966,12 +1003,14 @@ __global__ void __launch_bounds__(kRsThreads, kMinB) k_reg_solve(RsGeo geo, RsPh
         // (a per-block select from a shared-memory copy of all patterns, one grid barrier
         // instead of one per pass, measured slower: 42 vs 37 us per geometric evaluation --
         // shared-memory atomics on the clustered top digits and redundant passes)
-        m = rs_count(grid, okc, vlo, vhi, pcnt, pmm, s_part, s_mm, &s_m);
+        // the count comes out of the median's first histogram (one grid barrier fewer)
+        (void)okc;
+        (void)vlo;
+        (void)vhi;
         RS_MARK(2);
-        if (m > 0)
-          med = rs_median(grid, bits, n, m, s_mm[2 * (kRsThreads / 32)], s_mm[2 * (kRsThreads / 32) + 1], Hc,
-                          st->cand[par][f], &st->ncand[par][f], &st->vmin[par][f], sh, s_part, &s_bin, &s_before,
-                          s_min);
+        m = -1;
+        med = rs_median(grid, bits, n, &m, f == 0 ? rs_geo_stride(n, nthr) : 1, 0ull, 0ull, Hc, st->cand[par][f], &st->ncand[par][f],
+                        &st->vmin[par][f], sh, s_part, &s_bin, &s_before, s_min);
         if (blockIdx.x == 0 && tid == 0) {
           s_lm.cur_m[f] = m;
           s_lm.cur_med[f] = med;
