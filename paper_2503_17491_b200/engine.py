@@ -51,18 +51,53 @@ def ss_splats(t: dict) -> SsSplats:
     return SsSplats(n, *(t[k].data_ptr() for k in PARAM_NAMES))
 
 
+_STAGE: dict = {}
+
+
+def _host_pool():
+    pool = _STAGE.get("pool")
+    if pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        pool = _STAGE["pool"] = ThreadPoolExecutor(max_workers=5, thread_name_prefix="splat-upload")
+    return pool
+
+
 def splats_to_device(model, device=None) -> dict:
-    """float32 device copies of a SplatModel's raw parameters (reference or ours)."""
+    """float32 device copies of a SplatModel's raw parameters (reference or ours).
+
+    The host arrays are copied (in parallel, on host threads) into one reused pinned
+    staging buffer of their own dtype, uploaded with one DMA and rounded to float32 on the
+    device: a pageable upload per array and a host conversion pass cost more."""
     device = device or require_cuda()
-    out = {}
+    n = len(model)
+    arrs = []
     for k in PARAM_NAMES:
         a = np.ascontiguousarray(getattr(model, k))
         if a.dtype not in (np.float32, np.float64):
             a = a.astype(np.float64)
-        # float64 host arrays are uploaded as they are and rounded on the device (a host
-        # conversion pass costs more than the extra PCIe bytes)
-        t = torch.from_numpy(a).to(device).to(torch.float32).reshape(len(model), PARAM_WIDTH[k])
-        out[k] = t.reshape(-1) if k == "logit_opacity" else t.contiguous()
+        arrs.append(a)
+    dt = np.float64 if any(a.dtype == np.float64 for a in arrs) else np.float32
+    sizes = [n * PARAM_WIDTH[k] for k in PARAM_NAMES]
+    total = int(sum(sizes))
+    key = ("stage", dt)
+    st = _STAGE.get(key)
+    if st is None or st[0].numel() < total:
+        st = (torch.empty(max(total, 1), dtype=torch.float64 if dt == np.float64 else torch.float32).pin_memory(),
+              torch.cuda.Event())
+        _STAGE[key] = st
+    else:
+        st[1].synchronize()  # the previous upload from this buffer has left it
+    host = st[0].numpy()
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    list(_host_pool().map(lambda j: np.copyto(host[offs[j]:offs[j + 1]], arrs[j].reshape(-1), casting="unsafe"),
+                          range(len(arrs))))
+    dev_all = st[0][:total].to(device, non_blocking=True)
+    st[1].record()
+    dev32 = dev_all.to(torch.float32)
+    out = {}
+    for j, k in enumerate(PARAM_NAMES):
+        t = dev32[offs[j]:offs[j + 1]]
+        out[k] = t if k == "logit_opacity" else t.view(n, PARAM_WIDTH[k])
     return out
 
 
