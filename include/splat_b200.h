@@ -20,6 +20,7 @@
  *   ss_mapping_loss          mapping.py:128-196     range/normal/opacity losses
  *   ss_scale_loss            mapping.py:166-178     scale hinge
  *   ss_adam_step             mapping.py:367-379     Adam of refine (+ :495-496 clamp)
+ *   ss_render_finalize_adam_dev  the finalize fused with the refine step's Adam
  *   ss_reg_anchors           registration.py:190-213 sample_model (+ :430 thinning)
  *   ss_range_image           geometry.py:252-268     build_range_image
  *   ss_smooth_range_image    geometry.py:271-287     smooth_range_image (size 3)
@@ -204,6 +205,15 @@ int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, floa
                      const float* grads, float* m, float* v, int32_t n, int32_t* t_dev, float* bias_ws,
                      const double* lrs5, double beta1, double beta2, double eps, double log_scale_lo,
                      double log_scale_hi, void* stream);
+/* The finalize of ss_render_finalize (all rows, raw space, d_scales_extra the scale-hinge
+ * gradient) fused with ss_adam_step_dev: the raw gradient of each splat goes straight into
+ * the Adam step (mapping.py:479-496) on the splats' own parameter arrays (updated in place,
+ * the const of ss_splats notwithstanding) and the moments m, v; no gradient array.  Runs
+ * after ss_render_backward_blend; t_dev / bias_ws as for ss_adam_step_dev. */
+int ss_render_finalize_adam_dev(const ss_records* rec, const ss_splats* splats, const float* d_scales_extra,
+                                float* m, float* v, int32_t* t_dev, float* bias_ws, const double* lrs5,
+                                double beta1, double beta2, double eps, double log_scale_lo, double log_scale_hi,
+                                void* stream);
 
 /* history[*it_dev] = parts4 (the four mapping-loss parts of a step), *it_dev += 1. */
 int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream);

@@ -126,6 +126,8 @@ def lib() -> ctypes.CDLL:
     L.ss_adam_step.restype = ctypes.c_int
     L.ss_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, d, d, d, d, d, vp]
     L.ss_adam_step_dev.restype = ctypes.c_int
+    L.ss_render_finalize_adam_dev.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, vp, d, d, d, d, d, vp]
+    L.ss_render_finalize_adam_dev.restype = ctypes.c_int
     L.ss_store_loss_parts.argtypes = [vp, vp, vp, i32, vp]
     L.ss_store_loss_parts.restype = ctypes.c_int
     L.ss_range_image.argtypes = [ctypes.POINTER(SsCamera), vp, i32, vp, vp, vp]
@@ -174,7 +176,7 @@ EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",
             "ss_smooth_range_image", "ss_range_image_normals", "ss_leaf_tree_workspace_bytes", "ss_leaf_tree_build",
             "ss_records_set_deterministic", "ss_spawn_weights", "ss_densify_mask", "ss_spawn_splats",
-            "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact", "ss_adam_step_dev",
+            "ss_prune_workspace_bytes", "ss_prune_flags", "ss_prune_compact", "ss_adam_step_dev", "ss_render_finalize_adam_dev",
             "ss_store_loss_parts", "ss_records_sticky_overflow", "ss_records_reserve", "ss_records_generation",
             "ss_render_backward_blend", "ss_render_finalize", "ss_reg_solve_async",
             "ss_register_photo_batch"]

@@ -40,6 +40,7 @@
 // config 1, bound by 31 M L2 reduction sectors.)
 #include <cuda_pipeline.h>
 
+#include "adam.cuh"
 #include "common.cuh"
 
 namespace ss {
@@ -1028,7 +1029,9 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
                                                         float* __restrict__ acc,
                                                         const float* __restrict__ d_scales_extra,
                                                         float* __restrict__ out, int raw_space,
-                                                        int* __restrict__ bwd_ticket) {
+                                                        int* __restrict__ bwd_ticket, AdamK adam,
+                                                        const float* __restrict__ adam_bias,
+                                                        float* __restrict__ adam_m, float* __restrict__ adam_v) {
   pdl_wait();
   // the backward's persistent tile ticket restarts for the next backward pass
   if (blockIdx.x == 0 && threadIdx.x == 0) *bwd_ticket = 0;
@@ -1205,6 +1208,15 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   {  // consumed: leave the accumulators zeroed for the next backward pass
     float4* a4 = reinterpret_cast<float4*>(acc + (size_t)base * kAcc);
     for (int q = tid; q < cnt * 4; q += kFinBlock) a4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (adam_bias) {  // fused Adam step on the raw gradient (refine): parameters and moments in place
+    if (tid < cnt) {
+      float gg[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) gg[q] = s_out[tid * 12 + q];
+      adam_row(base + tid, adam, 1.f / adam_bias[0], 1.f / adam_bias[1], gg, adam_m, adam_v);
+    }
+    if (!out) return;
   }
   float* g = out + (size_t)base * nout;
   if (cnt == kFinBlock && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {

@@ -733,7 +733,8 @@ static int backward_blend(ss_records* rec, const ss_splats* splats, const float*
 // The finalize half on splats [begin, end): camera-frame -> world / raw gradients
 // into rows begin..end-1 of `grads`, clearing the consumed accumulators.
 static int backward_finalize(ss_records* rec, const ss_splats* splats, const float* d_scales_extra, float* grads,
-                             int raw_space, int begin, int end, cudaStream_t s) {
+                             int raw_space, int begin, int end, cudaStream_t s, const AdamK* adam = nullptr,
+                             const float* adam_bias = nullptr, float* adam_m = nullptr, float* adam_v = nullptr) {
   if (end <= begin) return SS_OK;
   const int w = raw_space ? 12 : 15;
   SplatsK sk = to_k(splats);
@@ -746,8 +747,8 @@ static int backward_finalize(ss_records* rec, const ss_splats* splats, const flo
   StageTimer tm(rec, ST_FINALIZE, s);
   SS_CUDA_TRY(pdl_launch(!rec->profiling, k_finalize, dim3((sk.n + kFinBlock - 1) / kFinBlock), dim3(kFinBlock), 0, s,
       sk, rec->pose, rec->rec64 + begin, rec->acc + (size_t)begin * kAcc,
-      d_scales_extra ? d_scales_extra + 2 * (size_t)begin : nullptr, grads + (size_t)begin * w, raw_space,
-      rec->misc + 5));
+      d_scales_extra ? d_scales_extra + 2 * (size_t)begin : nullptr, grads ? grads + (size_t)begin * w : nullptr,
+      raw_space, rec->misc + 5, adam ? *adam : AdamK{}, adam_bias, adam_m, adam_v));
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
@@ -1606,6 +1607,34 @@ int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, floa
   k_adam_dev<<<(n + 255) / 256, 256, 0, s>>>(n, a, bias_ws, grads, m, v);
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
+}
+
+int ss_render_finalize_adam_dev(const ss_records* rec, const ss_splats* splats, const float* d_scales_extra,
+                                float* m, float* v, int32_t* t_dev, float* bias_ws, const double* lrs5,
+                                double beta1, double beta2, double eps, double log_scale_lo, double log_scale_hi,
+                                void* stream) {
+  if (!rec || !splats || !m || !v || !t_dev || !bias_ws || !lrs5) return SS_ERR_INVALID_ARGUMENT;
+  ss_records* r = const_cast<ss_records*>(rec);
+  if (splats->n != r->n) return SS_ERR_STALE_RECORDS;
+  if (splats->n == 0) return SS_OK;
+  if (!r->acc) return SS_ERR_STALE_RECORDS;
+  cudaStream_t s = (cudaStream_t)stream;
+  AdamK a;
+  a.p[0] = const_cast<float*>(splats->centers);
+  a.p[1] = const_cast<float*>(splats->raw_t_alpha);
+  a.p[2] = const_cast<float*>(splats->raw_t_beta);
+  a.p[3] = const_cast<float*>(splats->log_scales);
+  a.p[4] = const_cast<float*>(splats->logit_opacity);
+  for (int q = 0; q < 5; ++q) a.lr[q] = (float)lrs5[q];
+  a.b1 = (float)beta1;
+  a.b2 = (float)beta2;
+  a.eps = (float)eps;
+  a.b1c = a.b2c = 1.f;
+  a.lo = (float)log_scale_lo;
+  a.hi = (float)log_scale_hi;
+  k_adam_tick<<<1, 1, 0, s>>>(t_dev, beta1, beta2, bias_ws);
+  SS_CUDA_TRY(cudaGetLastError());
+  return backward_finalize(r, splats, d_scales_extra, nullptr, 1, 0, splats->n, s, &a, bias_ws, m, v);
 }
 
 int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream) {

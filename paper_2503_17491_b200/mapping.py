@@ -326,17 +326,20 @@ class DeviceMap:
                 tuple(sorted(vars(cfg).items())), tuple(sorted(vars(raster).items())), self.scene_scale)
 
     def _graph_step(self, kf_index, cfg, raster):
-        g, parts = self.raw_gradient(kf_index, cfg, raster, sync=False)
+        # render, loss, blend backward; then the finalize fused with the Adam step (the raw
+        # gradient never leaves the kernel: the same arithmetic as step()'s two kernels)
+        parts = self.blend_gradient(kf_index, cfg, raster, sync=False)
         check(lib().ss_records_sticky_overflow(self.rec.ptr, ctypes.c_void_p(self._sticky.data_ptr()),
                                                ctypes.c_void_p(engine.stream_ptr())), "overflow flag")
         lrs = self.lrs(cfg)
-        check(lib().ss_adam_step_dev(*(ctypes.c_void_p(self.params[k].data_ptr()) for k in engine.PARAM_NAMES),
-                                     ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(self.m.data_ptr()),
-                                     ctypes.c_void_p(self.v.data_ptr()), self.n, ctypes.c_void_p(self._t_dev.data_ptr()),
-                                     ctypes.c_void_p(self._bias.data_ptr()), lrs.ctypes.data_as(ctypes.c_void_p), 0.9,
-                                     0.999, 1e-8, float(np.log(cfg.scale_floor)),
-                                     float(np.log(10.0 * cfg.scale_cap)), ctypes.c_void_p(engine.stream_ptr())),
-              "adam_step")
+        sp = engine.ss_splats(self.params)
+        check(lib().ss_render_finalize_adam_dev(self.rec.ptr, ctypes.byref(sp), ctypes.c_void_p(self.d_scales.data_ptr()),
+                                                ctypes.c_void_p(self.m.data_ptr()), ctypes.c_void_p(self.v.data_ptr()),
+                                                ctypes.c_void_p(self._t_dev.data_ptr()),
+                                                ctypes.c_void_p(self._bias.data_ptr()),
+                                                lrs.ctypes.data_as(ctypes.c_void_p), 0.9, 0.999, 1e-8,
+                                                float(np.log(cfg.scale_floor)), float(np.log(10.0 * cfg.scale_cap)),
+                                                ctypes.c_void_p(engine.stream_ptr())), "finalize + adam")
         check(lib().ss_store_loss_parts(ctypes.c_void_p(parts.data_ptr()), ctypes.c_void_p(self._hist.data_ptr()),
                                         ctypes.c_void_p(self._it.data_ptr()), self._HIST,
                                         ctypes.c_void_p(engine.stream_ptr())), "loss history")
