@@ -209,11 +209,13 @@ int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, floa
  * gradient) fused with ss_adam_step_dev: the raw gradient of each splat goes straight into
  * the Adam step (mapping.py:479-496) on the splats' own parameter arrays (updated in place,
  * the const of ss_splats notwithstanding) and the moments m, v; no gradient array.  Runs
- * after ss_render_backward_blend; t_dev / bias_ws as for ss_adam_step_dev. */
+ * after ss_render_backward_blend; t_dev / bias_ws as for ss_adam_step_dev.  scale_loss !=
+ * NULL: the scale hinge (mapping.py:166-178, ss_scale_loss) is evaluated here too, its
+ * loss added to *scale_loss, and d_scales_extra is ignored. */
 int ss_render_finalize_adam_dev(const ss_records* rec, const ss_splats* splats, const float* d_scales_extra,
                                 float* m, float* v, int32_t* t_dev, float* bias_ws, const double* lrs5,
                                 double beta1, double beta2, double eps, double log_scale_lo, double log_scale_hi,
-                                void* stream);
+                                double scale_cap, double w_scale, double* scale_loss, void* stream);
 
 /* history[*it_dev] = parts4 (the four mapping-loss parts of a step), *it_dev += 1. */
 int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream);

@@ -126,7 +126,8 @@ def lib() -> ctypes.CDLL:
     L.ss_adam_step.restype = ctypes.c_int
     L.ss_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, d, d, d, d, d, vp]
     L.ss_adam_step_dev.restype = ctypes.c_int
-    L.ss_render_finalize_adam_dev.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, vp, d, d, d, d, d, vp]
+    L.ss_render_finalize_adam_dev.argtypes = [vp, ctypes.POINTER(SsSplats), vp, vp, vp, vp, vp, vp, d, d, d, d, d, d, d,
+                                              vp, vp]
     L.ss_render_finalize_adam_dev.restype = ctypes.c_int
     L.ss_store_loss_parts.argtypes = [vp, vp, vp, i32, vp]
     L.ss_store_loss_parts.restype = ctypes.c_int

@@ -1031,7 +1031,9 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
                                                         float* __restrict__ out, int raw_space,
                                                         int* __restrict__ bwd_ticket, AdamK adam,
                                                         const float* __restrict__ adam_bias,
-                                                        float* __restrict__ adam_m, float* __restrict__ adam_v) {
+                                                        float* __restrict__ adam_m, float* __restrict__ adam_v,
+                                                        double hinge_cap, double hinge_w,
+                                                        double* __restrict__ hinge_loss) {
   pdl_wait();
   // the backward's persistent tile ticket restarts for the next backward pass
   if (blockIdx.x == 0 && threadIdx.x == 0) *bwd_ticket = 0;
@@ -1102,6 +1104,7 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
   }
   __syncthreads();
   const int nout = raw_space ? 12 : 15;
+  double hinge_acc = 0.0;
   double B[10];
   float4 ga, gb, gc, gd;
   if (tid < cnt) {
@@ -1196,13 +1199,30 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(SplatsK sp, PoseK pose, 
       o[3 + c] = (inner[c] - ui * u[c]) * ina;
       o[6 + c] = gb_[c];
     }
-    o[9] = (ds0 + s_ex[2 * tid]) * s0;
-    o[10] = (ds1 + s_ex[2 * tid + 1]) * s1;
+    float ex0 = s_ex[2 * tid], ex1 = s_ex[2 * tid + 1];
+    if (hinge_loss) {  // the scale hinge here instead of k_scale_loss (same float64 arithmetic)
+      const double e0 = exp((double)s_ls[2 * tid]), e1 = exp((double)s_ls[2 * tid + 1]);
+      const double over = fmax(e0, e1) - hinge_cap;
+      ex0 = ex1 = 0.f;
+      if (over > 0.0) {
+        hinge_acc = over;
+        if (e0 >= e1)
+          ex0 = (float)hinge_w;
+        else
+          ex1 = (float)hinge_w;
+      }
+    }
+    o[9] = (ds0 + ex0) * s0;
+    o[10] = (ds1 + ex1) * s1;
     const float xo = s_lo[tid];
     const float ex = __expf(-fabsf(xo));
     const float op = (xo >= 0.f ? 1.f : ex) * __frcp_rn(1.f + ex);
     o[11] = Oc * op * (1.f - op);
   }
+  }
+  if (hinge_loss) {  // block sum of the hinge, one float64 atomic per warp
+    for (int off = 16; off > 0; off >>= 1) hinge_acc += __shfl_xor_sync(0xffffffffu, hinge_acc, off);
+    if ((tid & 31) == 0 && hinge_acc != 0.0) atomicAdd(hinge_loss, hinge_acc);
   }
   __syncthreads();
   {  // consumed: leave the accumulators zeroed for the next backward pass

@@ -734,7 +734,8 @@ static int backward_blend(ss_records* rec, const ss_splats* splats, const float*
 // into rows begin..end-1 of `grads`, clearing the consumed accumulators.
 static int backward_finalize(ss_records* rec, const ss_splats* splats, const float* d_scales_extra, float* grads,
                              int raw_space, int begin, int end, cudaStream_t s, const AdamK* adam = nullptr,
-                             const float* adam_bias = nullptr, float* adam_m = nullptr, float* adam_v = nullptr) {
+                             const float* adam_bias = nullptr, float* adam_m = nullptr, float* adam_v = nullptr,
+                             double hinge_cap = 0.0, double hinge_w = 0.0, double* hinge_loss = nullptr) {
   if (end <= begin) return SS_OK;
   const int w = raw_space ? 12 : 15;
   SplatsK sk = to_k(splats);
@@ -748,7 +749,7 @@ static int backward_finalize(ss_records* rec, const ss_splats* splats, const flo
   SS_CUDA_TRY(pdl_launch(!rec->profiling, k_finalize, dim3((sk.n + kFinBlock - 1) / kFinBlock), dim3(kFinBlock), 0, s,
       sk, rec->pose, rec->rec64 + begin, rec->acc + (size_t)begin * kAcc,
       d_scales_extra ? d_scales_extra + 2 * (size_t)begin : nullptr, grads ? grads + (size_t)begin * w : nullptr,
-      raw_space, rec->misc + 5, adam ? *adam : AdamK{}, adam_bias, adam_m, adam_v));
+      raw_space, rec->misc + 5, adam ? *adam : AdamK{}, adam_bias, adam_m, adam_v, hinge_cap, hinge_w, hinge_loss));
   SS_CUDA_TRY(cudaGetLastError());
   return SS_OK;
 }
@@ -1612,7 +1613,7 @@ int ss_adam_step_dev(float* centers, float* raw_t_alpha, float* raw_t_beta, floa
 int ss_render_finalize_adam_dev(const ss_records* rec, const ss_splats* splats, const float* d_scales_extra,
                                 float* m, float* v, int32_t* t_dev, float* bias_ws, const double* lrs5,
                                 double beta1, double beta2, double eps, double log_scale_lo, double log_scale_hi,
-                                void* stream) {
+                                double scale_cap, double w_scale, double* scale_loss, void* stream) {
   if (!rec || !splats || !m || !v || !t_dev || !bias_ws || !lrs5) return SS_ERR_INVALID_ARGUMENT;
   ss_records* r = const_cast<ss_records*>(rec);
   if (splats->n != r->n) return SS_ERR_STALE_RECORDS;
@@ -1634,7 +1635,8 @@ int ss_render_finalize_adam_dev(const ss_records* rec, const ss_splats* splats, 
   a.hi = (float)log_scale_hi;
   k_adam_tick<<<1, 1, 0, s>>>(t_dev, beta1, beta2, bias_ws);
   SS_CUDA_TRY(cudaGetLastError());
-  return backward_finalize(r, splats, d_scales_extra, nullptr, 1, 0, splats->n, s, &a, bias_ws, m, v);
+  return backward_finalize(r, splats, d_scales_extra, nullptr, 1, 0, splats->n, s, &a, bias_ws, m, v, scale_cap,
+                           w_scale, scale_loss);
 }
 
 int ss_store_loss_parts(const double* parts4, double* history, int32_t* it_dev, int32_t cap, void* stream) {

@@ -239,9 +239,10 @@ class DeviceMap:
         return np.array([cfg.lr_centers * self.scene_scale, cfg.lr_tangents, cfg.lr_tangents, cfg.lr_log_scales,
                          cfg.lr_logit_opacity], dtype=np.float64)
 
-    def _render_loss(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None, sync: bool):
+    def _render_loss(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None, sync: bool,
+                     scale_loss: bool = True):
         """Render keyframe ``kf_index`` and its mapping loss: (dD, dN, dO, parts); the scale-loss
-        gradient lands in ``self.d_scales``."""
+        gradient lands in ``self.d_scales`` (scale_loss=False: left to the fused finalize)."""
         raster = raster or RasterConfig()
         kf = self.keyframes[kf_index]
         sp = self.params
@@ -249,10 +250,11 @@ class DeviceMap:
         dD, dN, dO, parts = engine.mapping_loss(D, N, O, kf.range, kf.valid, kf.normal, kf.nvalid,
                                                 w_opacity=cfg.w_opacity, w_normal=cfg.w_normal,
                                                 range_floor=cfg.range_weight_floor)
-        check(lib().ss_scale_loss(ctypes.c_void_p(sp["log_scales"].data_ptr()), self.n, float(cfg.scale_cap),
-                                  float(cfg.w_scale), ctypes.c_void_p(self.d_scales.data_ptr()),
-                                  ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(engine.stream_ptr())),
-              "scale_loss")
+        if scale_loss:
+            check(lib().ss_scale_loss(ctypes.c_void_p(sp["log_scales"].data_ptr()), self.n, float(cfg.scale_cap),
+                                      float(cfg.w_scale), ctypes.c_void_p(self.d_scales.data_ptr()),
+                                      ctypes.c_void_p(parts.data_ptr() + 3 * 8), ctypes.c_void_p(engine.stream_ptr())),
+                  "scale_loss")
         return dD, dN, dO, parts
 
     def raw_gradient(self, kf_index: int, cfg: MappingConfig, raster: RasterConfig | None = None,
@@ -326,9 +328,11 @@ class DeviceMap:
                 tuple(sorted(vars(cfg).items())), tuple(sorted(vars(raster).items())), self.scene_scale)
 
     def _graph_step(self, kf_index, cfg, raster):
-        # render, loss, blend backward; then the finalize fused with the Adam step (the raw
-        # gradient never leaves the kernel: the same arithmetic as step()'s two kernels)
-        parts = self.blend_gradient(kf_index, cfg, raster, sync=False)
+        # render, loss, blend backward; then the finalize fused with the scale hinge and the
+        # Adam step (the raw gradient never leaves the kernel: the same arithmetic as
+        # step()'s separate kernels)
+        dD, dN, dO, parts = self._render_loss(kf_index, cfg, raster, False, scale_loss=False)
+        engine.backward_blend(self.rec, self.params, dD, dN, dO)
         check(lib().ss_records_sticky_overflow(self.rec.ptr, ctypes.c_void_p(self._sticky.data_ptr()),
                                                ctypes.c_void_p(engine.stream_ptr())), "overflow flag")
         lrs = self.lrs(cfg)
@@ -339,6 +343,8 @@ class DeviceMap:
                                                 ctypes.c_void_p(self._bias.data_ptr()),
                                                 lrs.ctypes.data_as(ctypes.c_void_p), 0.9, 0.999, 1e-8,
                                                 float(np.log(cfg.scale_floor)), float(np.log(10.0 * cfg.scale_cap)),
+                                                float(cfg.scale_cap), float(cfg.w_scale),
+                                                ctypes.c_void_p(parts.data_ptr() + 3 * 8),
                                                 ctypes.c_void_p(engine.stream_ptr())), "finalize + adam")
         check(lib().ss_store_loss_parts(ctypes.c_void_p(parts.data_ptr()), ctypes.c_void_p(self._hist.data_ptr()),
                                         ctypes.c_void_p(self._it.data_ptr()), self._HIST,
