@@ -36,6 +36,13 @@ constexpr int kTileSortMax = SS_SORT_MAX;         // entries sorted in shared me
 constexpr int kTileSortBig = 8192;    // long-list variant (32 warps, 98 KB of dynamic shared memory)
 constexpr int kTileSortHuge = 16384;  // dense maps: lists up to this in 214 KB (one block per SM)
 constexpr int kMaxTieRun = 64;                    // longer runs of equal sort keys: the block's bitonic sort
+#ifndef SS_THREAD_TIE
+#define SS_THREAD_TIE 5
+#endif
+#ifndef SS_TIE_STAGE
+#define SS_TIE_STAGE 4  // runs at least this long stage their keys in shared memory
+#endif
+constexpr int kThreadTieRun = SS_THREAD_TIE;                 // runs up to this long: one thread's insertion sort
 constexpr int kMaxLongRuns = 128;                 // (more of them per list: merge-sort fallback)
 
 // np.mod(x, 2*pi) for x = d + pi with d a difference of two angles in
@@ -626,7 +633,10 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
   if (tid == 0) {
     m.bad[0] = 0;
     m.bad[1] = 0;  // long equal-key runs listed
+    m.bad[2] = 0;  // keys of the short runs staged in shared memory
+    m.bad[3] = 0;  // medium runs listed for the warps
   }
+  for (int i = tid; i < 256; i += NT) m.dtot[i] = 0;  // first-digit histogram
   __syncthreads();
   for (int w = 0; w < NW; ++w) {
     kmin = min(kmin, m.red[w]);
@@ -634,21 +644,69 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
   }
   const uint32_t span = kmax - kmin;
   const int shift = span >= 65536u ? (32 - __clz(span)) - 16 : 0;
+  // First (low) digit: the order among equal digits is irrelevant -- the second pass is
+  // stable and the tie-fix below puts equal 16-bit keys in exact order -- so shared-memory
+  // atomics rank the elements (a warp-ballot ranking costs ~70 instructions per 32)
+  uint32_t* const hist = m.dtot;
 #pragma unroll
   for (int j = 0; j < IPL; ++j) {
     const int i = tid + NT * j;
     if (NT * j >= L) break;
-    if (i < L) sk0[i] = (uint16_t)((kk[j] - kmin) >> shift);
+    if (i < L) {
+      const uint32_t k16 = (kk[j] - kmin) >> shift;
+      sk0[i] = (uint16_t)k16;
+      kk[j] = (k16 << 16) | atomicAdd(hist + (k16 & 0xffu), 1u);
+    }
+  }
+  __syncthreads();
+  {  // exclusive scan of the 256 digit counts, in place; thread t owns [t*DPT, (t+1)*DPT)
+    constexpr int DPT = NT >= 256 ? 1 : 256 / NT;
+    const bool act = tid * DPT < 256;  // warp-uniform
+    uint32_t sd[DPT], tsum = 0, inc = 0;
+    if (act) {
+#pragma unroll
+      for (int d = 0; d < DPT; ++d) {
+        sd[d] = hist[tid * DPT + d];
+        tsum += sd[d];
+      }
+      inc = tsum;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      if (lane == 31) m.red[warp] = inc;
+    }
+    __syncthreads();
+    if (act) {
+      uint32_t run = inc - tsum;
+      for (int w = 0; w < warp; ++w) run += m.red[w];
+#pragma unroll
+      for (int d = 0; d < DPT; ++d) {
+        hist[tid * DPT + d] = run;
+        run += sd[d];
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < IPL; ++j) {
+    const int i = tid + NT * j;
+    if (NT * j >= L) break;
+    if (i < L) {
+      const uint32_t pos = hist[(kk[j] >> 16) & 0xffu] + (kk[j] & 0xffffu);
+      sk1[pos] = (uint16_t)(kk[j] >> 16);
+      sv1[pos] = sv0[i];
+    }
   }
   __syncthreads();
   const int seg = ((L + NT - 1) / NT) * 32;  // warp w owns [w*seg, (w+1)*seg), lane-striped
   const uint32_t lt = lanemask_lt();
   const uint32_t sspan = span >> shift;
   uint16_t* wc = m.wcnt + warp * 256;
-  int cur = 0;
-  for (int p = 0; p < 2; ++p) {
+  int cur = 1;
+  for (int p = 1; p < 2; ++p) {
     const int sh = 8 * p;
-    if (p == 1 && sspan < 256u) break;  // high digit constant
+    if (sspan < 256u) break;  // high digit constant
     for (int i = tid; i < NW * 256; i += NT) m.wcnt[i] = 0;
     __syncthreads();
     uint16_t lr[IPL];
@@ -727,6 +785,8 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
   const uint16_t* K = cur ? sk1 : sk0;
   uint32_t* V = cur ? sv1 : sv0;
   int* runs = reinterpret_cast<int*>(m.dtot);  // (free after the digit passes) [2 * kMaxLongRuns]
+  unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(cur ? sv0 : sv1);  // free: MAX / 2 keys
+  uint32_t* wruns = reinterpret_cast<uint32_t*>(cur ? sk0 : sk1);  // free: MAX / 4 (start, key offset | n)
   for (int i = tid; i < L; i += NT) {
     const uint16_t k = K[i];
     if (i > 0 && K[i - 1] == k) continue;
@@ -743,6 +803,48 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
       }
       continue;
     }
+    // the run's float64 keys first go to a free buffer with independent loads, so the
+    // insertion sort compares in shared memory instead of a chain of dependent L2 loads
+    const int n = j - i;
+    const int off = n >= SS_TIE_STAGE ? atomicAdd(m.bad + 2, n) : MAX;
+    if (off + n <= MAX / 2) {
+      unsigned long long* kr = kbuf + off;
+      int x = 0;
+      for (; x + 4 <= n; x += 4) {
+        const unsigned long long a0 = key64[V[i + x]], a1 = key64[V[i + x + 1]];
+        const unsigned long long a2 = key64[V[i + x + 2]], a3 = key64[V[i + x + 3]];
+        kr[x] = a0;
+        kr[x + 1] = a1;
+        kr[x + 2] = a2;
+        kr[x + 3] = a3;
+      }
+      for (; x < n; ++x) kr[x] = key64[V[i + x]];
+      if (n > kThreadTieRun) {  // ranked by a warp after the barrier
+        const int q = atomicAdd(m.bad + 3, 1);
+        if (q < MAX / 4) {
+          wruns[2 * q] = (uint32_t)i;
+          wruns[2 * q + 1] = (uint32_t)off | ((uint32_t)n << 24);
+          continue;
+        }
+      }
+      uint32_t* Vr = V + i;
+      for (int x2 = 1; x2 < n; ++x2) {
+        const uint32_t v = Vr[x2];
+        const unsigned long long kv = kr[x2];
+        int y = x2 - 1;
+        while (y >= 0) {
+          const uint32_t w = Vr[y];
+          const unsigned long long kw = kr[y];
+          if (key_less(kw, w, kv, v)) break;
+          Vr[y + 1] = w;
+          kr[y + 1] = kw;
+          --y;
+        }
+        Vr[y + 1] = v;
+        kr[y + 1] = kv;
+      }
+      continue;
+    }
     for (int x = i + 1; x < j; ++x) {
       const uint32_t v = V[x];
       const unsigned long long kv = key64[v];
@@ -754,6 +856,32 @@ __device__ bool sort_tile_smem(const SortSmem& m, uint32_t* __restrict__ pairs, 
         --y;
       }
       V[y + 1] = v;
+    }
+  }
+  __syncthreads();
+  // medium runs (kThreadTieRun < n <= kMaxTieRun): one warp per run, each element's position is
+  // the number of (key, id) pairs of the run below its own, read from the staged keys
+  {
+    const int nw = min(m.bad[3], MAX / 4);
+    for (int q = warp; q < nw; q += NW) {
+      const int i = (int)wruns[2 * q];
+      const int off = (int)(wruns[2 * q + 1] & 0xffffffu), n = (int)(wruns[2 * q + 1] >> 24);
+      const unsigned long long* kr = kbuf + off;
+      uint32_t* Vr = V + i;
+      const bool h0 = lane < n, h1 = lane + 32 < n;
+      const uint32_t v0 = h0 ? Vr[lane] : 0u, v1 = h1 ? Vr[lane + 32] : 0u;
+      const unsigned long long k0 = h0 ? kr[lane] : 0ull, k1 = h1 ? kr[lane + 32] : 0ull;
+      int r0 = 0, r1 = 0;
+      for (int y = 0; y < n; ++y) {
+        const unsigned long long ky = kr[y];
+        const uint32_t vy = Vr[y];
+        r0 += key_less(ky, vy, k0, v0);
+        r1 += key_less(ky, vy, k1, v1);
+      }
+      __syncwarp();
+      if (h0) Vr[r0] = v0;
+      if (h1) Vr[r1] = v1;
+      __syncwarp();
     }
   }
   __syncthreads();

@@ -210,6 +210,30 @@ def test_tie_runs_in_shared_memory_sized_lists_bit_exact(cuda):
     assert np.array_equal(rec.pair_splats, ref["pair_splats"])
 
 
+@pytest.mark.parametrize("group", [12, 40, 90])
+def test_medium_tie_runs_bit_exact(cuda, group):
+    """Groups of splats at one range (and exact duplicates of a centre): per tile, runs of equal
+    16-bit sort keys of roughly the group's size -- one thread's insertion sort (<= 8), the
+    warp ranking (9-64) and the block bitonic sort (> 64) -- all put in the reference's
+    (range, index) order."""
+    params = _crowded_params(4000, 0, 13)
+    rng = np.random.default_rng(group)
+    c = params["centers"].astype(np.float64)
+    d = c / np.linalg.norm(c, axis=1, keepdims=True)
+    ng = 1200 // group
+    for g in range(ng):
+        sl = slice(g * group, (g + 1) * group)
+        c[sl] = d[sl] * rng.uniform(4.0, 12.0)
+    c[1200:1260] = c[1200]  # exact duplicates: equal float64 ranges, ordered by index
+    params["centers"] = np.ascontiguousarray(c, dtype=np.float32)
+    cam = W.synth_camera(512, 64)
+    ct = (cam.width, cam.height, cam.az_min, cam.az_max, cam.el_min, cam.el_max)
+    ref = O.render(ct, np.eye(3), np.zeros(3), params)
+    _, rec = rasterize_forward(cam, SE3Pose.identity(), SplatModel.from_params(params))
+    assert np.array_equal(rec.tile_ptr, ref["tile_ptr"])
+    assert np.array_equal(rec.pair_splats, ref["pair_splats"])
+
+
 def test_deterministic_backward_bit_identical(cuda):
     """RasterConfig(deterministic=True): fixed-order reduction, bit-identical gradients run to run,
     within the 1e-3 gate of the oracle; the default (atomic) path agrees to float rounding."""
