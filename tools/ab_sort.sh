@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for f in variants/lib_*.so; do
   n=$(basename $f .so)
-  for w in "prof_step.py 1" "map_step.py 4"; do
+  for w in "prof_step.py 1" ${AB_MAP-"map_step.py 4"}; do
     SPLAT_B200_LIB=$PWD/$f timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_tile_sort -s 6 -c 12 --csv \
       python tools/$w > gpurun_out/abs_${n}_${w%%.*}.csv 2>/dev/null
     python - "$n" "$w" gpurun_out/abs_${n}_${w%%.*}.csv <<'PY'
