@@ -166,6 +166,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, SS_FWD_MINB)
       for (int j = 0; j < PPL; ++j)
         if (mine[j]) bitmask[(size_t)(cbase + chunk) * (TS * TS) + lane + 32 * j] = word[j];
       __syncwarp();
+      // pass 3: once every pixel of the slot has hit the cut-off the rest of the segment is
+      // beyond their last contributions (the backward masks those chunks by `last`)
+      if (kPass == 3 && !__any_sync(0xffffffffu, live[0] || live[1])) break;
     }
     __pipeline_wait_prior(0);
     __syncwarp();

@@ -283,12 +283,32 @@ cudaError_t pdl_launch(bool allow, void (*kern)(KArgs...), dim3 grid, dim3 block
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-__global__ void k_count_contrib(long long nwords, const unsigned* __restrict__ bm, unsigned long long* out) {
+// Contributions U: the contribution bits of each pixel up to its last contributing list
+// position (the segment forward leaves words past a pixel's cut-off that no pass reads:
+// the backward masks them the same way).  One warp per tile.
+__global__ void k_count_contrib(CamK k, int ntiles, const int* __restrict__ tile_ptr, const int* __restrict__ chunk_ptr,
+                                const int* __restrict__ last, const unsigned* __restrict__ bm,
+                                unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+  const int TT = k.T * k.T;
   unsigned long long c = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x)
-    c += __popc(bm[i]);
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * blockDim.x) >> 5) {
+    const int tr = t / k.tx, tc = t % k.tx;
+    const int nch = (tile_ptr[t + 1] - tile_ptr[t] + 31) / 32;
+    const int cbase = chunk_ptr[t];
+    for (int q = lane; q < TT; q += 32) {
+      const int row = tr * k.T + q / k.T, col = tc * k.T + q % k.T;
+      if (row >= k.H || col >= k.W) continue;
+      const int l = last[(size_t)row * k.W + col];
+      for (int ch = 0; ch < nch && ch * 32 < l; ++ch) {
+        const int r = l - ch * 32;
+        const unsigned mask = r >= 32 ? 0xffffffffu : ((1u << r) - 1u);
+        c += __popc(bm[(size_t)(cbase + ch) * TT + q] & mask);
+      }
+    }
+  }
   for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+  if (lane == 0) atomicAdd(out, c);
 }
 
 void set_smem_attrs() {
@@ -867,8 +887,9 @@ int ss_records_work(const ss_records* rec, int64_t* evaluations, int64_t* contri
   unsigned long long* d_u = nullptr;
   SS_CUDA_TRY(cudaMallocAsync((void**)&d_u, sizeof(unsigned long long), s));
   SS_CUDA_TRY(cudaMemsetAsync(d_u, 0, sizeof(unsigned long long), s));
-  long long nwords = rec->n_chunks * (long long)rec->cam.T * rec->cam.T;
-  if (nwords > 0) k_count_contrib<<<148 * 4, 256, 0, s>>>(nwords, rec->bitmask, d_u);
+  if (rec->n_chunks > 0)
+    k_count_contrib<<<148 * 4, 256, 0, s>>>(rec->cam, rec->ntiles, rec->tiles, rec->tiles + (rec->ntiles + 1), rec->last,
+                                            rec->bitmask, d_u);
   unsigned long long hu = 0;
   SS_CUDA_TRY(cudaMemcpyAsync(&hu, d_u, sizeof(hu), cudaMemcpyDeviceToHost, s));
   SS_CUDA_TRY(cudaFreeAsync(d_u, s));
