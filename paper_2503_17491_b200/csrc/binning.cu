@@ -416,13 +416,14 @@ __global__ void __launch_bounds__(1024)
 // (in place) and the tile totals.  Block = 32 tiles x 32 block-segments.
 __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restrict__ totals, long long cap, int ntiles,
                                                       uint32_t* __restrict__ mat, int* __restrict__ tile_count,
-                                                      int chunk) {
+                                                      int chunk, int nb_fixed) {
   pdl_wait();
   __shared__ uint32_t part[32][33];
   const int tx = threadIdx.x, seg = threadIdx.y;
   const int t = blockIdx.x * 32 + tx;
   const long long n = min(totals[0], cap);
-  const int nb = (int)max(1LL, (n + chunk - 1) / chunk);
+  // (nb_fixed > 0: the direct binning's splat blocks, k_bin_count)
+  const int nb = nb_fixed > 0 ? nb_fixed : (int)max(1LL, (n + chunk - 1) / chunk);
   const int per = (nb + 31) / 32;
   const int b0 = min(seg * per, nb), b1 = min(b0 + per, nb);
   uint32_t s = 0;
@@ -453,7 +454,8 @@ __global__ void __launch_bounds__(1024) k_tile_prefix(const long long* __restric
 __global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __restrict__ tile_count,
                                                      int* __restrict__ tile_ptr, int* __restrict__ chunk_ptr,
                                                      long long* __restrict__ totals, int* __restrict__ long_list,
-                                                     int* __restrict__ n_long) {
+                                                     int* __restrict__ n_long, long long cap, int* __restrict__ overflow,
+                                                     int set_total) {
   pdl_wait();
   __shared__ long long wsum[32], tot;
   const int tid = threadIdx.x;
@@ -484,7 +486,162 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const int* __re
     tile_ptr[ntiles] = (int)(tot >> 32);
     chunk_ptr[ntiles] = (int)(tot & 0xffffffffll);
     totals[1] = tot & 0xffffffffll;
+    if (set_total) {  // direct binning: the pair total is first known here
+      totals[0] = tot >> 32;
+      if ((tot >> 32) > cap) *overflow = 1;
+    }
   }
+}
+
+// Direct binning (SS_DIRECT_BIN): no (tile, splat) pair list.  k_bin_count builds each
+// block's tile histogram straight from the splats' tile rectangles (row b of the blocks x
+// tiles matrix, as k_tile_hist_blocks does from the pair list), and k_bin_scatter
+// re-expands the rectangles into the tile buckets, staged by tile in shared memory so a
+// tile's pairs from one block land as one run (a block with more pairs than the stage
+// writes them directly).  Replaces k_scan_blocks + k_emit + k_tile_hist_blocks +
+// k_tile_scatter and the pair list's 16 bytes per pair of traffic.
+constexpr int kBinSplats = 2048;  // splats per binning block
+constexpr int kBinStage = 12288;  // pairs staged in shared memory per block
+constexpr uint32_t kBinLane = 8;  // rectangles of up to this many tiles expanded by one lane
+
+__device__ __forceinline__ int rect_tile(int rr, int c, int tx) { return rr * tx + (c >= tx ? c - tx : c); }
+
+// The (tile, splat) pairs of the warp's 32 splats, 32 at a time across the lanes (a splat
+// covering many tiles would otherwise hold its lane for its whole rectangle): pair q
+// belongs to the lane whose inclusive count prefix first exceeds q.  Warp-uniform call.
+template <class F>
+__device__ __forceinline__ void warp_pairs(int4 r, int i, int tx, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t all = (r.y >= r.x) ? (uint32_t)((r.y - r.x + 1) * r.w) : 0u;
+  // small rectangles (the common case) by their own lane
+  if (all <= kBinLane)
+    for (int rr = r.x; rr <= r.y; ++rr)
+      for (int q = 0; q < r.w; ++q) f(rect_tile(rr, r.z + q, tx), i);
+  const uint32_t cnt = all > kBinLane ? all : 0u;
+  if (!__any_sync(0xffffffffu, cnt > 0)) return;
+  uint32_t inc = cnt;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  const uint32_t wtot = __shfl_sync(0xffffffffu, inc, 31);
+  for (uint32_t q0 = 0; q0 < wtot; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    int owner = 0;
+    for (int b = 16; b > 0; b >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, inc, owner + b - 1);
+      if (v <= q) owner += b;
+    }
+    const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, owner);
+    const int rx = __shfl_sync(0xffffffffu, r.x, owner), rz = __shfl_sync(0xffffffffu, r.z, owner);
+    const int rw = __shfl_sync(0xffffffffu, r.w, owner), si = __shfl_sync(0xffffffffu, i, owner);
+    if (q < wtot) {
+      const uint32_t k = q - ex;
+      f(rect_tile(rx + (int)(k / (uint32_t)rw), rz + (int)(k % (uint32_t)rw), tx), si);
+    }
+  }
+}
+
+// The block's tile histogram as a 2-D difference array over the tile grid: four shared
+// atomics per rectangle (two rectangles when it wraps in azimuth), then row and column
+// prefix sums -- a splat covering many tiles costs no more than one covering a few.
+__global__ void __launch_bounds__(1024) k_bin_count(int n, const int4* __restrict__ rect, int tx, int ty,
+                                                    uint32_t* __restrict__ mat) {
+  pdl_wait();
+  extern __shared__ int dgrid[];  // (ty + 1) x (tx + 1)
+  const int W1 = tx + 1, ncell = (ty + 1) * W1, ntiles = tx * ty;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int q = tid; q < ncell; q += blockDim.x) dgrid[q] = 0;
+  __syncthreads();
+  auto add_rect = [&](int r0, int r1, int ca, int cb) {  // rows r0..r1, columns ca..cb
+    atomicAdd(&dgrid[r0 * W1 + ca], 1);
+    atomicAdd(&dgrid[r0 * W1 + cb + 1], -1);
+    atomicAdd(&dgrid[(r1 + 1) * W1 + ca], -1);
+    atomicAdd(&dgrid[(r1 + 1) * W1 + cb + 1], 1);
+  };
+  const int i1 = min((blockIdx.x + 1) * kBinSplats, n);
+  for (int i = blockIdx.x * kBinSplats + tid; i < i1; i += blockDim.x) {
+    const int4 r = rect[i];
+    if (r.y < r.x || r.w <= 0) continue;
+    const int cend = r.z + r.w - 1;
+    if (cend < tx) {
+      add_rect(r.x, r.y, r.z, cend);
+    } else {
+      add_rect(r.x, r.y, r.z, tx - 1);
+      add_rect(r.x, r.y, 0, cend - tx);
+    }
+  }
+  __syncthreads();
+  // prefix along each row (a warp per row, 32 columns at a time)
+  for (int row = warp; row < ty; row += (int)(blockDim.x >> 5)) {
+    int carry = 0;
+    for (int c0 = 0; c0 < tx; c0 += 32) {
+      const int c = c0 + lane;
+      int v = c < tx ? dgrid[row * W1 + c] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += y;
+      }
+      v += carry;
+      if (c < tx) dgrid[row * W1 + c] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  // ... then down each column, and out as row b of the blocks x tiles matrix
+  for (int c = tid; c < tx; c += blockDim.x) {
+    int run = 0;
+    for (int row = 0; row < ty; ++row) {
+      run += dgrid[row * W1 + c];
+      mat[(size_t)blockIdx.x * ntiles + row * tx + c] = (uint32_t)run;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    k_bin_scatter(int n, const int4* __restrict__ rect, int tx, int ntiles, const uint32_t* __restrict__ mat, int nbb,
+                  const int* __restrict__ tile_ptr, const int* __restrict__ tile_count,
+                  uint32_t* __restrict__ bucketed, const int* __restrict__ overflow) {
+  pdl_wait();
+  extern __shared__ uint32_t sm[];
+  uint32_t* lcur = sm;
+  uint32_t* gdel = sm + ntiles;
+  uint32_t* sspl = sm + 2 * ntiles;
+  uint16_t* stile = reinterpret_cast<uint16_t*>(sspl + kBinStage);
+  __shared__ long long wsum[32], tot;
+  if (*overflow) return;
+  const int tid = threadIdx.x;
+  const int per = (ntiles + 1023) / 1024;
+  const int t0 = min(tid * per, ntiles), t1 = min(t0 + per, ntiles);
+  const size_t row = (size_t)blockIdx.x * ntiles, next = row + ntiles;
+  const bool last_block = blockIdx.x + 1 >= nbb;
+  long long sum = 0;
+  for (int t = t0; t < t1; ++t) sum += (last_block ? (uint32_t)tile_count[t] : mat[next + t]) - mat[row + t];
+  long long run = block_exscan_1024(sum, wsum, &tot);
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t c = (last_block ? (uint32_t)tile_count[t] : mat[next + t]) - mat[row + t];
+    lcur[t] = (uint32_t)run;
+    gdel[t] = (uint32_t)tile_ptr[t] + mat[row + t] - (uint32_t)run;
+    run += c;
+  }
+  __syncthreads();
+  const bool staged = tot <= kBinStage;  // (block-uniform)
+  const int i1 = min((blockIdx.x + 1) * kBinSplats, n);
+  for (int i = blockIdx.x * kBinSplats + tid; i - (tid & 31) < i1; i += 1024) {
+    const int4 r = i < i1 ? rect[i] : make_int4(0, -1, 0, 0);
+    warp_pairs(r, i, tx, [&](int t, int si) {
+      const uint32_t slot = atomicAdd(&lcur[t], 1u);
+      if (staged) {
+        sspl[slot] = (uint32_t)si;
+        stile[slot] = (uint16_t)t;
+      } else {
+        bucketed[gdel[t] + slot] = (uint32_t)si;
+      }
+    });
+  }
+  __syncthreads();
+  if (staged)
+    for (int q = tid; q < (int)tot; q += 1024) bucketed[gdel[stile[q]] + q] = sspl[q];
 }
 
 __global__ void __launch_bounds__(1024)

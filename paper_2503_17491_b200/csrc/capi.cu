@@ -318,6 +318,9 @@ void set_smem_attrs() {
   cudaFuncSetAttribute(k_tile_hist_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(2 * bytes + (size_t)kPairChunkMany * 6));
+  cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * bytes + 16);
+  cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * bytes + (size_t)kBinStage * 6));
   cudaFuncSetAttribute(k_backward<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
   cudaFuncSetAttribute(k_backward<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdDynSmem);
@@ -420,10 +423,11 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
   if (ntiles > kMaxTiles) return SS_ERR_UNSUPPORTED;
   const int pchunk = num_sms() * 16 > ntiles ? kPairChunkFew : kPairChunkMany;
   const int pblocks = (int)((cap + pchunk - 1) / pchunk);
+  const int nbb = std::max(1, (n + kBinSplats - 1) / kBinSplats);  // direct binning blocks
   if (grow(rec->rec, rec->cap_rec, (size_t)n + 1, s) || grow(rec->rec64, rec->cap_rec64, (size_t)n + 1, s) ||
       grow(rec->key64, rec->cap_key64, (size_t)n + 1, s) || grow(rec->key32, rec->cap_key32, (size_t)n + 1, s) ||
       grow(rec->rect, rec->cap_rect, (size_t)n + 1, s) || grow(rec->bsum, rec->cap_bsum, (size_t)nb + 1, s) ||
-      grow(rec->mat, rec->cap_mat, (size_t)pblocks * ntiles, s) ||
+      grow(rec->mat, rec->cap_mat, (size_t)std::max(pblocks, nbb) * ntiles, s) ||
       grow(rec->tint, rec->cap_tint, (size_t)(k.tx + k.ty), s) ||
       grow(rec->tiles, rec->cap_tiles, (size_t)8 * (ntiles + 1), s) ||
       grow(rec->ptile, rec->cap_ptile, (size_t)cap, s) || grow(rec->psplat, rec->cap_psplat, (size_t)cap, s) ||
@@ -498,6 +502,23 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
       SS_CUDA_TRY(pdl_launch(pa, k_preprocess, dim3(nb), dim3(256), 0, s, sk, pk, k, rk, colt, rowt, rec->rec, rec->rec64, rec->key64, rec->key32,
                                       rec->rect, rec->bsum, status));
   }
+#if SS_DIRECT_BIN
+  // direct binning: tile histograms and buckets straight from the splats' tile rectangles
+  const size_t hsm = sizeof(uint32_t) * ntiles;
+  set_smem_attrs();
+  {
+    StageTimer tm(rec, ST_EMIT, s);
+    SS_CUDA_TRY(pdl_launch(pa, k_bin_count, dim3(nbb), dim3(1024), sizeof(int) * (k.tx + 1) * (k.ty + 1), s, n, rec->rect,
+                           k.tx, k.ty, rec->mat));
+  }
+  {
+    StageTimer tm(rec, ST_BUCKET, s);
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_prefix, dim3((ntiles + 31) / 32), dim3(dim3(32, 32)), 0, s, rec->totals, cap, ntiles, rec->mat, tile_count, pchunk, nbb));
+    SS_CUDA_TRY(pdl_launch(pa, k_scan_tiles, dim3(1), dim3(1024), 0, s, ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long, cap, overflow, 1));
+    SS_CUDA_TRY(pdl_launch(pa, k_bin_scatter, dim3(nbb), dim3(1024), 2 * hsm + (size_t)kBinStage * 6, s, n, rec->rect, k.tx,
+                           ntiles, rec->mat, nbb, tile_ptr, tile_count, rec->pbucket, overflow));
+  }
+#else
   if (n > 0) {
     StageTimer tm(rec, ST_EMIT, s);
     SS_CUDA_TRY(pdl_launch(pa, k_scan_blocks, dim3(1), dim3(1024), 0, s, nb, rec->bsum, rec->totals));
@@ -508,12 +529,13 @@ int ss_render_forward(const ss_camera* cam, const double* pose_Rt, const ss_spla
     const size_t hsm = sizeof(uint32_t) * ntiles;
     set_smem_attrs();
     SS_CUDA_TRY(pdl_launch(pa, k_tile_hist_blocks, dim3(pblocks), dim3(1024), hsm, s, rec->ptile, rec->totals, cap, ntiles, rec->mat, overflow, pchunk));
-    SS_CUDA_TRY(pdl_launch(pa, k_tile_prefix, dim3((ntiles + 31) / 32), dim3(dim3(32, 32)), 0, s, rec->totals, cap, ntiles, rec->mat, tile_count, pchunk));
-    SS_CUDA_TRY(pdl_launch(pa, k_scan_tiles, dim3(1), dim3(1024), 0, s, ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long));
+    SS_CUDA_TRY(pdl_launch(pa, k_tile_prefix, dim3((ntiles + 31) / 32), dim3(dim3(32, 32)), 0, s, rec->totals, cap, ntiles, rec->mat, tile_count, pchunk, 0));
+    SS_CUDA_TRY(pdl_launch(pa, k_scan_tiles, dim3(1), dim3(1024), 0, s, ntiles, tile_count, tile_ptr, chunk_ptr, rec->totals, long_list, n_long, cap, overflow, 0));
     SS_CUDA_TRY(pdl_launch(pa, k_tile_scatter, dim3(pblocks), dim3(1024), 2 * hsm + (size_t)pchunk * 6, s, rec->ptile,
                            rec->psplat, rec->totals, cap, ntiles, rec->mat, tile_ptr, rec->pbucket, overflow, pchunk,
                            tile_count));
   }
+#endif
   {
     StageTimer tm(rec, ST_TILE_SORT, s);
     // lists over kTileSortMax (listed by k_scan_tiles) sort on the side stream while the

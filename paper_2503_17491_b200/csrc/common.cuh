@@ -118,6 +118,9 @@ __device__ __forceinline__ void ray_at(const CamK& k, double u, double v, double
 #ifndef SS_HUGE_SORT
 #define SS_HUGE_SORT 256  // the 16,384-entry list sort pass when splats > this x tiles
 #endif
+#ifndef SS_DIRECT_BIN
+#define SS_DIRECT_BIN 1  // tile buckets straight from the splats' tile rectangles (no pair list)
+#endif
 #ifndef SS_SEG_MIN_LIST
 #define SS_SEG_MIN_LIST -1  // many tiles: lists this long are walked in segments (-1: a fair share, see k_tile_order)
 #endif
