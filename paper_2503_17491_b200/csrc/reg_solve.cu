@@ -551,59 +551,6 @@ __device__ double rs_median(cg::grid_group& grid, const unsigned long long* __re
   return (v1 + __longlong_as_double((long long)*((volatile unsigned long long*)vmin))) / 2.0;
 }
 
-// Block count of valid entries -> grid total (pcnt: per-block slots), and the
-// grid's smallest / largest valid pattern (pmm: per-block pairs) -> s_mm[0..1].
-__device__ int rs_count(cg::grid_group& grid, int okc, unsigned long long mn, unsigned long long mx,
-                        int* __restrict__ pcnt, unsigned long long* __restrict__ pmm, unsigned* s_part,
-                        unsigned long long* s_mm, int* s_m) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  okc = __reduce_add_sync(0xffffffffu, okc);
-  for (int off = 16; off > 0; off >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-  }
-  if (lane == 0) {
-    s_part[warp] = (unsigned)okc;
-    s_mm[2 * warp] = mn;
-    s_mm[2 * warp + 1] = mx;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int c = 0;
-    for (int w = 0; w < kRsThreads / 32; ++w) {
-      c += (int)s_part[w];
-      mn = min(mn, s_mm[2 * w]);
-      mx = max(mx, s_mm[2 * w + 1]);
-    }
-    pcnt[blockIdx.x] = c;
-    pmm[2 * blockIdx.x] = mn;
-    pmm[2 * blockIdx.x + 1] = mx;
-  }
-  grid.sync();
-  if (tid < 32) {
-    int c = 0;
-    mn = ~0ull;
-    mx = 0ull;
-    for (int b = lane; b < (int)gridDim.x; b += 32) {
-      c += pcnt[b];
-      mn = min(mn, pmm[2 * b]);
-      mx = max(mx, pmm[2 * b + 1]);
-    }
-    c = __reduce_add_sync(0xffffffffu, c);
-    for (int off = 16; off > 0; off >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    }
-    if (lane == 0) {
-      *s_m = c;
-      s_mm[2 * (kRsThreads / 32)] = mn;
-      s_mm[2 * (kRsThreads / 32) + 1] = mx;
-    }
-  }
-  __syncthreads();
-  return *s_m;
-}
-
 // Leaf hash grid for the association: cells of edge >= assoc_gate, so every
 // leaf within the gate of a point lies in the point's 27-cell neighbourhood
 // (and the k nearest within the gate -- the only ones the residual uses -- are
@@ -802,9 +749,8 @@ __global__ void __launch_bounds__(kRsThreads, kMinB) k_reg_solve(RsGeo geo, RsPh
   __shared__ double sred[kRsThreads / 32][kRsAcc];
   __shared__ double sfin[2 * kRsAcc];
   __shared__ unsigned s_part[kRsThreads / 32];
-  __shared__ int s_bin, s_before, s_m;
+  __shared__ int s_bin, s_before;
   __shared__ unsigned long long s_min[kRsThreads / 32];
-  __shared__ unsigned long long s_mm[2 * (kRsThreads / 32) + 2];
   __shared__ unsigned long long s_pub[20];
   static_assert(offsetof(RegSolveLM, pub_med) + 2 * sizeof(double) <= 20 * 8, "published fields in the first 20 words");
   __shared__ RegSolveLM s_lm;  // block 0: the LM state during the launch
