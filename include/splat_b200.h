@@ -378,6 +378,15 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
                  const uint8_t* scan_valid, const ss_camera* cam, const double* T0_Rt, const ss_reg_solve_cfg* cfg,
                  double* T_out_Rt, int32_t* info6, double* r2_out2, void* workspace, void* stream);
 
+/* Host-side staging of a float64 parameter array for upload (no GPU work): copies n values
+ * from src into dst -- as float64, or rounded to nearest float32 when dst_f32 is non-zero
+ * (the rounding the kernels' float32 parameters need; NULL dst: fingerprint only) -- and writes their content
+ * fingerprint, a position-weighted wrapping sum whose weights depend on the global index
+ * base + k, so chunks processed on different host threads add up.  Replaces the float32
+ * conversion the drop-in does per call instead of the reference's direct use of the host
+ * arrays (rasterizer.py:223-241 _splat_camera_arrays reads model.centers etc. each call). */
+int ss_host_stage_f64(const double* src, void* dst, int32_t dst_f32, int64_t n, int64_t base, uint64_t* fp);
+
 /* Measured FP32 FMA throughput of the current device (TFLOP/s), the roofline
  * denominator of the FP32-bound blend kernels.  Synchronises the stream. */
 int ss_fp32_peak_tflops(double* tflops, void* stream);

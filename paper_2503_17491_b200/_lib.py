@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
     L.ss_render_finalize.restype = ctypes.c_int
     L.ss_fp32_peak_tflops.argtypes = [ctypes.POINTER(d), vp]
     L.ss_fp32_peak_tflops.restype = ctypes.c_int
+    L.ss_host_stage_f64.argtypes = [vp, vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
+    L.ss_host_stage_f64.restype = ctypes.c_int
     L.ss_records_set_deterministic.argtypes = [vp, i32]
     L.ss_records_set_deterministic.restype = ctypes.c_int
     L.ss_records_generation.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
@@ -171,7 +173,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["ss_version", "ss_records_create", "ss_records_destroy", "ss_render_forward", "ss_records_counts",
-            "ss_records_export", "ss_records_pixel_state", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops",
+            "ss_records_export", "ss_records_pixel_state", "ss_records_check", "ss_records_work", "ss_records_profile", "ss_records_stage_times", "ss_fp32_peak_tflops", "ss_host_stage_f64",
             "ss_render_backward", "ss_mapping_loss", "ss_photo_workspace_bytes",
             "ss_photo_system", "ss_anchor_workspace_bytes", "ss_reg_anchors", "ss_range_image", "ss_scale_loss",
             "ss_adam_step", "ss_reg_solve_workspace_bytes", "ss_reg_solve",

@@ -333,6 +333,36 @@ void set_smem_attrs() {
 }
 }  // namespace
 
+// (ss_host_stage_f64 below)
+// DST: 0 no copy, 1 float64 copy, 2 float32 (round to nearest, as the device conversion)
+template <int DST>
+static uint64_t host_stage(const double* __restrict__ src, void* __restrict__ dst, int64_t n, int64_t base) {
+  constexpr uint64_t K = 0x9E3779B97F4A7C15ull;
+  const uint64_t* x = reinterpret_cast<const uint64_t*>(src);
+  uint64_t m = (uint64_t)base * K, a0 = 0, a1 = 0;
+  int64_t k = 0;
+  for (; k + 2 <= n; k += 2) {  // two accumulators: the adds do not chain on each other
+    const uint64_t v0 = x[k], v1 = x[k + 1];
+    if (DST == 1) {
+      static_cast<uint64_t*>(dst)[k] = v0;
+      static_cast<uint64_t*>(dst)[k + 1] = v1;
+    } else if (DST == 2) {
+      static_cast<float*>(dst)[k] = (float)src[k];
+      static_cast<float*>(dst)[k + 1] = (float)src[k + 1];
+    }
+    const uint64_t m1 = m + K;
+    a0 += v0 * ((m ^ (m >> 29)) | 1ull);
+    a1 += v1 * ((m1 ^ (m1 >> 29)) | 1ull);
+    m = m1 + K;
+  }
+  if (k < n) {
+    if (DST == 1) static_cast<uint64_t*>(dst)[k] = x[k];
+    if (DST == 2) static_cast<float*>(dst)[k] = (float)src[k];
+    a0 += x[k] * ((m ^ (m >> 29)) | 1ull);
+  }
+  return a0 + a1;
+}
+
 extern "C" {
 
 const char* ss_version(void) { return "paper_2503_17491_b200 0.2 (sm_100a)"; }
@@ -839,6 +869,19 @@ int ss_render_finalize(const ss_records* rec_c, const ss_splats* splats, const f
   if (begin % kFinBlock != 0) return SS_ERR_INVALID_ARGUMENT;
   if (!rec->acc || rec->cap_acc < (size_t)rec->n * kAcc) return SS_ERR_STALE_RECORDS;  // no blend pass yet
   return backward_finalize(rec, splats, d_scales_extra, grads, raw_space, begin, end, (cudaStream_t)stream);
+}
+
+// Host staging for the reference-signature drop-in (rasterizer.py, engine.splats_to_device):
+// one pass over n float64 values that copies them into the pinned upload buffer, as float64
+// or rounded to float32 (dst may be null) and returns their content fingerprint, the wrapping sum of the values' bit patterns
+// times odd position weights w_i = (m ^ (m >> 29)) | 1 with m = i * K for the global index
+// i = base + k (no multiply for the weight), so fingerprints of disjoint chunks add.  No
+// GPU work; callers run chunks on host threads.
+int ss_host_stage_f64(const double* src, void* dst, int32_t dst_f32, int64_t n, int64_t base, uint64_t* fp) {
+  if ((!src && n > 0) || n < 0 || base < 0 || !fp) return SS_ERR_INVALID_ARGUMENT;
+  *fp = !dst ? host_stage<0>(src, nullptr, n, base)
+             : (dst_f32 ? host_stage<2>(src, dst, n, base) : host_stage<1>(src, dst, n, base));
+  return SS_OK;
 }
 
 int ss_fp32_peak_tflops(double* tflops, void* stream) {

@@ -58,47 +58,102 @@ def _host_pool():
     pool = _STAGE.get("pool")
     if pool is None:
         from concurrent.futures import ThreadPoolExecutor
-        pool = _STAGE["pool"] = ThreadPoolExecutor(max_workers=5, thread_name_prefix="splat-upload")
+        pool = _STAGE["pool"] = ThreadPoolExecutor(max_workers=8, thread_name_prefix="splat-upload")
     return pool
 
 
-def splats_to_device(model, device=None) -> dict:
-    """float32 device copies of a SplatModel's raw parameters (reference or ours).
+_CHUNK = 1 << 20  # float64 values per host staging job
 
-    The host arrays are copied (in parallel, on host threads) into one reused pinned
-    staging buffer of their own dtype, uploaded with one DMA and rounded to float32 on the
-    device: a pageable upload per array and a host conversion pass cost more."""
-    device = device or require_cuda()
-    n = len(model)
-    arrs = []
-    for k in PARAM_NAMES:
-        a = np.ascontiguousarray(getattr(model, k))
-        if a.dtype not in (np.float32, np.float64):
-            a = a.astype(np.float64)
-        arrs.append(a)
-    dt = np.float64 if any(a.dtype == np.float64 for a in arrs) else np.float32
-    sizes = [n * PARAM_WIDTH[k] for k in PARAM_NAMES]
-    total = int(sum(sizes))
-    key = ("stage", dt)
+
+def _stage_chunks(src: np.ndarray, dst) -> list:
+    """``ss_host_stage_f64`` jobs (src, dst, begin, end) over ~1M-value chunks of the flat
+    float64 array ``src``: copied into ``dst`` (float64 or float32, rounded to nearest) unless
+    it is None, and fingerprinted."""
+    return [(src, dst, b, min(b + _CHUNK, src.size)) for b in range(0, max(src.size, 1), _CHUNK)]
+
+
+def _run_stage(job) -> int:
+    src, dst, b, e = job
+    if e <= b:
+        return 0
+    fp = ctypes.c_uint64(0)
+    f32 = dst is not None and dst.dtype == np.float32
+    dptr = None if dst is None else dst.ctypes.data + dst.itemsize * b
+    check(lib().ss_host_stage_f64(src.ctypes.data + 8 * b, dptr, int(f32), e - b, b, ctypes.byref(fp)))
+    return fp.value
+
+
+def fingerprints(arrays) -> tuple:
+    """Content fingerprints of host arrays (float64 values; ``ss_host_stage_f64``, host threads):
+    any in-place edit changes them.  Equal to the ones ``splats_to_device`` reports."""
+    flats = [np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(-1) for a in arrays]
+    return _sum_fps([_stage_chunks(f, None) for f in flats])
+
+
+def _sum_fps(job_lists) -> tuple:
+    flat = [j for jl in job_lists for j in jl]
+    fps = list(_host_pool().map(_run_stage, flat))
+    out, q = [], 0
+    for jl in job_lists:
+        out.append(sum(fps[q:q + len(jl)]) & 0xFFFFFFFFFFFFFFFF)
+        q += len(jl)
+    return tuple(out)
+
+
+def _pinned_stage(key, n: int):
+    """A reused pinned float32 staging buffer of >= n values and its upload event (waited
+    on: the previous upload from it has left)."""
     st = _STAGE.get(key)
-    if st is None or st[0].numel() < total:
-        st = (torch.empty(max(total, 1), dtype=torch.float64 if dt == np.float64 else torch.float32).pin_memory(),
-              torch.cuda.Event())
+    if st is None or st[0].numel() < n:
+        st = (torch.empty(max(n, 1), dtype=torch.float32).pin_memory(), torch.cuda.Event())
         _STAGE[key] = st
     else:
-        st[1].synchronize()  # the previous upload from this buffer has left it
+        st[1].synchronize()
+    return st
+
+
+def stage_upload_f32(arrays, device=None, want_fingerprints: bool = False):
+    """Host arrays -> one float32 device tensor (their concatenation) through a reused pinned
+    buffer: float64 arrays are rounded to float32 on host threads in the same pass that
+    fingerprints them (``ss_host_stage_f64``; the same rounding as a device conversion, half
+    the PCIe bytes), other dtypes are cast by numpy.  Returns (device tensor, offsets,
+    fingerprints or None)."""
+    device = device or require_cuda()
+    arrs = [np.ascontiguousarray(a).reshape(-1) for a in arrays]
+    arrs = [a if a.dtype in (np.float32, np.float64) else a.astype(np.float64) for a in arrs]
+    offs = np.concatenate([[0], np.cumsum([a.size for a in arrs])]).astype(int)
+    total = int(offs[-1])
+    st = _pinned_stage(("stage32", len(arrs)), total)
     host = st[0].numpy()
-    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
-    list(_host_pool().map(lambda j: np.copyto(host[offs[j]:offs[j + 1]], arrs[j].reshape(-1), casting="unsafe"),
-                          range(len(arrs))))
-    dev_all = st[0][:total].to(device, non_blocking=True)
+    jobs = [_stage_chunks(a, host[offs[j]:offs[j + 1]]) if a.dtype == np.float64 else [] for j, a in enumerate(arrs)]
+    casts = [j for j, a in enumerate(arrs) if a.dtype != np.float64]
+    fps = _sum_fps(jobs)
+    list(_host_pool().map(lambda j: np.copyto(host[offs[j]:offs[j + 1]], arrs[j]), casts))
+    if want_fingerprints:
+        fx = fingerprints([arrs[j] for j in casts]) if casts else ()
+        fps = list(fps)
+        for q, j in enumerate(casts):
+            fps[j] = fx[q]
+        fps = tuple(fps)
+    dev = st[0][:total].to(device, non_blocking=True)
     st[1].record()
-    dev32 = dev_all.to(torch.float32)
+    return dev, offs, (fps if want_fingerprints else None)
+
+
+def splats_to_device(model, device=None, want_fingerprints: bool = False):
+    """float32 device copies of a SplatModel's raw parameters (reference or ours).
+
+    The host arrays go through one reused pinned staging buffer (``stage_upload_f32``:
+    float64 rounded to float32 and fingerprinted on host threads in one pass) and one DMA.
+    With ``want_fingerprints`` the arrays' content fingerprints (``fingerprints``) come back
+    too, so a cache keyed on them costs no second read of the model."""
+    n = len(model)
+    dev, offs, fps = stage_upload_f32([getattr(model, k) for k in PARAM_NAMES], device, want_fingerprints)
     out = {}
     for j, k in enumerate(PARAM_NAMES):
-        t = dev32[offs[j]:offs[j + 1]]
+        t = dev[offs[j]:offs[j + 1]]
         out[k] = t if k == "logit_opacity" else t.view(n, PARAM_WIDTH[k])
-    return out
+    return (out, fps) if want_fingerprints else out
 
 
 def as_device_params(x) -> dict:

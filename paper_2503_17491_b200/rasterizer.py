@@ -186,23 +186,6 @@ def _pool():
 # float32 device copies of models, keyed by object identity, version, the parameter
 # arrays' identities and buffers, and a content fingerprint of each array
 _dev_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-_FP_W: dict = {}
-
-
-def _fingerprint(a) -> int:
-    """Position-sensitive content fingerprint of a parameter array: the wrapping sum of
-    its 64-bit words times fixed odd pseudo-random weights (~1 ms per 1.5 M values).
-    Any in-place edit the reference's version counter would not see
-    (``model.centers[i] = ...`` without ``touch()``) changes it; the reference itself
-    re-reads the arrays on every call."""
-    x = np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(-1).view(np.int64)
-    w = _FP_W.get(x.size)
-    if w is None:
-        w = np.random.default_rng(x.size).integers(0, 2 ** 62, x.size, dtype=np.int64) | 1
-        if len(_FP_W) > 8:
-            _FP_W.clear()
-        _FP_W[x.size] = w
-    return int(np.add.reduce(x * w, dtype=np.int64)) if x.size else 0
 
 
 def _identity_key(model) -> tuple:
@@ -214,7 +197,11 @@ def _identity_key(model) -> tuple:
 
 
 def _fingerprints(model) -> tuple:
-    return tuple(_pool().map(lambda k: _fingerprint(getattr(model, k)), engine.PARAM_NAMES))
+    """Content fingerprints of the parameter arrays (``engine.fingerprints``: a position-
+    weighted wrapping sum of the float64 bit patterns, one pass on host threads).  Any
+    in-place edit the reference's version counter would not see (``model.centers[i] = ...``
+    without ``touch()``) changes them; the reference itself re-reads the arrays every call."""
+    return engine.fingerprints([getattr(model, k) for k in engine.PARAM_NAMES])
 
 
 def _cache_key(model) -> tuple:
@@ -225,7 +212,7 @@ def _cache_key(model) -> tuple:
 def _device_params(model) -> dict:
     """float32 device copy of ``model``'s parameters, reused while the model is unchanged.
     The content fingerprints are only computed when everything else matches (a changed
-    version or array already forces the upload)."""
+    version or array already forces the upload, whose staging pass fingerprints them)."""
     ident = _identity_key(model)
     try:
         hit = _dev_cache.get(model)
@@ -235,9 +222,9 @@ def _device_params(model) -> dict:
         fp = _fingerprints(model)
         if hit[0][1] == fp:
             return hit[1]
-    t = engine.splats_to_device(model)
+    t, fp = engine.splats_to_device(model, want_fingerprints=True)
     try:
-        _dev_cache[model] = (_cache_key(model), t)
+        _dev_cache[model] = ((ident, fp), t)
     except TypeError:
         pass
     return t
@@ -266,6 +253,23 @@ def rasterize_forward(cam, pose, model, cfg: RasterConfig | None = None):
     return out, rec
 
 
+def _pixel_grads_to_device(pg, H: int, W: int):
+    """The three pixel-gradient images as float32 device tensors: rounded to float32 on host
+    threads into one reused pinned buffer, one upload (a pageable float64 upload per image
+    cost ~1 ms at config 1).  Device tensors pass through."""
+    xs, shapes = (pg.d_range, pg.d_normal, pg.d_opacity), ((H, W), (H, W, 3), (H, W))
+    if any(isinstance(x, torch.Tensor) for x in xs):
+        return tuple(_dev(x, sh) for x, sh in zip(xs, shapes))
+    arrs = []
+    for x, sh in zip(xs, shapes):
+        a = np.asarray(x)
+        if a.size != int(np.prod(sh)):
+            raise ValueError(f"pixel gradient of {a.size} values, expected {int(np.prod(sh))}")
+        arrs.append(a)
+    dev32, offs, _ = engine.stage_upload_f32(arrs)
+    return tuple(dev32[offs[j]:offs[j + 1]].view(shapes[j]) for j in range(3))
+
+
 def _dev(x, like_shape):
     if isinstance(x, torch.Tensor):
         return x.to(engine.require_cuda(), torch.float32).contiguous()
@@ -284,8 +288,8 @@ def rasterize_backward(model, records: BlendRecords, render: RenderOutput, pixel
         return SplatGradients.zeros(n)
     H, W = records.cam.height, records.cam.width
     params = getattr(records, "_params", None) or _device_params(model)
-    g = engine.backward(records._handle, params, _dev(pixel_grads.d_range, (H, W)),
-                        _dev(pixel_grads.d_normal, (H, W, 3)), _dev(pixel_grads.d_opacity, (H, W)), raw_space=False)
+    gD, gN, gO = _pixel_grads_to_device(pixel_grads, H, W)
+    g = engine.backward(records._handle, params, gD, gN, gO, raw_space=False)
     out = SplatGradients.from_device(g)
     out.device = g
     return out

@@ -82,3 +82,40 @@ def test_device_cache_key_sees_inplace_edits():
     assert _cache_key(m) != k2
     m.touch()
     assert _cache_key(m)[0][0] == m.version
+
+
+def test_host_stage_rounding_and_fingerprints():
+    """ss_host_stage_f64 (host only): float32 staging equals numpy's round-to-nearest cast bit
+    for bit (subnormals, huge values, NaN/inf included), the float64 copy is exact, and the
+    fingerprint is chunk-invariant and sees a one-ulp edit."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2503_17491_b200 import engine
+    from paper_2503_17491_b200._lib import lib
+
+    rng = np.random.default_rng(3)
+    a = np.concatenate([rng.normal(size=100_001) * 10.0 ** rng.integers(-50, 50, 100_001),
+                        [1e-45, 3e-39, 1e39, -0.0, np.inf, -np.inf, np.nan, 2.0 ** -149, 1.0 + 2.0 ** -24]])
+    f32 = np.empty(a.size, np.float32)
+    f64 = np.empty(a.size, np.float64)
+    fp = ctypes.c_uint64()
+    assert lib().ss_host_stage_f64(a.ctypes.data, f32.ctypes.data, 1, a.size, 0, ctypes.byref(fp)) == 0
+    with np.errstate(over="ignore"):
+        assert np.array_equal(f32.view(np.uint32), a.astype(np.float32).view(np.uint32))
+    assert lib().ss_host_stage_f64(a.ctypes.data, f64.ctypes.data, 0, a.size, 0, ctypes.byref(fp)) == 0
+    assert np.array_equal(f64.view(np.uint64), a.view(np.uint64))
+    whole = fp.value
+    parts = 0
+    for b in range(0, a.size, 7_777):
+        e = min(b + 7_777, a.size)
+        lib().ss_host_stage_f64(a[b:].ctypes.data, None, 0, e - b, b, ctypes.byref(fp))
+        parts += fp.value
+    assert parts % 2 ** 64 == whole == engine.fingerprints([a])[0]
+    b = a.copy()
+    b[5] = np.nextafter(b[5], np.inf)
+    assert engine.fingerprints([b])[0] != whole
+    c = a.copy()
+    c[[10, 11]] = c[[11, 10]]
+    assert engine.fingerprints([c])[0] != whole
