@@ -62,7 +62,7 @@ def _host_pool():
     return pool
 
 
-_CHUNK = 1 << 20  # float64 values per host staging job
+_CHUNK = 1 << 19  # float64 values per host staging job (and per pipelined upload)
 
 
 def _stage_chunks(src: np.ndarray, dst) -> list:
@@ -116,7 +116,8 @@ def stage_upload_f32(arrays, device=None, want_fingerprints: bool = False):
     """Host arrays -> one float32 device tensor (their concatenation) through a reused pinned
     buffer: float64 arrays are rounded to float32 on host threads in the same pass that
     fingerprints them (``ss_host_stage_f64``; the same rounding as a device conversion, half
-    the PCIe bytes), other dtypes are cast by numpy.  Returns (device tensor, offsets,
+    the PCIe bytes), other dtypes are cast by numpy.  Each ~1M-value chunk is uploaded as soon
+    as it is staged, so the host pass and the DMA overlap.  Returns (device tensor, offsets,
     fingerprints or None)."""
     device = device or require_cuda()
     arrs = [np.ascontiguousarray(a).reshape(-1) for a in arrays]
@@ -125,19 +126,30 @@ def stage_upload_f32(arrays, device=None, want_fingerprints: bool = False):
     total = int(offs[-1])
     st = _pinned_stage(("stage32", len(arrs)), total)
     host = st[0].numpy()
-    jobs = [_stage_chunks(a, host[offs[j]:offs[j + 1]]) if a.dtype == np.float64 else [] for j, a in enumerate(arrs)]
-    casts = [j for j, a in enumerate(arrs) if a.dtype != np.float64]
-    fps = _sum_fps(jobs)
-    list(_host_pool().map(lambda j: np.copyto(host[offs[j]:offs[j + 1]], arrs[j]), casts))
+    dev = torch.empty(max(total, 1), dtype=torch.float32, device=device)[:total]
+    pool = _host_pool()
+    pending = []  # (future, global begin, global end, array index or -1)
+    for j, a in enumerate(arrs):
+        o = int(offs[j])
+        if a.dtype == np.float64:
+            for job in _stage_chunks(a, host[o:int(offs[j + 1])]):
+                pending.append((pool.submit(_run_stage, job), o + job[2], o + job[3], j))
+        else:
+            pending.append((pool.submit(np.copyto, host[o:int(offs[j + 1])], a), o, int(offs[j + 1]), -1))
+    fps = [0] * len(arrs)
+    for fut, b, e, j in pending:
+        r = fut.result()
+        if j >= 0:
+            fps[j] = (fps[j] + r) & 0xFFFFFFFFFFFFFFFF
+        if e > b:
+            dev[b:e].copy_(st[0][b:e], non_blocking=True)
+    st[1].record()
     if want_fingerprints:
+        casts = [j for j, a in enumerate(arrs) if a.dtype != np.float64]
         fx = fingerprints([arrs[j] for j in casts]) if casts else ()
-        fps = list(fps)
         for q, j in enumerate(casts):
             fps[j] = fx[q]
-        fps = tuple(fps)
-    dev = st[0][:total].to(device, non_blocking=True)
-    st[1].record()
-    return dev, offs, (fps if want_fingerprints else None)
+    return dev, offs, (tuple(fps) if want_fingerprints else None)
 
 
 def splats_to_device(model, device=None, want_fingerprints: bool = False):

@@ -103,23 +103,30 @@ class SplatGradients:
     @classmethod
     def from_device(cls, g: torch.Tensor) -> "SplatGradients":
         """From the (n, 15) float32 device gradients: laid out field by field on the device,
-        one copy into a reused pinned buffer, then every field widened to a new float64
-        array on its own host thread (numpy's casts release the GIL)."""
+        each field copied into a reused pinned buffer behind its own event, and widened to a
+        new float64 array on a host thread as soon as its copy lands (numpy's casts release
+        the GIL), so the download and the widening overlap."""
         n = g.shape[0]
         cols = ((0, 3), (3, 6), (6, 9), (9, 12), (12, 14), (14, 15))
         flat = torch.cat([g[:, a:b].reshape(-1) for a, b in cols])
         buf = _pinned_f32(flat.numel())
-        buf.copy_(flat, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
         host = buf.numpy()
         outs, jobs, off = [], [], 0
         for a, b in cols:
             w = b - a
+            buf[off:off + n * w].copy_(flat[off:off + n * w], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
             o = np.empty((n, w) if w > 1 else (n,), dtype=np.float64)
-            jobs.append((o, host[off:off + n * w].reshape(o.shape)))
+            jobs.append((ev, o, host[off:off + n * w].reshape(o.shape)))
             outs.append(o)
             off += n * w
-        list(_pool().map(lambda j: np.copyto(j[0], j[1]), jobs))
+
+        def widen(j):
+            j[0].synchronize()
+            np.copyto(j[1], j[2])
+
+        list(_pool().map(widen, jobs))
         return cls(*outs)
 
     @classmethod
