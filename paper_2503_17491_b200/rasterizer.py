@@ -67,7 +67,7 @@ class RenderOutput:
 
     def _get(self, k):
         if self._host[k] is None:
-            self._host[k] = self._dev[k].detach().double().cpu().numpy()
+            self._host[k] = self._dev[k].detach().cpu().numpy().astype(np.float64)  # float32 over PCIe
         return self._host[k]
 
     range = property(lambda self: self._get("range"), lambda self, v: self._host.__setitem__("range", v))
