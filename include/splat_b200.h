@@ -380,7 +380,8 @@ int ss_reg_solve(const double* leaf_centroids, const double* leaf_normals, int32
 
 /* Host-side staging of a float64 parameter array for upload (no GPU work): copies n values
  * from src into dst -- as float64, or rounded to nearest float32 when dst_f32 is non-zero
- * (the rounding the kernels' float32 parameters need; NULL dst: fingerprint only) -- and writes their content
+ * (the rounding the kernels' float32 parameters need; NULL dst: fingerprint only) -- and, unless
+ * fp is NULL (conversion only; not both NULL), writes their content
  * fingerprint, a position-weighted wrapping sum whose weights depend on the global index
  * base + k, so chunks processed on different host threads add up.  Replaces the float32
  * conversion the drop-in does per call instead of the reference's direct use of the host

@@ -65,21 +65,22 @@ def _host_pool():
 _CHUNK = 1 << 19  # float64 values per host staging job (and per pipelined upload)
 
 
-def _stage_chunks(src: np.ndarray, dst) -> list:
-    """``ss_host_stage_f64`` jobs (src, dst, begin, end) over ~1M-value chunks of the flat
-    float64 array ``src``: copied into ``dst`` (float64 or float32, rounded to nearest) unless
-    it is None, and fingerprinted."""
-    return [(src, dst, b, min(b + _CHUNK, src.size)) for b in range(0, max(src.size, 1), _CHUNK)]
+def _stage_chunks(src: np.ndarray, dst, fp: bool = True) -> list:
+    """``ss_host_stage_f64`` jobs (src, dst, begin, end, fp) over chunks of the flat float64
+    array ``src``: copied into ``dst`` (float64 or float32, rounded to nearest) unless it is
+    None, and fingerprinted when ``fp``."""
+    return [(src, dst, b, min(b + _CHUNK, src.size), fp) for b in range(0, max(src.size, 1), _CHUNK)]
 
 
 def _run_stage(job) -> int:
-    src, dst, b, e = job
+    src, dst, b, e, want = job
     if e <= b:
         return 0
     fp = ctypes.c_uint64(0)
     f32 = dst is not None and dst.dtype == np.float32
     dptr = None if dst is None else dst.ctypes.data + dst.itemsize * b
-    check(lib().ss_host_stage_f64(src.ctypes.data + 8 * b, dptr, int(f32), e - b, b, ctypes.byref(fp)))
+    check(lib().ss_host_stage_f64(src.ctypes.data + 8 * b, dptr, int(f32), e - b, b,
+                                  ctypes.byref(fp) if want or dst is None else None))
     return fp.value
 
 
@@ -132,7 +133,7 @@ def stage_upload_f32(arrays, device=None, want_fingerprints: bool = False):
     for j, a in enumerate(arrs):
         o = int(offs[j])
         if a.dtype == np.float64:
-            for job in _stage_chunks(a, host[o:int(offs[j + 1])]):
+            for job in _stage_chunks(a, host[o:int(offs[j + 1])], want_fingerprints):
                 pending.append((pool.submit(_run_stage, job), o + job[2], o + job[3], j))
         else:
             pending.append((pool.submit(np.copyto, host[o:int(offs[j + 1])], a), o, int(offs[j + 1]), -1))

@@ -18,6 +18,7 @@ rng = np.random.default_rng(0)
 pg = PixelGradients(np.sign(rng.normal(size=(cam.height, cam.width))), 0.1 * rng.normal(size=(cam.height, cam.width, 3)),
                     0.05 * rng.normal(size=(cam.height, cam.width)))
 acc = {}
+dp = R._device_params
 
 
 def tick(name, t0):
@@ -35,7 +36,9 @@ for it in range(23):
     t = tick("params (stage + upload issue)", t)
     torch.cuda.current_stream().synchronize()
     t = tick("  wait upload", t)
+    R._device_params = lambda m, _p=params: _p  # (the cache lookup was timed above)
     out, rec = R.rasterize_forward(cam, pose, model)
+    R._device_params = dp
     t = tick("forward (incl. capacity check)", t)
     _ = out.range
     t = tick("range image to host", t)
