@@ -103,8 +103,8 @@ class SplatGradients:
     @classmethod
     def from_device(cls, g: torch.Tensor) -> "SplatGradients":
         """From the (n, 15) float32 device gradients: laid out field by field on the device,
-        each field copied into a reused pinned buffer behind its own event, and widened to a
-        new float64 array on a host thread as soon as its copy lands (numpy's casts release
+        each field copied into a reused pinned buffer in ~0.5 M-value pieces, each behind its
+        own event, and widened into a new float64 array on a host thread as soon as it lands (numpy's casts release
         the GIL), so the download and the widening overlap."""
         n = g.shape[0]
         cols = ((0, 3), (3, 6), (6, 9), (9, 12), (12, 14), (14, 15))
@@ -112,13 +112,17 @@ class SplatGradients:
         buf = _pinned_f32(flat.numel())
         host = buf.numpy()
         outs, jobs, off = [], [], 0
+        rows = max(1, (1 << 19) // 3)  # ~0.5 M values per piece
         for a, b in cols:
             w = b - a
-            buf[off:off + n * w].copy_(flat[off:off + n * w], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
             o = np.empty((n, w) if w > 1 else (n,), dtype=np.float64)
-            jobs.append((ev, o, host[off:off + n * w].reshape(o.shape)))
+            for r0 in range(0, n, rows):
+                r1 = min(n, r0 + rows)
+                p0, p1 = off + r0 * w, off + r1 * w
+                buf[p0:p1].copy_(flat[p0:p1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                jobs.append((ev, o[r0:r1], host[p0:p1].reshape(o[r0:r1].shape)))
             outs.append(o)
             off += n * w
 
@@ -186,7 +190,7 @@ def _pool():
     global _POOL
     if _POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=6, thread_name_prefix="splat-host")
+        _POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="splat-host")
     return _POOL
 
 
